@@ -1,0 +1,364 @@
+/*
+ * eqc_oracle.c -- plain, slow, single-threaded CPU oracle for the sort-last
+ * compositing + RLE transport hot path of Eilemann, "Parallel Rendering and
+ * Large Data Visualization" (arxiv 1902.08755, PhD thesis UZH 2019).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_1902_08755_b200/, libeqc.so) never links, calls or
+ * includes anything from here, and this file includes nothing from there.
+ *
+ * Citation keys: "P:n" = line n of the thesis text; "S:n" = line n
+ * of SPEC.md (used for test ideas only); "R-Cn" = reading Cn of the ambiguity
+ * register in DESIGN.md section 3 (= SURVEY.md section 8(c)).
+ *
+ * Pin status (see DESIGN.md section 4 and tests/test_oracle_*.py):
+ *   or_depth_composite   pinned: exhaustive brute force, worked example D,
+ *                        permutation/monotone-transform invariants.
+ *   or_blend_ordered     pinned: closed form for identical layers, expanded
+ *                        (non-recursive) exact-rational sum, a in {0,255}
+ *                        special cases, worked example B.
+ *   or_swizzle/unswizzle pinned: hand bit traces, bijection.
+ *   or_rle_encode/decode pinned: hand-derived byte strings (tests/golden),
+ *                        round trip, size bound, brute-force token
+ *                        minimality properties.  Compression MAGNITUDES vs the
+ *                        paper's 10/25/40 % are "parity unpinned" (the paper's
+ *                        dataset is unavailable).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#define OR_OK 0
+#define OR_E_INVALID (-1)
+#define OR_E_CAPACITY (-2)
+#define OR_E_CORRUPT (-3)
+#define OR_E_UNSUPPORTED (-4)
+
+/* ------------------------------------------------------------------------ */
+/* O1 depth-sorted sort-last compositing                                      */
+/* ------------------------------------------------------------------------ */
+/*
+ * "assigns the final pixel to the colour of the source with the
+ * front-most depth buffer values".  R-C1: depth is u32, smaller = nearer.
+ * R-C2: ties go to the lower source index.  Written as the plain definition:
+ * k* = argmin over i of the pair (depth_i[p], i), compared lexicographically.
+ * out_depth may be NULL (colour-only output, R-C15).
+ */
+void or_depth_composite(int n, const uint32_t *const *color,
+                        const uint32_t *const *depth, int w, int h,
+                        int64_t pitch, uint32_t *out_color,
+                        uint32_t *out_depth, int64_t out_pitch) {
+  for (int y = 0; y < h; ++y) {
+    for (int x = 0; x < w; ++x) {
+      int64_t p = (int64_t)y * pitch + x;
+      int best = 0;
+      for (int i = 1; i < n; ++i) {
+        uint32_t di = depth[i][p], db = depth[best][p];
+        /* lexicographic (depth, index): i > best always, so only a strictly
+           smaller depth makes i the new minimum */
+        if (di < db || (di == db && i < best)) best = i;
+      }
+      int64_t q = (int64_t)y * out_pitch + x;
+      out_color[q] = color[best][p];
+      if (out_depth) out_depth[q] = depth[best][p];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O2 ordered (spatial) back-to-front alpha compositing                       */
+/* ------------------------------------------------------------------------ */
+/*
+ * partial images are depth-sorted and "composited in order,
+ * typically with alpha-blending"; the application supplies the order
+ * (P:1598-1600).  R-C3: premultiplied Porter-Duff "over".  R-C4: the chain is
+ * evaluated exactly (double here) and rounded ONCE at the end, half up.
+ *   x_{-1} = bg_c / 255
+ *   x_k    = s_{k,c} / 255 + x_{k-1} * (1 - a_k / 255)     k = 0..n-1
+ *   out_c  = clamp(floor(255 * x_{n-1} + 1/2), 0, 255)
+ * Position k = 0 is the farthest layer; order[k] names the source drawn k-th
+ * (NULL = identity).  Byte c of a pixel is channel c (R-C7: R = byte 0,
+ * A = byte 3).
+ */
+void or_blend_ordered(int n, const uint32_t *const *color,
+                      const int32_t *order, int w, int h, int64_t pitch,
+                      uint32_t background, uint32_t *out_color,
+                      int64_t out_pitch) {
+  for (int y = 0; y < h; ++y) {
+    for (int x = 0; x < w; ++x) {
+      int64_t p = (int64_t)y * pitch + x;
+      double xc[4];
+      for (int c = 0; c < 4; ++c) xc[c] = (double)((background >> (8 * c)) & 0xFFu) / 255.0;
+      for (int k = 0; k < n; ++k) {
+        int src = order ? order[k] : k;
+        uint32_t s = color[src][p];
+        double a = (double)(s >> 24) / 255.0;
+        for (int c = 0; c < 4; ++c) {
+          double sc = (double)((s >> (8 * c)) & 0xFFu) / 255.0;
+          xc[c] = sc + xc[c] * (1.0 - a);
+        }
+      }
+      uint32_t o = 0;
+      for (int c = 0; c < 4; ++c) {
+        double v = floor(255.0 * xc[c] + 0.5);
+        if (v < 0.0) v = 0.0;
+        if (v > 255.0) v = 255.0;
+        o |= ((uint32_t)v) << (8 * c);
+      }
+      out_color[(int64_t)y * out_pitch + x] = o;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Swizzle preconditioner                                                     */
+/* ------------------------------------------------------------------------ */
+/*
+ * "reorders and interleaves the per-component bits ... by
+ * grouping them by significance".  The figure is missing;
+ * R-C9 takes S:429: output bit 4b + (3 - c) = bit b of channel c, channels
+ * c = 0 R, 1 G, 2 B, 3 A (bit 31 = R7, 30 = G7, 29 = B7, 28 = A7, ...,
+ * 0 = A0).  Written as the bit-by-bit definition.
+ */
+uint32_t or_swizzle(uint32_t v) {
+  uint32_t o = 0;
+  for (int c = 0; c < 4; ++c)
+    for (int b = 0; b < 8; ++b)
+      if ((v >> (8 * c + b)) & 1u) o |= 1u << (4 * b + (3 - c));
+  return o;
+}
+
+uint32_t or_unswizzle(uint32_t v) {
+  uint32_t o = 0;
+  for (int c = 0; c < 4; ++c)
+    for (int b = 0; b < 8; ++b)
+      if ((v >> (4 * b + (3 - c))) & 1u) o |= 1u << (8 * c + b);
+  return o;
+}
+
+/* ------------------------------------------------------------------------ */
+/* RLE-BP v1: per-component (byte-plane) RLE, chunked by row segments         */
+/* ------------------------------------------------------------------------ */
+/*
+ * "treat each colour component separately by producing four
+ * independent RLE-compressed output streams".  P:2427-2430: "All RLE
+ * compressors perform a data decomposition on the input image" (chunks).
+ * The bit stream is reading R-C8:
+ *   chunk = C = 2^log2c pixels of one row (last chunk of a row may be short);
+ *   plane p of a chunk = byte p of each (optionally swizzled) word, x order;
+ *   plane record = [ntok u8][ctrl u8 x ntok][payloads], where each maximal
+ *   run of >= 3 equal bytes is a REPEAT token (ctrl 0x80|(len-1), payload =
+ *   the byte) and each maximal span not covered by REPEAT tokens is a
+ *   LITERAL token (ctrl len-1, payload = the bytes);
+ *   stream = 32 B header, 8 B table entry per chunk {u32 payload offset,
+ *   u8 plane_size[4]}, then chunk records in chunk-id order.
+ */
+#define RLE_MAGIC 0x4C525145u /* "EQRL" little-endian */
+#define RLE_VERSION 1
+
+static void put_u32(uint8_t *d, uint32_t v) {
+  d[0] = (uint8_t)v; d[1] = (uint8_t)(v >> 8); d[2] = (uint8_t)(v >> 16); d[3] = (uint8_t)(v >> 24);
+}
+static void put_u64(uint8_t *d, uint64_t v) {
+  put_u32(d, (uint32_t)v); put_u32(d + 4, (uint32_t)(v >> 32));
+}
+static uint32_t get_u32(const uint8_t *d) {
+  return (uint32_t)d[0] | ((uint32_t)d[1] << 8) | ((uint32_t)d[2] << 16) | ((uint32_t)d[3] << 24);
+}
+static uint64_t get_u64(const uint8_t *d) {
+  return (uint64_t)get_u32(d) | ((uint64_t)get_u32(d + 4) << 32);
+}
+
+int64_t or_rle_max_size(int w, int h, int log2c) {
+  if (w <= 0 || h <= 0 || log2c < 5 || log2c > 7) return OR_E_INVALID;
+  int64_t C = 1 << log2c;
+  int64_t S = (w + C - 1) / C;
+  return 32 + 16 * S * (int64_t)h + 4 * (int64_t)w * h;
+}
+
+/*
+ * Encode one plane record of L bytes b[0..L) into out; returns its size.
+ * Step 1: find maximal runs.  Step 2: runs of length >= 3 -> REPEAT.
+ * Step 3: maximal spans of bytes not in a REPEAT -> one LITERAL each.
+ * Step 4: record = [ntok][ctrl...][payload...].
+ */
+int or_rle_encode_plane(const uint8_t *b, int L, uint8_t *out) {
+  uint8_t ctrl[256];
+  uint8_t payload[256];
+  int ntok = 0, npay = 0;
+  int lit_start = -1; /* start of the open literal span, -1 if none */
+  int i = 0;
+  while (i < L) {
+    int j = i + 1;
+    while (j < L && b[j] == b[i]) ++j; /* maximal run [i, j) */
+    int run = j - i;
+    if (run >= 3) {
+      if (lit_start >= 0) { /* close the pending literal span */
+        int len = i - lit_start;
+        ctrl[ntok++] = (uint8_t)(len - 1);
+        for (int k = lit_start; k < i; ++k) payload[npay++] = b[k];
+        lit_start = -1;
+      }
+      ctrl[ntok++] = (uint8_t)(0x80 | (run - 1));
+      payload[npay++] = b[i];
+    } else if (lit_start < 0) {
+      lit_start = i;
+    }
+    i = j;
+  }
+  if (lit_start >= 0) {
+    int len = L - lit_start;
+    ctrl[ntok++] = (uint8_t)(len - 1);
+    for (int k = lit_start; k < L; ++k) payload[npay++] = b[k];
+  }
+  out[0] = (uint8_t)ntok;
+  memcpy(out + 1, ctrl, (size_t)ntok);
+  memcpy(out + 1 + ntok, payload, (size_t)npay);
+  return 1 + ntok + npay;
+}
+
+/*
+ * Decode one plane record of exactly rec_size bytes into L bytes.
+ * Returns 0 or OR_E_CORRUPT (ntok < 1, token lengths not summing to L,
+ * payload size inconsistent with rec_size).
+ */
+int or_rle_decode_plane(const uint8_t *rec, int rec_size, int L, uint8_t *b) {
+  if (rec_size < 1) return OR_E_CORRUPT;
+  int ntok = rec[0];
+  if (ntok < 1 || 1 + ntok > rec_size) return OR_E_CORRUPT;
+  const uint8_t *ctrl = rec + 1;
+  int pay = 1 + ntok;
+  int pos = 0;
+  for (int t = 0; t < ntok; ++t) {
+    int len = (ctrl[t] & 0x7F) + 1;
+    if (pos + len > L) return OR_E_CORRUPT;
+    if (ctrl[t] & 0x80) {
+      if (pay + 1 > rec_size) return OR_E_CORRUPT;
+      for (int k = 0; k < len; ++k) b[pos + k] = rec[pay];
+      pay += 1;
+    } else {
+      if (pay + len > rec_size) return OR_E_CORRUPT;
+      for (int k = 0; k < len; ++k) b[pos + k] = rec[pay + k];
+      pay += len;
+    }
+    pos += len;
+  }
+  if (pos != L || pay != rec_size) return OR_E_CORRUPT;
+  return OR_OK;
+}
+
+/*
+ * Encode a W x H image of 32-bit words (row pitch in words) into dst.
+ * kind 0 = RGBA8 colour, 1 = depth u32; flags bit 0 = swizzle (colour only,
+ * R-C11).  Returns the stream size in bytes, or a negative error.
+ */
+int64_t or_rle_encode(const uint32_t *src, int w, int h, int64_t pitch,
+                      int kind, int flags, int log2c, uint8_t *dst,
+                      int64_t cap) {
+  if (!src || !dst || w <= 0 || h <= 0 || pitch < w) return OR_E_INVALID;
+  if (kind != 0 && kind != 1) return OR_E_INVALID;
+  if (flags & ~1) return OR_E_INVALID;
+  if (kind == 1 && (flags & 1)) return OR_E_UNSUPPORTED;
+  if (log2c < 5 || log2c > 7) return OR_E_INVALID;
+  int C = 1 << log2c;
+  int S = (w + C - 1) / C;
+  int64_t nchunks = (int64_t)S * h;
+  if (nchunks > 0xFFFFFFFFll) return OR_E_INVALID;
+  int64_t table = 32, payload0 = 32 + 8 * nchunks;
+  if (cap < payload0) return OR_E_CAPACITY;
+  uint8_t plane[128];
+  uint8_t rec[4][130];
+  int64_t off = 0; /* payload offset of the current chunk */
+  for (int y = 0; y < h; ++y) {
+    for (int k = 0; k < S; ++k) {
+      int x0 = k * C;
+      int L = (w - x0 < C) ? (w - x0) : C;
+      int sz[4];
+      for (int p = 0; p < 4; ++p) {
+        for (int i = 0; i < L; ++i) {
+          uint32_t v = src[(int64_t)y * pitch + x0 + i];
+          if (flags & 1) v = or_swizzle(v);
+          plane[i] = (uint8_t)(v >> (8 * p));
+        }
+        sz[p] = or_rle_encode_plane(plane, L, rec[p]);
+      }
+      int64_t chunk_id = (int64_t)y * S + k;
+      int64_t total = sz[0] + sz[1] + sz[2] + sz[3];
+      if (off > 0xFFFFFFFFll) return OR_E_INVALID; /* u32 offset field */
+      if (payload0 + off + total > cap) return OR_E_CAPACITY;
+      uint8_t *te = dst + table + 8 * chunk_id;
+      put_u32(te, (uint32_t)off);
+      for (int p = 0; p < 4; ++p) te[4 + p] = (uint8_t)sz[p];
+      uint8_t *o = dst + payload0 + off;
+      for (int p = 0; p < 4; ++p) { memcpy(o, rec[p], (size_t)sz[p]); o += sz[p]; }
+      off += total;
+    }
+  }
+  put_u32(dst + 0, RLE_MAGIC);
+  dst[4] = RLE_VERSION;
+  dst[5] = (uint8_t)kind;
+  dst[6] = (uint8_t)flags;
+  dst[7] = (uint8_t)log2c;
+  put_u32(dst + 8, (uint32_t)w);
+  put_u32(dst + 12, (uint32_t)h);
+  put_u32(dst + 16, (uint32_t)nchunks);
+  put_u32(dst + 20, 0);
+  put_u64(dst + 24, (uint64_t)off);
+  return payload0 + off;
+}
+
+/*
+ * Decode a stream into a W x H image (row pitch in words).  The caller states
+ * the expected W and H; the header must agree.  Validation follows DESIGN.md
+ * section 5: magic/version/kind/flags/log2c, W/H and chunk count, offsets
+ * monotone and contiguous, each plane record well formed, total size.
+ */
+int or_rle_decode(const uint8_t *src, int64_t src_bytes, uint32_t *dst,
+                  int64_t pitch, int w, int h) {
+  if (!src || !dst || w <= 0 || h <= 0 || pitch < w) return OR_E_INVALID;
+  if (src_bytes < 32) return OR_E_CORRUPT;
+  if (get_u32(src) != RLE_MAGIC || src[4] != RLE_VERSION) return OR_E_CORRUPT;
+  int kind = src[5], flags = src[6], log2c = src[7];
+  if (kind > 1 || (flags & ~1) || (kind == 1 && flags) || log2c < 5 || log2c > 7)
+    return OR_E_CORRUPT;
+  if ((int64_t)get_u32(src + 8) != w || (int64_t)get_u32(src + 12) != h) return OR_E_CORRUPT;
+  int C = 1 << log2c;
+  int S = (w + C - 1) / C;
+  int64_t nchunks = (int64_t)S * h;
+  if ((int64_t)get_u32(src + 16) != nchunks || get_u32(src + 20) != 0) return OR_E_CORRUPT;
+  uint64_t pbytes = get_u64(src + 24);
+  int64_t payload0 = 32 + 8 * nchunks;
+  if ((uint64_t)src_bytes < (uint64_t)payload0 || (uint64_t)(src_bytes - payload0) < pbytes)
+    return OR_E_CORRUPT;
+  uint8_t plane[128];
+  uint64_t expect = 0;
+  for (int y = 0; y < h; ++y) {
+    for (int k = 0; k < S; ++k) {
+      int x0 = k * C;
+      int L = (w - x0 < C) ? (w - x0) : C;
+      int64_t chunk_id = (int64_t)y * S + k;
+      const uint8_t *te = src + 32 + 8 * chunk_id;
+      uint64_t off = get_u32(te);
+      if (off != expect) return OR_E_CORRUPT; /* monotone and contiguous */
+      uint64_t total = (uint64_t)te[4] + te[5] + te[6] + te[7];
+      if (off + total > pbytes) return OR_E_CORRUPT;
+      const uint8_t *r = src + payload0 + off;
+      for (int i = 0; i < L; ++i) dst[(int64_t)y * pitch + x0 + i] = 0;
+      for (int p = 0; p < 4; ++p) {
+        int rc = or_rle_decode_plane(r, te[4 + p], L, plane);
+        if (rc) return rc;
+        for (int i = 0; i < L; ++i)
+          dst[(int64_t)y * pitch + x0 + i] |= (uint32_t)plane[i] << (8 * p);
+        r += te[4 + p];
+      }
+      if (flags & 1)
+        for (int i = 0; i < L; ++i)
+          dst[(int64_t)y * pitch + x0 + i] = or_unswizzle(dst[(int64_t)y * pitch + x0 + i]);
+      expect = off + total;
+    }
+  }
+  if (expect != pbytes) return OR_E_CORRUPT;
+  return OR_OK;
+}
