@@ -1,0 +1,244 @@
+// composite.cu -- per-pixel sort-last compositing kernels for sm_100a.
+//
+//  compositor_depth          depth-sorted compositing (R-C1, R-C2)
+//  compositor_blend_ordered  ordered back-to-front "over" (R-C3, R-C4)
+//
+// Both are HBM-bound streaming reductions over N source frames:
+// depth moves (8N + 8) B per output pixel (8N + 4 colour-only), blend (4N + 4).
+// Design: one thread owns 4 consecutive pixels of a row and
+// issues one 128-bit streaming load per source buffer (L1 no-allocate, L2
+// evict-first: every input byte is read exactly once), keeps the running
+// result in registers and writes one 128-bit streaming store per output buffer.
+// No shared memory, no tensor cores: there is no reuse and no contraction.
+#include "eqc_common.cuh"
+
+namespace {
+
+struct DepthParams {
+  const uint32_t *color[EQC_MAX_SOURCES];
+  const uint32_t *depth[EQC_MAX_SOURCES];
+  uint32_t *out_color;
+  uint32_t *out_depth;
+  int64_t pitch, out_pitch;
+  int n, w, h, groups_per_row;
+};
+
+// One running (depth, colour) minimum step per lane: strictly smaller depth
+// replaces, so for equal depths the earlier (lower-index) source is kept.
+__device__ __forceinline__ void zmin(uint32_t &bd, uint32_t &bc, uint32_t d, uint32_t c) {
+  bool t = d < bd;
+  bd = t ? d : bd;
+  bc = t ? c : bc;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) depth_composite_kernel(const __grid_constant__ DepthParams p) {
+  const int64_t total = (int64_t)p.groups_per_row * p.h;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(g / p.groups_per_row);
+    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+    const int64_t off = (int64_t)y * p.pitch + x;
+    const int64_t ooff = (int64_t)y * p.out_pitch + x;
+    if (VEC && x + 4 <= p.w) {
+      uint4 bd = ld_stream_u4(p.depth[0] + off);
+      uint4 bc = ld_stream_u4(p.color[0] + off);
+      int i = 1;
+      // batches of 4 sources: 8 independent 128-bit loads in flight per thread
+      for (; i + 4 <= p.n; i += 4) {
+        uint4 d[4], c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          d[j] = ld_stream_u4(p.depth[i + j] + off);
+          c[j] = ld_stream_u4(p.color[i + j] + off);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          zmin(bd.x, bc.x, d[j].x, c[j].x);
+          zmin(bd.y, bc.y, d[j].y, c[j].y);
+          zmin(bd.z, bc.z, d[j].z, c[j].z);
+          zmin(bd.w, bc.w, d[j].w, c[j].w);
+        }
+      }
+      for (; i < p.n; ++i) {
+        uint4 d = ld_stream_u4(p.depth[i] + off);
+        uint4 c = ld_stream_u4(p.color[i] + off);
+        zmin(bd.x, bc.x, d.x, c.x);
+        zmin(bd.y, bc.y, d.y, c.y);
+        zmin(bd.z, bc.z, d.z, c.z);
+        zmin(bd.w, bc.w, d.w, c.w);
+      }
+      st_stream_u4(p.out_color + ooff, bc);
+      if (p.out_depth) st_stream_u4(p.out_depth + ooff, bd);
+    } else {
+      const int cnt = min(4, p.w - x);
+      for (int k = 0; k < cnt; ++k) {
+        uint32_t bd = p.depth[0][off + k], bc = p.color[0][off + k];
+        for (int i = 1; i < p.n; ++i) zmin(bd, bc, p.depth[i][off + k], p.color[i][off + k]);
+        p.out_color[ooff + k] = bc;
+        if (p.out_depth) p.out_depth[ooff + k] = bd;
+      }
+    }
+  }
+}
+
+struct BlendParams {
+  const uint32_t *color[EQC_MAX_SOURCES];  // already in draw order, back first
+  uint32_t *out_color;
+  int64_t pitch, out_pitch;
+  int n, w, h, groups_per_row;
+  float bg[4];
+};
+
+// Exact float of byte k of v: build the bit pattern 0x4B0000bb (= 2^23 + bb)
+// with one byte permute, then remove the 2^23 bias (both steps exact).
+template <int K>
+__device__ __forceinline__ float byte_f(uint32_t v) {
+  return __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7440 + K)) - 8388608.0f;
+}
+
+struct Acc4 {
+  float r, g, b, a;
+};
+
+// x = s + x * (1 - a_s/255) per channel, all in units of 1/255 (fp32 FMAs).
+__device__ __forceinline__ void over(Acc4 &x, uint32_t s) {
+  // 255 - a exactly: (2^23 + 255) - (2^23 + a)
+  const float t = 8388863.0f - __uint_as_float(__byte_perm(s, 0x4B000000u, 0x7443));
+  const float f = t * (1.0f / 255.0f);
+  x.r = fmaf(x.r, f, byte_f<0>(s));
+  x.g = fmaf(x.g, f, byte_f<1>(s));
+  x.b = fmaf(x.b, f, byte_f<2>(s));
+  x.a = fmaf(x.a, f, byte_f<3>(s));
+}
+
+__device__ __forceinline__ uint32_t pack_round(const Acc4 &x) {
+  // one rounding to RGBA8 (round-to-nearest), clamped to [0, 255]
+  uint32_t r = min(__float2uint_rn(x.r), 255u);
+  uint32_t g = min(__float2uint_rn(x.g), 255u);
+  uint32_t b = min(__float2uint_rn(x.b), 255u);
+  uint32_t a = min(__float2uint_rn(x.a), 255u);
+  return r | (g << 8) | (b << 16) | (a << 24);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) blend_ordered_kernel(const __grid_constant__ BlendParams p) {
+  const int64_t total = (int64_t)p.groups_per_row * p.h;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(g / p.groups_per_row);
+    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+    const int64_t off = (int64_t)y * p.pitch + x;
+    const int64_t ooff = (int64_t)y * p.out_pitch + x;
+    if (VEC && x + 4 <= p.w) {
+      Acc4 acc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = Acc4{p.bg[0], p.bg[1], p.bg[2], p.bg[3]};
+      int k = 0;
+      for (; k + 4 <= p.n; k += 4) {
+        uint4 s[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[j] = ld_stream_u4(p.color[k + j] + off);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          over(acc[0], s[j].x);
+          over(acc[1], s[j].y);
+          over(acc[2], s[j].z);
+          over(acc[3], s[j].w);
+        }
+      }
+      for (; k < p.n; ++k) {
+        uint4 s = ld_stream_u4(p.color[k] + off);
+        over(acc[0], s.x);
+        over(acc[1], s.y);
+        over(acc[2], s.z);
+        over(acc[3], s.w);
+      }
+      uint4 o = make_uint4(pack_round(acc[0]), pack_round(acc[1]), pack_round(acc[2]), pack_round(acc[3]));
+      st_stream_u4(p.out_color + ooff, o);
+    } else {
+      const int cnt = min(4, p.w - x);
+      for (int q = 0; q < cnt; ++q) {
+        Acc4 acc{p.bg[0], p.bg[1], p.bg[2], p.bg[3]};
+        for (int k = 0; k < p.n; ++k) over(acc, p.color[k][off + q]);
+        p.out_color[ooff + q] = pack_round(acc);
+      }
+    }
+  }
+}
+
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+inline int grid_for(int64_t items) {
+  int64_t blocks = (items + 255) / 256;
+  int64_t cap = (int64_t)eqc_num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+}  // namespace
+
+extern "C" int compositor_depth(int n, const uint32_t *const *color, const uint32_t *const *depth,
+                                int w, int h, int64_t pitch, uint32_t *out_color,
+                                uint32_t *out_depth, int64_t out_pitch, void *stream) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color || !depth || !out_color) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
+  DepthParams p;
+  bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) && aligned16(out_color) &&
+             (!out_depth || aligned16(out_depth));
+  for (int i = 0; i < n; ++i) {
+    if (!color[i] || !depth[i]) return EQC_E_INVALID;
+    p.color[i] = color[i];
+    p.depth[i] = depth[i];
+    vec = vec && aligned16(color[i]) && aligned16(depth[i]);
+  }
+  p.out_color = out_color;
+  p.out_depth = out_depth;
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (vec)
+    depth_composite_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
+  else
+    depth_composite_kernel<false><<<grid_for(groups), 256, 0, s>>>(p);
+  return eqc_launch_status();
+}
+
+extern "C" int compositor_blend_ordered(int n, const uint32_t *const *color, const int32_t *order,
+                                        int w, int h, int64_t pitch, uint32_t background,
+                                        uint32_t *out_color, int64_t out_pitch, void *stream) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color || !out_color) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
+  BlendParams p;
+  bool seen[EQC_MAX_SOURCES] = {false};
+  bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) && aligned16(out_color);
+  for (int k = 0; k < n; ++k) {
+    int src = order ? order[k] : k;
+    if (src < 0 || src >= n || seen[src]) return EQC_E_INVALID;  // not a permutation
+    seen[src] = true;
+    if (!color[src]) return EQC_E_INVALID;
+    p.color[k] = color[src];
+    vec = vec && aligned16(color[src]);
+  }
+  p.out_color = out_color;
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  for (int c = 0; c < 4; ++c) p.bg[c] = (float)((background >> (8 * c)) & 0xFFu);
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (vec)
+    blend_ordered_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
+  else
+    blend_ordered_kernel<false><<<grid_for(groups), 256, 0, s>>>(p);
+  return eqc_launch_status();
+}

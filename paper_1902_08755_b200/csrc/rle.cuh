@@ -1,0 +1,300 @@
+// rle.cuh -- warp-level RLE-BP v1 chunk encoder/decoder (sm_100a).
+//
+// Thesis: per-component RLE, "four independent RLE-compressed output streams"
+// (P:2402-2405); bit-swizzle preconditioner grouping bits "by significance"
+// (P:2407-2425); data decomposition of the image into independently coded
+// sub-images.  Wire format: reading R-C8, DESIGN.md §5.
+//
+// GPU mapping: one warp codes one 128-pixel row chunk.  Lane l
+// owns pixels 4l..4l+3 (one 128-bit load), so the four byte planes of the
+// chunk are processed SIMD-within-a-word: byte p of every register word is
+// plane p.  Run detection is a per-byte equality flag (bit 7 of each byte);
+// the REPEAT cover of a byte is local (a byte is in a run of >= 3 iff one of
+// the three length-3 windows through it is constant), token starts and
+// payload-emitting bytes follow from the cover and one neighbour, and all
+// four planes' token / payload counts are prefix-summed at once as packed
+// bytes in two warp scans.
+#pragma once
+
+#include "eqc_common.cuh"
+
+namespace eqc_rle {
+
+constexpr uint32_t kMagic = 0x4C525145u;  // "EQRL"
+constexpr int kVersion = 1;
+constexpr int kLog2C = 7;
+constexpr int kC = 128;
+constexpr int kStageBytes = 544;  // >= 4 planes * (128 + 2) bytes, 16-aligned
+constexpr int kTokBytes = 512;    // token-start scratch: 4 planes * 128
+
+// ---- swizzle (R-C9): out bit 4b + (3 - c) = bit b of channel c ------------
+// Byte reversal maps channel c to c' = 3 - c; the remaining permutation of the
+// 5 bit-index bits (c'1 c'0 b2 b1 b0) -> (b2 b1 b0 c'1 c'0) is four
+// transpositions of index bits, each one delta swap.
+__device__ __forceinline__ uint32_t delta_swap(uint32_t x, int d, uint32_t m) {
+  uint32_t t = ((x >> d) ^ x) & m;
+  return x ^ t ^ (t << d);
+}
+__device__ __forceinline__ uint32_t swizzle(uint32_t v) {
+  v = __byte_perm(v, 0, 0x0123);
+  v = delta_swap(v, 12, 0x0000F0F0u);  // index bits 4 <-> 2
+  v = delta_swap(v, 6, 0x00CC00CCu);   // 3 <-> 1
+  v = delta_swap(v, 3, 0x0A0A0A0Au);   // 2 <-> 0
+  v = delta_swap(v, 1, 0x22222222u);   // 1 <-> 0
+  return v;
+}
+__device__ __forceinline__ uint32_t unswizzle(uint32_t v) {
+  v = delta_swap(v, 1, 0x22222222u);
+  v = delta_swap(v, 3, 0x0A0A0A0Au);
+  v = delta_swap(v, 6, 0x00CC00CCu);
+  v = delta_swap(v, 12, 0x0000F0F0u);
+  return __byte_perm(v, 0, 0x0123);
+}
+
+__device__ __forceinline__ uint32_t bytep(uint32_t v, int p) { return (v >> (8 * p)) & 0xFFu; }
+
+// Position-validity flag word for position i of a chunk of length L.
+__device__ __forceinline__ uint32_t vflag(bool ok) { return ok ? 0x80808080u : 0u; }
+
+struct EncodeOut {
+  int size;           // chunk record bytes
+  uint32_t psizes;    // byte p = plane p record size
+};
+
+// Encode the chunk whose pixels (already swizzled if requested) lane `lane`
+// holds in px[0..3] (positions 4*lane + j, valid while < L).  Writes the
+// chunk record (planes 0..3 concatenated) into the warp's staging buffer `st`
+// and returns its size.  `tp` is per-warp scratch of kTokBytes bytes.
+__device__ __forceinline__ EncodeOut encode_chunk(const uint32_t px[4], int L, int lane,
+                                                  uint8_t *st, uint8_t *tp) {
+  const int i0 = 4 * lane;
+  // ---- fast path: the whole chunk is one value (background, flat regions)
+  {
+    const uint32_t v0 = __shfl_sync(EQC_FULL, px[0], 0);
+    bool same = true;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) same = same && (i0 + j >= L || px[j] == v0);
+    if (__all_sync(EQC_FULL, same) && L >= 3) {
+      if (lane < 4) {
+        st[3 * lane + 0] = 1;
+        st[3 * lane + 1] = (uint8_t)(0x80 | (L - 1));
+        st[3 * lane + 2] = (uint8_t)bytep(v0, lane);
+      }
+      __syncwarp();
+      return EncodeOut{12, 0x03030303u};
+    }
+  }
+  // ---- neighbours: W[-2], W[-1] from the previous lane, W[4], W[5] from the next
+  const uint32_t wm2 = __shfl_up_sync(EQC_FULL, px[2], 1);
+  const uint32_t wm1 = __shfl_up_sync(EQC_FULL, px[3], 1);
+  const uint32_t wp4 = __shfl_down_sync(EQC_FULL, px[0], 1);
+  const uint32_t wp5 = __shfl_down_sync(EQC_FULL, px[1], 1);
+  // e[j] (j = -1..5): byte at position i0+j equals its predecessor, for
+  // 1 <= i0+j < L (no predecessor at the chunk start; nothing beyond L).
+  uint32_t e[7];
+  {
+    const uint32_t W[8] = {wm2, wm1, px[0], px[1], px[2], px[3], wp4, wp5};
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const int pos = i0 + k - 1;
+      e[k] = bytes_eq(W[k + 1], W[k]) & vflag(pos >= 1 && pos < L);
+    }
+  }
+  // P3[j] = e[j] & e[j+1]: the window (j-1, j, j+1) is constant (j = -1..4)
+  uint32_t p3[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) p3[k] = e[k] & e[k + 1];
+  // R[j]: position in a run of >= 3 (REPEAT cover)
+  uint32_t R[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) R[j] = p3[j] | p3[j + 1] | p3[j + 2];
+  uint32_t Rprev = __shfl_up_sync(EQC_FULL, R[3], 1);
+  if (lane == 0) Rprev = 0;
+  // T[j]: token start; E[j]: byte emits a payload byte (literal or REPEAT head)
+  uint32_t T[4], E[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t valid = vflag(i0 + j < L);
+    const uint32_t rp = (j == 0) ? Rprev : R[j - 1];
+    const uint32_t first = vflag(i0 + j == 0);
+    T[j] = (first | (R[j] ^ rp) | (R[j] & rp & ~e[j + 1])) & valid;
+    E[j] = (~R[j] | T[j]) & valid;
+  }
+  // nibble per plane: bit j of byte p = flag of position i0+j in plane p
+  const uint32_t nibT = ((T[0] >> 7) | (T[1] >> 6) | (T[2] >> 5) | (T[3] >> 4)) & 0x0F0F0F0Fu;
+  const uint32_t nibE = ((E[0] >> 7) | (E[1] >> 6) | (E[2] >> 5) | (E[3] >> 4)) & 0x0F0F0F0Fu;
+  const uint32_t nibR = ((R[0] >> 7) | (R[1] >> 6) | (R[2] >> 5) | (R[3] >> 4)) & 0x0F0F0F0Fu;
+  const uint32_t cT = bytes_popc_nibble(nibT);
+  const uint32_t cE = bytes_popc_nibble(nibE);
+  const uint32_t incT = warp_incl_scan_add(cT, lane);
+  const uint32_t incE = warp_incl_scan_add(cE, lane);
+  const uint32_t totT = __shfl_sync(EQC_FULL, incT, 31);
+  const uint32_t totE = __shfl_sync(EQC_FULL, incE, 31);
+  const uint32_t exT = incT - cT, exE = incE - cE;
+  int base[5];
+  base[0] = 0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) base[p + 1] = base[p] + 1 + (int)bytep(totT, p) + (int)bytep(totE, p);
+  // ---- scatter: token starts to tp, payload bytes to st
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t t = (nibT >> (8 * p)) & 15u, ev = (nibE >> (8 * p)) & 15u, r = (nibR >> (8 * p)) & 15u;
+    int tk = (int)bytep(exT, p);
+    int ek = base[p] + 1 + (int)bytep(totT, p) + (int)bytep(exE, p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if ((t >> j) & 1u) {
+        tp[p * kC + tk] = (uint8_t)((i0 + j) | (((r >> j) & 1u) << 7));
+        ++tk;
+      }
+      if ((ev >> j) & 1u) {
+        st[ek] = (uint8_t)bytep(px[j], p);
+        ++ek;
+      }
+    }
+  }
+  if (lane < 4) st[base[lane]] = (uint8_t)bytep(totT, lane);
+  __syncwarp();
+  // ---- ctrl bytes: token length = next token start - this start
+  const int n0 = (int)bytep(totT, 0), n1 = n0 + (int)bytep(totT, 1), n2 = n1 + (int)bytep(totT, 2),
+            n3 = n2 + (int)bytep(totT, 3);
+  for (int q = lane; q < n3; q += 32) {
+    const int p = (q >= n0) + (q >= n1) + (q >= n2);
+    const int pb = (p == 0) ? 0 : (p == 1) ? n0 : (p == 2) ? n1 : n2;
+    const int np = (p == 0) ? n0 : (p == 1) ? n1 - n0 : (p == 2) ? n2 - n1 : n3 - n2;
+    const int t = q - pb;
+    const uint32_t a = tp[p * kC + t];
+    const int next = (t + 1 < np) ? (int)(tp[p * kC + t + 1] & 0x7Fu) : L;
+    const int len = next - (int)(a & 0x7Fu);
+    const int bp = (p == 0) ? base[0] : (p == 1) ? base[1] : (p == 2) ? base[2] : base[3];
+    st[bp + 1 + t] = (uint8_t)((a & 0x80u) | (uint32_t)(len - 1));
+  }
+  __syncwarp();
+  uint32_t ps = 0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) ps |= (uint32_t)(base[p + 1] - base[p]) << (8 * p);
+  return EncodeOut{base[4], ps};
+}
+
+// Copy the warp's staged record (st[0..size)) to global bytes [g, g+size).
+// Interior 4-byte-aligned words are stored whole (funnel-shifted out of the
+// staging words); the <= 3 head and <= 3 tail bytes are byte stores.
+__device__ __forceinline__ void store_record(uint8_t *g, const uint8_t *st, int size, int lane) {
+  const uintptr_t ga = (uintptr_t)g;
+  const uintptr_t first_w = (ga + 3) & ~(uintptr_t)3;
+  const uintptr_t end = ga + (uintptr_t)size;
+  const uintptr_t last_w = end & ~(uintptr_t)3;
+  if (first_w >= last_w) {  // no whole word: all bytes individually
+    for (int k = lane; k < size; k += 32) g[k] = st[k];
+    return;
+  }
+  const int head = (int)(first_w - ga);
+  const int tail = (int)(end - last_w);
+  if (lane < head) g[lane] = st[lane];
+  if (lane >= 8 && lane < 8 + tail) g[(int)(last_w - ga) + lane - 8] = st[(int)(last_w - ga) + lane - 8];
+  const int nw = (int)((last_w - first_w) >> 2);
+  const uint32_t *st32 = reinterpret_cast<const uint32_t *>(st);
+  const int sh = head & 3;  // staging byte offset of each word's first byte, mod 4
+  uint32_t *gw = reinterpret_cast<uint32_t *>(first_w);
+  for (int k = lane; k < nw; k += 32) {
+    const int q = head + 4 * k;  // staging index of the word's first byte
+    const uint32_t lo = st32[q >> 2];
+    const uint32_t hi = sh ? st32[(q >> 2) + 1] : 0u;
+    gw[k] = sh ? __funnelshift_r(lo, hi, 8 * sh) : lo;
+  }
+}
+
+// ---- decoder ---------------------------------------------------------------
+
+// Decode plane record r[0..size) (staging bytes) of a chunk of length L into
+// byte p of out[0..3] (positions 4*lane + j).  `info` is per-warp scratch of
+// 128 uint16.  Returns false if the record is malformed (warp-uniform).
+__device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, int lane, int p,
+                                             uint32_t out[4], uint16_t *info) {
+  const int i0 = 4 * lane;
+  if (size < 2) return false;
+  const int ntok = r[0];
+  if (ntok < 1 || 1 + ntok > size) return false;
+  if (ntok == 1) {  // single-token fast paths (uniform)
+    const int c = r[1];
+    const int len = (c & 0x7F) + 1;
+    if (len != L) return false;
+    if (c & 0x80) {
+      if (size != 3) return false;
+      const uint32_t v = (uint32_t)r[2] << (8 * p);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) out[j] |= v;
+    } else {
+      if (size != 2 + L) return false;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i0 + j < L) out[j] |= (uint32_t)r[2 + i0 + j] << (8 * p);
+    }
+    return true;
+  }
+  // tokens 4*lane .. 4*lane+3
+  int sl = 0, sp = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = i0 + k;
+    if (t < ntok) {
+      const int c = r[1 + t];
+      const int len = (c & 0x7F) + 1;
+      const int pay = (c & 0x80) ? 1 : len;
+      sl += len;
+      sp += pay;
+    }
+  }
+  const uint32_t packed = (uint32_t)sl | ((uint32_t)sp << 16);
+  const uint32_t inc = warp_incl_scan_add(packed, lane);
+  const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
+  if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
+  uint32_t ex = inc - packed;
+  int spos = (int)(ex & 0xFFFFu);
+  int ppos = 1 + ntok + (int)(ex >> 16);
+  // clear the per-position info table, then mark each token start with
+  // (payload index | literal flag << 15)
+  reinterpret_cast<uint2 *>(info)[lane] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = i0 + k;
+    if (t < ntok) {
+      const int c = r[1 + t];
+      const int len = (c & 0x7F) + 1;
+      info[spos] = (uint16_t)(ppos | ((c & 0x80) ? 0 : 0x8000));
+      spos += len;
+      ppos += (c & 0x80) ? 1 : len;
+    }
+  }
+  __syncwarp();
+  // covering token start of each position: running max of start positions
+  const uint2 iw = reinterpret_cast<const uint2 *>(info)[lane];
+  const uint16_t inf[4] = {(uint16_t)(iw.x & 0xFFFF), (uint16_t)(iw.x >> 16), (uint16_t)(iw.y & 0xFFFF),
+                           (uint16_t)(iw.y >> 16)};
+  int lmax = -1;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (inf[j] != 0xFFFF && i0 + j < L) lmax = i0 + j;
+  int pre = lmax;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(EQC_FULL, pre, d);
+    if (lane >= d) pre = max(pre, o);
+  }
+  int run = __shfl_up_sync(EQC_FULL, pre, 1);
+  if (lane == 0) run = -1;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int i = i0 + j;
+    if (i < L) {
+      if (inf[j] != 0xFFFF) run = i;
+      const uint32_t ti = info[run];
+      const int pi = (int)(ti & 0x7FFFu) + ((ti & 0x8000u) ? (i - run) : 0);
+      out[j] |= (uint32_t)r[pi] << (8 * p);
+    }
+  }
+  return true;
+}
+
+}  // namespace eqc_rle

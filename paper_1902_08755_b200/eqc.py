@@ -1,0 +1,184 @@
+"""Thin ctypes binding of libeqc (include/eqc.h).  Argument marshalling only:
+every step of the path runs in the CUDA kernels of libeqc.so.
+
+Functions keep the C names.  Pixel buffers are passed as torch CUDA tensors
+(uint32 frames [H, pitch] viewed through [:, :W], or uint8 streams) or as raw
+device addresses (int).  ``stream`` is a torch.cuda.Stream, a raw handle (int)
+or None (= torch's current stream).  A negative return code raises EqcError.
+There is no CPU fallback: if libeqc.so is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libeqc.so")
+
+OK = 0
+E_INVALID, E_CAPACITY, E_CORRUPT, E_UNSUPPORTED, E_CUDA, E_NCCL = -1, -2, -3, -4, -5, -6
+MAX_SOURCES = 64
+KIND_RGBA8, KIND_DEPTH32 = 0, 1
+FLAG_SWIZZLE = 1
+
+
+class EqcError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {strerror(code)} ({code})")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libeqc.so not found at {LIB_PATH}: build it with "
+            "`python -m paper_1902_08755_b200.build` (there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
+    sig = {
+        "eqc_strerror": ([i32], ctypes.c_char_p),
+        "eqc_version": ([], i32),
+        "compositor_depth": ([i32, P, P, i32, i32, i64, P, P, i64, P], i32),
+        "compositor_blend_ordered": ([i32, P, P, i32, i32, i64, u32, P, i64, P], i32),
+        "image_rle_max_size": ([i32, i32], i64),
+        "image_rle_workspace_size": ([i32, i32], sz),
+        "image_rle_workspace_size_batch": ([i32, i32, i32], sz),
+        "image_compress_rle": ([P, i32, i32, i64, i32, i32, P, i64, P, P, sz, P], i32),
+        "image_decompress_rle": ([P, i64, P, i64, i32, i32, P, P], i32),
+        "image_compress_rle_batch": ([i32, P, i32, i32, i64, P, P, P, i64, P, P, sz, P], i32),
+        "image_decompress_rle_batch": ([i32, P, i64, P, i64, i32, i32, P, P], i32),
+        "compositor_depth_rle": ([i32, P, P, i64, i32, i32, P, P, i64, P, P], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def strerror(code: int) -> str:
+    return _lib.eqc_strerror(int(code)).decode()
+
+
+def version() -> int:
+    return int(_lib.eqc_version())
+
+
+def _check(rc: int, where: str) -> int:
+    if rc < 0:
+        raise EqcError(rc, where)
+    return rc
+
+
+def _addr(x) -> int | None:
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream)
+    if isinstance(s, int):
+        return s
+    return int(s.cuda_stream)
+
+
+def _ptrs(xs):
+    return (ctypes.c_void_p * len(xs))(*[_addr(x) for x in xs])
+
+
+def _frame_geom(t):
+    """(w, h, pitch) of a uint32 frame tensor [H, W] with row stride pitch."""
+    h, w = t.shape
+    assert t.stride(1) == 1, "frames must be row-major with unit column stride"
+    return w, h, t.stride(0)
+
+
+def compositor_depth(colors, depths, out_color, out_depth=None, stream=None):
+    n = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    _, _, opitch = _frame_geom(out_color)
+    rc = _lib.compositor_depth(n, _ptrs(colors), _ptrs(depths), w, h, pitch, _addr(out_color),
+                               _addr(out_depth), opitch, _stream(stream))
+    return _check(rc, "compositor_depth")
+
+
+def compositor_blend_ordered(colors, out_color, order=None, background: int = 0, stream=None):
+    n = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    _, _, opitch = _frame_geom(out_color)
+    ordp = None
+    if order is not None:
+        ordp = (ctypes.c_int32 * n)(*[int(v) for v in order])
+    rc = _lib.compositor_blend_ordered(n, _ptrs(colors), ordp, w, h, pitch, int(background) & 0xFFFFFFFF,
+                                       _addr(out_color), opitch, _stream(stream))
+    return _check(rc, "compositor_blend_ordered")
+
+
+def image_rle_max_size(w: int, h: int) -> int:
+    return _check(int(_lib.image_rle_max_size(w, h)), "image_rle_max_size")
+
+
+def image_rle_workspace_size(w: int, h: int) -> int:
+    return int(_lib.image_rle_workspace_size(w, h))
+
+
+def image_rle_workspace_size_batch(count: int, w: int, h: int) -> int:
+    return int(_lib.image_rle_workspace_size_batch(count, w, h))
+
+
+def image_compress_rle(src, kind: int, flags: int, dst, d_size, workspace, stream=None):
+    w, h, pitch = _frame_geom(src)
+    rc = _lib.image_compress_rle(_addr(src), w, h, pitch, kind, flags, _addr(dst), dst.numel(),
+                                 _addr(d_size), _addr(workspace), workspace.numel() * workspace.element_size(),
+                                 _stream(stream))
+    return _check(rc, "image_compress_rle")
+
+
+def image_decompress_rle(src, dst, d_status, src_bytes: int | None = None, stream=None):
+    w, h, pitch = _frame_geom(dst)
+    nb = src.numel() if src_bytes is None else src_bytes
+    rc = _lib.image_decompress_rle(_addr(src), nb, _addr(dst), pitch, w, h, _addr(d_status), _stream(stream))
+    return _check(rc, "image_decompress_rle")
+
+
+def image_compress_rle_batch(srcs, kinds, flags, dsts, d_sizes, workspace, stream=None):
+    n = len(srcs)
+    w, h, pitch = _frame_geom(srcs[0])
+    k = (ctypes.c_int * n)(*kinds)
+    f = (ctypes.c_int * n)(*flags)
+    cap = min(d.numel() for d in dsts)
+    rc = _lib.image_compress_rle_batch(n, _ptrs(srcs), w, h, pitch, k, f, _ptrs(dsts), cap, _addr(d_sizes),
+                                       _addr(workspace), workspace.numel() * workspace.element_size(),
+                                       _stream(stream))
+    return _check(rc, "image_compress_rle_batch")
+
+
+def image_decompress_rle_batch(srcs, dsts, d_status, src_bytes: int | None = None, stream=None):
+    n = len(srcs)
+    w, h, pitch = _frame_geom(dsts[0])
+    nb = min(s.numel() for s in srcs) if src_bytes is None else src_bytes
+    rc = _lib.image_decompress_rle_batch(n, _ptrs(srcs), nb, _ptrs(dsts), pitch, w, h, _addr(d_status),
+                                         _stream(stream))
+    return _check(rc, "image_decompress_rle_batch")
+
+
+def compositor_depth_rle(color_streams, depth_streams, out_color, out_depth, d_status,
+                         src_bytes: int | None = None, stream=None):
+    n = len(color_streams)
+    w, h, opitch = _frame_geom(out_color)
+    nb = min(s.numel() for s in list(color_streams) + list(depth_streams)) if src_bytes is None else src_bytes
+    rc = _lib.compositor_depth_rle(n, _ptrs(color_streams), _ptrs(depth_streams), nb, w, h, _addr(out_color),
+                                   _addr(out_depth), opitch, _addr(d_status), _stream(stream))
+    return _check(rc, "compositor_depth_rle")
