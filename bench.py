@@ -130,6 +130,12 @@ def make_inputs(seed, n, w, h):
     return c, d
 
 
+def launches_per_compose(n, exchange):
+    """Our kernels per compose_direct_send call: local pre-composite + band
+    composite (+ n-1 band encodes and one decode batch with RLE)."""
+    return 2 + ((n - 1) + 1 if exchange == "rle" else 0)
+
+
 def run_eqc(args):
     import torch
     import torch.distributed as dist
@@ -159,6 +165,12 @@ def run_eqc(args):
     out_c = torch.empty((H, W), dtype=torch.int32, device=dev)
     out_d = torch.empty((H, W), dtype=torch.int32, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
+    comm = None
+    final = None
+    if world > 1:
+        comm = eqc.Comm.from_torch_distributed()
+        final = torch.empty((H, W), dtype=torch.int32, device=dev) if rank == 0 else None
+    xflags = eqc.FLAG_RLE if args.exchange == "rle" else 0
 
     ev_enc = []  # per-launch kernel timing on the launching stream
 
@@ -173,6 +185,9 @@ def run_eqc(args):
         if timed_events is not None:
             e2.record(stream)
             timed_events.append((e0, e1, e2))
+        if comm is not None:
+            # screen-partition direct send of this GPU's partial frame
+            eqc.compose_direct_send(comm, [out_c], [out_d], final, dest_rank=0, flags=xflags, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -217,7 +232,7 @@ def run_eqc(args):
         for hsrc, dsrc in zip(host_in, imgs):
             dsrc.copy_(hsrc, non_blocking=True)
         step()
-        host_out.copy_(out_c, non_blocking=True)
+        host_out.copy_(final if final is not None else out_c, non_blocking=True)
 
     for _ in range(2):
         e2e_step()
@@ -237,9 +252,11 @@ def run_eqc(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     h2d = sum(x.numel() * 4 for x in host_in)
-    d2h = host_out.numel() * 4
+    d2h = host_out.numel() * 4 if (world == 1 or rank == 0) else 0
 
     if rank != 0:
+        if comm is not None:
+            comm.destroy()
         if world > 1:
             dist.destroy_process_group()
         return
@@ -298,10 +315,12 @@ def run_eqc(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(world * NSRC * P / (e2e_ms * 1e-3) / 1e6, 1), "unit": UNIT,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (2 if world == 1 else 2 + launches_per_compose(world, args.exchange)) * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.destroy()
     if world > 1:
         dist.destroy_process_group()
 
@@ -377,6 +396,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="rows of the frame in one CPU-oracle sample (0 = calibrate to a time budget)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="raw", choices=["raw", "rle"],
+                    help="direct-send band transport for N > 1 (raw bands or RLE streams)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "eqc":
         log("note: warmup raised to 3 (timing rule)")

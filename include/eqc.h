@@ -145,21 +145,23 @@ EQC_API int image_decompress_rle(const uint8_t *src, int64_t src_bytes, uint32_t
                          int w, int h, int32_t *d_status, void *stream);
 
 /*
- * Batched codec calls: `count` images of identical w x h in ONE launch
+ * Batched codec calls: `count` (<= 64) images of identical w x h in ONE launch
  * (the chunked data decomposition of P:2427-2430 applied across images).
  *   Per image i: src[i]/dst[i] device pointers (host arrays), kind[i] and
- *   flags[i] (host arrays), d_sizes[i] / one shared d_status.  Each dst[i]
- *   holds dst_capacity >= image_rle_max_size(w, h) bytes.  The workspace
- *   holds image_rle_workspace_size_batch(count, w, h) bytes.
+ *   flags[i] (host arrays), d_sizes[i] (device int64 array); one shared
+ *   d_status.  Encoder: each dst[i] holds dst_capacity >=
+ *   image_rle_max_size(w, h) bytes; the workspace holds
+ *   image_rle_workspace_size_batch(count, w, h) bytes.  Decoder:
+ *   src_bytes[i] (host array) = bytes readable at src[i].
  */
 EQC_API size_t image_rle_workspace_size_batch(int count, int w, int h);
 EQC_API int image_compress_rle_batch(int count, const uint32_t *const *src, int w, int h, int64_t pitch,
-                             const int *kind, const int *flags, uint8_t *const *dst,
-                             int64_t dst_capacity, int64_t *d_sizes, void *workspace,
-                             size_t workspace_bytes, void *stream);
-EQC_API int image_decompress_rle_batch(int count, const uint8_t *const *src, int64_t src_bytes,
-                               uint32_t *const *dst, int64_t pitch, int w, int h,
-                               int32_t *d_status, void *stream);
+                                     const int *kind, const int *flags, uint8_t *const *dst,
+                                     int64_t dst_capacity, int64_t *d_sizes, void *workspace,
+                                     size_t workspace_bytes, void *stream);
+EQC_API int image_decompress_rle_batch(int count, const uint8_t *const *src, const int64_t *src_bytes,
+                                       uint32_t *const *dst, int64_t pitch, int w, int h,
+                                       int32_t *d_status, void *stream);
 
 /*
  * compositor_depth_rle -- decode (stage 5) fused with depth assembly (stage 7)
@@ -167,15 +169,21 @@ EQC_API int image_decompress_rle_batch(int count, const uint8_t *const *src, int
  * as RLE streams (colour and depth), are decoded chunk by chunk into registers
  * and z-composited without materialising the decoded frames in HBM.  Same
  * result as image_decompress_rle on every stream followed by compositor_depth.
- *   color_rle, depth_rle  host arrays of n device stream pointers, each with
- *              src_bytes readable bytes; colour streams kind RGBA8 (any flags),
- *              depth streams kind DEPTH32, all w x h.
+ * Depth is decoded first; a source's colour chunk is decoded only where the
+ * source wins at least one pixel of the 128-pixel chunk (a hidden source's
+ * colour is never read).  Every stream's header and chunk table are
+ * validated; record-level validation covers the records that are decoded.
+ *   color_rle, depth_rle  host arrays of n device stream pointers (8-byte
+ *              aligned); color_bytes[i] / depth_bytes[i] (host) = bytes
+ *              readable at each.  Colour streams kind RGBA8 (any flags), depth
+ *              streams kind DEPTH32, all w x h with 128-pixel chunks.
  *   out_color  device [h][out_pitch]; out_depth nullable.
  *   d_status   as in image_decompress_rle.
  */
 EQC_API int compositor_depth_rle(int n, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
-                         int64_t src_bytes, int w, int h, uint32_t *out_color, uint32_t *out_depth,
-                         int64_t out_pitch, int32_t *d_status, void *stream);
+                                 const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h,
+                                 uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
+                                 int32_t *d_status, void *stream);
 
 #ifdef __cplusplus
 }

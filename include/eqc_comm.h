@@ -1,0 +1,121 @@
+/*
+ * eqc_comm.h -- multi-GPU parallel compositing schedules of libeqc.
+ *
+ * Thesis: "Two commonly used parallel compositing algorithms are direct send
+ * and binary swap.  Both distribute the compositing task equally over all
+ * available resources, then collect the composited tiles on the destination
+ * channel".  Direct send: each resource "fully composite[s] a
+ * single tile" after every channel "exchanges ... colour+depth tiles with its
+ * neighbours" (fDirectSend); binary swap "exchanges pixels
+ * between pairs of nodes using a binary compositing tree" (fBS);
+ * a "final colour-only output image" is assembled on the destination
+ * (P:1582-1584).  Readings: R-C5 (tie rule across schedules), R-C13 (balanced
+ * row bands), R-C14 (the destination is also a source), R-C15 (colour-only
+ * gather); DESIGN.md section 3.
+ *
+ * One process per GPU.  The transport is NCCL (NVLink 5 / NVSwitch); the
+ * unique id is bootstrapped by the caller (e.g. torch.distributed broadcast).
+ * Conventions as in eqc.h: device buffers owned by the caller, host arrays
+ * of device pointers, asynchronous on `stream`, negative EQC_E_* on error.
+ */
+#ifndef EQC_COMM_H
+#define EQC_COMM_H
+
+#include "eqc.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct eqc_comm eqc_comm;
+
+#define EQC_UNIQUE_ID_BYTES 128
+#define EQC_OP_DEPTH 0      /* depth-sorted compositing (compositor_depth semantics) */
+#define EQC_FLAG_RLE 1      /* ship bands as RLE-BP streams (colour swizzled + depth) */
+
+/* NCCL unique id of a new clique (rank 0 calls this and broadcasts the bytes). */
+EQC_API int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]);
+
+/*
+ * eqc_comm_init -- join the clique as `rank` of `nranks` on the CURRENT CUDA
+ * device (collective: every rank must call it).  *comm receives an opaque
+ * handle that owns the NCCL communicator and the schedule's scratch buffers
+ * (allocated lazily by the first compose call, reused afterwards).
+ */
+EQC_API int eqc_comm_init(eqc_comm **comm, int nranks, int rank, const uint8_t id[EQC_UNIQUE_ID_BYTES]);
+EQC_API int eqc_comm_destroy(eqc_comm *comm);
+
+/*
+ * Traffic counters of the last compose call on this rank:
+ * out[0] band messages sent (one per colour+depth band/region),
+ * out[1] gather messages sent (colour bands to the destination),
+ * out[2] payload bytes sent, out[3] payload bytes received.
+ */
+EQC_API int eqc_comm_stats(const eqc_comm *comm, int64_t out[4]);
+
+/*
+ * Host-side schedule plans (no GPU needed; used by the executors below and
+ * by the tests).
+ * eqc_plan_bands: row0[j] = floor(j*h/n), j = 0..n (band j = rows
+ *   [row0[j], row0[j+1]), R-C13).
+ * eqc_plan_binary_swap: for rank `rank` of n = 2^k ranks, fills k rounds of
+ *   6 ints {partner, low (1 if rank's bit r is 0), keep_y0, keep_y1, send_y0,
+ *   send_y1} (rows) and returns k; the region after the last round is the
+ *   rank's final band.  EQC_E_UNSUPPORTED if n is not a power of two.
+ */
+EQC_API int eqc_plan_bands(int h, int n, int *row0);
+EQC_API int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_rounds);
+
+/*
+ * compose_direct_send -- sort-last depth compositing of all ranks' sources
+ * with the direct-send schedule.  Rank g holds the n_local sources with
+ * global indices [g*n_local, (g+1)*n_local) (contiguous blocks, R-C5).
+ *   (1) local pre-composite of the rank's sources (compositor_depth);
+ *   (2) [EQC_FLAG_RLE: encode each outgoing band, exchange sizes];
+ *   (3) every rank sends band j (colour + depth) to rank j (NCCL grouped
+ *       send/recv over NVLink);
+ *   (4) [decode]; rank j composites the n partial bands in rank order;
+ *   (5) ranks send their composited colour band to dest_rank, which writes
+ *       the final image to out_color [h][out_pitch] (ignored on other ranks).
+ * Result: bit-identical to compositor_depth over all nranks*n_local sources.
+ * With EQC_FLAG_RLE the call synchronises `stream` once (message sizes).
+ */
+EQC_API int compose_direct_send(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                                const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream);
+
+/*
+ * compose_binary_swap -- same contract with the binary-swap schedule:
+ * log2(n) rounds; in round r the partner is rank ^ 2^r, the current row
+ * region [y0, y1) splits at m = y0 + floor((y1 - y0)/2), the rank whose bit
+ * r is 0 keeps [y0, m) and sends [m, y1), the partner the reverse; the kept
+ * half is composited with ties going to the bit-0 group (R-C5).  Finally
+ * every rank's region (colour) is gathered on dest_rank.
+ * EQC_E_UNSUPPORTED unless nranks is a power of two.
+ */
+EQC_API int compose_binary_swap(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                                const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream);
+
+/*
+ * Single-GPU "virtual rank" executors (the thesis's own testing trick of
+ * running a sort-last compound on several channels of one GPU):
+ * run the identical schedule for nranks virtual ranks in one process, with
+ * device-to-device copies standing in for NCCL.  color/depth hold
+ * nranks*n_local device pointers (rank-major).  Traffic counters are summed
+ * over all virtual ranks into out_stats[4] (nullable).
+ */
+EQC_API int compose_direct_send_local(int nranks, int n_local, const uint32_t *const *color,
+                                      const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
+                                      int flags, int dest_rank, uint32_t *out_color, int64_t out_pitch,
+                                      int64_t *out_stats, void *stream);
+EQC_API int compose_binary_swap_local(int nranks, int n_local, const uint32_t *const *color,
+                                      const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
+                                      int flags, int dest_rank, uint32_t *out_color, int64_t out_pitch,
+                                      int64_t *out_stats, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EQC_COMM_H */

@@ -1,0 +1,811 @@
+// compose.cu -- multi-GPU parallel compositing schedules (direct send,
+// binary swap) over NCCL, plus single-GPU "virtual rank" executors of the
+// identical schedule (device copies stand in for NCCL).
+//
+// Thesis: direct send and binary swap "distribute the compositing task
+// equally over all available resources, then collect the composited tiles on
+// the destination channel"; direct send exchanges colour+depth
+// tiles and composites one tile per channel; binary swap pairs
+// nodes in a binary compositing tree; the final image is
+// colour-only.  The optional RLE band transport is stages
+// (2)-(5) of the asynchronous compositing pipeline.
+//
+// Every per-pixel step runs in the libeqc kernels (compositor_depth,
+// image_compress_rle_batch, image_decompress_rle_batch); this file only
+// plans the schedule and moves bytes (NCCL grouped send/recv on the caller's
+// stream, NVLink 5 / NVSwitch).
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+#include "../../include/eqc_comm.h"
+#include "eqc_common.cuh"
+
+namespace {
+
+#define EQC_NCCL_TRY(expr)                 \
+  do {                                     \
+    ncclResult_t _r = (expr);              \
+    if (_r != ncclSuccess) return EQC_E_NCCL; \
+  } while (0)
+
+#define EQC_TRY(expr)           \
+  do {                          \
+    int _rc = (expr);           \
+    if (_rc != EQC_OK) return _rc; \
+  } while (0)
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t n = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= n) return EQC_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return EQC_E_CUDA;
+    n = bytes;
+    return EQC_OK;
+  }
+  int ensure_zeroed(size_t bytes) {
+    if (bytes <= n) return EQC_OK;
+    EQC_TRY(ensure(bytes));
+    return cudaMemset(p, 0, bytes) == cudaSuccess ? EQC_OK : EQC_E_CUDA;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  template <typename T>
+  T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+// Per-rank scratch of a schedule.
+struct RankState {
+  int rank = 0;
+  const uint32_t *const *color = nullptr;  // host array of n_local device ptrs
+  const uint32_t *const *depth = nullptr;
+  DevBuf part_c[2], part_d[2];  // partial frame (ping-pong for binary swap), pitch w
+  DevBuf recv_c, recv_d;        // incoming bands/halves
+  DevBuf fin_c;                 // finished colour band awaiting the gather
+  DevBuf enc, dec, sizes, ws, status;
+  int64_t *h_sizes = nullptr;   // pinned
+  int cur = 0;                  // binary swap: index of the live partial buffer
+  int64_t stats[4] = {0, 0, 0, 0};
+
+  void release() {
+    for (int i = 0; i < 2; ++i) {
+      part_c[i].release();
+      part_d[i].release();
+    }
+    recv_c.release();
+    recv_d.release();
+    fin_c.release();
+    enc.release();
+    dec.release();
+    sizes.release();
+    ws.release();
+    status.release();
+    if (h_sizes) cudaFreeHost(h_sizes);
+    h_sizes = nullptr;
+  }
+};
+
+struct Geometry {
+  int n = 1;          // ranks
+  int n_local = 1;    // sources per rank
+  int w = 0, h = 0;
+  int64_t pitch = 0;  // of the source frames
+  int flags = 0;
+  int dest = 0;
+  uint32_t *out = nullptr;
+  int64_t out_pitch = 0;
+  std::vector<int> row0;  // direct-send bands
+};
+
+// ---- transports -------------------------------------------------------------
+struct Transport {
+  virtual ~Transport() {}
+  virtual int start() = 0;
+  virtual int send(RankState &me, int peer, const void *buf, size_t bytes) = 0;
+  virtual int recv(RankState &me, int peer, void *buf, size_t bytes) = 0;
+  virtual int end() = 0;
+};
+
+struct NcclTransport : Transport {
+  ncclComm_t comm;
+  cudaStream_t s;
+  NcclTransport(ncclComm_t c, cudaStream_t st) : comm(c), s(st) {}
+  int start() override {
+    EQC_NCCL_TRY(ncclGroupStart());
+    return EQC_OK;
+  }
+  int send(RankState &me, int peer, const void *buf, size_t bytes) override {
+    me.stats[2] += (int64_t)bytes;
+    EQC_NCCL_TRY(ncclSend(buf, bytes, ncclUint8, peer, comm, s));
+    return EQC_OK;
+  }
+  int recv(RankState &me, int peer, void *buf, size_t bytes) override {
+    me.stats[3] += (int64_t)bytes;
+    EQC_NCCL_TRY(ncclRecv(buf, bytes, ncclUint8, peer, comm, s));
+    return EQC_OK;
+  }
+  int end() override {
+    EQC_NCCL_TRY(ncclGroupEnd());
+    return EQC_OK;
+  }
+};
+
+// Virtual ranks in one process: sends are matched FIFO per (from, to) pair
+// with receives at end(), exactly like NCCL's in-order p2p matching.
+struct LocalTransport : Transport {
+  cudaStream_t s;
+  struct Msg {
+    int from, to;
+    const void *src;
+    void *dst;
+    size_t bytes;
+    bool used;
+  };
+  std::vector<Msg> sends, recvs;
+  explicit LocalTransport(cudaStream_t st) : s(st) {}
+  int start() override {
+    sends.clear();
+    recvs.clear();
+    return EQC_OK;
+  }
+  int send(RankState &me, int peer, const void *buf, size_t bytes) override {
+    me.stats[2] += (int64_t)bytes;
+    sends.push_back(Msg{me.rank, peer, buf, nullptr, bytes, false});
+    return EQC_OK;
+  }
+  int recv(RankState &me, int peer, void *buf, size_t bytes) override {
+    me.stats[3] += (int64_t)bytes;
+    recvs.push_back(Msg{peer, me.rank, nullptr, buf, bytes, false});
+    return EQC_OK;
+  }
+  int end() override {
+    for (auto &r : recvs) {
+      bool matched = false;
+      for (auto &sd : sends) {
+        if (!sd.used && sd.from == r.from && sd.to == r.to) {
+          if (sd.bytes != r.bytes) return EQC_E_INVALID;  // size mismatch = schedule bug
+          sd.used = true;
+          matched = true;
+          if (r.bytes) EQC_CUDA_TRY(cudaMemcpyAsync(r.dst, sd.src, r.bytes, cudaMemcpyDeviceToDevice, s));
+          break;
+        }
+      }
+      if (!matched) return EQC_E_INVALID;
+    }
+    for (auto &sd : sends)
+      if (!sd.used) return EQC_E_INVALID;
+    return EQC_OK;
+  }
+};
+
+// ---- plans --------------------------------------------------------------------
+void plan_bands(int h, int n, int *row0) {
+  for (int j = 0; j <= n; ++j) row0[j] = (int)((int64_t)j * h / n);
+}
+
+struct BsRound {
+  int partner, low, keep_y0, keep_y1, send_y0, send_y1;
+};
+
+int plan_bs(int h, int n, int rank, std::vector<BsRound> &out) {
+  if (n < 1 || (n & (n - 1))) return EQC_E_UNSUPPORTED;
+  out.clear();
+  int y0 = 0, y1 = h;
+  for (int r = 0; (1 << r) < n; ++r) {
+    const int m = y0 + (y1 - y0) / 2;
+    BsRound b;
+    b.partner = rank ^ (1 << r);
+    b.low = ((rank >> r) & 1) == 0;
+    if (b.low) {
+      b.keep_y0 = y0, b.keep_y1 = m, b.send_y0 = m, b.send_y1 = y1;
+    } else {
+      b.keep_y0 = m, b.keep_y1 = y1, b.send_y0 = y0, b.send_y1 = m;
+    }
+    out.push_back(b);
+    y0 = b.keep_y0;
+    y1 = b.keep_y1;
+  }
+  return (int)out.size();
+}
+
+void final_region_bs(int h, int n, int rank, int &y0, int &y1) {
+  std::vector<BsRound> rr;
+  plan_bs(h, n, rank, rr);
+  y0 = 0;
+  y1 = h;
+  if (!rr.empty()) {
+    y0 = rr.back().keep_y0;
+    y1 = rr.back().keep_y1;
+  }
+}
+
+// ---- shared steps ---------------------------------------------------------------
+inline size_t frame_bytes(const Geometry &g, int rows) { return (size_t)rows * g.w * 4; }
+
+int alloc_common(RankState &r, const Geometry &g, size_t recv_rows, size_t band_rows, int nbuf) {
+  const size_t full = frame_bytes(g, g.h);
+  for (int i = 0; i < nbuf; ++i) {
+    EQC_TRY(r.part_c[i].ensure(full));
+    EQC_TRY(r.part_d[i].ensure(full));
+  }
+  EQC_TRY(r.recv_c.ensure(std::max<size_t>(4, recv_rows * g.w * 4)));
+  EQC_TRY(r.recv_d.ensure(std::max<size_t>(4, recv_rows * g.w * 4)));
+  EQC_TRY(r.fin_c.ensure(std::max<size_t>(4, band_rows * g.w * 4)));
+  EQC_TRY(r.status.ensure_zeroed(64));
+  if (!r.h_sizes && cudaMallocHost(&r.h_sizes, 4 * 2 * EQC_MAX_SOURCES * sizeof(int64_t)) != cudaSuccess)
+    return EQC_E_CUDA;
+  return EQC_OK;
+}
+
+int local_precomposite(RankState &r, const Geometry &g, cudaStream_t s) {
+  r.cur = 0;
+  return compositor_depth(g.n_local, r.color, r.depth, g.w, g.h, g.pitch, r.part_c[0].as<uint32_t>(),
+                          r.part_d[0].as<uint32_t>(), g.w, s);
+}
+
+// Encode `count` (<= 2 per band) colour+depth bands: slot k of `enc`.
+inline int64_t band_cap(const Geometry &g, int rows) {
+  return rows > 0 ? image_rle_max_size(g.w, rows) : 32;
+}
+
+int encode_band(RankState &r, const Geometry &g, int slot, const uint32_t *c, const uint32_t *d, int rows,
+                int64_t cap, cudaStream_t s) {
+  const uint32_t *src[2] = {c, d};
+  int kinds[2] = {EQC_KIND_RGBA8, EQC_KIND_DEPTH32};
+  int flags[2] = {EQC_FLAG_SWIZZLE, 0};
+  uint8_t *dst[2] = {r.enc.as<uint8_t>() + (size_t)(2 * slot) * cap,
+                     r.enc.as<uint8_t>() + (size_t)(2 * slot + 1) * cap};
+  return image_compress_rle_batch(2, src, g.w, rows, g.w, kinds, flags, dst, cap,
+                                  r.sizes.as<int64_t>() + 2 * slot, r.ws.p, r.ws.n, s);
+}
+
+// ---- direct send ----------------------------------------------------------------
+int ds_alloc(RankState &r, const Geometry &g) {
+  int maxband = 0;
+  for (int j = 0; j < g.n; ++j) maxband = std::max(maxband, g.row0[j + 1] - g.row0[j]);
+  EQC_TRY(alloc_common(r, g, (size_t)g.n * maxband, maxband, 1));
+  if (g.flags & EQC_FLAG_RLE) {
+    const int64_t cap = band_cap(g, maxband);
+    EQC_TRY(r.enc.ensure((size_t)2 * g.n * cap));
+    EQC_TRY(r.dec.ensure((size_t)2 * g.n * cap));
+    EQC_TRY(r.sizes.ensure((size_t)4 * g.n * sizeof(int64_t)));
+    EQC_TRY(r.ws.ensure_zeroed(image_rle_workspace_size_batch(2, g.w, std::max(1, maxband))));
+  }
+  return EQC_OK;
+}
+
+// Phase (2)+(3): send band j of the partial to rank j, receive my band from all.
+int ds_exchange_raw(RankState &r, const Geometry &g, Transport &T, int maxband) {
+  const int me = r.rank;
+  const int my_rows = g.row0[me + 1] - g.row0[me];
+  for (int j = 0; j < g.n; ++j) {
+    const int rows = g.row0[j + 1] - g.row0[j];
+    if (j == me || rows == 0) continue;
+    const size_t off = (size_t)g.row0[j] * g.w;
+    EQC_TRY(T.send(r, j, r.part_c[0].as<uint32_t>() + off, frame_bytes(g, rows)));
+    EQC_TRY(T.send(r, j, r.part_d[0].as<uint32_t>() + off, frame_bytes(g, rows)));
+    r.stats[0] += 1;
+  }
+  for (int src = 0; src < g.n; ++src) {
+    if (src == me || my_rows == 0) continue;
+    const size_t slot = (size_t)src * maxband * g.w;
+    EQC_TRY(T.recv(r, src, r.recv_c.as<uint32_t>() + slot, frame_bytes(g, my_rows)));
+    EQC_TRY(T.recv(r, src, r.recv_d.as<uint32_t>() + slot, frame_bytes(g, my_rows)));
+  }
+  return EQC_OK;
+}
+
+int ds_encode(RankState &r, const Geometry &g, cudaStream_t s) {
+  const int me = r.rank;
+  int maxband = 0;
+  for (int j = 0; j < g.n; ++j) maxband = std::max(maxband, g.row0[j + 1] - g.row0[j]);
+  const int64_t cap = band_cap(g, maxband);
+  for (int j = 0; j < g.n; ++j) {
+    const int rows = g.row0[j + 1] - g.row0[j];
+    if (j == me || rows == 0) continue;
+    const size_t off = (size_t)g.row0[j] * g.w;
+    EQC_TRY(encode_band(r, g, j, r.part_c[0].as<uint32_t>() + off, r.part_d[0].as<uint32_t>() + off, rows, cap, s));
+  }
+  return EQC_OK;
+}
+
+// sizes layout: [0, 2n) sizes of my outgoing streams, [2n, 4n) incoming
+int ds_exchange_sizes(RankState &r, const Geometry &g, Transport &T) {
+  const int me = r.rank;
+  const int my_rows = g.row0[me + 1] - g.row0[me];
+  int64_t *sz = r.sizes.as<int64_t>();
+  for (int j = 0; j < g.n; ++j) {
+    const int rows = g.row0[j + 1] - g.row0[j];
+    if (j == me || rows == 0) continue;
+    EQC_TRY(T.send(r, j, sz + 2 * j, 2 * sizeof(int64_t)));
+  }
+  for (int src = 0; src < g.n; ++src) {
+    if (src == me || my_rows == 0) continue;
+    EQC_TRY(T.recv(r, src, sz + 2 * g.n + 2 * src, 2 * sizeof(int64_t)));
+  }
+  return EQC_OK;
+}
+
+int ds_exchange_rle(RankState &r, const Geometry &g, Transport &T, int64_t cap) {
+  const int me = r.rank;
+  const int my_rows = g.row0[me + 1] - g.row0[me];
+  const int64_t *hs = r.h_sizes;
+  for (int j = 0; j < g.n; ++j) {
+    const int rows = g.row0[j + 1] - g.row0[j];
+    if (j == me || rows == 0) continue;
+    EQC_TRY(T.send(r, j, r.enc.as<uint8_t>() + (size_t)(2 * j) * cap, (size_t)hs[2 * j]));
+    EQC_TRY(T.send(r, j, r.enc.as<uint8_t>() + (size_t)(2 * j + 1) * cap, (size_t)hs[2 * j + 1]));
+    r.stats[0] += 1;
+  }
+  for (int src = 0; src < g.n; ++src) {
+    if (src == me || my_rows == 0) continue;
+    EQC_TRY(T.recv(r, src, r.dec.as<uint8_t>() + (size_t)(2 * src) * cap, (size_t)hs[2 * g.n + 2 * src]));
+    EQC_TRY(T.recv(r, src, r.dec.as<uint8_t>() + (size_t)(2 * src + 1) * cap, (size_t)hs[2 * g.n + 2 * src + 1]));
+  }
+  return EQC_OK;
+}
+
+int ds_decode(RankState &r, const Geometry &g, int maxband, int64_t cap, cudaStream_t s) {
+  const int me = r.rank;
+  const int my_rows = g.row0[me + 1] - g.row0[me];
+  if (my_rows == 0 || g.n < 2) return EQC_OK;
+  std::vector<const uint8_t *> src;
+  std::vector<uint32_t *> dst;
+  for (int q = 0; q < g.n; ++q) {
+    if (q == me) continue;
+    const size_t slot = (size_t)q * maxband * g.w;
+    src.push_back(r.dec.as<uint8_t>() + (size_t)(2 * q) * cap);
+    dst.push_back(r.recv_c.as<uint32_t>() + slot);
+    src.push_back(r.dec.as<uint8_t>() + (size_t)(2 * q + 1) * cap);
+    dst.push_back(r.recv_d.as<uint32_t>() + slot);
+  }
+  // at most 2*(64-1) streams: decode in batches of 64
+  const std::vector<int64_t> caps(src.size(), cap);
+  for (size_t b = 0; b < src.size(); b += 64) {
+    const int cnt = (int)std::min<size_t>(64, src.size() - b);
+    EQC_TRY(image_decompress_rle_batch(cnt, src.data() + b, caps.data() + b, dst.data() + b, g.w, g.w, my_rows,
+                                       r.status.as<int32_t>(), s));
+  }
+  return EQC_OK;
+}
+
+// Phase (4): composite the n partial bands of my band in rank order.
+int ds_band_composite(RankState &r, const Geometry &g, int maxband, cudaStream_t s) {
+  const int me = r.rank;
+  const int y0 = g.row0[me], rows = g.row0[me + 1] - y0;
+  if (rows == 0) return EQC_OK;
+  std::vector<const uint32_t *> c(g.n), d(g.n);
+  for (int q = 0; q < g.n; ++q) {
+    if (q == me) {
+      c[q] = r.part_c[0].as<uint32_t>() + (size_t)y0 * g.w;
+      d[q] = r.part_d[0].as<uint32_t>() + (size_t)y0 * g.w;
+    } else {
+      const size_t slot = (size_t)q * maxband * g.w;
+      c[q] = r.recv_c.as<uint32_t>() + slot;
+      d[q] = r.recv_d.as<uint32_t>() + slot;
+    }
+  }
+  uint32_t *out;
+  int64_t opitch;
+  if (me == g.dest) {
+    out = g.out + (size_t)y0 * g.out_pitch;
+    opitch = g.out_pitch;
+  } else {
+    out = r.fin_c.as<uint32_t>();
+    opitch = g.w;
+  }
+  return compositor_depth(g.n, c.data(), d.data(), g.w, rows, g.w, out, nullptr, opitch, s);
+}
+
+// Phase (5): gather colour bands/regions to the destination.  rows_of(q)
+// gives (y0, y1) of rank q's finished region; src_of(r) its device pointer.
+template <typename RegionFn>
+int gather(RankState &r, const Geometry &g, Transport &T, RegionFn region, const uint32_t *mine, cudaStream_t s,
+           int phase) {
+  // phase 0: post messages; phase 1 (dest only, after end()): 2-D copies for
+  // pitched output.
+  const int me = r.rank;
+  const bool contiguous = g.out_pitch == g.w;
+  if (phase == 0) {
+    if (me != g.dest) {
+      int y0, y1;
+      region(me, y0, y1);
+      if (y1 > y0) {
+        EQC_TRY(T.send(r, g.dest, mine, frame_bytes(g, y1 - y0)));
+        r.stats[1] += 1;
+      }
+    } else {
+      size_t scratch_off = 0;
+      for (int q = 0; q < g.n; ++q) {
+        if (q == me) continue;
+        int y0, y1;
+        region(q, y0, y1);
+        if (y1 <= y0) continue;
+        uint32_t *dst;
+        if (contiguous) {
+          dst = g.out + (size_t)y0 * g.w;
+        } else {
+          dst = r.recv_c.as<uint32_t>() + scratch_off;  // staged, copied in phase 1
+          scratch_off += (size_t)(y1 - y0) * g.w;
+        }
+        EQC_TRY(T.recv(r, q, dst, frame_bytes(g, y1 - y0)));
+      }
+    }
+  } else if (me == g.dest && !contiguous) {
+    size_t scratch_off = 0;
+    for (int q = 0; q < g.n; ++q) {
+      if (q == me) continue;
+      int y0, y1;
+      region(q, y0, y1);
+      if (y1 <= y0) continue;
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)y0 * g.out_pitch, g.out_pitch * 4,
+                                     r.recv_c.as<uint32_t>() + scratch_off, (size_t)g.w * 4, (size_t)g.w * 4,
+                                     y1 - y0, cudaMemcpyDeviceToDevice, s));
+      scratch_off += (size_t)(y1 - y0) * g.w;
+    }
+  }
+  return EQC_OK;
+}
+
+// ---- the schedules over a set of rank states (1 with NCCL, n when virtual) ----
+int run_direct_send(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaStream_t s) {
+  g.row0.assign(g.n + 1, 0);
+  plan_bands(g.h, g.n, g.row0.data());
+  int maxband = 0;
+  for (int j = 0; j < g.n; ++j) maxband = std::max(maxband, g.row0[j + 1] - g.row0[j]);
+  const bool rle = (g.flags & EQC_FLAG_RLE) != 0;
+  const int64_t cap = band_cap(g, maxband);
+  for (RankState *r : ranks) {
+    for (int i = 0; i < 4; ++i) r->stats[i] = 0;
+    EQC_TRY(ds_alloc(*r, g));
+    // the band composite needs the gather scratch for pitched output too
+    if (g.out_pitch != g.w && r->rank == g.dest)
+      EQC_TRY(r->recv_c.ensure(std::max(r->recv_c.n, frame_bytes(g, g.h))));
+    EQC_TRY(local_precomposite(*r, g, s));
+  }
+  if (g.n > 1) {
+    if (!rle) {
+      EQC_TRY(T.start());
+      for (RankState *r : ranks) EQC_TRY(ds_exchange_raw(*r, g, T, maxband));
+      EQC_TRY(T.end());
+    } else {
+      for (RankState *r : ranks) EQC_TRY(ds_encode(*r, g, s));
+      EQC_TRY(T.start());
+      for (RankState *r : ranks) EQC_TRY(ds_exchange_sizes(*r, g, T));
+      EQC_TRY(T.end());
+      for (RankState *r : ranks) {
+        EQC_CUDA_TRY(cudaMemcpyAsync(r->h_sizes, r->sizes.p, 4 * g.n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      }
+      EQC_CUDA_TRY(cudaStreamSynchronize(s));
+      EQC_TRY(T.start());
+      for (RankState *r : ranks) EQC_TRY(ds_exchange_rle(*r, g, T, cap));
+      EQC_TRY(T.end());
+      for (RankState *r : ranks) EQC_TRY(ds_decode(*r, g, maxband, cap, s));
+    }
+  }
+  for (RankState *r : ranks) EQC_TRY(ds_band_composite(*r, g, maxband, s));
+  auto region = [&](int q, int &y0, int &y1) {
+    y0 = g.row0[q];
+    y1 = g.row0[q + 1];
+  };
+  if (g.n > 1) {
+    EQC_TRY(T.start());
+    for (RankState *r : ranks) EQC_TRY(gather(*r, g, T, region, r->fin_c.as<uint32_t>(), s, 0));
+    EQC_TRY(T.end());
+    for (RankState *r : ranks) EQC_TRY(gather(*r, g, T, region, r->fin_c.as<uint32_t>(), s, 1));
+  }
+  return EQC_OK;
+}
+
+int bs_alloc(RankState &r, const Geometry &g) {
+  const int half = (g.h + 1) / 2;
+  EQC_TRY(alloc_common(r, g, std::max(half, g.out_pitch != g.w && r.rank == g.dest ? g.h : 0), 1, 2));
+  if (g.flags & EQC_FLAG_RLE) {
+    const int64_t cap = band_cap(g, half);
+    EQC_TRY(r.enc.ensure((size_t)2 * cap));
+    EQC_TRY(r.dec.ensure((size_t)2 * cap));
+    EQC_TRY(r.sizes.ensure((size_t)4 * sizeof(int64_t)));
+    EQC_TRY(r.ws.ensure_zeroed(image_rle_workspace_size_batch(2, g.w, std::max(1, half))));
+  }
+  return EQC_OK;
+}
+
+int run_binary_swap(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaStream_t s) {
+  std::vector<std::vector<BsRound>> plans(ranks.size());
+  int k = 0;
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    k = plan_bs(g.h, g.n, ranks[i]->rank, plans[i]);
+    if (k < 0) return k;
+  }
+  const bool rle = (g.flags & EQC_FLAG_RLE) != 0;
+  const int64_t cap = band_cap(g, (g.h + 1) / 2);
+  for (RankState *r : ranks) {
+    for (int i = 0; i < 4; ++i) r->stats[i] = 0;
+    EQC_TRY(bs_alloc(*r, g));
+    EQC_TRY(local_precomposite(*r, g, s));
+  }
+  for (int rd = 0; rd < k; ++rd) {
+    if (rle) {
+      for (size_t i = 0; i < ranks.size(); ++i) {
+        RankState &r = *ranks[i];
+        const BsRound &b = plans[i][rd];
+        const int rows = b.send_y1 - b.send_y0;
+        if (rows > 0) {
+          const size_t off = (size_t)b.send_y0 * g.w;
+          EQC_TRY(encode_band(r, g, 0, r.part_c[r.cur].as<uint32_t>() + off, r.part_d[r.cur].as<uint32_t>() + off,
+                              rows, cap, s));
+        }
+      }
+      EQC_TRY(T.start());
+      for (size_t i = 0; i < ranks.size(); ++i) {
+        RankState &r = *ranks[i];
+        const BsRound &b = plans[i][rd];
+        int64_t *sz = r.sizes.as<int64_t>();
+        if (b.send_y1 > b.send_y0) EQC_TRY(T.send(r, b.partner, sz, 2 * sizeof(int64_t)));
+        if (b.keep_y1 > b.keep_y0) EQC_TRY(T.recv(r, b.partner, sz + 2, 2 * sizeof(int64_t)));
+      }
+      EQC_TRY(T.end());
+      for (RankState *r : ranks)
+        EQC_CUDA_TRY(cudaMemcpyAsync(r->h_sizes, r->sizes.p, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      EQC_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    EQC_TRY(T.start());
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      RankState &r = *ranks[i];
+      const BsRound &b = plans[i][rd];
+      const int srows = b.send_y1 - b.send_y0, krows = b.keep_y1 - b.keep_y0;
+      if (srows > 0) {
+        if (rle) {
+          EQC_TRY(T.send(r, b.partner, r.enc.as<uint8_t>(), (size_t)r.h_sizes[0]));
+          EQC_TRY(T.send(r, b.partner, r.enc.as<uint8_t>() + cap, (size_t)r.h_sizes[1]));
+        } else {
+          const size_t off = (size_t)b.send_y0 * g.w;
+          EQC_TRY(T.send(r, b.partner, r.part_c[r.cur].as<uint32_t>() + off, frame_bytes(g, srows)));
+          EQC_TRY(T.send(r, b.partner, r.part_d[r.cur].as<uint32_t>() + off, frame_bytes(g, srows)));
+        }
+        r.stats[0] += 1;
+      }
+      if (krows > 0) {
+        if (rle) {
+          EQC_TRY(T.recv(r, b.partner, r.dec.as<uint8_t>(), (size_t)r.h_sizes[2]));
+          EQC_TRY(T.recv(r, b.partner, r.dec.as<uint8_t>() + cap, (size_t)r.h_sizes[3]));
+        } else {
+          EQC_TRY(T.recv(r, b.partner, r.recv_c.p, frame_bytes(g, krows)));
+          EQC_TRY(T.recv(r, b.partner, r.recv_d.p, frame_bytes(g, krows)));
+        }
+      }
+    }
+    EQC_TRY(T.end());
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      RankState &r = *ranks[i];
+      const BsRound &b = plans[i][rd];
+      const int krows = b.keep_y1 - b.keep_y0;
+      if (krows <= 0) {
+        r.cur ^= 1;
+        continue;
+      }
+      if (rle) {
+        const uint8_t *src[2] = {r.dec.as<uint8_t>(), r.dec.as<uint8_t>() + cap};
+        uint32_t *dst[2] = {r.recv_c.as<uint32_t>(), r.recv_d.as<uint32_t>()};
+        const int64_t caps[2] = {cap, cap};
+        EQC_TRY(image_decompress_rle_batch(2, src, caps, dst, g.w, g.w, krows, r.status.as<int32_t>(), s));
+      }
+      const size_t off = (size_t)b.keep_y0 * g.w;
+      const uint32_t *mine_c = r.part_c[r.cur].as<uint32_t>() + off, *mine_d = r.part_d[r.cur].as<uint32_t>() + off;
+      const uint32_t *their_c = r.recv_c.as<uint32_t>(), *their_d = r.recv_d.as<uint32_t>();
+      // ties go to the group whose bit r is 0 (lower global source indices)
+      const uint32_t *c[2] = {b.low ? mine_c : their_c, b.low ? their_c : mine_c};
+      const uint32_t *d[2] = {b.low ? mine_d : their_d, b.low ? their_d : mine_d};
+      const int nxt = r.cur ^ 1;
+      EQC_TRY(compositor_depth(2, c, d, g.w, krows, g.w, r.part_c[nxt].as<uint32_t>() + off,
+                               r.part_d[nxt].as<uint32_t>() + off, g.w, s));
+      r.cur = nxt;
+    }
+  }
+  // gather final regions (colour) to the destination
+  auto region = [&](int q, int &y0, int &y1) { final_region_bs(g.h, g.n, q, y0, y1); };
+  for (RankState *r : ranks) {
+    if (r->rank != g.dest) continue;
+    int y0, y1;
+    region(r->rank, y0, y1);
+    if (y1 > y0)
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)y0 * g.out_pitch, g.out_pitch * 4,
+                                     r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w, (size_t)g.w * 4,
+                                     (size_t)g.w * 4, y1 - y0, cudaMemcpyDeviceToDevice, s));
+  }
+  if (g.n > 1) {
+    EQC_TRY(T.start());
+    for (RankState *r : ranks) {
+      int y0, y1;
+      region(r->rank, y0, y1);
+      EQC_TRY(gather(*r, g, T, region, r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w, s, 0));
+    }
+    EQC_TRY(T.end());
+    for (RankState *r : ranks) {
+      int y0, y1;
+      region(r->rank, y0, y1);
+      EQC_TRY(gather(*r, g, T, region, r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w, s, 1));
+    }
+  }
+  return EQC_OK;
+}
+
+int validate(int nranks, int n_local, const void *color, const void *depth, int w, int h, int64_t pitch, int op,
+             int flags, int dest, const void *out, int64_t out_pitch, bool is_dest) {
+  if (nranks < 1 || n_local < 1 || n_local > EQC_MAX_SOURCES || nranks > EQC_MAX_SOURCES) return EQC_E_INVALID;
+  if (!color || !depth || w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
+  if (op != EQC_OP_DEPTH) return EQC_E_UNSUPPORTED;
+  if (flags & ~EQC_FLAG_RLE) return EQC_E_INVALID;
+  if (dest < 0 || dest >= nranks) return EQC_E_INVALID;
+  if (is_dest && (!out || out_pitch < w)) return EQC_E_INVALID;
+  return EQC_OK;
+}
+
+}  // namespace
+
+// ---- communicator ---------------------------------------------------------------
+struct eqc_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0;
+  RankState st;
+};
+
+extern "C" int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]) {
+  if (!id) return EQC_E_INVALID;
+  static_assert(sizeof(ncclUniqueId) == EQC_UNIQUE_ID_BYTES, "NCCL unique id size");
+  ncclUniqueId u;
+  EQC_NCCL_TRY(ncclGetUniqueId(&u));
+  std::memcpy(id, &u, sizeof(u));
+  return EQC_OK;
+}
+
+extern "C" int eqc_comm_init(eqc_comm **comm, int nranks, int rank, const uint8_t id[EQC_UNIQUE_ID_BYTES]) {
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return EQC_E_INVALID;
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  eqc_comm *c = new eqc_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->st.rank = rank;
+  if (ncclCommInitRank(&c->nccl, nranks, u, rank) != ncclSuccess) {
+    delete c;
+    return EQC_E_NCCL;
+  }
+  *comm = c;
+  return EQC_OK;
+}
+
+extern "C" int eqc_comm_destroy(eqc_comm *comm) {
+  if (!comm) return EQC_E_INVALID;
+  cudaDeviceSynchronize();
+  comm->st.release();
+  int rc = EQC_OK;
+  if (comm->nccl && ncclCommDestroy(comm->nccl) != ncclSuccess) rc = EQC_E_NCCL;
+  delete comm;
+  return rc;
+}
+
+extern "C" int eqc_comm_stats(const eqc_comm *comm, int64_t out[4]) {
+  if (!comm || !out) return EQC_E_INVALID;
+  for (int i = 0; i < 4; ++i) out[i] = comm->st.stats[i];
+  return EQC_OK;
+}
+
+extern "C" int eqc_plan_bands(int h, int n, int *row0) {
+  if (h <= 0 || n < 1 || !row0) return EQC_E_INVALID;
+  plan_bands(h, n, row0);
+  return EQC_OK;
+}
+
+extern "C" int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_rounds) {
+  if (h <= 0 || n < 1 || rank < 0 || rank >= n) return EQC_E_INVALID;
+  std::vector<BsRound> rr;
+  const int k = plan_bs(h, n, rank, rr);
+  if (k < 0) return k;
+  if (k > max_rounds || (k > 0 && !rounds)) return EQC_E_CAPACITY;
+  for (int i = 0; i < k; ++i) {
+    const BsRound &b = rr[i];
+    const int v[6] = {b.partner, b.low, b.keep_y0, b.keep_y1, b.send_y0, b.send_y1};
+    std::memcpy(rounds + 6 * i, v, sizeof(v));
+  }
+  return k;
+}
+
+static int compose_nccl(bool ds, eqc_comm *comm, int n_local, const uint32_t *const *color,
+                        const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags, int dest_rank,
+                        uint32_t *out_color, int64_t out_pitch, void *stream) {
+  if (!comm) return EQC_E_INVALID;
+  EQC_TRY(validate(comm->nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+                   comm->rank == dest_rank));
+  if (!ds && (comm->nranks & (comm->nranks - 1))) return EQC_E_UNSUPPORTED;
+  Geometry g;
+  g.n = comm->nranks;
+  g.n_local = n_local;
+  g.w = w;
+  g.h = h;
+  g.pitch = pitch;
+  g.flags = flags;
+  g.dest = dest_rank;
+  g.out = out_color;
+  g.out_pitch = comm->rank == dest_rank ? out_pitch : w;
+  comm->st.color = color;
+  comm->st.depth = depth;
+  cudaStream_t s = (cudaStream_t)stream;
+  NcclTransport T(comm->nccl, s);
+  std::vector<RankState *> ranks{&comm->st};
+  return ds ? run_direct_send(ranks, g, T, s) : run_binary_swap(ranks, g, T, s);
+}
+
+extern "C" int compose_direct_send(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                                   const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                   int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream) {
+  return compose_nccl(true, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+                      stream);
+}
+
+extern "C" int compose_binary_swap(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                                   const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                   int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream) {
+  return compose_nccl(false, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+                      stream);
+}
+
+static int compose_local(bool ds, int nranks, int n_local, const uint32_t *const *color,
+                         const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags, int dest_rank,
+                         uint32_t *out_color, int64_t out_pitch, int64_t *out_stats, void *stream) {
+  EQC_TRY(validate(nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch, true));
+  if (!ds && (nranks & (nranks - 1))) return EQC_E_UNSUPPORTED;
+  Geometry g;
+  g.n = nranks;
+  g.n_local = n_local;
+  g.w = w;
+  g.h = h;
+  g.pitch = pitch;
+  g.flags = flags;
+  g.dest = dest_rank;
+  g.out = out_color;
+  g.out_pitch = out_pitch;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<RankState> states(nranks);
+  std::vector<RankState *> ranks;
+  for (int q = 0; q < nranks; ++q) {
+    states[q].rank = q;
+    states[q].color = color + (size_t)q * n_local;
+    states[q].depth = depth + (size_t)q * n_local;
+    ranks.push_back(&states[q]);
+  }
+  LocalTransport T(s);
+  int rc = ds ? run_direct_send(ranks, g, T, s) : run_binary_swap(ranks, g, T, s);
+  cudaStreamSynchronize(s);  // scratch is freed below
+  if (out_stats) {
+    for (int i = 0; i < 4; ++i) out_stats[i] = 0;
+    for (auto &st : states)
+      for (int i = 0; i < 4; ++i) out_stats[i] += st.stats[i];
+  }
+  for (auto &st : states) st.release();
+  return rc;
+}
+
+extern "C" int compose_direct_send_local(int nranks, int n_local, const uint32_t *const *color,
+                                         const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                         int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                         void *stream) {
+  return compose_local(true, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+                       out_stats, stream);
+}
+
+extern "C" int compose_binary_swap_local(int nranks, int n_local, const uint32_t *const *color,
+                                         const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                         int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                         void *stream) {
+  return compose_local(false, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+                       out_stats, stream);
+}

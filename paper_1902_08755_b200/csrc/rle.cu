@@ -9,23 +9,28 @@
 //  compositor_depth_rle         stages (5) + (7) fused: decode in registers,
 //                               depth-composite, one HBM write
 //
-// Encoder: single pass.  Warp w of a CTA codes chunk 8*tile + w into shared
-// memory; the chunk sizes are prefix-summed across the CTA and across CTAs by
-// a decoupled look-back (CTA order from an atomic ticket), then each warp
-// stores its record at its final offset.  The look-back state lives in a
-// caller-owned workspace that the kernel leaves reusable: status words carry
-// a 16-bit epoch tag and the last CTA to finish bumps the epoch and resets
-// the ticket/done counters, so no memset is needed between calls.
+// Encoder: single pass over the input.  A CTA owns a tile of 8 warps x 8
+// consecutive chunks; each warp codes its chunks into shared memory back to
+// back, the warp runs are prefix-summed across the CTA and across CTAs by a
+// decoupled look-back (tile order = an atomic ticket), then each warp stores
+// its contiguous run of records at the final offset.  The look-back state is
+// a caller-owned workspace the kernel leaves reusable: the ticket word holds
+// {epoch:32 | ticket:32}, status words carry a 16-bit epoch tag, and the CTA
+// holding the last ticket bumps the epoch and zeroes the ticket after its
+// look-back, so no memset is needed between calls.
 #include "rle.cuh"
 
 using namespace eqc_rle;
 
 namespace {
 
-constexpr int kWarps = 8;     // chunks per CTA (one warp each)
+constexpr int kWarps = 8;          // warps per CTA
+constexpr int kCPW = 8;            // consecutive chunks per warp (encoder)
+constexpr int kTileChunks = kWarps * kCPW;
+constexpr int kWarpStage = kCPW * 520 + 16;  // records of one warp, back to back
 constexpr int kMaxBatch = 64;
 
-// workspace layout (uint64): [0] ticket, [1] done, [2] epoch, [3] pad,
+// workspace layout (uint64): [0] {epoch << 32 | ticket}, [1..3] pad,
 // [4 + t] look-back status of tile t.
 constexpr int kWsHeader = 4;
 constexpr uint64_t kFlagAgg = 1ull << 46;
@@ -116,42 +121,54 @@ __device__ __forceinline__ void load_chunk(const uint32_t *row, int L, int lane,
 }
 
 __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
-  __shared__ __align__(16) uint8_t stage[kWarps][kStageBytes];
+  __shared__ __align__(16) uint8_t stage[kWarps][kWarpStage];
   __shared__ __align__(16) uint8_t toks[kWarps][kTokBytes];
   __shared__ int wsize[kWarps];
   __shared__ int64_t woff[kWarps];
-  __shared__ int64_t s_tile;
-  __shared__ uint64_t s_epoch;
+  __shared__ unsigned long long s_tk;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t *ws = p.ws;
-  if (tid == 0) {
-    s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
-    s_epoch = poll(ws + 2);
-  }
+  if (tid == 0) s_tk = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
   __syncthreads();
-  const int64_t tile = s_tile;
-  const uint64_t epoch = s_epoch;
+  const int64_t tile = (int64_t)(s_tk & 0xFFFFFFFFull);
+  const uint64_t epoch = s_tk >> 32;
   const int m = (int)(tile / p.tiles_per_image);
   const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
   const EncImage im = p.img[m];
-  const int64_t c = lt * kWarps + warp;
-  const bool active = c < p.nchunks;
-  int y = 0, L = 0;
-  EncodeOut eo{0, 0};
-  if (active) {
-    y = (int)(c / p.S);
-    const int k = (int)(c - (int64_t)y * p.S);
-    const int x0 = k * kC;
-    L = min(kC, p.w - x0);
-    uint32_t px[4];
-    load_chunk(im.src + (int64_t)y * p.pitch + x0, L, lane, p.vec != 0, px);
-    if (im.flags & EQC_FLAG_SWIZZLE) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) px[j] = swizzle(px[j]);
+  const int64_t c0 = (lt * kWarps + warp) * kCPW;
+  // software pipeline: the next chunk's 128-bit loads are in flight while
+  // the current chunk is coded
+  auto chunk_len = [&](int64_t c) -> int {
+    if (c >= p.nchunks) return 0;
+    const int x0 = (int)(c % p.S) * kC;
+    return min(kC, p.w - x0);
+  };
+  auto chunk_row = [&](int64_t c) -> const uint32_t * {
+    const int64_t y = c / p.S;
+    return im.src + y * p.pitch + (c - y * p.S) * kC;
+  };
+  uint32_t cur[4] = {0, 0, 0, 0}, nxt[4] = {0, 0, 0, 0};
+  int Lc = chunk_len(c0);
+  if (Lc > 0) load_chunk(chunk_row(c0), Lc, lane, p.vec != 0, cur);
+  int run = 0;
+  uint32_t my_ps = 0;  // lane j < kCPW keeps chunk j's plane sizes and offset in the run
+  int my_pre = 0;
+  const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
+#pragma unroll 1
+  for (int j = 0; j < kCPW && Lc > 0; ++j) {
+    const int Ln = chunk_len(c0 + j + 1);
+    if (j + 1 < kCPW && Ln > 0) load_chunk(chunk_row(c0 + j + 1), Ln, lane, p.vec != 0, nxt);
+    const EncodeOut eo = encode_chunk(cur, Lc, lane, swz, stage[warp] + run, toks[warp]);
+    if (lane == j) {
+      my_ps = eo.psizes;
+      my_pre = run;
     }
-    eo = encode_chunk(px, L, lane, stage[warp], toks[warp]);
+    run += eo.size;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+    Lc = (j + 1 < kCPW) ? Ln : 0;
   }
-  if (lane == 0) wsize[warp] = eo.size;
+  if (lane == 0) wsize[warp] = run;
   __syncthreads();
   if (warp == 0) {
     const int v = lane < kWarps ? wsize[lane] : 0;
@@ -159,43 +176,38 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
     const int agg = __shfl_sync(EQC_FULL, inc, 31);
     const int64_t excl = lookback(ws + kWsHeader, (int64_t)m * p.tiles_per_image, lt, agg, epoch, lane);
     if (lane < kWarps) woff[lane] = excl + inc - v;
-    if (lt == p.tiles_per_image - 1 && lane == 0) {
-      // last tile of the image: total payload known -> header + size
-      const int64_t payload = excl + agg;
-      const int64_t payload0 = 32 + 8 * p.nchunks;
-      uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
-      h32[0] = kMagic;
-      h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
-               ((uint32_t)kLog2C << 24);
-      h32[2] = (uint32_t)p.w;
-      h32[3] = (uint32_t)p.h;
-      h32[4] = (uint32_t)p.nchunks;
-      h32[5] = 0u;
-      h32[6] = (uint32_t)(uint64_t)payload;
-      h32[7] = (uint32_t)((uint64_t)payload >> 32);
-      *im.d_size = payload0 + payload;
+    if (lane == 0) {
+      if (lt == p.tiles_per_image - 1) {
+        // last tile of the image: total payload known -> header + size
+        const int64_t payload = excl + agg;
+        const int64_t payload0 = 32 + 8 * p.nchunks;
+        uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
+        h32[0] = kMagic;
+        h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
+                 ((uint32_t)kLog2C << 24);
+        h32[2] = (uint32_t)p.w;
+        h32[3] = (uint32_t)p.h;
+        h32[4] = (uint32_t)p.nchunks;
+        h32[5] = 0u;
+        h32[6] = (uint32_t)(uint64_t)payload;
+        h32[7] = (uint32_t)((uint64_t)payload >> 32);
+        *im.d_size = payload0 + payload;
+      }
+      if (tile == (int64_t)p.count * p.tiles_per_image - 1) {
+        // every ticket is taken and every tile of this launch has read its
+        // epoch: open the next epoch with ticket 0
+        atomicExch(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)((epoch + 1) << 32));
+      }
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    // this CTA no longer touches the look-back state
-    __threadfence();
-    const unsigned long long total = (unsigned long long)p.count * p.tiles_per_image;
-    const unsigned long long d = atomicAdd(reinterpret_cast<unsigned long long *>(ws + 1), 1ull);
-    if (d == total - 1) {
-      atomicExch(reinterpret_cast<unsigned long long *>(ws + 0), 0ull);
-      atomicExch(reinterpret_cast<unsigned long long *>(ws + 1), 0ull);
-      atomicExch(reinterpret_cast<unsigned long long *>(ws + 2), (unsigned long long)(epoch + 1));
-    }
-  }
-  if (active) {
+  if (run > 0) {
     const int64_t off = woff[warp];
-    if (lane == 0) {
-      uint32_t *te = reinterpret_cast<uint32_t *>(im.dst + 32 + 8 * c);
-      te[0] = (uint32_t)off;
-      te[1] = eo.psizes;
+    if (lane < kCPW && c0 + lane < p.nchunks) {
+      uint2 *te = reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (c0 + lane));
+      *te = make_uint2((uint32_t)(off + my_pre), my_ps);
     }
-    store_record(im.dst + 32 + 8 * p.nchunks + off, stage[warp], eo.size, lane);
+    store_record(im.dst + 32 + 8 * p.nchunks + off, stage[warp], run, lane);
   }
 }
 
@@ -239,37 +251,40 @@ __device__ StreamHdr read_header(const uint8_t *src, int64_t src_bytes, int w, i
   return hd;
 }
 
-// Decode chunk (y, k) of a validated stream into px[0..3] (lane positions
-// 4*lane + j of the chunk).  Returns false (warp-uniform) on corruption.
-__device__ bool decode_chunk(const uint8_t *src, int64_t src_bytes, const StreamHdr &hd, int w, int y,
-                             int k, int lane, uint8_t *stage, uint16_t *info, uint32_t px[4], int &L) {
-  const int C = 1 << hd.log2c;
-  const int x0 = k * C;
-  L = min(C, w - x0);
-  const int64_t c = (int64_t)y * hd.S + k;
-  const uint2 te = *reinterpret_cast<const uint2 *>(src + 32 + 8 * c);
-  const int64_t off = te.x;
-  const uint32_t ps = te.y;
+// Constant-chunk probe (lane-local): a record of four 3-byte planes
+// [01][0x80 | (L-1)][v] is one value for the whole chunk.  Reads the 12
+// bytes as aligned words (an aligned word that starts inside the stream
+// never leaves its allocation) and funnel-shifts them into place.
+__device__ __forceinline__ bool probe_const(const uint8_t *rec, uint32_t ps, int L, uint32_t &v) {
+  if (ps != 0x03030303u) return false;
+  const uint32_t *a = reinterpret_cast<const uint32_t *>((uintptr_t)rec & ~(uintptr_t)3);
+  const int sh = 8 * (int)((uintptr_t)rec & 3);
+  const uint32_t q0 = __ldg(a), q1 = __ldg(a + 1), q2 = __ldg(a + 2);
+  const uint32_t q3 = sh ? __ldg(a + 3) : 0u;
+  const uint32_t w0 = __funnelshift_r(q0, q1, sh), w1 = __funnelshift_r(q1, q2, sh),
+                 w2 = __funnelshift_r(q2, q3, sh);
+  // bytes: [01 c v0 01][c v1 01 c][v2 01 c v3]
+  const uint32_t c = 0x80u | (uint32_t)(L - 1);
+  const bool ok = (w0 & 0xFF00FFFFu) == (0x01000001u | (c << 8)) &&
+                  (w1 & 0xFFFF00FFu) == (c | 0x00010000u | (c << 24)) && (w2 & 0x00FFFF00u) == (0x0100u | (c << 16));
+  v = __byte_perm(w0, w1, 0x0652) | 0u;  // v0 = byte 2 of w0, v1 = byte 1 of w1 (= byte 5)
+  v = (v & 0xFFFFu) | (__byte_perm(w2, 0, 0x3000) & 0xFF000000u) | ((w2 & 0xFFu) << 16);
+  return ok;
+}
+
+// Stage a record (aligned 4-byte words; byte loads at the stream end) and
+// decode its four planes into px[0..3].  Warp-cooperative; returns false
+// (warp-uniform) on a malformed record.
+__device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8_t *rec, uint32_t ps, int L,
+                              int lane, uint8_t *stage, uint16_t *info, uint32_t px[4]) {
   const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
   const int total = s0 + s1 + s2 + s3;
-  // offsets monotone and contiguous: chunk c starts where chunk c-1 ends,
-  // and the last chunk ends at payload_bytes
-  int64_t expect = 0;
-  if (c > 0) {
-    const uint2 tp = *reinterpret_cast<const uint2 *>(src + 32 + 8 * (c - 1));
-    expect = (int64_t)tp.x + (tp.y & 0xFF) + ((tp.y >> 8) & 0xFF) + ((tp.y >> 16) & 0xFF) + (tp.y >> 24);
-  }
-  bool ok = off == expect && off + total <= hd.payload_bytes && s0 <= L + 2 && s1 <= L + 2 &&
-            s2 <= L + 2 && s3 <= L + 2;
-  if (c == hd.nchunks - 1) ok = ok && off + total == hd.payload_bytes;
-  if (!ok) return false;
-  // stage the record (aligned 4-byte words; byte loads at the stream end)
-  const uint8_t *rec = src + hd.payload0 + off;
   const uintptr_t a0 = (uintptr_t)rec & ~(uintptr_t)3;
   const int sh = (int)((uintptr_t)rec & 3);
   const int nwords = (sh + total + 3) >> 2;
   const uintptr_t lim = (uintptr_t)src + (uintptr_t)src_bytes;
   uint32_t *st32 = reinterpret_cast<uint32_t *>(stage);
+  __syncwarp();  // the previous record's readers are done with the stage
   for (int q = lane; q < nwords; q += 32) {
     const uintptr_t a = a0 + 4 * (uintptr_t)q;
     uint32_t v;
@@ -286,15 +301,10 @@ __device__ bool decode_chunk(const uint8_t *src, int64_t src_bytes, const Stream
 #pragma unroll
   for (int j = 0; j < 4; ++j) px[j] = 0;
   const uint8_t *r = stage + sh;
-  ok = decode_plane(r, s0, L, lane, 0, px, info);
+  bool ok = decode_plane(r, s0, L, lane, 0, px, info);
   ok = ok && decode_plane(r + s0, s1, L, lane, 1, px, info);
   ok = ok && decode_plane(r + s0 + s1, s2, L, lane, 2, px, info);
   ok = ok && decode_plane(r + s0 + s1 + s2, s3, L, lane, 3, px, info);
-  __syncwarp();  // stage/info are reused by the next chunk
-  if (ok && (hd.flags & EQC_FLAG_SWIZZLE)) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) px[j] = unswizzle(px[j]);
-  }
   return ok;
 }
 
@@ -316,19 +326,48 @@ __device__ __forceinline__ void set_corrupt(int32_t *status) {
 struct DecImage {
   const uint8_t *src;
   uint32_t *dst;
+  int64_t src_bytes;
 };
 
 struct DecParams {
   DecImage img[kMaxBatch];
   int32_t *status;
-  int64_t pitch, src_bytes;
+  int64_t pitch;
   int count, w, h;
-  int segs_per_row;      // 128-pixel segments per row
-  int64_t tiles_per_image;
+  int64_t tiles_per_image;  // CTAs per image: 8 warps x 32 slots of 128 pixels
   int vec;
 };
 
-// One warp per 128-pixel row segment (1, 2 or 4 chunks for log2c 7, 6, 5).
+constexpr int kGroup = 32;  // chunks classified per warp pass (one per lane)
+
+// Lane-parallel table read for chunk c (valid if `has`): entry, and the
+// monotone/contiguous check against chunk c-1 (the previous lane's entry, or
+// a load for lane 0).  Returns ok.
+__device__ __forceinline__ bool entry_lane(const uint8_t *src, int64_t payload_bytes, int64_t nchunks, int64_t c,
+                                           bool has, int L, int lane, int64_t &off, uint32_t &ps) {
+  uint2 te = make_uint2(0, 0);
+  if (has) te = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * c));
+  off = te.x;
+  ps = te.y;
+  const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
+  const int64_t end = off + s0 + s1 + s2 + s3;
+  int64_t prev = __shfl_up_sync(EQC_FULL, end, 1);
+  if (lane == 0) {
+    prev = 0;
+    if (has && c > 0) {
+      const uint2 tp = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * (c - 1)));
+      prev = (int64_t)tp.x + (tp.y & 0xFF) + ((tp.y >> 8) & 0xFF) + ((tp.y >> 16) & 0xFF) + (tp.y >> 24);
+    }
+  }
+  if (!has) return true;
+  bool ok = off == prev && end <= payload_bytes && s0 <= L + 2 && s1 <= L + 2 && s2 <= L + 2 && s3 <= L + 2;
+  if (c == nchunks - 1) ok = ok && end == payload_bytes;
+  return ok;
+}
+
+// One warp per 32 x (128 / C) chunks: lane-parallel table validation and
+// constant-chunk classification, then constant chunks are filled with one
+// 128-bit store per lane and the others decoded warp-cooperatively.
 __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_constant__ DecParams p) {
   __shared__ __align__(16) uint8_t stage[kWarps][kStageBytes];
   __shared__ __align__(16) uint16_t info[kWarps][kC];
@@ -338,26 +377,61 @@ __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_co
   const int64_t lt = blockIdx.x - (int64_t)m * p.tiles_per_image;
   const DecImage im = p.img[m];
   if (tid == 0) {
-    s_hd = read_header(im.src, p.src_bytes, p.w, p.h);
+    s_hd = read_header(im.src, im.src_bytes, p.w, p.h);
     if (!s_hd.ok) set_corrupt(p.status);
   }
   __syncthreads();
   const StreamHdr hd = s_hd;
   if (!hd.ok) return;
-  const int64_t seg = lt * kWarps + warp;
-  if (seg >= (int64_t)p.segs_per_row * p.h) return;
-  const int y = (int)(seg / p.segs_per_row);
-  const int xs = (int)(seg - (int64_t)y * p.segs_per_row) * kC;
   const int C = 1 << hd.log2c;
-  for (int k = xs / C; k * C < min(xs + kC, p.w); ++k) {
-    uint32_t px[4];
-    int L;
-    const bool ok = decode_chunk(im.src, p.src_bytes, hd, p.w, y, k, lane, stage[warp], info[warp], px, L);
-    if (!ok) {
-      if (lane == 0) set_corrupt(p.status);
-      continue;
+  const int r = kC / C;
+  const bool swz = (hd.flags & EQC_FLAG_SWIZZLE) != 0;
+  for (int sub = 0; sub < r; ++sub) {
+    const int64_t cb = ((lt * kWarps + warp) * r + sub) * kGroup;
+    if (cb >= hd.nchunks) break;
+    const int64_t c = cb + lane;
+    const bool has = c < hd.nchunks;
+    const int y = has ? (int)(c / hd.S) : 0;
+    const int k = has ? (int)(c - (int64_t)y * hd.S) : 0;
+    const int L = has ? min(C, p.w - k * C) : 0;
+    int64_t off;
+    uint32_t ps;
+    const bool ok = entry_lane(im.src, hd.payload_bytes, hd.nchunks, c, has, L, lane, off, ps);
+    uint32_t v = 0;
+    bool cst = false;
+    if (has && ok) {
+      cst = probe_const(im.src + hd.payload0 + off, ps, L, v);
+      if (cst && swz) v = unswizzle(v);
     }
-    store_px(im.dst + (int64_t)y * p.pitch + k * C, L, lane, p.vec != 0 && C == kC, px);
+    const unsigned bad = __ballot_sync(EQC_FULL, has && !ok);
+    if (bad && lane == 0) set_corrupt(p.status);
+    const int nhere = (int)min((int64_t)kGroup, hd.nchunks - cb);
+    for (int i = 0; i < nhere; ++i) {
+      if ((bad >> i) & 1u) continue;
+      const int yi = __shfl_sync(EQC_FULL, y, i);
+      const int ki = __shfl_sync(EQC_FULL, k, i);
+      const int Li = __shfl_sync(EQC_FULL, L, i);
+      const bool ci = __shfl_sync(EQC_FULL, (int)cst, i) != 0;
+      uint32_t px[4];
+      if (ci) {
+        const uint32_t vi = __shfl_sync(EQC_FULL, v, i);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) px[j] = vi;
+      } else {
+        const int64_t offi = __shfl_sync(EQC_FULL, off, i);
+        const uint32_t psi = __shfl_sync(EQC_FULL, ps, i);
+        if (!decode_record(im.src, im.src_bytes, im.src + hd.payload0 + offi, psi, Li, lane, stage[warp],
+                           info[warp], px)) {
+          if (lane == 0) set_corrupt(p.status);
+          continue;
+        }
+        if (swz) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) px[j] = unswizzle(px[j]);
+        }
+      }
+      store_px(im.dst + (int64_t)yi * p.pitch + (int64_t)ki * C, Li, lane, p.vec != 0 && C == kC, px);
+    }
   }
 }
 
@@ -366,71 +440,161 @@ __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_co
 // ---------------------------------------------------------------------------
 
 struct FusedParams {
-  const uint8_t *color[EQC_MAX_SOURCES];
-  const uint8_t *depth[EQC_MAX_SOURCES];
+  const uint8_t *src[2 * EQC_MAX_SOURCES];  // colour streams 0..n-1, depth streams n..2n-1
+  int64_t src_bytes[2 * EQC_MAX_SOURCES];
   uint32_t *out_color, *out_depth;
   int32_t *status;
-  int64_t out_pitch, src_bytes;
-  int n, w, h, segs_per_row;
+  int64_t out_pitch;
+  int n, w, h, S;
   int vec;
 };
 
+constexpr int kMaxStreams = 2 * EQC_MAX_SOURCES;
+constexpr int kSrcBatch = 4;  // sources classified per unrolled batch
+
+// Warp per 32 consecutive chunk positions.
+//  Phase A (lane = position): for every source, the depth and colour table
+//   entries are validated and probed for constant chunks; while every
+//   stream of a position is constant the depth composite is evaluated on the
+//   scalar values (z-test over sources in index order).
+//  Phase B: positions whose streams were all constant are written with one
+//   128-bit store per lane per output; every other position is decoded
+//   warp-cooperatively, depth first: a source's colour chunk is decoded only
+//   if the source wins at least one pixel of the chunk.
 __global__ void __launch_bounds__(kWarps * 32) depth_rle_kernel(const __grid_constant__ FusedParams p) {
   __shared__ __align__(16) uint8_t stage[kWarps][kStageBytes];
   __shared__ __align__(16) uint16_t info[kWarps][kC];
-  __shared__ StreamHdr s_hd[2 * EQC_MAX_SOURCES];
+  __shared__ int64_t s_pb[kMaxStreams];
+  __shared__ uint8_t s_flags[kMaxStreams];
   __shared__ int s_bad;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = p.n, ns = 2 * n;
   if (tid == 0) s_bad = 0;
   __syncthreads();
-  for (int q = tid; q < 2 * p.n; q += blockDim.x) {
-    const bool is_depth = q >= p.n;
-    const int i = is_depth ? q - p.n : q;
-    StreamHdr hd = read_header(is_depth ? p.depth[i] : p.color[i], p.src_bytes, p.w, p.h);
-    if (hd.ok && hd.kind != (is_depth ? 1 : 0)) hd.ok = 0;
-    if (hd.ok && hd.log2c != kLog2C) hd.ok = 0;  // fused path: 128-pixel chunks only
-    s_hd[q] = hd;
-    if (!hd.ok) s_bad = 1;
+  for (int q = tid; q < ns; q += blockDim.x) {
+    const bool is_depth = q >= n;
+    StreamHdr hd = read_header(p.src[q], p.src_bytes[q], p.w, p.h);
+    if (!hd.ok || hd.kind != (is_depth ? 1 : 0) || hd.log2c != kLog2C) s_bad = 1;
+    s_pb[q] = hd.payload_bytes;
+    s_flags[q] = (uint8_t)hd.flags;
   }
   __syncthreads();
   if (s_bad) {
     if (tid == 0) set_corrupt(p.status);
     return;
   }
-  const int64_t seg = (int64_t)blockIdx.x * kWarps + warp;
-  if (seg >= (int64_t)p.segs_per_row * p.h) return;
-  const int y = (int)(seg / p.segs_per_row);
-  const int k = (int)(seg - (int64_t)y * p.segs_per_row);
-  uint32_t bc[4], bd[4];
-  int L = 0;
-  bool ok = true;
-  for (int i = 0; i < p.n && ok; ++i) {
-    uint32_t c[4], d[4];
-    ok = decode_chunk(p.color[i], p.src_bytes, s_hd[i], p.w, y, k, lane, stage[warp], info[warp], c, L);
-    ok = ok && decode_chunk(p.depth[i], p.src_bytes, s_hd[p.n + i], p.w, y, k, lane, stage[warp],
-                            info[warp], d, L);
-    if (i == 0) {
+  const int64_t nchunks = (int64_t)p.S * p.h;
+  const int64_t payload0 = 32 + 8 * nchunks;
+  const int64_t cb = ((int64_t)blockIdx.x * kWarps + warp) * kGroup;
+  if (cb >= nchunks) return;
+  const int64_t c = cb + lane;
+  const bool has = c < nchunks;
+  const int y = has ? (int)(c / p.S) : 0;
+  const int k = has ? (int)(c - (int64_t)y * p.S) : 0;
+  const int L = has ? min(kC, p.w - k * kC) : 0;
+  // ---- phase A
+  bool ok = true, allc = true;
+  uint32_t sd = 0, sc = 0;  // scalar composite of constant positions
+  for (int i0 = 0; i0 < n; i0 += kSrcBatch) {
+    int64_t offd[kSrcBatch], offc[kSrcBatch];
+    uint32_t psd[kSrcBatch], psc[kSrcBatch];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        bc[j] = c[j];
-        bd[j] = d[j];
+    for (int b = 0; b < kSrcBatch; ++b) {
+      const int i = i0 + b;
+      if (i < n) {
+        ok = entry_lane(p.src[n + i], s_pb[n + i], nchunks, c, has, L, lane, offd[b], psd[b]) && ok;
+        ok = entry_lane(p.src[i], s_pb[i], nchunks, c, has, L, lane, offc[b], psc[b]) && ok;
       }
-    } else {
+    }
+    if (has && ok && allc) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool t = d[j] < bd[j];  // strictly nearer replaces: ties keep the lower index
-        bd[j] = t ? d[j] : bd[j];
-        bc[j] = t ? c[j] : bc[j];
+      for (int b = 0; b < kSrcBatch; ++b) {
+        const int i = i0 + b;
+        if (i < n && allc) {
+          uint32_t dv, cv;
+          const bool dc = probe_const(p.src[n + i] + payload0 + offd[b], psd[b], L, dv);
+          const bool cc = dc && probe_const(p.src[i] + payload0 + offc[b], psc[b], L, cv);
+          if (dc && cc) {
+            if (i == 0 || dv < sd) {  // strictly nearer: ties keep the lower index
+              sd = dv;
+              sc = (s_flags[i] & EQC_FLAG_SWIZZLE) ? unswizzle(cv) : cv;
+            }
+          } else {
+            allc = false;
+          }
+        }
       }
     }
   }
-  if (!ok) {
+  const unsigned bad = __ballot_sync(EQC_FULL, has && !ok);
+  if (bad) {
     if (lane == 0) set_corrupt(p.status);
     return;
   }
-  const int64_t row = (int64_t)y * p.out_pitch + (int64_t)k * kC;
-  store_px(p.out_color + row, L, lane, p.vec != 0, bc);
-  if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, bd);
+  const unsigned cmask = __ballot_sync(EQC_FULL, has && allc);
+  const unsigned gmask = __ballot_sync(EQC_FULL, has && !allc);
+  // ---- phase B1: all-constant positions
+  for (unsigned mm = cmask; mm; mm &= mm - 1) {
+    const int i = __ffs(mm) - 1;
+    const int yi = __shfl_sync(EQC_FULL, y, i), ki = __shfl_sync(EQC_FULL, k, i), Li = __shfl_sync(EQC_FULL, L, i);
+    const uint32_t ci = __shfl_sync(EQC_FULL, sc, i), di = __shfl_sync(EQC_FULL, sd, i);
+    const uint32_t pc[4] = {ci, ci, ci, ci}, pd[4] = {di, di, di, di};
+    const int64_t row = (int64_t)yi * p.out_pitch + (int64_t)ki * kC;
+    store_px(p.out_color + row, Li, lane, p.vec != 0, pc);
+    if (p.out_depth) store_px(p.out_depth + row, Li, lane, p.vec != 0, pd);
+  }
+  // ---- phase B2: positions with at least one non-constant chunk
+  for (unsigned mm = gmask; mm; mm &= mm - 1) {
+    const int ii = __ffs(mm) - 1;
+    const int64_t ci = cb + ii;
+    const int yi = __shfl_sync(EQC_FULL, y, ii), ki = __shfl_sync(EQC_FULL, k, ii), Li = __shfl_sync(EQC_FULL, L, ii);
+    uint32_t bc[4] = {0, 0, 0, 0}, bd[4] = {0, 0, 0, 0};
+    bool good = true;
+    for (int i = 0; i < n && good; ++i) {
+      const int qd = n + i, qc = i;
+      // entries were validated in phase A; re-read them (uniform, cached)
+      const uint2 ted = __ldg(reinterpret_cast<const uint2 *>(p.src[qd] + 32 + 8 * ci));
+      const uint8_t *recd = p.src[qd] + payload0 + ted.x;
+      uint32_t d[4], v;
+      if (probe_const(recd, ted.y, Li, v)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[j] = v;
+      } else if (!decode_record(p.src[qd], p.src_bytes[qd], recd, ted.y, Li, lane, stage[warp], info[warp], d)) {
+        good = false;
+        break;
+      }
+      bool t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = (i == 0) || d[j] < bd[j];  // ties keep the lower index
+      if (!__any_sync(EQC_FULL, t[0] || t[1] || t[2] || t[3])) continue;  // hidden: colour never read
+      const uint2 tec = __ldg(reinterpret_cast<const uint2 *>(p.src[qc] + 32 + 8 * ci));
+      const uint8_t *recc = p.src[qc] + payload0 + tec.x;
+      uint32_t col[4];
+      if (probe_const(recc, tec.y, Li, v)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) col[j] = v;
+      } else if (!decode_record(p.src[qc], p.src_bytes[qc], recc, tec.y, Li, lane, stage[warp], info[warp], col)) {
+        good = false;
+        break;
+      }
+      if (s_flags[qc] & EQC_FLAG_SWIZZLE) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bd[j] = t[j] ? d[j] : bd[j];
+        bc[j] = t[j] ? col[j] : bc[j];
+      }
+    }
+    if (!good) {
+      if (lane == 0) set_corrupt(p.status);
+      continue;
+    }
+    const int64_t row = (int64_t)yi * p.out_pitch + (int64_t)ki * kC;
+    store_px(p.out_color + row, Li, lane, p.vec != 0, bc);
+    if (p.out_depth) store_px(p.out_depth + row, Li, lane, p.vec != 0, bd);
+  }
 }
 
 inline bool aligned(const void *q, uintptr_t a) { return ((uintptr_t)q & (a - 1)) == 0; }
@@ -440,9 +604,9 @@ inline int64_t rle_max_size(int w, int h) {
   return 32 + 16 * S * (int64_t)h + 4 * (int64_t)w * h;
 }
 
-inline int64_t tiles_per_image(int w, int h) {
+inline int64_t enc_tiles_per_image(int w, int h) {
   const int64_t S = (w + kC - 1) / kC;
-  return (S * h + kWarps - 1) / kWarps;
+  return (S * h + kTileChunks - 1) / kTileChunks;
 }
 
 }  // namespace
@@ -454,7 +618,7 @@ extern "C" int64_t image_rle_max_size(int w, int h) {
 
 extern "C" size_t image_rle_workspace_size_batch(int count, int w, int h) {
   if (count <= 0 || w <= 0 || h <= 0) return 0;
-  return (size_t)(kWsHeader + (int64_t)count * tiles_per_image(w, h)) * sizeof(uint64_t);
+  return (size_t)(kWsHeader + (int64_t)count * enc_tiles_per_image(w, h)) * sizeof(uint64_t);
 }
 
 extern "C" size_t image_rle_workspace_size(int w, int h) { return image_rle_workspace_size_batch(1, w, h); }
@@ -489,7 +653,7 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   p.count = count;
   p.w = w;
   p.h = h;
-  p.tiles_per_image = (int)tiles_per_image(w, h);
+  p.tiles_per_image = (int)enc_tiles_per_image(w, h);
   p.vec = vec ? 1 : 0;
   const int64_t grid = (int64_t)count * p.tiles_per_image;
   if (grid > 0x7FFFFFFFll) return EQC_E_INVALID;
@@ -506,27 +670,25 @@ extern "C" int image_compress_rle(const uint32_t *src, int w, int h, int64_t pit
                                   workspace_bytes, stream);
 }
 
-extern "C" int image_decompress_rle_batch(int count, const uint8_t *const *src, int64_t src_bytes,
+extern "C" int image_decompress_rle_batch(int count, const uint8_t *const *src, const int64_t *src_bytes,
                                           uint32_t *const *dst, int64_t pitch, int w, int h,
                                           int32_t *d_status, void *stream) {
-  if (count < 1 || count > kMaxBatch || !src || !dst || !d_status) return EQC_E_INVALID;
-  if (w <= 0 || h <= 0 || pitch < w || src_bytes < 32) return EQC_E_INVALID;
+  if (count < 1 || count > kMaxBatch || !src || !src_bytes || !dst || !d_status) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
   DecParams p;
   bool vec = (pitch % 4) == 0;
   for (int i = 0; i < count; ++i) {
-    if (!src[i] || !dst[i]) return EQC_E_INVALID;
+    if (!src[i] || !dst[i] || src_bytes[i] < 32) return EQC_E_INVALID;
     if (!aligned(src[i], 8) || !aligned(dst[i], 4)) return EQC_E_INVALID;
     vec = vec && aligned(dst[i], 16);
-    p.img[i] = DecImage{src[i], dst[i]};
+    p.img[i] = DecImage{src[i], dst[i], src_bytes[i]};
   }
   p.status = d_status;
   p.pitch = pitch;
-  p.src_bytes = src_bytes;
   p.count = count;
   p.w = w;
   p.h = h;
-  p.segs_per_row = (w + kC - 1) / kC;
-  p.tiles_per_image = ((int64_t)p.segs_per_row * h + kWarps - 1) / kWarps;
+  p.tiles_per_image = ((int64_t)((w + kC - 1) / kC) * h + kWarps * kGroup - 1) / (kWarps * kGroup);
   p.vec = vec ? 1 : 0;
   const int64_t grid = (int64_t)count * p.tiles_per_image;
   if (grid > 0x7FFFFFFFll) return EQC_E_INVALID;
@@ -538,35 +700,37 @@ extern "C" int image_decompress_rle(const uint8_t *src, int64_t src_bytes, uint3
                                     int w, int h, int32_t *d_status, void *stream) {
   const uint8_t *s[1] = {src};
   uint32_t *d[1] = {dst};
-  return image_decompress_rle_batch(1, s, src_bytes, d, pitch, w, h, d_status, stream);
+  return image_decompress_rle_batch(1, s, &src_bytes, d, pitch, w, h, d_status, stream);
 }
 
 extern "C" int compositor_depth_rle(int n, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
-                                    int64_t src_bytes, int w, int h, uint32_t *out_color,
-                                    uint32_t *out_depth, int64_t out_pitch, int32_t *d_status,
-                                    void *stream) {
-  if (n < 1 || n > EQC_MAX_SOURCES || !color_rle || !depth_rle || !out_color || !d_status)
+                                    const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h,
+                                    uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
+                                    int32_t *d_status, void *stream) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color_rle || !depth_rle || !color_bytes || !depth_bytes || !out_color ||
+      !d_status)
     return EQC_E_INVALID;
-  if (w <= 0 || h <= 0 || out_pitch < w || src_bytes < 32) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || out_pitch < w) return EQC_E_INVALID;
   FusedParams p;
   for (int i = 0; i < n; ++i) {
-    if (!color_rle[i] || !depth_rle[i]) return EQC_E_INVALID;
+    if (!color_rle[i] || !depth_rle[i] || color_bytes[i] < 32 || depth_bytes[i] < 32) return EQC_E_INVALID;
     if (!aligned(color_rle[i], 8) || !aligned(depth_rle[i], 8)) return EQC_E_INVALID;
-    p.color[i] = color_rle[i];
-    p.depth[i] = depth_rle[i];
+    p.src[i] = color_rle[i];
+    p.src[n + i] = depth_rle[i];
+    p.src_bytes[i] = color_bytes[i];
+    p.src_bytes[n + i] = depth_bytes[i];
   }
   if (!aligned(out_color, 4) || (out_depth && !aligned(out_depth, 4))) return EQC_E_INVALID;
   p.out_color = out_color;
   p.out_depth = out_depth;
   p.status = d_status;
   p.out_pitch = out_pitch;
-  p.src_bytes = src_bytes;
   p.n = n;
   p.w = w;
   p.h = h;
-  p.segs_per_row = (w + kC - 1) / kC;
+  p.S = (w + kC - 1) / kC;
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
-  const int64_t grid = ((int64_t)p.segs_per_row * h + kWarps - 1) / kWarps;
+  const int64_t grid = ((int64_t)p.S * h + kWarps * kGroup - 1) / (kWarps * kGroup);
   if (grid > 0x7FFFFFFFll) return EQC_E_INVALID;
   depth_rle_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();

@@ -61,36 +61,53 @@ struct EncodeOut {
   uint32_t psizes;    // byte p = plane p record size
 };
 
-// Encode the chunk whose pixels (already swizzled if requested) lane `lane`
-// holds in px[0..3] (positions 4*lane + j, valid while < L).  Writes the
-// chunk record (planes 0..3 concatenated) into the warp's staging buffer `st`
-// and returns its size.  `tp` is per-warp scratch of kTokBytes bytes.
-__device__ __forceinline__ EncodeOut encode_chunk(const uint32_t px[4], int L, int lane,
-                                                  uint8_t *st, uint8_t *tp) {
+// Select x[i] for a warp-uniform or lane-dependent i in [0, 4) without
+// dynamic register indexing (which would spill the array to local memory).
+__device__ __forceinline__ int sel4(int i, int a, int b, int c, int d) {
+  return i == 0 ? a : i == 1 ? b : i == 2 ? c : d;
+}
+
+// Encode one chunk.  Lane `lane` holds the RAW pixels px[0..3] (positions
+// 4*lane + j, valid while < L); `swz` applies the swizzle preconditioner.
+// Writes the chunk record (planes 0..3 concatenated) into `st` (any byte
+// alignment) and returns its size.  `tp` is per-warp scratch of kTokBytes.
+//
+// Plane classes (warp-uniform): CONSTANT (one REPEAT of L, 3 bytes),
+// LITERAL-ONLY (no run of >= 3: one LITERAL, L + 2 bytes, the bytes in
+// order), GENERAL (scatter of token starts and payload bytes by prefix
+// counts).  A chunk whose 128 pixels are all equal is detected before the
+// swizzle (a bijection) and emitted as four CONSTANT planes.
+__device__ __forceinline__ EncodeOut encode_chunk(uint32_t px[4], int L, int lane, bool swz, uint8_t *st,
+                                                  uint8_t *tp) {
   const int i0 = 4 * lane;
-  // ---- fast path: the whole chunk is one value (background, flat regions)
+  // ---- whole chunk one value (background, flat regions)
   {
     const uint32_t v0 = __shfl_sync(EQC_FULL, px[0], 0);
     bool same = true;
 #pragma unroll
     for (int j = 0; j < 4; ++j) same = same && (i0 + j >= L || px[j] == v0);
     if (__all_sync(EQC_FULL, same) && L >= 3) {
+      const uint32_t v = swz ? swizzle(v0) : v0;
       if (lane < 4) {
         st[3 * lane + 0] = 1;
         st[3 * lane + 1] = (uint8_t)(0x80 | (L - 1));
-        st[3 * lane + 2] = (uint8_t)bytep(v0, lane);
+        st[3 * lane + 2] = (uint8_t)bytep(v, lane);
       }
       __syncwarp();
       return EncodeOut{12, 0x03030303u};
     }
+  }
+  if (swz) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) px[j] = swizzle(px[j]);
   }
   // ---- neighbours: W[-2], W[-1] from the previous lane, W[4], W[5] from the next
   const uint32_t wm2 = __shfl_up_sync(EQC_FULL, px[2], 1);
   const uint32_t wm1 = __shfl_up_sync(EQC_FULL, px[3], 1);
   const uint32_t wp4 = __shfl_down_sync(EQC_FULL, px[0], 1);
   const uint32_t wp5 = __shfl_down_sync(EQC_FULL, px[1], 1);
-  // e[j] (j = -1..5): byte at position i0+j equals its predecessor, for
-  // 1 <= i0+j < L (no predecessor at the chunk start; nothing beyond L).
+  // e[k] (position i0+k-1, k = 0..6): byte equals its predecessor, for
+  // 1 <= position < L (no predecessor at the chunk start; nothing beyond L).
   uint32_t e[7];
   {
     const uint32_t W[8] = {wm2, wm1, px[0], px[1], px[2], px[3], wp4, wp5};
@@ -100,80 +117,121 @@ __device__ __forceinline__ EncodeOut encode_chunk(const uint32_t px[4], int L, i
       e[k] = bytes_eq(W[k + 1], W[k]) & vflag(pos >= 1 && pos < L);
     }
   }
-  // P3[j] = e[j] & e[j+1]: the window (j-1, j, j+1) is constant (j = -1..4)
+  // p3[k] = e[k] & e[k+1]: window (pos-1, pos, pos+1) constant, pos = i0+k-1
   uint32_t p3[6];
 #pragma unroll
   for (int k = 0; k < 6; ++k) p3[k] = e[k] & e[k + 1];
-  // R[j]: position in a run of >= 3 (REPEAT cover)
+  // R[j]: position i0+j lies in a run of >= 3 (REPEAT cover)
   uint32_t R[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) R[j] = p3[j] | p3[j + 1] | p3[j + 2];
-  uint32_t Rprev = __shfl_up_sync(EQC_FULL, R[3], 1);
-  if (lane == 0) Rprev = 0;
-  // T[j]: token start; E[j]: byte emits a payload byte (literal or REPEAT head)
-  uint32_t T[4], E[4];
+  // ---- plane classes
+  uint32_t allE = 0x80808080u, anyR = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t valid = vflag(i0 + j < L);
-    const uint32_t rp = (j == 0) ? Rprev : R[j - 1];
-    const uint32_t first = vflag(i0 + j == 0);
-    T[j] = (first | (R[j] ^ rp) | (R[j] & rp & ~e[j + 1])) & valid;
-    E[j] = (~R[j] | T[j]) & valid;
+    if (i0 + j >= 1 && i0 + j < L) allE &= e[j + 1];
+    anyR |= R[j];
   }
-  // nibble per plane: bit j of byte p = flag of position i0+j in plane p
-  const uint32_t nibT = ((T[0] >> 7) | (T[1] >> 6) | (T[2] >> 5) | (T[3] >> 4)) & 0x0F0F0F0Fu;
-  const uint32_t nibE = ((E[0] >> 7) | (E[1] >> 6) | (E[2] >> 5) | (E[3] >> 4)) & 0x0F0F0F0Fu;
-  const uint32_t nibR = ((R[0] >> 7) | (R[1] >> 6) | (R[2] >> 5) | (R[3] >> 4)) & 0x0F0F0F0Fu;
-  const uint32_t cT = bytes_popc_nibble(nibT);
-  const uint32_t cE = bytes_popc_nibble(nibE);
-  const uint32_t incT = warp_incl_scan_add(cT, lane);
-  const uint32_t incE = warp_incl_scan_add(cE, lane);
-  const uint32_t totT = __shfl_sync(EQC_FULL, incT, 31);
-  const uint32_t totE = __shfl_sync(EQC_FULL, incE, 31);
-  const uint32_t exT = incT - cT, exE = incE - cE;
-  int base[5];
-  base[0] = 0;
-#pragma unroll
-  for (int p = 0; p < 4; ++p) base[p + 1] = base[p] + 1 + (int)bytep(totT, p) + (int)bytep(totE, p);
-  // ---- scatter: token starts to tp, payload bytes to st
+  const uint32_t cst = __reduce_and_sync(EQC_FULL, allE);  // bit 7 of byte p: plane p constant
+  const uint32_t rep = __reduce_or_sync(EQC_FULL, anyR);   // bit 7 of byte p: plane p has a REPEAT
+  // class per plane: 0 literal-only, 1 constant, 2 general
+  int cls[4];
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    const uint32_t t = (nibT >> (8 * p)) & 15u, ev = (nibE >> (8 * p)) & 15u, r = (nibR >> (8 * p)) & 15u;
-    int tk = (int)bytep(exT, p);
-    int ek = base[p] + 1 + (int)bytep(totT, p) + (int)bytep(exE, p);
+    const bool r = (rep >> (8 * p + 7)) & 1u, c = (cst >> (8 * p + 7)) & 1u;
+    cls[p] = !r ? 0 : (c ? 1 : 2);
+  }
+  const bool any_general = cls[0] == 2 || cls[1] == 2 || cls[2] == 2 || cls[3] == 2;
+  uint32_t nibT = 0, nibE = 0, nibR = 0, exT = 0, exE = 0, totT = 0, totE = 0;
+  if (any_general) {
+    uint32_t Rprev = __shfl_up_sync(EQC_FULL, R[3], 1);
+    if (lane == 0) Rprev = 0;
+    uint32_t T[4], E[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if ((t >> j) & 1u) {
-        tp[p * kC + tk] = (uint8_t)((i0 + j) | (((r >> j) & 1u) << 7));
-        ++tk;
+      const uint32_t valid = vflag(i0 + j < L);
+      const uint32_t rp = (j == 0) ? Rprev : R[j - 1];
+      const uint32_t first = vflag(i0 + j == 0);
+      T[j] = (first | (R[j] ^ rp) | (R[j] & rp & ~e[j + 1])) & valid;
+      E[j] = (~R[j] | T[j]) & valid;
+    }
+    nibT = ((T[0] >> 7) | (T[1] >> 6) | (T[2] >> 5) | (T[3] >> 4)) & 0x0F0F0F0Fu;
+    nibE = ((E[0] >> 7) | (E[1] >> 6) | (E[2] >> 5) | (E[3] >> 4)) & 0x0F0F0F0Fu;
+    nibR = ((R[0] >> 7) | (R[1] >> 6) | (R[2] >> 5) | (R[3] >> 4)) & 0x0F0F0F0Fu;
+    const uint32_t cT = bytes_popc_nibble(nibT);
+    const uint32_t cE = bytes_popc_nibble(nibE);
+    const uint32_t incT = warp_incl_scan_add(cT, lane);
+    const uint32_t incE = warp_incl_scan_add(cE, lane);
+    totT = __shfl_sync(EQC_FULL, incT, 31);
+    totE = __shfl_sync(EQC_FULL, incE, 31);
+    exT = incT - cT;
+    exE = incE - cE;
+  }
+  int size[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+    size[p] = cls[p] == 0 ? L + 2 : cls[p] == 1 ? 3 : 1 + (int)bytep(totT, p) + (int)bytep(totE, p);
+  const int b0 = 0, b1 = size[0], b2 = b1 + size[1], b3 = b2 + size[2], b4 = b3 + size[3];
+  // ---- emit each plane by class
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int base = p == 0 ? b0 : p == 1 ? b1 : p == 2 ? b2 : b3;
+    if (cls[p] == 1) {
+      if (lane == 0) {
+        st[base] = 1;
+        st[base + 1] = (uint8_t)(0x80 | (L - 1));
+        st[base + 2] = (uint8_t)bytep(px[0], p);
       }
-      if ((ev >> j) & 1u) {
-        st[ek] = (uint8_t)bytep(px[j], p);
-        ++ek;
+    } else if (cls[p] == 0) {
+      if (lane == 0) {
+        st[base] = 1;
+        st[base + 1] = (uint8_t)(L - 1);
       }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i0 + j < L) st[base + 2 + i0 + j] = (uint8_t)bytep(px[j], p);
+    } else {
+      const uint32_t t = (nibT >> (8 * p)) & 15u, ev = (nibE >> (8 * p)) & 15u, r = (nibR >> (8 * p)) & 15u;
+      int tk = (int)bytep(exT, p);
+      int ek = base + 1 + (int)bytep(totT, p) + (int)bytep(exE, p);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if ((t >> j) & 1u) {
+          tp[p * kC + tk] = (uint8_t)((i0 + j) | (((r >> j) & 1u) << 7));
+          ++tk;
+        }
+        if ((ev >> j) & 1u) {
+          st[ek] = (uint8_t)bytep(px[j], p);
+          ++ek;
+        }
+      }
+      if (lane == 0) st[base] = (uint8_t)bytep(totT, p);
     }
   }
-  if (lane < 4) st[base[lane]] = (uint8_t)bytep(totT, lane);
-  __syncwarp();
-  // ---- ctrl bytes: token length = next token start - this start
-  const int n0 = (int)bytep(totT, 0), n1 = n0 + (int)bytep(totT, 1), n2 = n1 + (int)bytep(totT, 2),
-            n3 = n2 + (int)bytep(totT, 3);
-  for (int q = lane; q < n3; q += 32) {
-    const int p = (q >= n0) + (q >= n1) + (q >= n2);
-    const int pb = (p == 0) ? 0 : (p == 1) ? n0 : (p == 2) ? n1 : n2;
-    const int np = (p == 0) ? n0 : (p == 1) ? n1 - n0 : (p == 2) ? n2 - n1 : n3 - n2;
-    const int t = q - pb;
-    const uint32_t a = tp[p * kC + t];
-    const int next = (t + 1 < np) ? (int)(tp[p * kC + t + 1] & 0x7Fu) : L;
-    const int len = next - (int)(a & 0x7Fu);
-    const int bp = (p == 0) ? base[0] : (p == 1) ? base[1] : (p == 2) ? base[2] : base[3];
-    st[bp + 1 + t] = (uint8_t)((a & 0x80u) | (uint32_t)(len - 1));
+  if (any_general) {
+    __syncwarp();
+    // ---- ctrl bytes of GENERAL planes: token length = next start - this start
+    const int g0 = cls[0] == 2 ? (int)bytep(totT, 0) : 0;
+    const int g1 = cls[1] == 2 ? (int)bytep(totT, 1) : 0;
+    const int g2 = cls[2] == 2 ? (int)bytep(totT, 2) : 0;
+    const int g3 = cls[3] == 2 ? (int)bytep(totT, 3) : 0;
+    const int n0 = g0, n1 = n0 + g1, n2 = n1 + g2, n3 = n2 + g3;
+    for (int q = lane; q < n3; q += 32) {
+      const int p = (q >= n0) + (q >= n1) + (q >= n2);
+      const int pb = sel4(p, 0, n0, n1, n2);
+      const int np = sel4(p, g0, g1, g2, g3);
+      const int t = q - pb;
+      const uint32_t a = tp[p * kC + t];
+      const int next = (t + 1 < np) ? (int)(tp[p * kC + t + 1] & 0x7Fu) : L;
+      const int len = next - (int)(a & 0x7Fu);
+      const int bp = sel4(p, b0, b1, b2, b3);
+      st[bp + 1 + t] = (uint8_t)((a & 0x80u) | (uint32_t)(len - 1));
+    }
   }
   __syncwarp();
-  uint32_t ps = 0;
-#pragma unroll
-  for (int p = 0; p < 4; ++p) ps |= (uint32_t)(base[p + 1] - base[p]) << (8 * p);
-  return EncodeOut{base[4], ps};
+  const uint32_t ps = (uint32_t)size[0] | ((uint32_t)size[1] << 8) | ((uint32_t)size[2] << 16) |
+                      ((uint32_t)size[3] << 24);
+  return EncodeOut{b4, ps};
 }
 
 // Copy the warp's staged record (st[0..size)) to global bytes [g, g+size).

@@ -20,6 +20,9 @@ E_INVALID, E_CAPACITY, E_CORRUPT, E_UNSUPPORTED, E_CUDA, E_NCCL = -1, -2, -3, -4
 MAX_SOURCES = 64
 KIND_RGBA8, KIND_DEPTH32 = 0, 1
 FLAG_SWIZZLE = 1
+UNIQUE_ID_BYTES = 128
+OP_DEPTH = 0
+FLAG_RLE = 1
 
 
 class EqcError(RuntimeError):
@@ -46,8 +49,19 @@ def _load():
         "image_compress_rle": ([P, i32, i32, i64, i32, i32, P, i64, P, P, sz, P], i32),
         "image_decompress_rle": ([P, i64, P, i64, i32, i32, P, P], i32),
         "image_compress_rle_batch": ([i32, P, i32, i32, i64, P, P, P, i64, P, P, sz, P], i32),
-        "image_decompress_rle_batch": ([i32, P, i64, P, i64, i32, i32, P, P], i32),
-        "compositor_depth_rle": ([i32, P, P, i64, i32, i32, P, P, i64, P, P], i32),
+        "image_decompress_rle_batch": ([i32, P, P, P, i64, i32, i32, P, P], i32),
+        "compositor_depth_rle": ([i32, P, P, P, P, i32, i32, P, P, i64, P, P], i32),
+        # eqc_comm.h
+        "eqc_comm_get_unique_id": ([P], i32),
+        "eqc_comm_init": ([P, i32, i32, P], i32),
+        "eqc_comm_destroy": ([P], i32),
+        "eqc_comm_stats": ([P, P], i32),
+        "eqc_plan_bands": ([i32, i32, P], i32),
+        "eqc_plan_binary_swap": ([i32, i32, i32, P, i32], i32),
+        "compose_direct_send": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
+        "compose_binary_swap": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
+        "compose_direct_send_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
+        "compose_binary_swap_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -165,20 +179,130 @@ def image_compress_rle_batch(srcs, kinds, flags, dsts, d_sizes, workspace, strea
     return _check(rc, "image_compress_rle_batch")
 
 
-def image_decompress_rle_batch(srcs, dsts, d_status, src_bytes: int | None = None, stream=None):
+def _i64s(vals):
+    return (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+def image_decompress_rle_batch(srcs, dsts, d_status, src_bytes=None, stream=None):
+    """src_bytes: per-stream readable bytes (default: each tensor's numel)."""
     n = len(srcs)
     w, h, pitch = _frame_geom(dsts[0])
-    nb = min(s.numel() for s in srcs) if src_bytes is None else src_bytes
-    rc = _lib.image_decompress_rle_batch(n, _ptrs(srcs), nb, _ptrs(dsts), pitch, w, h, _addr(d_status),
+    nb = [s.numel() for s in srcs] if src_bytes is None else src_bytes
+    rc = _lib.image_decompress_rle_batch(n, _ptrs(srcs), _i64s(nb), _ptrs(dsts), pitch, w, h, _addr(d_status),
                                          _stream(stream))
     return _check(rc, "image_decompress_rle_batch")
 
 
 def compositor_depth_rle(color_streams, depth_streams, out_color, out_depth, d_status,
-                         src_bytes: int | None = None, stream=None):
+                         color_bytes=None, depth_bytes=None, stream=None):
+    """color_bytes / depth_bytes: per-stream readable bytes (default: numel)."""
     n = len(color_streams)
     w, h, opitch = _frame_geom(out_color)
-    nb = min(s.numel() for s in list(color_streams) + list(depth_streams)) if src_bytes is None else src_bytes
-    rc = _lib.compositor_depth_rle(n, _ptrs(color_streams), _ptrs(depth_streams), nb, w, h, _addr(out_color),
-                                   _addr(out_depth), opitch, _addr(d_status), _stream(stream))
+    cb = [s.numel() for s in color_streams] if color_bytes is None else color_bytes
+    db = [s.numel() for s in depth_streams] if depth_bytes is None else depth_bytes
+    rc = _lib.compositor_depth_rle(n, _ptrs(color_streams), _ptrs(depth_streams), _i64s(cb), _i64s(db), w, h,
+                                   _addr(out_color), _addr(out_depth), opitch, _addr(d_status), _stream(stream))
     return _check(rc, "compositor_depth_rle")
+
+
+# ---------------------------------------------------------------- eqc_comm.h
+def eqc_plan_bands(h: int, n: int):
+    """Row boundaries of the n direct-send bands (R-C13): [row0[0] .. row0[n]]."""
+    row0 = (ctypes.c_int * (n + 1))()
+    _check(_lib.eqc_plan_bands(h, n, row0), "eqc_plan_bands")
+    return list(row0)
+
+
+def eqc_plan_binary_swap(h: int, n: int, rank: int):
+    """Rounds of rank's binary-swap plan: [(partner, low, keep_y0, keep_y1, send_y0, send_y1), ...]."""
+    buf = (ctypes.c_int * (6 * 32))()
+    k = _check(_lib.eqc_plan_binary_swap(h, n, rank, buf, 32), "eqc_plan_binary_swap")
+    return [tuple(buf[6 * i:6 * i + 6]) for i in range(k)]
+
+
+class Comm:
+    """An eqc_comm: NCCL clique of one process per GPU (current device)."""
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes):
+        assert len(unique_id) == UNIQUE_ID_BYTES
+        self.nranks, self.rank = nranks, rank
+        self._h = ctypes.c_void_p()
+        idbuf = (ctypes.c_uint8 * UNIQUE_ID_BYTES)(*unique_id)
+        _check(_lib.eqc_comm_init(ctypes.byref(self._h), nranks, rank, idbuf), "eqc_comm_init")
+
+    @staticmethod
+    def get_unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * UNIQUE_ID_BYTES)()
+        _check(_lib.eqc_comm_get_unique_id(buf), "eqc_comm_get_unique_id")
+        return bytes(buf)
+
+    @classmethod
+    def from_torch_distributed(cls, group=None):
+        """Bootstrap the NCCL unique id over an initialised torch.distributed group."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        del torch
+        return cls(world, rank, obj[0])
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stats(self):
+        out = (ctypes.c_int64 * 4)()
+        _check(_lib.eqc_comm_stats(self._h, out), "eqc_comm_stats")
+        return list(out)
+
+    def destroy(self):
+        if self._h:
+            _check(_lib.eqc_comm_destroy(self._h), "eqc_comm_destroy")
+            self._h = ctypes.c_void_p()
+
+
+def _compose(fn, name, comm, colors, depths, out_color, dest_rank, flags, op, stream):
+    n = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    opitch = _frame_geom(out_color)[2] if out_color is not None else w
+    rc = fn(comm.handle, n, _ptrs(colors), _ptrs(depths), w, h, pitch, op, flags, dest_rank, _addr(out_color),
+            opitch, _stream(stream))
+    return _check(rc, name)
+
+
+def compose_direct_send(comm, colors, depths, out_color=None, dest_rank: int = 0, flags: int = 0,
+                        op: int = OP_DEPTH, stream=None):
+    return _compose(_lib.compose_direct_send, "compose_direct_send", comm, colors, depths, out_color, dest_rank,
+                    flags, op, stream)
+
+
+def compose_binary_swap(comm, colors, depths, out_color=None, dest_rank: int = 0, flags: int = 0,
+                        op: int = OP_DEPTH, stream=None):
+    return _compose(_lib.compose_binary_swap, "compose_binary_swap", comm, colors, depths, out_color, dest_rank,
+                    flags, op, stream)
+
+
+def _compose_local(fn, name, nranks, colors, depths, out_color, dest_rank, flags, op, stream):
+    total = len(colors)
+    assert total % nranks == 0
+    w, h, pitch = _frame_geom(colors[0])
+    opitch = _frame_geom(out_color)[2]
+    stats = (ctypes.c_int64 * 4)()
+    rc = fn(nranks, total // nranks, _ptrs(colors), _ptrs(depths), w, h, pitch, op, flags, dest_rank,
+            _addr(out_color), opitch, stats, _stream(stream))
+    _check(rc, name)
+    return list(stats)
+
+
+def compose_direct_send_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
+                              op: int = OP_DEPTH, stream=None):
+    """Virtual-rank direct send on one GPU; returns summed traffic counters."""
+    return _compose_local(_lib.compose_direct_send_local, "compose_direct_send_local", nranks, colors, depths,
+                          out_color, dest_rank, flags, op, stream)
+
+
+def compose_binary_swap_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
+                              op: int = OP_DEPTH, stream=None):
+    return _compose_local(_lib.compose_binary_swap_local, "compose_binary_swap_local", nranks, colors, depths,
+                          out_color, dest_rank, flags, op, stream)

@@ -1,0 +1,63 @@
+"""One process per GPU: compose_direct_send / compose_binary_swap over NCCL
+(NVLink) against the oracle over all ranks' sources.  Launched by
+tests/test_gpu_multi.py with torch.distributed.run."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_1902_08755_b200 import eqc  # noqa: E402
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    comm = eqc.Comm.from_torch_distributed()
+    dev = torch.device("cuda", local)
+    failures = []
+    cases = [("ds", 2, 640, 361, 0, 0), ("ds", 1, 300, 41, world - 1, 1), ("ds", 2, 1920, 1080, 0, 1)]
+    if world & (world - 1) == 0:
+        cases += [("bs", 2, 640, 361, 0, 0), ("bs", 1, 300, 41, world - 1, 1), ("bs", 2, 1920, 1080, 0, 1)]
+    for algo, nl, w, h, dest, rle in cases:
+        N = world * nl
+        c, d = synth.depth_sources(synth.SEED_BASE + 3 + N + w, N, w, h)
+        mine = range(rank * nl, (rank + 1) * nl)
+        dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
+        dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
+        out = torch.zeros((h, w), dtype=torch.int32, device=dev)
+        fn = eqc.compose_direct_send if algo == "ds" else eqc.compose_binary_swap
+        for _ in range(2):  # the second call reuses the communicator's scratch
+            fn(comm, dc, dd, out if rank == dest else None, dest_rank=dest, flags=eqc.FLAG_RLE if rle else 0)
+        torch.cuda.synchronize()
+        st = comm.stats()
+        if rank == dest:
+            want, _ = oracle.depth_composite(c, d)
+            got = out.cpu().numpy().view(np.uint32)
+            if not (got == want).all():
+                failures.append(f"{algo} nl={nl} {w}x{h} rle={rle}: mismatch {(got != want).sum()} px")
+        if algo == "ds" and st[0] != world - 1:
+            failures.append(f"{algo}: rank {rank} sent {st[0]} band messages, want {world - 1}")
+        dist.barrier()
+    comm.destroy()
+    t = torch.tensor([len(failures)], device=dev)
+    dist.all_reduce(t)
+    for f in failures:
+        print(f"rank {rank}: {f}", flush=True)
+    if rank == 0 and int(t.item()) == 0:
+        print("ALL OK", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if int(t.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

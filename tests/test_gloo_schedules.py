@@ -1,0 +1,160 @@
+"""Multi-process (gloo, CPU) execution of libeqc's direct-send and binary-swap
+plans: world_size 2 and 4 processes each hold a contiguous block of sources,
+exchange real bytes over torch.distributed (gloo, 127.0.0.1), composite with
+the CPU oracle at every step and must reproduce the oracle over ALL sources
+bit-exactly (schedule soundness; tie rule R-C5).  This pins the host
+logic of the N > 1 path (plans, tie preference, band bookkeeping) without a
+GPU; the GPU/NCCL path executes the same plans (tests/test_gpu_multi.py).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_1902_08755_b200 import eqc
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _send(arr, dst):
+    dist.send(torch.from_numpy(np.ascontiguousarray(arr).view(np.int32)), dst)
+
+
+def _recv(shape, src):
+    t = torch.empty(shape, dtype=torch.int32)
+    dist.recv(t, src)
+    return t.numpy().view(np.uint32)
+
+
+def _exchange(sends, recvs):
+    """Post all sends and receives of one step (non-blocking), then wait."""
+    reqs = []
+    for arr, dst in sends:
+        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(arr).view(np.int32)), dst))
+    outs = []
+    for shape, src in recvs:
+        t = torch.empty(shape, dtype=torch.int32)
+        reqs.append(dist.irecv(t, src))
+        outs.append(t)
+    for r in reqs:
+        r.wait()
+    return [o.numpy().view(np.uint32) for o in outs]
+
+
+def _worker(rank, world, port, algo, n_local, w, h, dest, tie_alphabet, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = world * n_local
+        if tie_alphabet:
+            c, d = synth.random_frames(77, n, w, h, depth_alphabet=[0, 3, 0xFFFFFFFF])
+        else:
+            c, d = synth.depth_sources(20190213 + 3, n, w, h)
+        mine_c = c[rank * n_local:(rank + 1) * n_local]
+        mine_d = d[rank * n_local:(rank + 1) * n_local]
+        pc, pd = oracle.depth_composite(mine_c, mine_d)  # local pre-composite
+        msgs = 0
+        if algo == "ds":
+            row0 = eqc.eqc_plan_bands(h, world)
+            y0, y1 = row0[rank], row0[rank + 1]
+            sends, recvs = [], []
+            for j in range(world):
+                if j != rank and row0[j + 1] > row0[j]:
+                    sends += [(pc[row0[j]:row0[j + 1]], j), (pd[row0[j]:row0[j + 1]], j)]
+                    msgs += 1
+            srcs = [q for q in range(world) if q != rank and y1 > y0]
+            for q in srcs:
+                recvs += [((y1 - y0, w), q), ((y1 - y0, w), q)]
+            got = _exchange(sends, recvs)
+            bands_c, bands_d = [], []
+            it = iter(got)
+            recv_map = {q: (next(it), next(it)) for q in srcs}
+            for q in range(world):
+                if q == rank:
+                    bands_c.append(pc[y0:y1])
+                    bands_d.append(pd[y0:y1])
+                elif y1 > y0:
+                    bands_c.append(recv_map[q][0])
+                    bands_d.append(recv_map[q][1])
+            fin = oracle.depth_composite(bands_c, bands_d)[0] if y1 > y0 else np.zeros((0, w), np.uint32)
+            regions = [(row0[q], row0[q + 1]) for q in range(world)]
+        else:
+            plan = eqc.eqc_plan_binary_swap(h, world, rank)
+            cur_c, cur_d = pc.copy(), pd.copy()
+            for partner, low, ky0, ky1, sy0, sy1 in plan:
+                sends = [(cur_c[sy0:sy1], partner), (cur_d[sy0:sy1], partner)] if sy1 > sy0 else []
+                recvs = [((ky1 - ky0, w), partner)] * 2 if ky1 > ky0 else []
+                msgs += 1 if sy1 > sy0 else 0
+                got = _exchange(sends, recvs)
+                if ky1 > ky0:
+                    mc, md = cur_c[ky0:ky1], cur_d[ky0:ky1]
+                    tc, td = got
+                    cs = [mc, tc] if low else [tc, mc]  # ties -> group whose bit r is 0
+                    ds = [md, td] if low else [td, md]
+                    oc, od = oracle.depth_composite(cs, ds)
+                    cur_c[ky0:ky1] = oc
+                    cur_d[ky0:ky1] = od
+            regions = []
+            for q in range(world):
+                pq = eqc.eqc_plan_binary_swap(h, world, q)
+                regions.append((pq[-1][2], pq[-1][3]) if pq else (0, h))
+            y0, y1 = regions[rank]
+            fin = cur_c[y0:y1]
+        # gather colour to dest
+        if rank != dest:
+            if y1 > y0:
+                _send(fin, dest)
+            result_q.put((rank, msgs, None))
+        else:
+            out = np.zeros((h, w), np.uint32)
+            out[y0:y1] = fin
+            for q in range(world):
+                qy0, qy1 = regions[q]
+                if q != dest and qy1 > qy0:
+                    out[qy0:qy1] = _recv((qy1 - qy0, w), q)
+            want, _ = oracle.depth_composite(c, d)
+            result_q.put((rank, msgs, bool((out == want).all())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("algo,world,n_local,w,h,dest,ties", [
+    ("ds", 2, 2, 64, 41, 0, False),
+    ("ds", 3, 1, 50, 31, 2, True),
+    ("ds", 4, 2, 33, 9, 1, True),
+    ("bs", 2, 3, 40, 33, 1, True),
+    ("bs", 4, 1, 64, 37, 0, False),
+    ("bs", 4, 2, 16, 5, 3, True),
+])
+def test_schedule_equals_oracle_over_all_sources(algo, world, n_local, w, h, dest, ties):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, algo, n_local, w, h, dest, ties, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ok = [r[2] for r in res if r[0] == dest]
+    assert ok == [True]
+    msgs = sum(r[1] for r in res)
+    if algo == "ds":
+        assert msgs == world * (world - 1)  # n(n-1) band messages
+    else:
+        assert msgs == world * (world.bit_length() - 1)  # n log2 n swaps

@@ -1,0 +1,76 @@
+"""Host-side schedule plans of libeqc (eqc_comm.h), checked on the CPU.
+
+Direct send: n balanced row bands (R-C13), one
+band per rank; message pattern of fDirectSend: each of n ranks sends n-1
+colour+depth tiles, the destination assembles n-1 colour tiles,
+i.e. n(n-1) + (n-1) messages.  Binary swap: log2 n
+rounds with partner rank ^ 2^r; final regions partition the frame in
+bit-reversed order; non-power-of-two n is unsupported.
+"""
+import pytest
+
+from paper_1902_08755_b200 import eqc
+
+
+@pytest.mark.parametrize("h,n", [(1080, 1), (1080, 2), (1081, 3), (2160, 4), (7, 8), (3, 5), (4320, 8)])
+def test_bands_partition_and_balance(h, n):
+    row0 = eqc.eqc_plan_bands(h, n)
+    assert row0[0] == 0 and row0[-1] == h and len(row0) == n + 1
+    sizes = [row0[j + 1] - row0[j] for j in range(n)]
+    assert all(s >= 0 for s in sizes)
+    assert max(sizes) - min(sizes) <= 1
+    assert row0 == [j * h // n for j in range(n + 1)]
+
+
+def bitrev(x, k):
+    return int(format(x, f"0{k}b")[::-1], 2) if k else 0
+
+
+@pytest.mark.parametrize("h,n", [(1080, 1), (1080, 2), (1081, 4), (4320, 8), (5, 8), (2160, 16)])
+def test_binary_swap_plan(h, n):
+    k = n.bit_length() - 1
+    plans = [eqc.eqc_plan_binary_swap(h, n, r) for r in range(n)]
+    assert all(len(p) == k for p in plans)  # log2 n rounds (n = 4 -> 2 rounds)
+    for r in range(n):
+        for rd, (partner, low, ky0, ky1, sy0, sy1) in enumerate(plans[r]):
+            assert partner == r ^ (1 << rd)
+            assert low == int(((r >> rd) & 1) == 0)
+            p = plans[partner][rd]
+            # the partner keeps exactly what I send and sends what I keep
+            assert (p[2], p[3]) == (sy0, sy1) and (p[4], p[5]) == (ky0, ky1)
+            # the kept half of the low rank is the upper rows
+            if low:
+                assert ky0 <= ky1 == sy0 <= sy1
+            else:
+                assert sy0 <= sy1 == ky0 <= ky1
+    finals = []
+    for r in range(n):
+        y0, y1 = (plans[r][-1][2], plans[r][-1][3]) if k else (0, h)
+        finals.append((y0, y1, r))
+    finals.sort()
+    # final regions tile [0, h) with no overlap, in bit-reversed rank order
+    pos = 0
+    for y0, y1, r in finals:
+        assert y0 == pos
+        pos = y1
+    assert pos == h
+    if h >= n:
+        assert [r for _, _, r in finals] == [bitrev(i, k) for i in range(n)]
+
+
+def test_binary_swap_rejects_non_power_of_two():
+    with pytest.raises(eqc.EqcError) as e:
+        eqc.eqc_plan_binary_swap(100, 3, 0)
+    assert e.value.code == eqc.E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_direct_send_message_count(n):
+    """n(n-1) band exchanges + (n-1) gathers; for n = 3: two
+    colour+depth tiles sent per channel, two colour tiles assembled at the
+    destination."""
+    row0 = eqc.eqc_plan_bands(2160, n)
+    band_msgs = sum(1 for me in range(n) for j in range(n) if j != me and row0[j + 1] > row0[j])
+    gathers = sum(1 for q in range(n) if q != 0 and row0[q + 1] > row0[q])
+    assert band_msgs == n * (n - 1)
+    assert gathers == n - 1
