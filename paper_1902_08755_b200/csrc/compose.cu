@@ -253,7 +253,9 @@ int local_precomposite(RankState &r, const Geometry &g, cudaStream_t s) {
 
 // Encode `count` (<= 2 per band) colour+depth bands: slot k of `enc`.
 inline int64_t band_cap(const Geometry &g, int rows) {
-  return rows > 0 ? image_rle_max_size(g.w, rows) : 32;
+  // streams must start 8-byte aligned: round each slot up to 256 bytes
+  const int64_t b = rows > 0 ? image_rle_max_size(g.w, rows) : 32;
+  return (b + 255) & ~(int64_t)255;
 }
 
 int encode_band(RankState &r, const Geometry &g, int slot, const uint32_t *c, const uint32_t *d, int rows,

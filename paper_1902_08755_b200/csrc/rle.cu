@@ -136,28 +136,30 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
   const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
   const EncImage im = p.img[m];
   const int64_t c0 = (lt * kWarps + warp) * kCPW;
+  // chunk coordinates advance incrementally (no 64-bit division per chunk);
   // software pipeline: the next chunk's 128-bit loads are in flight while
   // the current chunk is coded
-  auto chunk_len = [&](int64_t c) -> int {
-    if (c >= p.nchunks) return 0;
-    const int x0 = (int)(c % p.S) * kC;
-    return min(kC, p.w - x0);
-  };
-  auto chunk_row = [&](int64_t c) -> const uint32_t * {
-    const int64_t y = c / p.S;
-    return im.src + y * p.pitch + (c - y * p.S) * kC;
-  };
+  const int nch = (int)p.nchunks;  // < 2^31 (u32 table field)
+  int cc = (int)c0;
+  int yy = cc / p.S, kk = cc - yy * p.S;
+  auto len_of = [&](int c, int k) -> int { return c < nch ? min(kC, p.w - k * kC) : 0; };
+  auto row_of = [&](int y, int k) -> const uint32_t * { return im.src + (int64_t)y * p.pitch + k * kC; };
   uint32_t cur[4] = {0, 0, 0, 0}, nxt[4] = {0, 0, 0, 0};
-  int Lc = chunk_len(c0);
-  if (Lc > 0) load_chunk(chunk_row(c0), Lc, lane, p.vec != 0, cur);
+  int Lc = len_of(cc, kk);
+  if (Lc > 0) load_chunk(row_of(yy, kk), Lc, lane, p.vec != 0, cur);
   int run = 0;
   uint32_t my_ps = 0;  // lane j < kCPW keeps chunk j's plane sizes and offset in the run
   int my_pre = 0;
   const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
 #pragma unroll 1
   for (int j = 0; j < kCPW && Lc > 0; ++j) {
-    const int Ln = chunk_len(c0 + j + 1);
-    if (j + 1 < kCPW && Ln > 0) load_chunk(chunk_row(c0 + j + 1), Ln, lane, p.vec != 0, nxt);
+    int yn = yy, kn = kk + 1;
+    if (kn == p.S) {
+      kn = 0;
+      ++yn;
+    }
+    const int Ln = (j + 1 < kCPW) ? len_of(cc + 1, kn) : 0;
+    if (Ln > 0) load_chunk(row_of(yn, kn), Ln, lane, p.vec != 0, nxt);
     const EncodeOut eo = encode_chunk(cur, Lc, lane, swz, stage[warp] + run, toks[warp]);
     if (lane == j) {
       my_ps = eo.psizes;
@@ -166,7 +168,10 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
     run += eo.size;
 #pragma unroll
     for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
-    Lc = (j + 1 < kCPW) ? Ln : 0;
+    Lc = Ln;
+    cc += 1;
+    yy = yn;
+    kk = kn;
   }
   if (lane == 0) wsize[warp] = run;
   __syncthreads();
@@ -341,18 +346,19 @@ struct DecParams {
 constexpr int kGroup = 32;  // chunks classified per warp pass (one per lane)
 
 // Lane-parallel table read for chunk c (valid if `has`): entry, and the
-// monotone/contiguous check against chunk c-1 (the previous lane's entry, or
-// a load for lane 0).  Returns ok.
+// monotone/contiguous check against chunk c-1, whose entry lane
+// `lane - delta` holds (lanes below `delta` load it).  Must be called by the
+// whole warp.  Returns ok.
 __device__ __forceinline__ bool entry_lane(const uint8_t *src, int64_t payload_bytes, int64_t nchunks, int64_t c,
-                                           bool has, int L, int lane, int64_t &off, uint32_t &ps) {
+                                           bool has, int L, int lane, int64_t &off, uint32_t &ps, int delta = 1) {
   uint2 te = make_uint2(0, 0);
   if (has) te = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * c));
   off = te.x;
   ps = te.y;
   const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
   const int64_t end = off + s0 + s1 + s2 + s3;
-  int64_t prev = __shfl_up_sync(EQC_FULL, end, 1);
-  if (lane == 0) {
+  int64_t prev = __shfl_up_sync(EQC_FULL, end, delta);
+  if (lane < delta) {
     prev = 0;
     if (has && c > 0) {
       const uint2 tp = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * (c - 1)));
@@ -391,8 +397,8 @@ __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_co
     if (cb >= hd.nchunks) break;
     const int64_t c = cb + lane;
     const bool has = c < hd.nchunks;
-    const int y = has ? (int)(c / hd.S) : 0;
-    const int k = has ? (int)(c - (int64_t)y * hd.S) : 0;
+    const int y = has ? (int)((uint32_t)c / (uint32_t)hd.S) : 0;
+    const int k = has ? (int)c - y * hd.S : 0;
     const int L = has ? min(C, p.w - k * C) : 0;
     int64_t off;
     uint32_t ps;
@@ -450,17 +456,18 @@ struct FusedParams {
 };
 
 constexpr int kMaxStreams = 2 * EQC_MAX_SOURCES;
-constexpr int kSrcBatch = 4;  // sources classified per unrolled batch
+constexpr int kPosPerWarp = 8;  // chunk positions per warp (4 lanes each in phase A)
 
-// Warp per 32 consecutive chunk positions.
-//  Phase A (lane = position): for every source, the depth and colour table
-//   entries are validated and probed for constant chunks; while every
-//   stream of a position is constant the depth composite is evaluated on the
-//   scalar values (z-test over sources in index order).
-//  Phase B: positions whose streams were all constant are written with one
-//   128-bit store per lane per output; every other position is decoded
-//   warp-cooperatively, depth first: a source's colour chunk is decoded only
-//   if the source wins at least one pixel of the chunk.
+// Warp per 8 consecutive chunk positions.
+//  Phase A (4 lanes per position, lane sub = lane & 3 takes sources
+//   i = sub, sub + 4, ...): the depth and colour table entries of every
+//   stream are validated and probed for constant chunks; while all streams of
+//   a position are constant the depth composite is evaluated on the scalar
+//   values, then the four partial minima are merged by (depth, index).
+//  Phase B: all-constant positions are written with one 128-bit store per
+//   lane per output; every other position is decoded warp-cooperatively,
+//   depth first: a source's colour chunk is decoded only if the source wins
+//   at least one pixel of the chunk.
 __global__ void __launch_bounds__(kWarps * 32) depth_rle_kernel(const __grid_constant__ FusedParams p) {
   __shared__ __align__(16) uint8_t stage[kWarps][kStageBytes];
   __shared__ __align__(16) uint16_t info[kWarps][kC];
@@ -483,57 +490,64 @@ __global__ void __launch_bounds__(kWarps * 32) depth_rle_kernel(const __grid_con
     if (tid == 0) set_corrupt(p.status);
     return;
   }
-  const int64_t nchunks = (int64_t)p.S * p.h;
-  const int64_t payload0 = 32 + 8 * nchunks;
-  const int64_t cb = ((int64_t)blockIdx.x * kWarps + warp) * kGroup;
-  if (cb >= nchunks) return;
-  const int64_t c = cb + lane;
-  const bool has = c < nchunks;
-  const int y = has ? (int)(c / p.S) : 0;
-  const int k = has ? (int)(c - (int64_t)y * p.S) : 0;
+  const int nch = p.S * p.h;
+  const int64_t payload0 = 32 + 8 * (int64_t)nch;
+  const int cb = (blockIdx.x * kWarps + warp) * kPosPerWarp;
+  if (cb >= nch) return;
+  const int pos = lane >> 2, sub = lane & 3;
+  const int c = cb + pos;
+  const bool has = c < nch;
+  const int y = has ? c / p.S : 0;
+  const int k = has ? c - y * p.S : 0;
   const int L = has ? min(kC, p.w - k * kC) : 0;
   // ---- phase A
   bool ok = true, allc = true;
-  uint32_t sd = 0, sc = 0;  // scalar composite of constant positions
-  for (int i0 = 0; i0 < n; i0 += kSrcBatch) {
-    int64_t offd[kSrcBatch], offc[kSrcBatch];
-    uint32_t psd[kSrcBatch], psc[kSrcBatch];
-#pragma unroll
-    for (int b = 0; b < kSrcBatch; ++b) {
-      const int i = i0 + b;
-      if (i < n) {
-        ok = entry_lane(p.src[n + i], s_pb[n + i], nchunks, c, has, L, lane, offd[b], psd[b]) && ok;
-        ok = entry_lane(p.src[i], s_pb[i], nchunks, c, has, L, lane, offc[b], psc[b]) && ok;
-      }
-    }
-    if (has && ok && allc) {
-#pragma unroll
-      for (int b = 0; b < kSrcBatch; ++b) {
-        const int i = i0 + b;
-        if (i < n && allc) {
-          uint32_t dv, cv;
-          const bool dc = probe_const(p.src[n + i] + payload0 + offd[b], psd[b], L, dv);
-          const bool cc = dc && probe_const(p.src[i] + payload0 + offc[b], psc[b], L, cv);
-          if (dc && cc) {
-            if (i == 0 || dv < sd) {  // strictly nearer: ties keep the lower index
-              sd = dv;
-              sc = (s_flags[i] & EQC_FLAG_SWIZZLE) ? unswizzle(cv) : cv;
-            }
-          } else {
-            allc = false;
-          }
+  uint32_t sd = 0xFFFFFFFFu, sc = 0;  // lane-partial scalar composite
+  int sidx = 0x7FFFFFFF;
+  for (int i0 = 0; i0 < n; i0 += 4) {
+    const int i = i0 + sub;
+    const bool hi = has && i < n;
+    const int ii = min(i, n - 1);
+    int64_t od, oc;
+    uint32_t pd, pc;
+    ok = entry_lane(p.src[n + ii], s_pb[n + ii], nch, c, hi, L, lane, od, pd, 4) && ok;
+    ok = entry_lane(p.src[ii], s_pb[ii], nch, c, hi, L, lane, oc, pc, 4) && ok;
+    if (hi && ok && allc) {
+      uint32_t dv, cv;
+      const bool dc = probe_const(p.src[n + ii] + payload0 + od, pd, L, dv);
+      const bool cc = dc && probe_const(p.src[ii] + payload0 + oc, pc, L, cv);
+      if (dc && cc) {
+        if (dv < sd) {  // sources visited in increasing index: strict < keeps the lower
+          sd = dv;
+          sidx = i;
+          sc = (s_flags[ii] & EQC_FLAG_SWIZZLE) ? unswizzle(cv) : cv;
         }
+      } else {
+        allc = false;
       }
     }
+  }
+  // merge the four partial minima of a position by (depth, index)
+#pragma unroll
+  for (int d = 1; d <= 2; d <<= 1) {
+    const uint32_t od = __shfl_xor_sync(EQC_FULL, sd, d), oc = __shfl_xor_sync(EQC_FULL, sc, d);
+    const int oi = __shfl_xor_sync(EQC_FULL, sidx, d);
+    if (od < sd || (od == sd && oi < sidx)) {
+      sd = od;
+      sc = oc;
+      sidx = oi;
+    }
+    allc = __shfl_xor_sync(EQC_FULL, (int)allc, d) && allc;
+    ok = __shfl_xor_sync(EQC_FULL, (int)ok, d) && ok;
   }
   const unsigned bad = __ballot_sync(EQC_FULL, has && !ok);
   if (bad) {
     if (lane == 0) set_corrupt(p.status);
     return;
   }
-  const unsigned cmask = __ballot_sync(EQC_FULL, has && allc);
-  const unsigned gmask = __ballot_sync(EQC_FULL, has && !allc);
-  // ---- phase B1: all-constant positions
+  const unsigned cmask = __ballot_sync(EQC_FULL, sub == 0 && has && allc);
+  const unsigned gmask = __ballot_sync(EQC_FULL, sub == 0 && has && !allc);
+  // ---- phase B1: all-constant positions (bit 4*pos set)
   for (unsigned mm = cmask; mm; mm &= mm - 1) {
     const int i = __ffs(mm) - 1;
     const int yi = __shfl_sync(EQC_FULL, y, i), ki = __shfl_sync(EQC_FULL, k, i), Li = __shfl_sync(EQC_FULL, L, i);
@@ -546,7 +560,7 @@ __global__ void __launch_bounds__(kWarps * 32) depth_rle_kernel(const __grid_con
   // ---- phase B2: positions with at least one non-constant chunk
   for (unsigned mm = gmask; mm; mm &= mm - 1) {
     const int ii = __ffs(mm) - 1;
-    const int64_t ci = cb + ii;
+    const int64_t ci = cb + (ii >> 2);
     const int yi = __shfl_sync(EQC_FULL, y, ii), ki = __shfl_sync(EQC_FULL, k, ii), Li = __shfl_sync(EQC_FULL, L, ii);
     uint32_t bc[4] = {0, 0, 0, 0}, bd[4] = {0, 0, 0, 0};
     bool good = true;
@@ -730,8 +744,8 @@ extern "C" int compositor_depth_rle(int n, const uint8_t *const *color_rle, cons
   p.h = h;
   p.S = (w + kC - 1) / kC;
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
-  const int64_t grid = ((int64_t)p.S * h + kWarps * kGroup - 1) / (kWarps * kGroup);
-  if (grid > 0x7FFFFFFFll) return EQC_E_INVALID;
+  const int64_t grid = ((int64_t)p.S * h + kWarps * kPosPerWarp - 1) / (kWarps * kPosPerWarp);
+  if (grid > 0x7FFFFFFFll || (int64_t)p.S * h > 0x7FFFFFFFll) return EQC_E_INVALID;
   depth_rle_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
