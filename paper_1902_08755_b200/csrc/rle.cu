@@ -18,6 +18,8 @@
 // {epoch:32 | ticket:32}, status words carry a 16-bit epoch tag, and the CTA
 // holding the last ticket bumps the epoch and zeroes the ticket after its
 // look-back, so no memset is needed between calls.
+#include <algorithm>
+
 #include "rle.cuh"
 
 using namespace eqc_rle;
@@ -25,13 +27,13 @@ using namespace eqc_rle;
 namespace {
 
 constexpr int kWarps = 8;          // warps per CTA
-constexpr int kCPW = 8;            // consecutive chunks per warp (encoder)
+constexpr int kCPW = 4;            // consecutive chunks per warp (encoder)
 constexpr int kTileChunks = kWarps * kCPW;
 constexpr int kWarpStage = kCPW * 520 + 16;  // records of one warp, back to back
 constexpr int kMaxBatch = 64;
 
-// workspace layout (uint64): [0] {epoch << 32 | ticket}, [1..3] pad,
-// [4 + t] look-back status of tile t.
+// workspace layout (uint64): [0] {epoch << 32 | ticket}, [1] CTAs done,
+// [2..3] pad, [4 + t] look-back status of tile t.
 constexpr int kWsHeader = 4;
 constexpr uint64_t kFlagAgg = 1ull << 46;
 constexpr uint64_t kFlagIncl = 2ull << 46;
@@ -120,69 +122,119 @@ __device__ __forceinline__ void load_chunk(const uint32_t *row, int L, int lane,
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
-  __shared__ __align__(16) uint8_t stage[kWarps][kWarpStage];
-  __shared__ __align__(16) uint8_t toks[kWarps][kTokBytes];
-  __shared__ int wsize[kWarps];
-  __shared__ int64_t woff[kWarps];
-  __shared__ unsigned long long s_tk;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t *ws = p.ws;
-  if (tid == 0) s_tk = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
-  __syncthreads();
-  const int64_t tile = (int64_t)(s_tk & 0xFFFFFFFFull);
-  const uint64_t epoch = s_tk >> 32;
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+struct EncSmem {
+  uint4 in[2][kWarps][kCPW][32];            // double-buffered input tiles (32 KB)
+  uint8_t stage[kWarps][kWarpStage];        // coded records, back to back per warp
+  uint8_t toks[kWarps][kTokBytes];          // token-start scratch
+  int wsize[kWarps];
+  int64_t woff[kWarps];
+  unsigned long long tk[2];
+};
+
+// Issue the loads of this warp's kCPW chunks of `tile` into `buf`: one 16-byte
+// cp.async per lane per chunk (ragged or unaligned chunks: plain loads).
+__device__ __forceinline__ void enc_issue(const EncParams &p, int64_t tile, int warp, int lane,
+                                          uint4 (*buf)[32]) {
   const int m = (int)(tile / p.tiles_per_image);
   const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
-  const EncImage im = p.img[m];
-  const int64_t c0 = (lt * kWarps + warp) * kCPW;
-  // chunk coordinates advance incrementally (no 64-bit division per chunk);
-  // software pipeline: the next chunk's 128-bit loads are in flight while
-  // the current chunk is coded
-  const int nch = (int)p.nchunks;  // < 2^31 (u32 table field)
-  int cc = (int)c0;
-  int yy = cc / p.S, kk = cc - yy * p.S;
-  auto len_of = [&](int c, int k) -> int { return c < nch ? min(kC, p.w - k * kC) : 0; };
-  auto row_of = [&](int y, int k) -> const uint32_t * { return im.src + (int64_t)y * p.pitch + k * kC; };
-  uint32_t cur[4] = {0, 0, 0, 0}, nxt[4] = {0, 0, 0, 0};
-  int Lc = len_of(cc, kk);
-  if (Lc > 0) load_chunk(row_of(yy, kk), Lc, lane, p.vec != 0, cur);
-  int run = 0;
-  uint32_t my_ps = 0;  // lane j < kCPW keeps chunk j's plane sizes and offset in the run
-  int my_pre = 0;
-  const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
-#pragma unroll 1
-  for (int j = 0; j < kCPW && Lc > 0; ++j) {
-    int yn = yy, kn = kk + 1;
-    if (kn == p.S) {
-      kn = 0;
-      ++yn;
-    }
-    const int Ln = (j + 1 < kCPW) ? len_of(cc + 1, kn) : 0;
-    if (Ln > 0) load_chunk(row_of(yn, kn), Ln, lane, p.vec != 0, nxt);
-    const EncodeOut eo = encode_chunk(cur, Lc, lane, swz, stage[warp] + run, toks[warp]);
-    if (lane == j) {
-      my_ps = eo.psizes;
-      my_pre = run;
-    }
-    run += eo.size;
+  const uint32_t *src = p.img[m].src;
+  const int c0 = (int)((lt * kWarps + warp) * kCPW);
+  const int nch = (int)p.nchunks;
+  int y = c0 / p.S, k = c0 - y * p.S;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
-    Lc = Ln;
-    cc += 1;
-    yy = yn;
-    kk = kn;
+  for (int j = 0; j < kCPW; ++j) {
+    if (c0 + j < nch) {
+      const int L = min(kC, p.w - k * kC);
+      const uint32_t *row = src + (int64_t)y * p.pitch + k * kC;
+      if (p.vec && L == kC) {
+        cp_async16(&buf[j][lane], row + 4 * lane);
+      } else {
+        uint32_t px[4];
+        load_chunk(row, L, lane, false, px);
+        buf[j][lane] = make_uint4(px[0], px[1], px[2], px[3]);
+      }
+    }
+    if (++k == p.S) {
+      k = 0;
+      ++y;
+    }
   }
-  if (lane == 0) wsize[warp] = run;
+  cp_async_commit();
+}
+
+// Persistent, software-pipelined single-pass encoder.  Each CTA loops over
+// tiles taken from the ticket counter; the loads of its next tile (cp.async
+// into the other input buffer) are in flight while it codes the current
+// tile, waits for the look-back and stores the records.
+__global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t *ws = p.ws;
+  const int64_t total = (int64_t)p.count * p.tiles_per_image;
+  if (tid == 0) sm.tk[0] = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
   __syncthreads();
-  if (warp == 0) {
-    const int v = lane < kWarps ? wsize[lane] : 0;
-    const int inc = (int)warp_incl_scan_add((uint32_t)v, lane);
-    const int agg = __shfl_sync(EQC_FULL, inc, 31);
-    const int64_t excl = lookback(ws + kWsHeader, (int64_t)m * p.tiles_per_image, lt, agg, epoch, lane);
-    if (lane < kWarps) woff[lane] = excl + inc - v;
-    if (lane == 0) {
-      if (lt == p.tiles_per_image - 1) {
+  unsigned long long tk = sm.tk[0];
+  const uint64_t epoch = tk >> 32;
+  int buf = 0;
+  if ((int64_t)(tk & 0xFFFFFFFFull) < total) enc_issue(p, (int64_t)(tk & 0xFFFFFFFFull), warp, lane, sm.in[0][warp]);
+  const int nch = (int)p.nchunks;
+  while (true) {
+    const int64_t tile = (int64_t)(tk & 0xFFFFFFFFull);
+    if (tile >= total) break;
+    if (tid == 0) sm.tk[buf ^ 1] = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
+    __syncthreads();  // next ticket visible; the other input buffer is free
+    const unsigned long long tkn = sm.tk[buf ^ 1];
+    const int64_t tnext = (int64_t)(tkn & 0xFFFFFFFFull);
+    if (tnext < total) {
+      enc_issue(p, tnext, warp, lane, sm.in[buf ^ 1][warp]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    // ---- code this warp's chunks
+    const int m = (int)(tile / p.tiles_per_image);
+    const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
+    const EncImage im = p.img[m];
+    const int c0 = (int)((lt * kWarps + warp) * kCPW);
+    const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
+    int k = c0 % p.S;
+    int run = 0;
+    uint32_t my_ps = 0;
+    int my_pre = 0;
+#pragma unroll 1
+    for (int j = 0; j < kCPW && c0 + j < nch; ++j) {
+      const int L = min(kC, p.w - k * kC);
+      const uint4 v = sm.in[buf][warp][j][lane];
+      uint32_t px[4] = {v.x, v.y, v.z, v.w};
+      const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[warp] + run, sm.toks[warp]);
+      if (lane == j) {
+        my_ps = eo.psizes;
+        my_pre = run;
+      }
+      run += eo.size;
+      if (++k == p.S) k = 0;
+    }
+    if (lane == 0) sm.wsize[warp] = run;
+    __syncthreads();
+    if (warp == 0) {
+      const int v = lane < kWarps ? sm.wsize[lane] : 0;
+      const int inc = (int)warp_incl_scan_add((uint32_t)v, lane);
+      const int agg = __shfl_sync(EQC_FULL, inc, 31);
+      const int64_t excl = lookback(ws + kWsHeader, (int64_t)m * p.tiles_per_image, lt, agg, epoch, lane);
+      if (lane < kWarps) sm.woff[lane] = excl + inc - v;
+      if (lane == 0 && lt == p.tiles_per_image - 1) {
         // last tile of the image: total payload known -> header + size
         const int64_t payload = excl + agg;
         const int64_t payload0 = 32 + 8 * p.nchunks;
@@ -198,21 +250,29 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
         h32[7] = (uint32_t)((uint64_t)payload >> 32);
         *im.d_size = payload0 + payload;
       }
-      if (tile == (int64_t)p.count * p.tiles_per_image - 1) {
-        // every ticket is taken and every tile of this launch has read its
-        // epoch: open the next epoch with ticket 0
-        atomicExch(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)((epoch + 1) << 32));
+    }
+    __syncthreads();
+    if (run > 0) {
+      const int64_t off = sm.woff[warp];
+      if (lane < kCPW && c0 + lane < nch) {
+        uint2 *te = reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (int64_t)(c0 + lane));
+        *te = make_uint2((uint32_t)(off + my_pre), my_ps);
       }
+      store_record(im.dst + 32 + 8 * p.nchunks + off, sm.stage[warp], run, lane);
     }
+    buf ^= 1;
+    tk = tkn;
   }
+  // every CTA holds a ticket >= total here; the last CTA out opens the next
+  // epoch (ticket 0) so the workspace is reusable without a memset
   __syncthreads();
-  if (run > 0) {
-    const int64_t off = woff[warp];
-    if (lane < kCPW && c0 + lane < p.nchunks) {
-      uint2 *te = reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (c0 + lane));
-      *te = make_uint2((uint32_t)(off + my_pre), my_ps);
+  if (tid == 0) {
+    __threadfence();
+    const unsigned long long d = atomicAdd(reinterpret_cast<unsigned long long *>(ws + 1), 1ull);
+    if (d == gridDim.x - 1) {
+      atomicExch(reinterpret_cast<unsigned long long *>(ws + 1), 0ull);
+      atomicExch(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)((epoch + 1) << 32));
     }
-    store_record(im.dst + 32 + 8 * p.nchunks + off, stage[warp], run, lane);
   }
 }
 
@@ -669,9 +729,22 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   p.h = h;
   p.tiles_per_image = (int)enc_tiles_per_image(w, h);
   p.vec = vec ? 1 : 0;
-  const int64_t grid = (int64_t)count * p.tiles_per_image;
-  if (grid > 0x7FFFFFFFll) return EQC_E_INVALID;
-  rle_encode_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
+  const int64_t tiles = (int64_t)count * p.tiles_per_image;
+  if (tiles > 0x7FFFFFFFll || p.nchunks > 0x7FFFFFFFll) return EQC_E_INVALID;
+  static int max_ctas = 0;
+  const size_t smem = sizeof(EncSmem);
+  if (max_ctas == 0) {
+    if (cudaFuncSetAttribute(rle_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return EQC_E_CUDA;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rle_encode_kernel, kWarps * 32, smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    max_ctas = per_sm * eqc_num_sms();
+  }
+  const int grid = (int)std::min<int64_t>(tiles, max_ctas);
+  rle_encode_kernel<<<grid, kWarps * 32, smem, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
 

@@ -26,6 +26,7 @@ constexpr int kLog2C = 7;
 constexpr int kC = 128;
 constexpr int kStageBytes = 544;  // >= 4 planes * (128 + 2) bytes, 16-aligned
 constexpr int kTokBytes = 512;    // token-start scratch: 4 planes * 128
+constexpr int kTokenLoopMax = 24; // decode: token-sequential expansion up to this many tokens
 
 // ---- swizzle (R-C9): out bit 4b + (3 - c) = bit b of channel c ------------
 // Byte reversal maps channel c to c' = 3 - c; the remaining permutation of the
@@ -290,7 +291,41 @@ __device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, 
     }
     return true;
   }
-  // tokens 4*lane .. 4*lane+3
+  if (ntok <= kTokenLoopMax) {
+    // few tokens (typical of mixed background/foreground chunks): walk the
+    // tokens in order; the warp expands each one, 32 positions per step,
+    // into a plane-major byte buffer (the info scratch), then each lane reads
+    // its 4 positions back as one word.
+    uint8_t *pb = reinterpret_cast<uint8_t *>(info);
+    __syncwarp();
+    int pos = 0, pay = 1 + ntok;
+    for (int t = 0; t < ntok; ++t) {
+      const int c = r[1 + t];
+      const int len = (c & 0x7F) + 1;
+      if (pos + len > L) return false;
+      if (c & 0x80) {
+        if (pay + 1 > size) return false;
+        const uint8_t v = r[pay];
+        for (int k = lane; k < len; k += 32) pb[pos + k] = v;
+        pay += 1;
+      } else {
+        if (pay + len > size) return false;
+        for (int k = lane; k < len; k += 32) pb[pos + k] = r[pay + k];
+        pay += len;
+      }
+      pos += len;
+    }
+    if (pos != L || pay != size) return false;
+    __syncwarp();
+    const uint32_t w4 = reinterpret_cast<const uint32_t *>(pb)[lane];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (i0 + j < L) out[j] |= ((w4 >> (8 * j)) & 0xFFu) << (8 * p);
+    __syncwarp();
+    return true;
+  }
+  // many tokens: tokens 4*lane .. 4*lane+3 per lane, positions by prefix sums
+  __syncwarp();  // the info scratch may still be read by the previous plane
   int sl = 0, sp = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
