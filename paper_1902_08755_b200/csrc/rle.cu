@@ -29,6 +29,7 @@ namespace {
 constexpr int kWarps = 8;          // warps per CTA
 constexpr int kCPW = 4;            // consecutive chunks per warp (encoder)
 constexpr int kTileChunks = kWarps * kCPW;
+static_assert(kTileChunks == 32, "the look-back warp writes one table entry per lane");
 constexpr int kWarpStage = kCPW * 520 + 16;  // records of one warp, back to back
 constexpr int kMaxBatch = 64;
 
@@ -132,17 +133,30 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+constexpr int kEncThreads = (kWarps + 1) * 32;  // 8 coder warps + 1 look-back/store warp
+
 struct EncSmem {
   uint4 in[2][kWarps][kCPW][32];            // double-buffered input tiles (32 KB)
-  uint8_t stage[kWarps][kWarpStage];        // coded records, back to back per warp
+  uint8_t stage[2][kWarps][kWarpStage];     // double-buffered coded records, back to back per warp
   uint8_t toks[kWarps][kTokBytes];          // token-start scratch
-  int wsize[kWarps];
-  int64_t woff[kWarps];
+  uint2 cinfo[2][kWarps * kCPW];            // per chunk {offset in its warp's run, plane sizes}
+  int wsize[2][kWarps];
+  int64_t tile_of[2];                       // tile coded into stage[b] (-1: no more tiles)
   unsigned long long tk[2];
 };
 
-// Issue the loads of this warp's kCPW chunks of `tile` into `buf`: one 16-byte
-// cp.async per lane per chunk (ragged or unaligned chunks: plain loads).
+// named barriers (0 is __syncthreads)
+constexpr int kBarCoders = 1;   // 256 coder threads
+constexpr int kBarFull = 2;     // + b: coders arrive, look-back warp waits (288)
+constexpr int kBarEmpty = 4;    // + b: look-back warp arrives, coders wait (288)
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Issue the loads of coder warp `warp`'s kCPW chunks of `tile` into `buf`: one
+// 16-byte cp.async per lane per chunk (ragged or unaligned chunks: plain loads).
 __device__ __forceinline__ void enc_issue(const EncParams &p, int64_t tile, int warp, int lane,
                                           uint4 (*buf)[32]) {
   const int m = (int)(tile / p.tiles_per_image);
@@ -172,11 +186,15 @@ __device__ __forceinline__ void enc_issue(const EncParams &p, int64_t tile, int 
   cp_async_commit();
 }
 
-// Persistent, software-pipelined single-pass encoder.  Each CTA loops over
-// tiles taken from the ticket counter; the loads of its next tile (cp.async
-// into the other input buffer) are in flight while it codes the current
-// tile, waits for the look-back and stores the records.
-__global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
+// Persistent, warp-specialised single-pass encoder.
+//  Coder warps 0-7: take tiles from the ticket counter, prefetch the next
+//   tile (cp.async into the other input buffer), code the current tile into
+//   stage[b] and hand it to the look-back warp.
+//  Warp 8: publishes the tile aggregate, runs the decoupled look-back, then
+//   stores the table entries and the records at their final offsets and
+//   releases stage[b].  Its look-back latency overlaps the coding of the next
+//   tile.
+__global__ void __launch_bounds__(kEncThreads) rle_encode_kernel(const __grid_constant__ EncParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -184,60 +202,76 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
   const int64_t total = (int64_t)p.count * p.tiles_per_image;
   if (tid == 0) sm.tk[0] = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
   __syncthreads();
-  unsigned long long tk = sm.tk[0];
-  const uint64_t epoch = tk >> 32;
-  int buf = 0;
-  if ((int64_t)(tk & 0xFFFFFFFFull) < total) enc_issue(p, (int64_t)(tk & 0xFFFFFFFFull), warp, lane, sm.in[0][warp]);
+  const uint64_t epoch = sm.tk[0] >> 32;
   const int nch = (int)p.nchunks;
-  while (true) {
-    const int64_t tile = (int64_t)(tk & 0xFFFFFFFFull);
-    if (tile >= total) break;
-    if (tid == 0) sm.tk[buf ^ 1] = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
-    __syncthreads();  // next ticket visible; the other input buffer is free
-    const unsigned long long tkn = sm.tk[buf ^ 1];
-    const int64_t tnext = (int64_t)(tkn & 0xFFFFFFFFull);
-    if (tnext < total) {
-      enc_issue(p, tnext, warp, lane, sm.in[buf ^ 1][warp]);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncwarp();
-    // ---- code this warp's chunks
-    const int m = (int)(tile / p.tiles_per_image);
-    const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
-    const EncImage im = p.img[m];
-    const int c0 = (int)((lt * kWarps + warp) * kCPW);
-    const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
-    int k = c0 % p.S;
-    int run = 0;
-    uint32_t my_ps = 0;
-    int my_pre = 0;
-#pragma unroll 1
-    for (int j = 0; j < kCPW && c0 + j < nch; ++j) {
-      const int L = min(kC, p.w - k * kC);
-      const uint4 v = sm.in[buf][warp][j][lane];
-      uint32_t px[4] = {v.x, v.y, v.z, v.w};
-      const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[warp] + run, sm.toks[warp]);
-      if (lane == j) {
-        my_ps = eo.psizes;
-        my_pre = run;
+  if (warp < kWarps) {
+    // ---------------------------------------------------------------- coders
+    unsigned long long tk = sm.tk[0];
+    if ((int64_t)(tk & 0xFFFFFFFFull) < total)
+      enc_issue(p, (int64_t)(tk & 0xFFFFFFFFull), warp, lane, sm.in[0][warp]);
+    for (int it = 0;; ++it) {
+      const int b = it & 1;
+      const int64_t tile = (int64_t)(tk & 0xFFFFFFFFull);
+      int64_t tnext = total;
+      unsigned long long tkn = 0;
+      if (tile < total) {
+        if (tid == 0) sm.tk[b ^ 1] = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
+        bar_sync(kBarCoders, kWarps * 32);  // next ticket visible; in[b^1] free
+        tkn = sm.tk[b ^ 1];
+        tnext = (int64_t)(tkn & 0xFFFFFFFFull);
+        if (tnext < total) {
+          enc_issue(p, tnext, warp, lane, sm.in[b ^ 1][warp]);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncwarp();
       }
-      run += eo.size;
-      if (++k == p.S) k = 0;
+      if (it >= 2) bar_sync(kBarEmpty + b, kEncThreads);  // stage[b] stored by the look-back warp
+      if (tile >= total) {
+        if (tid == 0) sm.tile_of[b] = -1;  // sentinel
+        bar_arrive(kBarFull + b, kEncThreads);
+        break;
+      }
+      const int m = (int)(tile / p.tiles_per_image);
+      const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
+      const bool swz = (p.img[m].flags & EQC_FLAG_SWIZZLE) != 0;
+      const int c0 = (int)((lt * kWarps + warp) * kCPW);
+      int k = c0 % p.S;
+      int run = 0;
+#pragma unroll 1
+      for (int j = 0; j < kCPW && c0 + j < nch; ++j) {
+        const int L = min(kC, p.w - k * kC);
+        const uint4 v = sm.in[b][warp][j][lane];
+        uint32_t px[4] = {v.x, v.y, v.z, v.w};
+        const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[b][warp] + run, sm.toks[warp]);
+        if (lane == 0) sm.cinfo[b][warp * kCPW + j] = make_uint2((uint32_t)run, eo.psizes);
+        run += eo.size;
+        if (++k == p.S) k = 0;
+      }
+      if (lane == 0) sm.wsize[b][warp] = run;
+      if (tid == 0) sm.tile_of[b] = tile;
+      bar_arrive(kBarFull + b, kEncThreads);
+      tk = tkn;
     }
-    if (lane == 0) sm.wsize[warp] = run;
-    __syncthreads();
-    if (warp == 0) {
-      const int v = lane < kWarps ? sm.wsize[lane] : 0;
+  } else {
+    // -------------------------------------------------- look-back + stores
+    for (int it = 0;; ++it) {
+      const int b = it & 1;
+      bar_sync(kBarFull + b, kEncThreads);
+      const int64_t tile = sm.tile_of[b];
+      if (tile < 0) break;
+      const int m = (int)(tile / p.tiles_per_image);
+      const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
+      const EncImage im = p.img[m];
+      const int v = lane < kWarps ? sm.wsize[b][lane] : 0;
       const int inc = (int)warp_incl_scan_add((uint32_t)v, lane);
       const int agg = __shfl_sync(EQC_FULL, inc, 31);
       const int64_t excl = lookback(ws + kWsHeader, (int64_t)m * p.tiles_per_image, lt, agg, epoch, lane);
-      if (lane < kWarps) sm.woff[lane] = excl + inc - v;
+      const int64_t wexcl = excl + inc - v;  // lane w < 8: payload offset of coder warp w's run
       if (lane == 0 && lt == p.tiles_per_image - 1) {
         // last tile of the image: total payload known -> header + size
         const int64_t payload = excl + agg;
-        const int64_t payload0 = 32 + 8 * p.nchunks;
         uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
         h32[0] = kMagic;
         h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
@@ -248,20 +282,24 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
         h32[5] = 0u;
         h32[6] = (uint32_t)(uint64_t)payload;
         h32[7] = (uint32_t)((uint64_t)payload >> 32);
-        *im.d_size = payload0 + payload;
+        *im.d_size = 32 + 8 * p.nchunks + payload;
       }
-    }
-    __syncthreads();
-    if (run > 0) {
-      const int64_t off = sm.woff[warp];
-      if (lane < kCPW && c0 + lane < nch) {
-        uint2 *te = reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (int64_t)(c0 + lane));
-        *te = make_uint2((uint32_t)(off + my_pre), my_ps);
+      // table entries: one chunk per lane (kWarps * kCPW == 32)
+      const int c = (int)(lt * kTileChunks) + lane;
+      const int64_t woff_l = __shfl_sync(EQC_FULL, wexcl, lane / kCPW);
+      if (c < nch) {
+        const uint2 ci = sm.cinfo[b][lane];
+        *reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (int64_t)c) = make_uint2((uint32_t)(woff_l + ci.x), ci.y);
       }
-      store_record(im.dst + 32 + 8 * p.nchunks + off, sm.stage[warp], run, lane);
+      uint8_t *payload = im.dst + 32 + 8 * p.nchunks;
+#pragma unroll 1
+      for (int w = 0; w < kWarps; ++w) {
+        const int run = __shfl_sync(EQC_FULL, v, w);
+        if (run > 0) store_record(payload + __shfl_sync(EQC_FULL, wexcl, w), sm.stage[b][w], run, lane);
+      }
+      __syncwarp();
+      bar_arrive(kBarEmpty + b, kEncThreads);
     }
-    buf ^= 1;
-    tk = tkn;
   }
   // every CTA holds a ticket >= total here; the last CTA out opens the next
   // epoch (ticket 0) so the workspace is reusable without a memset
@@ -738,13 +776,13 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
         cudaSuccess)
       return EQC_E_CUDA;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rle_encode_kernel, kWarps * 32, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rle_encode_kernel, kEncThreads, smem) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
     max_ctas = per_sm * eqc_num_sms();
   }
   const int grid = (int)std::min<int64_t>(tiles, max_ctas);
-  rle_encode_kernel<<<grid, kWarps * 32, smem, (cudaStream_t)stream>>>(p);
+  rle_encode_kernel<<<grid, kEncThreads, smem, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
 
