@@ -26,15 +26,17 @@ using namespace eqc_rle;
 
 namespace {
 
-constexpr int kWarps = 8;          // warps per CTA
-constexpr int kCPW = 4;            // consecutive chunks per warp (encoder)
-constexpr int kTileChunks = kWarps * kCPW;
-static_assert(kTileChunks == 32, "the look-back warp writes one table entry per lane");
-constexpr int kWarpStage = kCPW * 520 + 16;  // records of one warp, back to back
+constexpr int kWarps = 8;            // warps per CTA
+constexpr int kSTChunksPerWarp = 64; // encoder: consecutive chunks per warp in a super-tile
+constexpr int kSTChunks = kWarps * kSTChunksPerWarp;  // chunks per super-tile (look-back unit)
+constexpr int kRecMax = 4 * (kC + 2);                  // worst-case chunk record bytes (520)
+constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 33280 = 260 x 128 B
+constexpr int kPrefetch = 4;         // chunks in flight per coder warp (cp.async ring)
 constexpr int kMaxBatch = 64;
 
-// workspace layout (uint64): [0] {epoch << 32 | ticket}, [1] CTAs done,
-// [2..3] pad, [4 + t] look-back status of tile t.
+// workspace layout: uint64 [0] {epoch << 32 | ticket}, [1..3] pad,
+// [4 + t] look-back status of super-tile t; then (256-byte aligned) the
+// record scratch: kScratchPerWarp bytes per coder warp of every super-tile.
 constexpr int kWsHeader = 4;
 constexpr uint64_t kFlagAgg = 1ull << 46;
 constexpr uint64_t kFlagIncl = 2ull << 46;
@@ -63,6 +65,7 @@ struct EncImage {
 struct EncParams {
   EncImage img[kMaxBatch];
   uint64_t *ws;
+  uint8_t *scratch;      // record scratch (inside the workspace)
   int64_t pitch;
   int64_t nchunks;       // per image
   int count, w, h, S;    // S = chunks per row
@@ -133,144 +136,131 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-constexpr int kEncThreads = (kWarps + 1) * 32;  // 8 coder warps + 1 look-back/store warp
+// Copy `size` bytes from a 16-byte aligned global source (the warp's record
+// scratch) to an arbitrary global destination: whole 4-byte destination
+// words are funnel-shifted out of aligned source words; the <= 3 head and
+// <= 3 tail bytes are byte copies.
+__device__ __forceinline__ void copy_run(uint8_t *g, const uint8_t *src, int64_t size, int lane) {
+  const uintptr_t ga = (uintptr_t)g;
+  const uintptr_t first_w = (ga + 3) & ~(uintptr_t)3;
+  const uintptr_t end = ga + (uintptr_t)size;
+  const uintptr_t last_w = end & ~(uintptr_t)3;
+  if (first_w >= last_w) {
+    for (int64_t k = lane; k < size; k += 32) g[k] = src[k];
+    return;
+  }
+  const int head = (int)(first_w - ga);
+  const int tail = (int)(end - last_w);
+  if (lane < head) g[lane] = src[lane];
+  if (lane >= 8 && lane < 8 + tail) {
+    const int64_t q = (int64_t)(last_w - ga) + lane - 8;
+    g[q] = src[q];
+  }
+  const int64_t nw = (int64_t)((last_w - first_w) >> 2);
+  const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+  const int sh = head & 3;
+  uint32_t *gw = reinterpret_cast<uint32_t *>(first_w);
+  for (int64_t k = lane; k < nw; k += 32) {
+    const int64_t q = head + 4 * k;
+    const uint32_t lo = s32[q >> 2];
+    const uint32_t hi = sh ? s32[(q >> 2) + 1] : 0u;
+    gw[k] = sh ? __funnelshift_r(lo, hi, 8 * sh) : lo;
+  }
+}
+
+__device__ __forceinline__ void discard_l2(const void *p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 
 struct EncSmem {
-  uint4 in[2][kWarps][kCPW][32];            // double-buffered input tiles (32 KB)
-  uint8_t stage[2][kWarps][kWarpStage];     // double-buffered coded records, back to back per warp
-  uint8_t toks[kWarps][kTokBytes];          // token-start scratch
-  uint2 cinfo[2][kWarps * kCPW];            // per chunk {offset in its warp's run, plane sizes}
-  int wsize[2][kWarps];
-  int64_t tile_of[2];                       // tile coded into stage[b] (-1: no more tiles)
-  unsigned long long tk[2];
+  uint4 in[kWarps][kPrefetch][32];     // per-warp cp.async ring of input chunks (16 KB)
+  uint8_t stage[kWarps][kStageBytes];  // one coded record per warp
+  uint8_t toks[kWarps][kTokBytes];     // token-start scratch
+  uint2 cinfo[kSTChunks];              // per chunk {offset in its warp's run, plane sizes}
+  int wsize[kWarps];
+  int64_t woff[kWarps];
+  unsigned long long tk;
 };
 
-// named barriers (0 is __syncthreads)
-constexpr int kBarCoders = 1;   // 256 coder threads
-constexpr int kBarFull = 2;     // + b: coders arrive, look-back warp waits (288)
-constexpr int kBarEmpty = 4;    // + b: look-back warp arrives, coders wait (288)
-
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// Issue the loads of coder warp `warp`'s kCPW chunks of `tile` into `buf`: one
-// 16-byte cp.async per lane per chunk (ragged or unaligned chunks: plain loads).
-__device__ __forceinline__ void enc_issue(const EncParams &p, int64_t tile, int warp, int lane,
-                                          uint4 (*buf)[32]) {
-  const int m = (int)(tile / p.tiles_per_image);
-  const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
-  const uint32_t *src = p.img[m].src;
-  const int c0 = (int)((lt * kWarps + warp) * kCPW);
-  const int nch = (int)p.nchunks;
-  int y = c0 / p.S, k = c0 - y * p.S;
-#pragma unroll
-  for (int j = 0; j < kCPW; ++j) {
-    if (c0 + j < nch) {
-      const int L = min(kC, p.w - k * kC);
-      const uint32_t *row = src + (int64_t)y * p.pitch + k * kC;
-      if (p.vec && L == kC) {
-        cp_async16(&buf[j][lane], row + 4 * lane);
-      } else {
-        uint32_t px[4];
-        load_chunk(row, L, lane, false, px);
-        buf[j][lane] = make_uint4(px[0], px[1], px[2], px[3]);
-      }
-    }
-    if (++k == p.S) {
-      k = 0;
-      ++y;
-    }
-  }
-  cp_async_commit();
-}
-
-// Persistent, warp-specialised single-pass encoder.
-//  Coder warps 0-7: take tiles from the ticket counter, prefetch the next
-//   tile (cp.async into the other input buffer), code the current tile into
-//   stage[b] and hand it to the look-back warp.
-//  Warp 8: publishes the tile aggregate, runs the decoupled look-back, then
-//   stores the table entries and the records at their final offsets and
-//   releases stage[b].  Its look-back latency overlaps the coding of the next
-//   tile.
-__global__ void __launch_bounds__(kEncThreads) rle_encode_kernel(const __grid_constant__ EncParams p) {
+// Single-pass encoder.  A CTA codes one super-tile of 512 consecutive chunks
+// (CTA order = atomic ticket): each coder warp streams its 64 chunks through
+// a 4-deep cp.async ring, codes each into shared memory and appends the
+// record to its slice of a record scratch (L2-resident); then the CTA's
+// total is prefix-summed across super-tiles by a decoupled look-back (one
+// look-back per 256 KB of input keeps the look-back chain far off the
+// critical path), and every warp copies its run to the final offset, writes
+// its 64 table entries and discards its scratch lines from L2.
+__global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t *ws = p.ws;
-  const int64_t total = (int64_t)p.count * p.tiles_per_image;
-  if (tid == 0) sm.tk[0] = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
+  if (tid == 0) sm.tk = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
   __syncthreads();
-  const uint64_t epoch = sm.tk[0] >> 32;
+  const unsigned long long tk = sm.tk;
+  const uint64_t epoch = tk >> 32;
+  const int64_t tile = (int64_t)(tk & 0xFFFFFFFFull);
+  const int64_t total = (int64_t)p.count * p.tiles_per_image;
+  const int m = (int)(tile / p.tiles_per_image);
+  const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
+  const EncImage im = p.img[m];
   const int nch = (int)p.nchunks;
-  if (warp < kWarps) {
-    // ---------------------------------------------------------------- coders
-    unsigned long long tk = sm.tk[0];
-    if ((int64_t)(tk & 0xFFFFFFFFull) < total)
-      enc_issue(p, (int64_t)(tk & 0xFFFFFFFFull), warp, lane, sm.in[0][warp]);
-    for (int it = 0;; ++it) {
-      const int b = it & 1;
-      const int64_t tile = (int64_t)(tk & 0xFFFFFFFFull);
-      int64_t tnext = total;
-      unsigned long long tkn = 0;
-      if (tile < total) {
-        if (tid == 0) sm.tk[b ^ 1] = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
-        bar_sync(kBarCoders, kWarps * 32);  // next ticket visible; in[b^1] free
-        tkn = sm.tk[b ^ 1];
-        tnext = (int64_t)(tkn & 0xFFFFFFFFull);
-        if (tnext < total) {
-          enc_issue(p, tnext, warp, lane, sm.in[b ^ 1][warp]);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        __syncwarp();
+  const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
+  uint8_t *scr = p.scratch + ((size_t)tile * kWarps + warp) * kScratchPerWarp;
+  const int c0 = (int)(lt * kSTChunks) + warp * kSTChunksPerWarp;
+  const int cnt = max(0, min(kSTChunksPerWarp, nch - c0));
+  // ---- cp.async ring: chunk j lives in slot j % kPrefetch
+  int iy = c0 / p.S, ik = c0 - iy * p.S;  // coordinates of the next chunk to issue
+  auto issue = [&](int j) {
+    if (j < cnt) {
+      const int L = min(kC, p.w - ik * kC);
+      const uint32_t *row = im.src + (int64_t)iy * p.pitch + ik * kC;
+      uint4 *slot = &sm.in[warp][j % kPrefetch][lane];
+      if (p.vec && L == kC) {
+        cp_async16(slot, row + 4 * lane);
+      } else {
+        uint32_t px[4];
+        load_chunk(row, L, lane, false, px);
+        *slot = make_uint4(px[0], px[1], px[2], px[3]);
       }
-      if (it >= 2) bar_sync(kBarEmpty + b, kEncThreads);  // stage[b] stored by the look-back warp
-      if (tile >= total) {
-        if (tid == 0) sm.tile_of[b] = -1;  // sentinel
-        bar_arrive(kBarFull + b, kEncThreads);
-        break;
+      if (++ik == p.S) {
+        ik = 0;
+        ++iy;
       }
-      const int m = (int)(tile / p.tiles_per_image);
-      const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
-      const bool swz = (p.img[m].flags & EQC_FLAG_SWIZZLE) != 0;
-      const int c0 = (int)((lt * kWarps + warp) * kCPW);
-      int k = c0 % p.S;
-      int run = 0;
-#pragma unroll 1
-      for (int j = 0; j < kCPW && c0 + j < nch; ++j) {
-        const int L = min(kC, p.w - k * kC);
-        const uint4 v = sm.in[b][warp][j][lane];
-        uint32_t px[4] = {v.x, v.y, v.z, v.w};
-        const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[b][warp] + run, sm.toks[warp]);
-        if (lane == 0) sm.cinfo[b][warp * kCPW + j] = make_uint2((uint32_t)run, eo.psizes);
-        run += eo.size;
-        if (++k == p.S) k = 0;
-      }
-      if (lane == 0) sm.wsize[b][warp] = run;
-      if (tid == 0) sm.tile_of[b] = tile;
-      bar_arrive(kBarFull + b, kEncThreads);
-      tk = tkn;
     }
-  } else {
-    // -------------------------------------------------- look-back + stores
-    for (int it = 0;; ++it) {
-      const int b = it & 1;
-      bar_sync(kBarFull + b, kEncThreads);
-      const int64_t tile = sm.tile_of[b];
-      if (tile < 0) break;
-      const int m = (int)(tile / p.tiles_per_image);
-      const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
-      const EncImage im = p.img[m];
-      const int v = lane < kWarps ? sm.wsize[b][lane] : 0;
-      const int inc = (int)warp_incl_scan_add((uint32_t)v, lane);
-      const int agg = __shfl_sync(EQC_FULL, inc, 31);
-      const int64_t excl = lookback(ws + kWsHeader, (int64_t)m * p.tiles_per_image, lt, agg, epoch, lane);
-      const int64_t wexcl = excl + inc - v;  // lane w < 8: payload offset of coder warp w's run
-      if (lane == 0 && lt == p.tiles_per_image - 1) {
-        // last tile of the image: total payload known -> header + size
+    cp_async_commit();  // (possibly empty) group per chunk index keeps the counting uniform
+  };
+#pragma unroll
+  for (int j = 0; j < kPrefetch - 1; ++j) issue(j);
+  int k = c0 % p.S;
+  int run = 0;
+#pragma unroll 1
+  for (int j = 0; j < cnt; ++j) {
+    issue(j + kPrefetch - 1);
+    cp_async_wait<kPrefetch - 1>();
+    __syncwarp();
+    const uint4 v = sm.in[warp][j % kPrefetch][lane];
+    __syncwarp();
+    uint32_t px[4] = {v.x, v.y, v.z, v.w};
+    const int L = min(kC, p.w - k * kC);
+    const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[warp], sm.toks[warp]);
+    store_record(scr + run, sm.stage[warp], eo.size, lane);
+    if (lane == 0) sm.cinfo[warp * kSTChunksPerWarp + j] = make_uint2((uint32_t)run, eo.psizes);
+    run += eo.size;
+    if (++k == p.S) k = 0;
+  }
+  cp_async_wait<0>();
+  if (lane == 0) sm.wsize[warp] = run;
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < kWarps ? sm.wsize[lane] : 0;
+    const int inc = (int)warp_incl_scan_add((uint32_t)v, lane);
+    const int agg = __shfl_sync(EQC_FULL, inc, 31);
+    const int64_t excl = lookback(ws + kWsHeader, (int64_t)m * p.tiles_per_image, lt, agg, epoch, lane);
+    if (lane < kWarps) sm.woff[lane] = excl + inc - v;
+    if (lane == 0) {
+      if (lt == p.tiles_per_image - 1) {
+        // last super-tile of the image: total payload known -> header + size
         const int64_t payload = excl + agg;
         uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
         h32[0] = kMagic;
@@ -284,33 +274,22 @@ __global__ void __launch_bounds__(kEncThreads) rle_encode_kernel(const __grid_co
         h32[7] = (uint32_t)((uint64_t)payload >> 32);
         *im.d_size = 32 + 8 * p.nchunks + payload;
       }
-      // table entries: one chunk per lane (kWarps * kCPW == 32)
-      const int c = (int)(lt * kTileChunks) + lane;
-      const int64_t woff_l = __shfl_sync(EQC_FULL, wexcl, lane / kCPW);
-      if (c < nch) {
-        const uint2 ci = sm.cinfo[b][lane];
-        *reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (int64_t)c) = make_uint2((uint32_t)(woff_l + ci.x), ci.y);
+      if (tile == total - 1) {
+        // every ticket is taken and read its epoch: open the next epoch
+        atomicExch(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)((epoch + 1) << 32));
       }
-      uint8_t *payload = im.dst + 32 + 8 * p.nchunks;
-#pragma unroll 1
-      for (int w = 0; w < kWarps; ++w) {
-        const int run = __shfl_sync(EQC_FULL, v, w);
-        if (run > 0) store_record(payload + __shfl_sync(EQC_FULL, wexcl, w), sm.stage[b][w], run, lane);
-      }
-      __syncwarp();
-      bar_arrive(kBarEmpty + b, kEncThreads);
     }
   }
-  // every CTA holds a ticket >= total here; the last CTA out opens the next
-  // epoch (ticket 0) so the workspace is reusable without a memset
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned long long d = atomicAdd(reinterpret_cast<unsigned long long *>(ws + 1), 1ull);
-    if (d == gridDim.x - 1) {
-      atomicExch(reinterpret_cast<unsigned long long *>(ws + 1), 0ull);
-      atomicExch(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)((epoch + 1) << 32));
+  if (cnt > 0) {
+    const int64_t off = sm.woff[warp];
+    for (int j = lane; j < cnt; j += 32) {
+      const uint2 ci = sm.cinfo[warp * kSTChunksPerWarp + j];
+      *reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (int64_t)(c0 + j)) = make_uint2((uint32_t)(off + ci.x), ci.y);
     }
+    copy_run(im.dst + 32 + 8 * p.nchunks + off, scr, run, lane);
+    __syncwarp();
+    for (int l = lane; l * 128 < run; l += 32) discard_l2(scr + 128 * l);
   }
 }
 
@@ -718,7 +697,11 @@ inline int64_t rle_max_size(int w, int h) {
 
 inline int64_t enc_tiles_per_image(int w, int h) {
   const int64_t S = (w + kC - 1) / kC;
-  return (S * h + kTileChunks - 1) / kTileChunks;
+  return (S * h + kSTChunks - 1) / kSTChunks;
+}
+
+inline size_t enc_scratch_offset(int64_t tiles) {
+  return (((size_t)(kWsHeader + tiles) * sizeof(uint64_t)) + 255) & ~(size_t)255;
 }
 
 }  // namespace
@@ -730,7 +713,8 @@ extern "C" int64_t image_rle_max_size(int w, int h) {
 
 extern "C" size_t image_rle_workspace_size_batch(int count, int w, int h) {
   if (count <= 0 || w <= 0 || h <= 0) return 0;
-  return (size_t)(kWsHeader + (int64_t)count * enc_tiles_per_image(w, h)) * sizeof(uint64_t);
+  const int64_t tiles = (int64_t)count * enc_tiles_per_image(w, h);
+  return enc_scratch_offset(tiles) + (size_t)tiles * kWarps * kScratchPerWarp;
 }
 
 extern "C" size_t image_rle_workspace_size(int w, int h) { return image_rle_workspace_size_batch(1, w, h); }
@@ -769,20 +753,16 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   p.vec = vec ? 1 : 0;
   const int64_t tiles = (int64_t)count * p.tiles_per_image;
   if (tiles > 0x7FFFFFFFll || p.nchunks > 0x7FFFFFFFll) return EQC_E_INVALID;
-  static int max_ctas = 0;
+  p.scratch = reinterpret_cast<uint8_t *>(workspace) + enc_scratch_offset(tiles);
+  static bool configured = false;
   const size_t smem = sizeof(EncSmem);
-  if (max_ctas == 0) {
+  if (!configured) {
     if (cudaFuncSetAttribute(rle_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return EQC_E_CUDA;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rle_encode_kernel, kEncThreads, smem) != cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-    max_ctas = per_sm * eqc_num_sms();
+    configured = true;
   }
-  const int grid = (int)std::min<int64_t>(tiles, max_ctas);
-  rle_encode_kernel<<<grid, kEncThreads, smem, (cudaStream_t)stream>>>(p);
+  rle_encode_kernel<<<(unsigned)tiles, kWarps * 32, smem, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
 
