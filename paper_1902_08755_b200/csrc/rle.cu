@@ -75,6 +75,10 @@ struct EncParams {
 
 // Warp-cooperative decoupled look-back; returns the exclusive prefix of tile
 // `lt` of the image whose tile 0 has status index `t0`.  Called by one warp.
+// Each pass inspects kLbPerLane * 32 = 256 predecessors (lane l takes
+// distances 8l+1 .. 8l+8), so a whole 4K image's chain (127 super-tiles) is
+// resolved in one pass once its predecessors have published aggregates.
+constexpr int kLbPerLane = 8;
 __device__ int64_t lookback(uint64_t *status, int64_t t0, int64_t lt, int64_t agg, uint64_t epoch,
                             int lane) {
   const uint64_t tag = (epoch & 0xFFFFull) << 48;
@@ -86,27 +90,44 @@ __device__ int64_t lookback(uint64_t *status, int64_t t0, int64_t lt, int64_t ag
   int64_t excl = 0;
   int64_t pred = lt - 1;
   while (true) {
-    const int64_t idx = pred - lane;
-    uint64_t s;
-    if (idx >= 0) {
-      do {
-        s = poll(status + t0 + idx);
-      } while ((s & 0xFFFF000000000000ull) != tag || (s & kFlagMask) == 0);
-    } else {
-      s = kFlagIncl;  // before tile 0: nothing
+    uint64_t st[kLbPerLane];
+#pragma unroll
+    for (int q = 0; q < kLbPerLane; ++q) {
+      const int64_t idx = pred - (lane * kLbPerLane + q);
+      st[q] = idx >= 0 ? poll(status + t0 + idx) : kFlagIncl;  // before tile 0: nothing
     }
-    const unsigned incl = __ballot_sync(EQC_FULL, (s & kFlagMask) == kFlagIncl);
-    int64_t v = (int64_t)(s & kValMask);
+#pragma unroll
+    for (int q = 0; q < kLbPerLane; ++q) {
+      const int64_t idx = pred - (lane * kLbPerLane + q);
+      while (idx >= 0 && ((st[q] & 0xFFFF000000000000ull) != tag || (st[q] & kFlagMask) == 0)) {
+        __nanosleep(64);
+        st[q] = poll(status + t0 + idx);
+      }
+    }
+    // nearest INCL: first lane holding one, first slot within that lane
+    int qi = kLbPerLane;
+    int64_t part = 0, full = 0;
+#pragma unroll
+    for (int q = kLbPerLane - 1; q >= 0; --q)
+      if ((st[q] & kFlagMask) == kFlagIncl) qi = q;
+#pragma unroll
+    for (int q = 0; q < kLbPerLane; ++q) {
+      const int64_t v = (int64_t)(st[q] & kValMask);
+      full += v;
+      if (q <= qi) part += v;
+    }
+    const unsigned incl = __ballot_sync(EQC_FULL, qi < kLbPerLane);
+    int64_t v;
     if (incl) {
       const int k = __ffs(incl) - 1;
-      if (lane > k) v = 0;
-      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(EQC_FULL, v, d);
-      excl += v;
-      break;
+      v = lane < k ? full : (lane == k ? part : 0);
+    } else {
+      v = full;
     }
     for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(EQC_FULL, v, d);
     excl += v;
-    pred -= 32;
+    if (incl) break;
+    pred -= 32 * kLbPerLane;
   }
   if (lane == 0) publish(status + t0 + lt, status_word(epoch, kFlagIncl, (uint64_t)(excl + agg)));
   return excl;
@@ -383,11 +404,14 @@ __device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8
 #pragma unroll
   for (int j = 0; j < 4; ++j) px[j] = 0;
   const uint8_t *r = stage + sh;
-  bool ok = decode_plane(r, s0, L, lane, 0, px, info);
-  ok = ok && decode_plane(r + s0, s1, L, lane, 1, px, info);
-  ok = ok && decode_plane(r + s0 + s1, s2, L, lane, 2, px, info);
-  ok = ok && decode_plane(r + s0 + s1 + s2, s3, L, lane, 3, px, info);
-  return ok;
+  // one (not unrolled) loop over the planes keeps the decoder body small
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const int sz = (int)((ps >> (8 * q)) & 0xFFu);
+    if (!decode_plane(r, sz, L, lane, q, px, info)) return false;
+    r += sz;
+  }
+  return true;
 }
 
 __device__ __forceinline__ void store_px(uint32_t *row, int L, int lane, bool vec, const uint32_t px[4]) {

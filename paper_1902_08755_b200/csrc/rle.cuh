@@ -26,7 +26,6 @@ constexpr int kLog2C = 7;
 constexpr int kC = 128;
 constexpr int kStageBytes = 544;  // >= 4 planes * (128 + 2) bytes, 16-aligned
 constexpr int kTokBytes = 512;    // token-start scratch: 4 planes * 128
-constexpr int kTokenLoopMax = 24; // decode: token-sequential expansion up to this many tokens
 
 // ---- swizzle (R-C9): out bit 4b + (3 - c) = bit b of channel c ------------
 // Byte reversal maps channel c to c' = 3 - c; the remaining permutation of the
@@ -291,37 +290,49 @@ __device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, 
     }
     return true;
   }
-  if (ntok <= kTokenLoopMax) {
-    // few tokens (typical of mixed background/foreground chunks): walk the
-    // tokens in order; the warp expands each one, 32 positions per step,
-    // into a plane-major byte buffer (the info scratch), then each lane reads
-    // its 4 positions back as one word.
-    uint8_t *pb = reinterpret_cast<uint8_t *>(info);
+  if (ntok <= 32) {
+    // lane t holds token t: start positions and payload indices by one packed
+    // warp scan; each position finds its token as the last start at or before
+    // it (token-index markers + a running max over positions) and reads the
+    // token's {start, payload index, type} with one shuffle.
+    const int c = lane < ntok ? r[1 + lane] : 0;
+    const int len = lane < ntok ? (c & 0x7F) + 1 : 0;
+    const int pay = (c & 0x80) ? 1 : len;
+    const uint32_t packed = (uint32_t)len | ((uint32_t)pay << 16);
+    const uint32_t inc = warp_incl_scan_add(packed, lane);
+    const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
+    if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
+    const uint32_t ex = inc - packed;
+    const int tstart = (int)(ex & 0xFFFFu);
+    const int tpay = 1 + ntok + (int)(ex >> 16);
+    const uint32_t tinfo = (uint32_t)tstart | ((uint32_t)tpay << 8) | ((uint32_t)(c & 0x80) << 24);
+    uint8_t *mk = reinterpret_cast<uint8_t *>(info);
     __syncwarp();
-    int pos = 0, pay = 1 + ntok;
-    for (int t = 0; t < ntok; ++t) {
-      const int c = r[1 + t];
-      const int len = (c & 0x7F) + 1;
-      if (pos + len > L) return false;
-      if (c & 0x80) {
-        if (pay + 1 > size) return false;
-        const uint8_t v = r[pay];
-        for (int k = lane; k < len; k += 32) pb[pos + k] = v;
-        pay += 1;
-      } else {
-        if (pay + len > size) return false;
-        for (int k = lane; k < len; k += 32) pb[pos + k] = r[pay + k];
-        pay += len;
-      }
-      pos += len;
-    }
-    if (pos != L || pay != size) return false;
+    reinterpret_cast<uint32_t *>(mk)[lane] = 0u;
     __syncwarp();
-    const uint32_t w4 = reinterpret_cast<const uint32_t *>(pb)[lane];
+    if (lane < ntok) mk[tstart] = (uint8_t)(lane + 1);
+    __syncwarp();
+    const uint32_t w4 = reinterpret_cast<const uint32_t *>(mk)[lane];
+    // markers grow with position, so the running max is the last marker
+    const int lmax = (int)max(max(w4 & 0xFFu, (w4 >> 8) & 0xFFu), max((w4 >> 16) & 0xFFu, w4 >> 24));
+    int pre = lmax;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (i0 + j < L) out[j] |= ((w4 >> (8 * j)) & 0xFFu) << (8 * p);
-    __syncwarp();
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(EQC_FULL, pre, d);
+      if (lane >= d) pre = max(pre, o);
+    }
+    int run = __shfl_up_sync(EQC_FULL, pre, 1);
+    if (lane == 0) run = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      run = max(run, (int)((w4 >> (8 * j)) & 0xFFu));
+      const uint32_t ti = __shfl_sync(EQC_FULL, tinfo, max(run - 1, 0));
+      const int i = i0 + j;
+      if (i < L) {
+        const int pi = (int)((ti >> 8) & 0xFFFFu) + ((ti >> 31) ? 0 : i - (int)(ti & 0xFFu));
+        out[j] |= (uint32_t)r[pi] << (8 * p);
+      }
+    }
     return true;
   }
   // many tokens: tokens 4*lane .. 4*lane+3 per lane, positions by prefix sums
