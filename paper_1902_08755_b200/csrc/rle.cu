@@ -28,6 +28,7 @@ namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
 constexpr int kSTChunksPerWarp = 64; // encoder: consecutive chunks per warp in a super-tile
+static_assert(kSTChunksPerWarp <= 64, "two table-entry registers per lane");
 constexpr int kSTChunks = kWarps * kSTChunksPerWarp;  // chunks per super-tile (look-back unit)
 constexpr int kRecMax = 4 * (kC + 2);                  // worst-case chunk record bytes (520)
 constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 33280 = 260 x 128 B
@@ -197,7 +198,6 @@ struct EncSmem {
   uint4 in[kWarps][kPrefetch][32];     // per-warp cp.async ring of input chunks (16 KB)
   uint8_t stage[kWarps][kStageBytes];  // one coded record per warp
   uint8_t toks[kWarps][kTokBytes];     // token-start scratch
-  uint2 cinfo[kSTChunks];              // per chunk {offset in its warp's run, plane sizes}
   int wsize[kWarps];
   int64_t woff[kWarps];
   unsigned long long tk;
@@ -230,23 +230,26 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
   uint8_t *scr = p.scratch + ((size_t)tile * kWarps + warp) * kScratchPerWarp;
   const int c0 = (int)(lt * kSTChunks) + warp * kSTChunksPerWarp;
   const int cnt = max(0, min(kSTChunksPerWarp, nch - c0));
-  // ---- cp.async ring: chunk j lives in slot j % kPrefetch
-  int iy = c0 / p.S, ik = c0 - iy * p.S;  // coordinates of the next chunk to issue
+  const int Llast = p.w - (p.S - 1) * kC;  // length of the last chunk of a row
+  // ---- cp.async ring: chunk j lives in slot j % kPrefetch; the issue
+  // pointer walks the rows incrementally
+  int ik = c0 % p.S;
+  const uint32_t *irow = im.src + (int64_t)(c0 / p.S) * p.pitch;
   auto issue = [&](int j) {
     if (j < cnt) {
-      const int L = min(kC, p.w - ik * kC);
-      const uint32_t *row = im.src + (int64_t)iy * p.pitch + ik * kC;
+      const int L = ik == p.S - 1 ? Llast : kC;
+      const uint32_t *ptr = irow + ik * kC;
       uint4 *slot = &sm.in[warp][j % kPrefetch][lane];
       if (p.vec && L == kC) {
-        cp_async16(slot, row + 4 * lane);
+        cp_async16(slot, ptr + 4 * lane);
       } else {
         uint32_t px[4];
-        load_chunk(row, L, lane, false, px);
+        load_chunk(ptr, L, lane, false, px);
         *slot = make_uint4(px[0], px[1], px[2], px[3]);
       }
       if (++ik == p.S) {
         ik = 0;
-        ++iy;
+        irow += p.pitch;
       }
     }
     cp_async_commit();  // (possibly empty) group per chunk index keeps the counting uniform
@@ -255,6 +258,7 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
   for (int j = 0; j < kPrefetch - 1; ++j) issue(j);
   int k = c0 % p.S;
   int run = 0;
+  uint2 ent0 = make_uint2(0, 0), ent1 = make_uint2(0, 0);  // {run offset, plane sizes} of chunks lane, lane+32
 #pragma unroll 1
   for (int j = 0; j < cnt; ++j) {
     issue(j + kPrefetch - 1);
@@ -263,11 +267,26 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
     const uint4 v = sm.in[warp][j % kPrefetch][lane];
     __syncwarp();
     uint32_t px[4] = {v.x, v.y, v.z, v.w};
-    const int L = min(kC, p.w - k * kC);
-    const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[warp], sm.toks[warp]);
-    store_record(scr + run, sm.stage[warp], eo.size, lane);
-    if (lane == 0) sm.cinfo[warp * kSTChunksPerWarp + j] = make_uint2((uint32_t)run, eo.psizes);
-    run += eo.size;
+    const int L = k == p.S - 1 ? Llast : kC;
+    uint32_t v0, psz;
+    int size;
+    if (chunk_is_constant(px, L, lane, v0)) {
+      emit_constant_record(scr + run, swz ? swizzle(v0) : v0, L, lane);
+      psz = 0x03030303u;
+      size = 12;
+    } else {
+      const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[warp], sm.toks[warp]);
+      store_record(scr + run, sm.stage[warp], eo.size, lane);
+      psz = eo.psizes;
+      size = eo.size;
+    }
+    if (lane == (j & 31)) {
+      if (j < 32)
+        ent0 = make_uint2((uint32_t)run, psz);
+      else
+        ent1 = make_uint2((uint32_t)run, psz);
+    }
+    run += size;
     if (++k == p.S) k = 0;
   }
   cp_async_wait<0>();
@@ -304,10 +323,9 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
   __syncthreads();
   if (cnt > 0) {
     const int64_t off = sm.woff[warp];
-    for (int j = lane; j < cnt; j += 32) {
-      const uint2 ci = sm.cinfo[warp * kSTChunksPerWarp + j];
-      *reinterpret_cast<uint2 *>(im.dst + 32 + 8 * (int64_t)(c0 + j)) = make_uint2((uint32_t)(off + ci.x), ci.y);
-    }
+    uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
+    if (lane < cnt) table[lane] = make_uint2((uint32_t)(off + ent0.x), ent0.y);
+    if (lane + 32 < cnt) table[lane + 32] = make_uint2((uint32_t)(off + ent1.x), ent1.y);
     copy_run(im.dst + 32 + 8 * p.nchunks + off, scr, run, lane);
     __syncwarp();
     for (int l = lane; l * 128 < run; l += 32) discard_l2(scr + 128 * l);

@@ -75,28 +75,11 @@ __device__ __forceinline__ int sel4(int i, int a, int b, int c, int d) {
 // Plane classes (warp-uniform): CONSTANT (one REPEAT of L, 3 bytes),
 // LITERAL-ONLY (no run of >= 3: one LITERAL, L + 2 bytes, the bytes in
 // order), GENERAL (scatter of token starts and payload bytes by prefix
-// counts).  A chunk whose 128 pixels are all equal is detected before the
-// swizzle (a bijection) and emitted as four CONSTANT planes.
+// counts).  Chunks whose pixels are all equal never get here: the caller
+// emits them directly (chunk_is_constant / emit_constant_record).
 __device__ __forceinline__ EncodeOut encode_chunk(uint32_t px[4], int L, int lane, bool swz, uint8_t *st,
                                                   uint8_t *tp) {
   const int i0 = 4 * lane;
-  // ---- whole chunk one value (background, flat regions)
-  {
-    const uint32_t v0 = __shfl_sync(EQC_FULL, px[0], 0);
-    bool same = true;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) same = same && (i0 + j >= L || px[j] == v0);
-    if (__all_sync(EQC_FULL, same) && L >= 3) {
-      const uint32_t v = swz ? swizzle(v0) : v0;
-      if (lane < 4) {
-        st[3 * lane + 0] = 1;
-        st[3 * lane + 1] = (uint8_t)(0x80 | (L - 1));
-        st[3 * lane + 2] = (uint8_t)bytep(v, lane);
-      }
-      __syncwarp();
-      return EncodeOut{12, 0x03030303u};
-    }
-  }
   if (swz) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) px[j] = swizzle(px[j]);
@@ -232,6 +215,27 @@ __device__ __forceinline__ EncodeOut encode_chunk(uint32_t px[4], int L, int lan
   const uint32_t ps = (uint32_t)size[0] | ((uint32_t)size[1] << 8) | ((uint32_t)size[2] << 16) |
                       ((uint32_t)size[3] << 24);
   return EncodeOut{b4, ps};
+}
+
+// Whole-chunk constancy test on the RAW pixels (the swizzle is a bijection,
+// so this equals constancy after it); v0 receives the value.
+__device__ __forceinline__ bool chunk_is_constant(const uint32_t px[4], int L, int lane, uint32_t &v0) {
+  const int i0 = 4 * lane;
+  v0 = __shfl_sync(EQC_FULL, px[0], 0);
+  bool same = true;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) same = same && (i0 + j >= L || px[j] == v0);
+  return __all_sync(EQC_FULL, same) && L >= 3;
+}
+
+// The 12-byte record of a constant chunk (four planes [01][0x80|(L-1)][v_p]),
+// written straight to global memory by lanes 0..11 (one byte each).
+__device__ __forceinline__ void emit_constant_record(uint8_t *g, uint32_t v, int L, int lane) {
+  if (lane < 12) {
+    const int p = lane / 3, q = lane - 3 * p;
+    const uint32_t b = q == 0 ? 1u : q == 1 ? (0x80u | (uint32_t)(L - 1)) : bytep(v, p);
+    g[lane] = (uint8_t)b;
+  }
 }
 
 // Copy the warp's staged record (st[0..size)) to global bytes [g, g+size).
