@@ -9,15 +9,15 @@
 //  compositor_depth_rle         stages (5) + (7) fused: decode in registers,
 //                               depth-composite, one HBM write
 //
-// Encoder: single pass over the input.  A CTA owns a tile of 8 warps x 8
-// consecutive chunks; each warp codes its chunks into shared memory back to
-// back, the warp runs are prefix-summed across the CTA and across CTAs by a
-// decoupled look-back (tile order = an atomic ticket), then each warp stores
-// its contiguous run of records at the final offset.  The look-back state is
-// a caller-owned workspace the kernel leaves reusable: the ticket word holds
-// {epoch:32 | ticket:32}, status words carry a 16-bit epoch tag, and the CTA
-// holding the last ticket bumps the epoch and zeroes the ticket after its
-// look-back, so no memset is needed between calls.
+// Encoder: two kernels, no inter-CTA waiting.  rle_encode_kernel codes one
+// super-tile of 512 consecutive chunks per CTA: each warp streams its 64
+// chunks through a 4-deep cp.async ring, codes each in registers/shared
+// memory and appends the record to its slice of an (L2-resident) record
+// scratch, and writes its table entries relative to the super-tile.
+// rle_compact_kernel then gives every super-tile its payload offset (the sum
+// of the preceding super-tiles' sizes of the same image -- at most a few
+// hundred values, summed directly, no look-back chain), moves the records to
+// their final place, rebases the table entries and writes the header.
 #include <algorithm>
 
 #include "rle.cuh"
@@ -35,26 +35,11 @@ constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 33280 = 260 x 12
 constexpr int kPrefetch = 4;         // chunks in flight per coder warp (cp.async ring)
 constexpr int kMaxBatch = 64;
 
-// workspace layout: uint64 [0] {epoch << 32 | ticket}, [1..3] pad,
-// [4 + t] look-back status of super-tile t; then (256-byte aligned) the
-// record scratch: kScratchPerWarp bytes per coder warp of every super-tile.
-constexpr int kWsHeader = 4;
-constexpr uint64_t kFlagAgg = 1ull << 46;
-constexpr uint64_t kFlagIncl = 2ull << 46;
-constexpr uint64_t kFlagMask = 3ull << 46;
-constexpr uint64_t kValMask = (1ull << 46) - 1;
-
-__device__ __forceinline__ uint64_t status_word(uint64_t epoch, uint64_t flag, uint64_t v) {
-  return ((epoch & 0xFFFFull) << 48) | flag | (v & kValMask);
-}
-__device__ __forceinline__ void publish(uint64_t *p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t poll(const uint64_t *p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
+// workspace layout: tile_info[count * tiles_per_image][16] int32 (super-tile
+// total, then the 8 warp-run offsets inside the super-tile), then (256-byte
+// aligned) the record scratch: kScratchPerWarp bytes per coder warp of every
+// super-tile.  No state survives between calls (no zeroing needed).
+constexpr int kTileInfo = 16;
 
 struct EncImage {
   const uint32_t *src;
@@ -65,7 +50,7 @@ struct EncImage {
 
 struct EncParams {
   EncImage img[kMaxBatch];
-  uint64_t *ws;
+  int32_t *tile_info;    // inside the workspace
   uint8_t *scratch;      // record scratch (inside the workspace)
   int64_t pitch;
   int64_t nchunks;       // per image
@@ -73,66 +58,6 @@ struct EncParams {
   int tiles_per_image;
   int vec;               // 128-bit loads allowed
 };
-
-// Warp-cooperative decoupled look-back; returns the exclusive prefix of tile
-// `lt` of the image whose tile 0 has status index `t0`.  Called by one warp.
-// Each pass inspects kLbPerLane * 32 = 256 predecessors (lane l takes
-// distances 8l+1 .. 8l+8), so a whole 4K image's chain (127 super-tiles) is
-// resolved in one pass once its predecessors have published aggregates.
-constexpr int kLbPerLane = 8;
-__device__ int64_t lookback(uint64_t *status, int64_t t0, int64_t lt, int64_t agg, uint64_t epoch,
-                            int lane) {
-  const uint64_t tag = (epoch & 0xFFFFull) << 48;
-  if (lt == 0) {
-    if (lane == 0) publish(status + t0, status_word(epoch, kFlagIncl, (uint64_t)agg));
-    return 0;
-  }
-  if (lane == 0) publish(status + t0 + lt, status_word(epoch, kFlagAgg, (uint64_t)agg));
-  int64_t excl = 0;
-  int64_t pred = lt - 1;
-  while (true) {
-    uint64_t st[kLbPerLane];
-#pragma unroll
-    for (int q = 0; q < kLbPerLane; ++q) {
-      const int64_t idx = pred - (lane * kLbPerLane + q);
-      st[q] = idx >= 0 ? poll(status + t0 + idx) : kFlagIncl;  // before tile 0: nothing
-    }
-#pragma unroll
-    for (int q = 0; q < kLbPerLane; ++q) {
-      const int64_t idx = pred - (lane * kLbPerLane + q);
-      while (idx >= 0 && ((st[q] & 0xFFFF000000000000ull) != tag || (st[q] & kFlagMask) == 0)) {
-        __nanosleep(64);
-        st[q] = poll(status + t0 + idx);
-      }
-    }
-    // nearest INCL: first lane holding one, first slot within that lane
-    int qi = kLbPerLane;
-    int64_t part = 0, full = 0;
-#pragma unroll
-    for (int q = kLbPerLane - 1; q >= 0; --q)
-      if ((st[q] & kFlagMask) == kFlagIncl) qi = q;
-#pragma unroll
-    for (int q = 0; q < kLbPerLane; ++q) {
-      const int64_t v = (int64_t)(st[q] & kValMask);
-      full += v;
-      if (q <= qi) part += v;
-    }
-    const unsigned incl = __ballot_sync(EQC_FULL, qi < kLbPerLane);
-    int64_t v;
-    if (incl) {
-      const int k = __ffs(incl) - 1;
-      v = lane < k ? full : (lane == k ? part : 0);
-    } else {
-      v = full;
-    }
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(EQC_FULL, v, d);
-    excl += v;
-    if (incl) break;
-    pred -= 32 * kLbPerLane;
-  }
-  if (lane == 0) publish(status + t0 + lt, status_word(epoch, kFlagIncl, (uint64_t)(excl + agg)));
-  return excl;
-}
 
 __device__ __forceinline__ void load_chunk(const uint32_t *row, int L, int lane, bool vec, uint32_t px[4]) {
   const int i0 = 4 * lane;
@@ -215,13 +140,7 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t *ws = p.ws;
-  if (tid == 0) sm.tk = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 1ull);
-  __syncthreads();
-  const unsigned long long tk = sm.tk;
-  const uint64_t epoch = tk >> 32;
-  const int64_t tile = (int64_t)(tk & 0xFFFFFFFFull);
-  const int64_t total = (int64_t)p.count * p.tiles_per_image;
+  const int64_t tile = blockIdx.x;
   const int m = (int)(tile / p.tiles_per_image);
   const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
   const EncImage im = p.img[m];
@@ -292,16 +211,53 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
   cp_async_wait<0>();
   if (lane == 0) sm.wsize[warp] = run;
   __syncthreads();
+  // offsets of the warp runs inside the super-tile
+  const int wv = lane < kWarps ? sm.wsize[lane] : 0;
+  const int winc = (int)warp_incl_scan_add((uint32_t)wv, lane);
+  const int wexcl = __shfl_sync(EQC_FULL, winc - wv, warp);
+  const int ttot = __shfl_sync(EQC_FULL, winc, 31);
   if (warp == 0) {
-    const int v = lane < kWarps ? sm.wsize[lane] : 0;
-    const int inc = (int)warp_incl_scan_add((uint32_t)v, lane);
-    const int agg = __shfl_sync(EQC_FULL, inc, 31);
-    const int64_t excl = lookback(ws + kWsHeader, (int64_t)m * p.tiles_per_image, lt, agg, epoch, lane);
-    if (lane < kWarps) sm.woff[lane] = excl + inc - v;
+    int32_t *ti = p.tile_info + tile * kTileInfo;
+    if (lane == 0) ti[0] = ttot;
+    if (lane < kWarps) ti[1 + lane] = winc - wv;
+  }
+  if (cnt > 0) {
+    // table entries relative to the super-tile (rebased by the compaction)
+    uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
+    if (lane < cnt) table[lane] = make_uint2((uint32_t)(wexcl + ent0.x), ent0.y);
+    if (lane + 32 < cnt) table[lane + 32] = make_uint2((uint32_t)(wexcl + ent1.x), ent1.y);
+  }
+}
+
+struct CompactParams {
+  EncImage img[kMaxBatch];
+  const int32_t *tile_info;
+  const uint8_t *scratch;
+  int64_t nchunks;
+  int w, h, tiles_per_image;
+};
+
+// One CTA per super-tile: payload offset = sum of the preceding super-tiles'
+// totals of the same image (summed directly by warp 0), then every warp
+// moves its run from the scratch to the stream, rebases its 64 table entries
+// and discards its scratch lines from L2; the last super-tile of an image
+// writes the header and the stream size.
+__global__ void __launch_bounds__(kWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
+  __shared__ int64_t s_off;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tile = blockIdx.x;
+  const int m = (int)(tile / p.tiles_per_image);
+  const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
+  const int64_t t0 = (int64_t)m * p.tiles_per_image;
+  const EncImage im = p.img[m];
+  if (warp == 0) {
+    int64_t acc = 0;
+    for (int64_t q = lane; q < lt; q += 32) acc += __ldg(p.tile_info + (t0 + q) * kTileInfo);
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(EQC_FULL, acc, d);
     if (lane == 0) {
+      s_off = acc;
       if (lt == p.tiles_per_image - 1) {
-        // last super-tile of the image: total payload known -> header + size
-        const int64_t payload = excl + agg;
+        const int64_t payload = acc + __ldg(p.tile_info + tile * kTileInfo);
         uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
         h32[0] = kMagic;
         h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
@@ -314,21 +270,29 @@ __global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_co
         h32[7] = (uint32_t)((uint64_t)payload >> 32);
         *im.d_size = 32 + 8 * p.nchunks + payload;
       }
-      if (tile == total - 1) {
-        // every ticket is taken and read its epoch: open the next epoch
-        atomicExch(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)((epoch + 1) << 32));
-      }
     }
   }
   __syncthreads();
-  if (cnt > 0) {
-    const int64_t off = sm.woff[warp];
-    uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
-    if (lane < cnt) table[lane] = make_uint2((uint32_t)(off + ent0.x), ent0.y);
-    if (lane + 32 < cnt) table[lane + 32] = make_uint2((uint32_t)(off + ent1.x), ent1.y);
-    copy_run(im.dst + 32 + 8 * p.nchunks + off, scr, run, lane);
+  const int64_t base = s_off;
+  const int nch = (int)p.nchunks;
+  const int c0 = (int)(lt * kSTChunks) + warp * kSTChunksPerWarp;
+  const int cnt = max(0, min(kSTChunksPerWarp, nch - c0));
+  if (cnt <= 0) return;
+  const int32_t *ti = p.tile_info + tile * kTileInfo;
+  const int64_t woff = __ldg(ti + 1 + warp);
+  const int64_t wend = warp + 1 < kWarps ? __ldg(ti + 2 + warp) : __ldg(ti);
+  const int64_t run = wend - woff;
+  const uint8_t *scr = p.scratch + ((size_t)tile * kWarps + warp) * kScratchPerWarp;
+  uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
+  for (int j = lane; j < cnt; j += 32) {
+    uint2 e = table[j];
+    e.x = (uint32_t)(base + e.x);
+    table[j] = e;
+  }
+  if (run > 0) {
+    copy_run(im.dst + 32 + 8 * p.nchunks + base + woff, scr, run, lane);
     __syncwarp();
-    for (int l = lane; l * 128 < run; l += 32) discard_l2(scr + 128 * l);
+    for (int l = lane; (int64_t)l * 128 < run; l += 32) discard_l2(scr + 128 * l);
   }
 }
 
@@ -743,7 +707,7 @@ inline int64_t enc_tiles_per_image(int w, int h) {
 }
 
 inline size_t enc_scratch_offset(int64_t tiles) {
-  return (((size_t)(kWsHeader + tiles) * sizeof(uint64_t)) + 255) & ~(size_t)255;
+  return (((size_t)tiles * kTileInfo * sizeof(int32_t)) + 255) & ~(size_t)255;
 }
 
 }  // namespace
@@ -784,7 +748,6 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
     vec = vec && aligned(src[i], 16);
     p.img[i] = EncImage{src[i], dst[i], d_sizes + i, kind[i], flags[i]};
   }
-  p.ws = reinterpret_cast<uint64_t *>(workspace);
   p.pitch = pitch;
   p.S = (w + kC - 1) / kC;
   p.nchunks = (int64_t)p.S * h;
@@ -795,6 +758,7 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   p.vec = vec ? 1 : 0;
   const int64_t tiles = (int64_t)count * p.tiles_per_image;
   if (tiles > 0x7FFFFFFFll || p.nchunks > 0x7FFFFFFFll) return EQC_E_INVALID;
+  p.tile_info = reinterpret_cast<int32_t *>(workspace);
   p.scratch = reinterpret_cast<uint8_t *>(workspace) + enc_scratch_offset(tiles);
   static bool configured = false;
   const size_t smem = sizeof(EncSmem);
@@ -804,7 +768,17 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
       return EQC_E_CUDA;
     configured = true;
   }
-  rle_encode_kernel<<<(unsigned)tiles, kWarps * 32, smem, (cudaStream_t)stream>>>(p);
+  cudaStream_t st = (cudaStream_t)stream;
+  rle_encode_kernel<<<(unsigned)tiles, kWarps * 32, smem, st>>>(p);
+  CompactParams c;
+  for (int i = 0; i < count; ++i) c.img[i] = p.img[i];
+  c.tile_info = p.tile_info;
+  c.scratch = p.scratch;
+  c.nchunks = p.nchunks;
+  c.w = w;
+  c.h = h;
+  c.tiles_per_image = p.tiles_per_image;
+  rle_compact_kernel<<<(unsigned)tiles, kWarps * 32, 0, st>>>(c);
   return eqc_launch_status();
 }
 
