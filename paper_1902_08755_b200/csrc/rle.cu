@@ -104,13 +104,24 @@ __device__ __forceinline__ void copy_run(uint8_t *g, const uint8_t *src, int64_t
     g[q] = src[q];
   }
   const int64_t nw = (int64_t)((last_w - first_w) >> 2);
-  const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+  const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src) + (head >> 2);
   const int sh = head & 3;
   uint32_t *gw = reinterpret_cast<uint32_t *>(first_w);
-  for (int64_t k = lane; k < nw; k += 32) {
-    const int64_t q = head + 4 * k;
-    const uint32_t lo = s32[q >> 2];
-    const uint32_t hi = sh ? s32[(q >> 2) + 1] : 0u;
+  // 4 independent loads in flight per lane per step
+  int64_t k = lane;
+  for (; k + 96 < nw; k += 128) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      lo[u] = __ldg(s32 + k + 32 * u);
+      hi[u] = sh ? __ldg(s32 + k + 32 * u + 1) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) gw[k + 32 * u] = sh ? __funnelshift_r(lo[u], hi[u], 8 * sh) : lo[u];
+  }
+  for (; k < nw; k += 32) {
+    const uint32_t lo = __ldg(s32 + k);
+    const uint32_t hi = sh ? __ldg(s32 + k + 1) : 0u;
     gw[k] = sh ? __funnelshift_r(lo, hi, 8 * sh) : lo;
   }
 }
@@ -540,6 +551,7 @@ struct FusedParams {
 
 constexpr int kMaxStreams = 2 * EQC_MAX_SOURCES;
 constexpr int kPosPerWarp = 8;  // chunk positions per warp (4 lanes each in phase A)
+constexpr int kFWarps = 2;      // small CTAs: the per-warp work is uneven (mixed vs background chunks)
 
 // Warp per 8 consecutive chunk positions.
 //  Phase A (4 lanes per position, lane sub = lane & 3 takes sources
@@ -551,9 +563,9 @@ constexpr int kPosPerWarp = 8;  // chunk positions per warp (4 lanes each in pha
 //   lane per output; every other position is decoded warp-cooperatively,
 //   depth first: a source's colour chunk is decoded only if the source wins
 //   at least one pixel of the chunk.
-__global__ void __launch_bounds__(kWarps * 32) depth_rle_kernel(const __grid_constant__ FusedParams p) {
-  __shared__ __align__(16) uint8_t stage[kWarps][kStageBytes];
-  __shared__ __align__(16) uint16_t info[kWarps][kC];
+__global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_constant__ FusedParams p) {
+  __shared__ __align__(16) uint8_t stage[kFWarps][kStageBytes];
+  __shared__ __align__(16) uint16_t info[kFWarps][kC];
   __shared__ int64_t s_pb[kMaxStreams];
   __shared__ uint8_t s_flags[kMaxStreams];
   __shared__ int s_bad;
@@ -575,7 +587,7 @@ __global__ void __launch_bounds__(kWarps * 32) depth_rle_kernel(const __grid_con
   }
   const int nch = p.S * p.h;
   const int64_t payload0 = 32 + 8 * (int64_t)nch;
-  const int cb = (blockIdx.x * kWarps + warp) * kPosPerWarp;
+  const int cb = (blockIdx.x * kFWarps + warp) * kPosPerWarp;
   if (cb >= nch) return;
   const int pos = lane >> 2, sub = lane & 3;
   const int c = cb + pos;
@@ -851,8 +863,8 @@ extern "C" int compositor_depth_rle(int n, const uint8_t *const *color_rle, cons
   p.h = h;
   p.S = (w + kC - 1) / kC;
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
-  const int64_t grid = ((int64_t)p.S * h + kWarps * kPosPerWarp - 1) / (kWarps * kPosPerWarp);
+  const int64_t grid = ((int64_t)p.S * h + kFWarps * kPosPerWarp - 1) / (kFWarps * kPosPerWarp);
   if (grid > 0x7FFFFFFFll || (int64_t)p.S * h > 0x7FFFFFFFll) return EQC_E_INVALID;
-  depth_rle_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
+  depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }

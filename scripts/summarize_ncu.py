@@ -1,0 +1,130 @@
+"""Summarise ncu captures into profiles/ (run here, on the CPU box).
+
+    python scripts/summarize_ncu.py TAG [--rep gpurun_out/prof_TAG.ncu-rep]
+                                        [--launches gpurun_out/launches_TAG.csv]
+
+Writes profiles/ncu_<TAG>.md (per-kernel key metrics of the --set full
+capture + per-launch times/DRAM bytes of the launch list and each kernel's
+share) and profiles/traffic.json (dram read+write bytes per launch of each
+kernel, read by bench.py for roofline.traffic).
+"""
+import argparse
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "Executed Ipc Active",
+        "Issue Slots Busy", "No Eligible", "Achieved Occupancy", "Theoretical Occupancy", "Registers Per Thread",
+        "Block Limit Registers", "Block Limit Shared Mem", "Executed Instructions", "L2 Hit Rate",
+        "Warp Cycles Per Issued Instruction"]
+RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "smsp__inst_executed.sum",
+       "sm__warps_active.avg.pct_of_peak_sustained_active"]
+STALLS = "smsp__pcsamp_warps_issue_stalled_"
+
+
+def short(name):
+    return name.split("(")[0].replace("<unnamed>::", "").replace("void ", "")
+
+
+def ncu_csv(args):
+    out = subprocess.run(["ncu", "-i", *args, "--csv"], capture_output=True, text=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("tag")
+    ap.add_argument("--rep")
+    ap.add_argument("--launches")
+    a = ap.parse_args()
+    rep = a.rep or os.path.join(ROOT, "gpurun_out", f"prof_{a.tag}.ncu-rep")
+    launches = a.launches or os.path.join(ROOT, "gpurun_out", f"launches_{a.tag}.csv")
+    lines = [f"# ncu summary `{a.tag}`", "",
+             "Captured under gpurun on one B200 with `--clock-control none` (scripts/gpu_prof.sh running "
+             "scripts/prof_step.py: 8 x 3840x2160 sources, encode batch -> fused decode+composite, plain "
+             "decode batch, plain depth composite, 16-brick blend). Per-launch times under ncu are cold-cache "
+             "and serialised: compare SHARES, not absolutes.", ""]
+    traffic = {}
+    if os.path.exists(launches):
+        rows = list(csv.reader(open(launches)))
+        hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+        hdr = rows[hi]
+        ki, mi, vi, idi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("ID")
+        per = collections.OrderedDict()
+        for r in rows[hi + 1:]:
+            per.setdefault((int(r[idi]), short(r[ki])), {})[r[mi]] = float(r[vi].replace(",", ""))
+        lines += ["## Launch list (gpu__time_duration, dram bytes)", "",
+                  "| ID | kernel | time us | DRAM read MB | DRAM write MB |", "|---|---|---|---|---|"]
+        tot = collections.defaultdict(list)
+        for (i, k), m in per.items():
+            t = m.get("gpu__time_duration.sum", 0) / 1e3
+            rd = m.get("dram__bytes_read.sum", 0) / 1e6
+            wr = m.get("dram__bytes_write.sum", 0) / 1e6
+            lines.append(f"| {i} | {k} | {t:.1f} | {rd:.1f} | {wr:.1f} |")
+            tot[k].append((t, rd + wr))
+        lines += ["", "Per kernel (mean over launches):", "", "| kernel | launches | mean us | DRAM MB/launch |",
+                  "|---|---|---|---|"]
+        for k, v in tot.items():
+            mt = sum(x[0] for x in v) / len(v)
+            mb = sum(x[1] for x in v) / len(v)
+            traffic[k] = int(mb * 1e6)
+            lines.append(f"| {k} | {len(v)} | {mt:.1f} | {mb:.1f} |")
+        lines.append("")
+    if os.path.exists(rep):
+        rows = ncu_csv([rep, "--page", "details"])
+        hdr = rows[0]
+        ki, mi, vi, ui, idi = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit", "ID"))
+        per = collections.OrderedDict()
+        for r in rows[1:]:
+            if r[mi] in KEYS:
+                per.setdefault((r[idi], short(r[ki])), {})[r[mi]] = f"{r[vi]} {r[ui]}".strip()
+        raw = ncu_csv([rep, "--page", "raw"])
+        rh = raw[0]
+        rki = rh.index("Kernel Name")
+        stalls = {}
+        for r in raw[2:]:
+            d = {}
+            for h, v in zip(rh, r):
+                if h.startswith(STALLS) and not h.endswith("not_issued"):
+                    try:
+                        d[h[len(STALLS):]] = float(v.replace(",", ""))
+                    except ValueError:
+                        pass
+            top = sorted(d.items(), key=lambda x: -x[1])[:5]
+            stalls.setdefault(short(r[rki]), []).append(", ".join(f"{k} {int(v)}" for k, v in top))
+        lines += ["## `--set full` capture (selected metrics)", ""]
+        seen = collections.Counter()
+        for (i, k), m in per.items():
+            seen[k] += 1
+            lines.append(f"### {k} (ID {i})")
+            for key in KEYS:
+                if key in m:
+                    lines.append(f"- {key}: {m[key]}")
+            st = stalls.get(k, [])
+            if st:
+                lines.append(f"- top stall samples: {st[min(seen[k], len(st)) - 1]}")
+            lines.append("")
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", f"ncu_{a.tag}.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    if traffic:
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        old = json.load(open(tpath)) if os.path.exists(tpath) else {}
+        # bench names its kernels by the C-ABI call; map the encode pair and the fused kernel
+        m = {"rle_encode_kernel": "image_compress_rle_batch", "depth_rle_kernel": "compositor_depth_rle"}
+        for k, v in traffic.items():
+            old[m.get(k, k)] = v
+        if "rle_compact_kernel" in traffic and "rle_encode_kernel" in traffic:
+            old["image_compress_rle_batch"] = traffic["rle_encode_kernel"] + traffic["rle_compact_kernel"]
+        old["_source"] = f"profiles/ncu_{a.tag}.md (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+        json.dump(old, open(tpath, "w"), indent=1)
+    print("\n".join(lines[:60]))
+
+
+if __name__ == "__main__":
+    sys.exit(main())
