@@ -133,6 +133,8 @@ def make_inputs(seed, n, w, h):
 def launches_per_compose(n, exchange):
     """Our kernels per compose_direct_send call: local pre-composite + band
     composite (+ n-1 band encodes and one decode batch with RLE)."""
+    if exchange == "raw":  # pre-composite, 2 flag barriers, fused pull+composite
+        return 4
     return 2 + ((n - 1) + 1 if exchange == "rle" else 0)
 
 
@@ -170,7 +172,7 @@ def run_eqc(args):
     if world > 1:
         comm = eqc.Comm.from_torch_distributed()
         final = torch.empty((H, W), dtype=torch.int32, device=dev) if rank == 0 else None
-    xflags = eqc.FLAG_RLE if args.exchange == "rle" else 0
+    xflags = {"raw": 0, "rle": eqc.FLAG_RLE, "nccl": eqc.FLAG_NCCL}[args.exchange]
 
     ev_enc = []  # per-launch kernel timing on the launching stream
 
@@ -396,8 +398,9 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="rows of the frame in one CPU-oracle sample (0 = calibrate to a time budget)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="raw", choices=["raw", "rle"],
-                    help="direct-send band transport for N > 1 (raw bands or RLE streams)")
+    ap.add_argument("--exchange", default="raw", choices=["raw", "rle", "nccl"],
+                    help="direct-send band transport for N > 1: raw = NVLink peer-memory pull fused with the "
+                         "band composite, nccl = raw bands over NCCL send/recv, rle = RLE streams over NCCL")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "eqc":
         log("note: warmup raised to 3 (timing rule)")

@@ -32,6 +32,7 @@ typedef struct eqc_comm eqc_comm;
 #define EQC_UNIQUE_ID_BYTES 128
 #define EQC_OP_DEPTH 0      /* depth-sorted compositing (compositor_depth semantics) */
 #define EQC_FLAG_RLE 1      /* ship bands as RLE-BP streams (colour swizzled + depth) */
+#define EQC_FLAG_NCCL 2     /* direct send: force NCCL grouped send/recv instead of the NVLink peer-memory path */
 
 /* NCCL unique id of a new clique (rank 0 calls this and broadcasts the bytes). */
 EQC_API int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]);
@@ -78,7 +79,14 @@ EQC_API int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_ro
  *   (5) ranks send their composited colour band to dest_rank, which writes
  *       the final image to out_color [h][out_pitch] (ignored on other ranks).
  * Result: bit-identical to compositor_depth over all nranks*n_local sources.
- * With EQC_FLAG_RLE the call synchronises `stream` once (message sizes).
+ * Transport: without EQC_FLAG_RLE (raw bands) and when every rank can map
+ * every peer's memory (CUDA IPC over NVLink, agreed collectively at the first
+ * call), steps (2)-(4) are ONE kernel per rank: the band composite reads band
+ * j of every peer's partial frame directly over NVLink and stores its result
+ * directly into the destination's frame (two peer-memory flag barriers order
+ * the steps; no staging, no NCCL on the data path).  Otherwise, or with
+ * EQC_FLAG_NCCL, the bands move with NCCL grouped send/recv.  With
+ * EQC_FLAG_RLE the call synchronises `stream` once (message sizes).
  */
 EQC_API int compose_direct_send(eqc_comm *comm, int n_local, const uint32_t *const *color,
                                 const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,

@@ -645,11 +645,72 @@ int validate(int nranks, int n_local, const void *color, const void *depth, int 
   if (nranks < 1 || n_local < 1 || n_local > EQC_MAX_SOURCES || nranks > EQC_MAX_SOURCES) return EQC_E_INVALID;
   if (!color || !depth || w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
   if (op != EQC_OP_DEPTH) return EQC_E_UNSUPPORTED;
-  if (flags & ~EQC_FLAG_RLE) return EQC_E_INVALID;
+  if (flags & ~(EQC_FLAG_RLE | EQC_FLAG_NCCL)) return EQC_E_INVALID;
   if (dest < 0 || dest >= nranks) return EQC_E_INVALID;
   if (is_dest && (!out || out_pitch < w)) return EQC_E_INVALID;
   return EQC_OK;
 }
+
+}  // namespace
+
+// ---- peer-memory (NVLink P2P) direct send ------------------------------------
+//
+// The exchange and the band composite are one kernel: rank j's band-composite
+// launch reads band j of every peer's partial frame straight out of the
+// peer's HBM over NVLink (CUDA IPC mappings) and writes the composited band
+// straight into the destination's frame buffer (peer stores), so the bytes
+// cross NVLink once and are never staged.  Two flag barriers (peer-memory
+// release/acquire) order the steps: partials complete before peers read them,
+// bands complete before the destination copies them out.
+namespace {
+
+struct BarrierArgs {
+  int *peer_flags[EQC_MAX_SOURCES];  // flags array of every rank (own = local)
+  int *my_flags;
+  int n, rank, epoch;
+};
+
+__global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
+  const int i = threadIdx.x;
+  __threadfence_system();
+  if (i < a.n) {
+    int *f = a.peer_flags[i] + a.rank;
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(a.epoch) : "memory");
+  }
+  if (i < a.n) {
+    const int *f = a.my_flags + i;
+    int v;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v - a.epoch >= 0) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+struct P2PState {
+  int capable = -1;  // -1 unknown, 0 no (NCCL transport), 1 yes
+  int64_t cap_px = 0;
+  DevBuf part_c, part_d, fin_c, flags, xfer;
+  std::vector<uint32_t *> peer_part_c, peer_part_d, peer_fin_c;
+  std::vector<int *> peer_flags;
+  int epoch = 0;
+
+  void close_peers(int rank) {
+    for (size_t q = 0; q < peer_part_c.size(); ++q) {
+      if ((int)q == rank) continue;
+      if (peer_part_c[q]) cudaIpcCloseMemHandle(peer_part_c[q]);
+      if (peer_part_d[q]) cudaIpcCloseMemHandle(peer_part_d[q]);
+      if (peer_fin_c[q]) cudaIpcCloseMemHandle(peer_fin_c[q]);
+      if (peer_flags[q]) cudaIpcCloseMemHandle(peer_flags[q]);
+    }
+    peer_part_c.clear();
+    peer_part_d.clear();
+    peer_fin_c.clear();
+    peer_flags.clear();
+  }
+};
 
 }  // namespace
 
@@ -658,7 +719,138 @@ struct eqc_comm {
   ncclComm_t nccl = nullptr;
   int nranks = 1, rank = 0;
   RankState st;
+  P2PState p2p;
 };
+
+namespace {
+
+// (Re)build the IPC mappings for frames of `px` pixels.  Collective.
+int p2p_setup(eqc_comm *c, int64_t px, cudaStream_t s) {
+  P2PState &P = c->p2p;
+  if (P.capable == 0) return EQC_OK;
+  if (P.capable == 1 && px <= P.cap_px) return EQC_OK;
+  cudaStreamSynchronize(s);
+  P.close_peers(c->rank);
+  const size_t bytes = (size_t)px * 4;
+  EQC_TRY(P.part_c.ensure(bytes));
+  EQC_TRY(P.part_d.ensure(bytes));
+  EQC_TRY(P.fin_c.ensure(bytes));
+  P.flags.release();
+  EQC_TRY(P.flags.ensure_zeroed(EQC_MAX_SOURCES * sizeof(int)));
+  P.epoch = 0;
+  const int n = c->nranks;
+  constexpr int kH = sizeof(cudaIpcMemHandle_t);
+  std::vector<uint8_t> mine(4 * kH), all((size_t)n * 4 * kH);
+  int ok = 1;
+  void *ptrs[4] = {P.part_c.p, P.part_d.p, P.fin_c.p, P.flags.p};
+  for (int i = 0; i < 4; ++i) {
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, ptrs[i]) != cudaSuccess) ok = 0;
+    std::memcpy(mine.data() + i * kH, &h, kH);
+  }
+  EQC_TRY(P.xfer.ensure((size_t)(n + 1) * 4 * kH + 64));
+  uint8_t *dx = P.xfer.as<uint8_t>();
+  EQC_CUDA_TRY(cudaMemcpyAsync(dx, mine.data(), 4 * kH, cudaMemcpyHostToDevice, s));
+  EQC_NCCL_TRY(ncclAllGather(dx, dx + 4 * kH, 4 * kH, ncclUint8, c->nccl, s));
+  EQC_CUDA_TRY(cudaMemcpyAsync(all.data(), dx + 4 * kH, all.size(), cudaMemcpyDeviceToHost, s));
+  EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  P.peer_part_c.assign(n, nullptr);
+  P.peer_part_d.assign(n, nullptr);
+  P.peer_fin_c.assign(n, nullptr);
+  P.peer_flags.assign(n, nullptr);
+  for (int q = 0; q < n && ok; ++q) {
+    if (q == c->rank) {
+      P.peer_part_c[q] = P.part_c.as<uint32_t>();
+      P.peer_part_d[q] = P.part_d.as<uint32_t>();
+      P.peer_fin_c[q] = P.fin_c.as<uint32_t>();
+      P.peer_flags[q] = P.flags.as<int>();
+      continue;
+    }
+    void *o[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int i = 0; i < 4 && ok; ++i) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, all.data() + ((size_t)q * 4 + i) * kH, kH);
+      if (cudaIpcOpenMemHandle(&o[i], h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
+    }
+    P.peer_part_c[q] = (uint32_t *)o[0];
+    P.peer_part_d[q] = (uint32_t *)o[1];
+    P.peer_fin_c[q] = (uint32_t *)o[2];
+    P.peer_flags[q] = (int *)o[3];
+  }
+  cudaGetLastError();  // a failed open is reported through `ok`
+  // agree on the transport: P2P only if every rank mapped every peer
+  int *dok = reinterpret_cast<int *>(dx);
+  EQC_CUDA_TRY(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+  EQC_NCCL_TRY(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->nccl, s));
+  EQC_CUDA_TRY(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  P.capable = ok ? 1 : 0;
+  P.cap_px = ok ? px : 0;
+  if (!ok) P.close_peers(c->rank);
+  return EQC_OK;
+}
+
+int p2p_barrier(eqc_comm *c, cudaStream_t s) {
+  P2PState &P = c->p2p;
+  BarrierArgs a;
+  for (int q = 0; q < c->nranks; ++q) a.peer_flags[q] = P.peer_flags[q];
+  a.my_flags = P.flags.as<int>();
+  a.n = c->nranks;
+  a.rank = c->rank;
+  a.epoch = ++P.epoch;
+  p2p_barrier_kernel<<<1, 64, 0, s>>>(a);
+  return eqc_launch_status();
+}
+
+int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *color, const uint32_t *const *depth,
+                    cudaStream_t s) {
+  P2PState &P = c->p2p;
+  Geometry g = g0;
+  const int n = c->nranks, me = c->rank;
+  int64_t *stats = c->st.stats;
+  for (int i = 0; i < 4; ++i) stats[i] = 0;
+  std::vector<int> row0(n + 1);
+  plan_bands(g.h, n, row0.data());
+  // (1) local pre-composite into the IPC-exposed partial frame
+  EQC_TRY(compositor_depth(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
+                           P.part_d.as<uint32_t>(), g.w, s));
+  EQC_TRY(p2p_barrier(c, s));
+  // (2)+(3)+(4) band composite pulling every peer's band over NVLink, output
+  // pushed into the destination's frame
+  const int y0 = row0[me], rows = row0[me + 1] - row0[me];
+  if (rows > 0) {
+    std::vector<const uint32_t *> cs(n), ds(n);
+    for (int q = 0; q < n; ++q) {
+      cs[q] = P.peer_part_c[q] + (size_t)y0 * g.w;
+      ds[q] = P.peer_part_d[q] + (size_t)y0 * g.w;
+      if (q != me) {
+        stats[0] += 1;
+        stats[3] += (int64_t)rows * g.w * 8;
+      }
+    }
+    uint32_t *out = me == g.dest ? g.out + (size_t)y0 * g.out_pitch : P.peer_fin_c[g.dest] + (size_t)y0 * g.w;
+    const int64_t opitch = me == g.dest ? g.out_pitch : g.w;
+    EQC_TRY(compositor_depth(n, cs.data(), ds.data(), g.w, rows, g.w, out, nullptr, opitch, s));
+    if (me != g.dest) {
+      stats[1] += 1;
+      stats[2] += (int64_t)rows * g.w * 4;
+    }
+  }
+  EQC_TRY(p2p_barrier(c, s));
+  // (5) destination: move the pushed bands into the caller's frame
+  if (me == g.dest) {
+    for (int q = 0; q < n; ++q) {
+      const int qy0 = row0[q], qrows = row0[q + 1] - row0[q];
+      if (q == me || qrows == 0) continue;
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)qy0 * g.out_pitch, g.out_pitch * 4,
+                                     P.fin_c.as<uint32_t>() + (size_t)qy0 * g.w, (size_t)g.w * 4, (size_t)g.w * 4,
+                                     qrows, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return EQC_OK;
+}
+
+}  // namespace
 
 extern "C" int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]) {
   if (!id) return EQC_E_INVALID;
@@ -688,6 +880,12 @@ extern "C" int eqc_comm_init(eqc_comm **comm, int nranks, int rank, const uint8_
 extern "C" int eqc_comm_destroy(eqc_comm *comm) {
   if (!comm) return EQC_E_INVALID;
   cudaDeviceSynchronize();
+  comm->p2p.close_peers(comm->rank);
+  comm->p2p.part_c.release();
+  comm->p2p.part_d.release();
+  comm->p2p.fin_c.release();
+  comm->p2p.flags.release();
+  comm->p2p.xfer.release();
   comm->st.release();
   int rc = EQC_OK;
   if (comm->nccl && ncclCommDestroy(comm->nccl) != ncclSuccess) rc = EQC_E_NCCL;
@@ -741,6 +939,10 @@ static int compose_nccl(bool ds, eqc_comm *comm, int n_local, const uint32_t *co
   comm->st.color = color;
   comm->st.depth = depth;
   cudaStream_t s = (cudaStream_t)stream;
+  if (ds && comm->nranks > 1 && !(flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) {
+    EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
+    if (comm->p2p.capable == 1) return direct_send_p2p(comm, g, color, depth, s);
+  }
   NcclTransport T(comm->nccl, s);
   std::vector<RankState *> ranks{&comm->st};
   return ds ? run_direct_send(ranks, g, T, s) : run_binary_swap(ranks, g, T, s);

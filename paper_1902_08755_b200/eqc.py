@@ -23,6 +23,7 @@ FLAG_SWIZZLE = 1
 UNIQUE_ID_BYTES = 128
 OP_DEPTH = 0
 FLAG_RLE = 1
+FLAG_NCCL = 2
 
 
 class EqcError(RuntimeError):

@@ -6,9 +6,9 @@ N=$(nvidia-smi -L | wc -l)
 nvidia-smi topo -m > gpurun_out/topo_n${N}.txt 2>&1
 timeout 900 python -m pytest tests/test_gpu_multi.py -q -k nccl > gpurun_out/pytest_multi_n${N}.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_multi_n${N}.log
-for X in raw rle; do
+for X in raw nccl rle; do
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29511 \
   bench.py --gpus $N --steps 50 --warmup 5 --no-cpu-baseline --exchange $X > gpurun_out/bench_n${N}_${X}.json 2> gpurun_out/bench_n${N}_${X}.log
 echo "bench $X rc=$?" >> gpurun_out/bench_n${N}_${X}.log
 done
-tail -5 gpurun_out/pytest_multi_n${N}.log; cat gpurun_out/bench_n${N}_*.json; tail -3 gpurun_out/bench_n${N}_*.log
+tail -5 gpurun_out/pytest_multi_n${N}.log; for f in gpurun_out/bench_n${N}_*.json; do python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[1], d['value'], d['ms_per_step'])" $f; done; for f in gpurun_out/bench_n${N}_*.log; do tail -n 3 $f; done

@@ -25,9 +25,13 @@ def main():
     comm = eqc.Comm.from_torch_distributed()
     dev = torch.device("cuda", local)
     failures = []
-    cases = [("ds", 2, 640, 361, 0, 0), ("ds", 1, 300, 41, world - 1, 1), ("ds", 2, 1920, 1080, 0, 1)]
+    # (algo, n_local, w, h, dest, flags): flags 0 = NVLink peer-memory direct send,
+    # FLAG_NCCL = NCCL grouped send/recv, FLAG_RLE = RLE streams over NCCL
+    R, X = eqc.FLAG_RLE, eqc.FLAG_NCCL
+    cases = [("ds", 2, 640, 361, 0, 0), ("ds", 1, 300, 41, world - 1, 0), ("ds", 2, 1920, 1080, 1 % world, 0),
+             ("ds", 2, 640, 361, 0, X), ("ds", 1, 300, 41, world - 1, R), ("ds", 2, 1920, 1080, 0, R)]
     if world & (world - 1) == 0:
-        cases += [("bs", 2, 640, 361, 0, 0), ("bs", 1, 300, 41, world - 1, 1), ("bs", 2, 1920, 1080, 0, 1)]
+        cases += [("bs", 2, 640, 361, 0, 0), ("bs", 1, 300, 41, world - 1, R), ("bs", 2, 1920, 1080, 0, R)]
     for algo, nl, w, h, dest, rle in cases:
         N = world * nl
         c, d = synth.depth_sources(synth.SEED_BASE + 3 + N + w, N, w, h)
@@ -37,7 +41,7 @@ def main():
         out = torch.zeros((h, w), dtype=torch.int32, device=dev)
         fn = eqc.compose_direct_send if algo == "ds" else eqc.compose_binary_swap
         for _ in range(2):  # the second call reuses the communicator's scratch
-            fn(comm, dc, dd, out if rank == dest else None, dest_rank=dest, flags=eqc.FLAG_RLE if rle else 0)
+            fn(comm, dc, dd, out if rank == dest else None, dest_rank=dest, flags=rle)
         torch.cuda.synchronize()
         st = comm.stats()
         if rank == dest:
