@@ -39,8 +39,16 @@ UNIT = "source Mpixel/s"
 L2_BYTES = 126 * 1024 * 1024
 
 
+_OUT = sys.stdout
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def emit(line):
+    _OUT.write(json.dumps(line) + "\n")
+    _OUT.flush()
 
 
 def measured_peaks():
@@ -178,7 +186,7 @@ def run_eqc(args):
 
     def step(timed_events=None):
         if timed_events is not None:
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
             e0.record(stream)
         eqc.image_compress_rle_batch(imgs, kinds, flags, streams, sizes, ws, stream=stream)
         if timed_events is not None:
@@ -186,10 +194,12 @@ def run_eqc(args):
         eqc.compositor_depth_rle(streams[:NSRC], streams[NSRC:], out_c, out_d, status, stream=stream)
         if timed_events is not None:
             e2.record(stream)
-            timed_events.append((e0, e1, e2))
         if comm is not None:
             # screen-partition direct send of this GPU's partial frame
             eqc.compose_direct_send(comm, [out_c], [out_d], final, dest_rank=0, flags=xflags, stream=stream)
+        if timed_events is not None:
+            e3.record(stream)
+            timed_events.append((e0, e1, e2, e3))
 
     for _ in range(args.warmup):
         step()
@@ -217,8 +227,9 @@ def run_eqc(args):
     if world > 1:
         dist.barrier()
     ms_total = t0.elapsed_time(t1)
-    enc_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in evs)
-    dec_ms = statistics.mean(b.elapsed_time(c) for _, b, c in evs)
+    enc_ms = statistics.mean(a.elapsed_time(b) for a, b, _, _ in evs)
+    dec_ms = statistics.mean(b.elapsed_time(c) for _, b, c, _ in evs)
+    comp_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in evs) if world > 1 else 0.0
     ms = ms_total / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -308,6 +319,7 @@ def run_eqc(args):
             "parallelism": f"screen-partition direct send over {world} GPU(s)" if world > 1 else "single GPU",
         },
         "output_mpx_per_s": round(world * P / (ms * 1e-3) / 1e6, 1),
+        "compose_direct_send_ms_rank0": round(comp_ms, 4) if world > 1 else None,
         "achieved_hbm_gbs_step": round(step_bytes / (ms * 1e-3) / 1e9, 1),
         "kernels": {k: {"ms": round(v["ms"], 4), "alg_bytes": v["bytes"], "gbs": round(v["gbs"], 1),
                         "frac": round(v["frac"], 3)} for k, v in kern.items()},
@@ -320,7 +332,7 @@ def run_eqc(args):
         "gpu_launches": (2 if world == 1 else 2 + launches_per_compose(world, args.exchange)) * args.steps,
         "clocks": clocks,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if comm is not None:
         comm.destroy()
     if world > 1:
@@ -386,10 +398,16 @@ def run_reference(args):
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
+    # stdout carries exactly one JSON line: everything else (NCCL banners,
+    # library prints) goes to stderr
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    global _OUT
+    _OUT = os.fdopen(json_fd, "w")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)

@@ -29,7 +29,8 @@ namespace {
 constexpr int kWarps = 8;            // warps per CTA
 constexpr int kSTChunksPerWarp = 64; // encoder: consecutive chunks per warp in a super-tile
 static_assert(kSTChunksPerWarp <= 64, "two table-entry registers per lane");
-constexpr int kSTChunks = kWarps * kSTChunksPerWarp;  // chunks per super-tile (look-back unit)
+constexpr int kEncWarps = 4;                            // coder warps per CTA (encoder)
+constexpr int kSTChunks = kEncWarps * kSTChunksPerWarp; // chunks per super-tile (CTA of the encoder)
 constexpr int kRecMax = 4 * (kC + 2);                  // worst-case chunk record bytes (520)
 constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 33280 = 260 x 128 B
 constexpr int kPrefetch = 4;         // chunks in flight per coder warp (cp.async ring)
@@ -107,22 +108,30 @@ __device__ __forceinline__ void copy_run(uint8_t *g, const uint8_t *src, int64_t
   const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src) + (head >> 2);
   const int sh = head & 3;
   uint32_t *gw = reinterpret_cast<uint32_t *>(first_w);
-  // 4 independent loads in flight per lane per step
+  // 8 independent loads in flight per lane per step (the scratch usually
+  // comes back from DRAM: enough bytes in flight to cover its latency)
   int64_t k = lane;
-  for (; k + 96 < nw; k += 128) {
-    uint32_t lo[4], hi[4];
+  for (; k + 224 < nw; k += 256) {
+    uint32_t lo[8], hi[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       lo[u] = __ldg(s32 + k + 32 * u);
       hi[u] = sh ? __ldg(s32 + k + 32 * u + 1) : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) gw[k + 32 * u] = sh ? __funnelshift_r(lo[u], hi[u], 8 * sh) : lo[u];
+    for (int u = 0; u < 8; ++u) gw[k + 32 * u] = sh ? __funnelshift_r(lo[u], hi[u], 8 * sh) : lo[u];
   }
-  for (; k < nw; k += 32) {
-    const uint32_t lo = __ldg(s32 + k);
-    const uint32_t hi = sh ? __ldg(s32 + k + 1) : 0u;
-    gw[k] = sh ? __funnelshift_r(lo, hi, 8 * sh) : lo;
+  uint32_t lo[8], hi[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int64_t kk = k + 32 * u;
+    lo[u] = kk < nw ? __ldg(s32 + kk) : 0u;
+    hi[u] = (kk < nw && sh) ? __ldg(s32 + kk + 1) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int64_t kk = k + 32 * u;
+    if (kk < nw) gw[kk] = sh ? __funnelshift_r(lo[u], hi[u], 8 * sh) : lo[u];
   }
 }
 
@@ -130,113 +139,291 @@ __device__ __forceinline__ void discard_l2(const void *p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
+// Per-warp shared memory of the encoder.
+struct WarpEnc {
+  uint32_t pm[32][33];   // batch of 8 chunks, plane-major: row 4c+p = plane p of chunk c (128 B + pad);
+                         // reused as the record assembly area (8 records x 528 B) after coding
+  uint8_t ctl[32][132];  // per-lane (= per plane) ctrl bytes
+  uint8_t pay[32][132];  // per-lane payload bytes
+  uint32_t cval[kSTChunksPerWarp];   // constant chunks: the (swizzled) value
+  uint32_t cps[kSTChunksPerWarp];    // plane sizes of each chunk record
+  uint16_t csize[kSTChunksPerWarp];  // record size of each chunk
+  uint8_t gidx[kSTChunksPerWarp];    // positions of the non-constant chunks
+};
+constexpr int kRecSlot = 528;        // record assembly slot (>= 520)
+
 struct EncSmem {
-  uint4 in[kWarps][kPrefetch][32];     // per-warp cp.async ring of input chunks (16 KB)
-  uint8_t stage[kWarps][kStageBytes];  // one coded record per warp
-  uint8_t toks[kWarps][kTokBytes];     // token-start scratch
-  int wsize[kWarps];
-  int64_t woff[kWarps];
-  unsigned long long tk;
+  WarpEnc w[kEncWarps];
+  int wsize[kEncWarps];
 };
 
-// Single-pass encoder.  A CTA codes one super-tile of 512 consecutive chunks
-// (CTA order = atomic ticket): each coder warp streams its 64 chunks through
-// a 4-deep cp.async ring, codes each into shared memory and appends the
-// record to its slice of a record scratch (L2-resident); then the CTA's
-// total is prefix-summed across super-tiles by a decoupled look-back (one
-// look-back per 256 KB of input keeps the look-back chain far off the
-// critical path), and every warp copies its run to the final offset, writes
-// its 64 table entries and discards its scratch lines from L2.
-__global__ void __launch_bounds__(kWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
+// Serial RLE of one byte plane (the lane's): bytes arrive 4 at a time as
+// little-endian words; tokens follow the rules of R-C8 exactly (the same
+// maximal runs the oracle finds): every byte is appended to the payload
+// tentatively; when a run reaches 3 the pending literal span (if any) is
+// closed and the run's second byte is dropped from the payload (its first
+// byte is the REPEAT value); when a REPEAT run ends its ctrl byte is written.
+// A word whose bytes all differ from their predecessors (literal noise) or
+// all continue a REPEAT takes a short path.
+struct PlaneCoder {
+  uint32_t prev;  // previous byte (0x100 = none)
+  int run, lit, ntok, npay;
+  bool inrep;
+  __device__ __forceinline__ void init() {
+    prev = 0x100u;
+    run = 0;
+    lit = 0;
+    ntok = 0;
+    npay = 0;
+    inrep = false;
+  }
+  __device__ __forceinline__ void byte(uint32_t b, int i, uint8_t *ctl, uint8_t *pay) {
+    const bool eq = b == prev;
+    const int runp = run;
+    run = eq ? run + 1 : 1;
+    if (!eq && inrep) {  // REPEAT ended at i - 1
+      ctl[ntok++] = (uint8_t)(0x80 | (runp - 1));
+      lit = i;
+      inrep = false;
+    }
+    if (eq && run == 3) {  // bytes i-2, i-1, i start a REPEAT
+      const int litlen = i - 2 - lit;
+      if (litlen > 0) ctl[ntok++] = (uint8_t)(litlen - 1);
+      npay -= 1;
+      inrep = true;
+    }
+    if (!inrep) pay[npay++] = (uint8_t)b;
+    prev = b;
+  }
+  // 4 bytes (positions i0..i0+3, all < L)
+  __device__ __forceinline__ void word(uint32_t w, int i0, uint8_t *ctl, uint8_t *pay) {
+    const uint32_t shifted = (w << 8) | (prev & 0xFFu);
+    uint32_t eqf = bytes_eq(w, shifted);
+    if (prev > 0xFFu) eqf &= ~0x80u;  // no predecessor for the first byte
+    if (eqf == 0) {
+      // fast literal: no byte equals its predecessor; a REPEAT in progress
+      // ends before the first byte
+      if (inrep) {
+        ctl[ntok++] = (uint8_t)(0x80 | (run - 1));
+        lit = i0;
+        inrep = false;
+      }
+      pay[npay] = (uint8_t)w;
+      pay[npay + 1] = (uint8_t)(w >> 8);
+      pay[npay + 2] = (uint8_t)(w >> 16);
+      pay[npay + 3] = (uint8_t)(w >> 24);
+      npay += 4;
+      run = 1;
+      prev = w >> 24;
+      return;
+    }
+    if (eqf == 0x80808080u && inrep) {  // the REPEAT continues through the word
+      run += 4;
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) byte((w >> (8 * j)) & 0xFFu, i0 + j, ctl, pay);
+  }
+  __device__ __forceinline__ void finish(int L, uint8_t *ctl) {
+    if (inrep) {
+      ctl[ntok++] = (uint8_t)(0x80 | (run - 1));
+    } else {
+      const int litlen = L - lit;
+      if (litlen > 0) ctl[ntok++] = (uint8_t)(litlen - 1);
+    }
+  }
+};
+
+// Encoder.  A CTA codes one super-tile of 256 consecutive chunks (4 warps x
+// 64).  Per warp:
+//  A. classify: stream the 64 chunks (coalesced 128-bit loads, 8 in flight
+//     per lane); a chunk whose pixels are all equal (76 % of the target
+//     workload) only records its value;
+//  B. code the other chunks in batches of 8: the warp stages a batch
+//     plane-major in shared memory (swizzled if colour) and lane 4c+p codes
+//     plane p of chunk c serially (PlaneCoder); the four plane records of a
+//     chunk are assembled into one record and stored to the record scratch at
+//     its offset in the warp's run;
+//  C. the constant chunks' 12-byte records are written lane-parallel.
+// The compaction kernel then moves the runs to their final offsets.
+__global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  WarpEnc &W = sm.w[warp];
   const int64_t tile = blockIdx.x;
   const int m = (int)(tile / p.tiles_per_image);
   const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
   const EncImage im = p.img[m];
   const int nch = (int)p.nchunks;
   const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
-  uint8_t *scr = p.scratch + ((size_t)tile * kWarps + warp) * kScratchPerWarp;
+  uint8_t *scr = p.scratch + ((size_t)tile * kEncWarps + warp) * kScratchPerWarp;
   const int c0 = (int)(lt * kSTChunks) + warp * kSTChunksPerWarp;
   const int cnt = max(0, min(kSTChunksPerWarp, nch - c0));
-  const int Llast = p.w - (p.S - 1) * kC;  // length of the last chunk of a row
-  // ---- cp.async ring: chunk j lives in slot j % kPrefetch; the issue
-  // pointer walks the rows incrementally
-  int ik = c0 % p.S;
-  const uint32_t *irow = im.src + (int64_t)(c0 / p.S) * p.pitch;
-  auto issue = [&](int j) {
-    if (j < cnt) {
-      const int L = ik == p.S - 1 ? Llast : kC;
-      const uint32_t *ptr = irow + ik * kC;
-      uint4 *slot = &sm.in[warp][j % kPrefetch][lane];
-      if (p.vec && L == kC) {
-        cp_async16(slot, ptr + 4 * lane);
-      } else {
-        uint32_t px[4];
-        load_chunk(ptr, L, lane, false, px);
-        *slot = make_uint4(px[0], px[1], px[2], px[3]);
-      }
-      if (++ik == p.S) {
-        ik = 0;
-        irow += p.pitch;
-      }
-    }
-    cp_async_commit();  // (possibly empty) group per chunk index keeps the counting uniform
+  const int Llast = p.w - (p.S - 1) * kC;
+  const int k0 = c0 % p.S;
+  const uint32_t *row0 = im.src + (int64_t)(c0 / p.S) * p.pitch;
+  // chunk j of the run -> (row pointer, length)
+  auto chunk_ptr = [&](int j, int &L) -> const uint32_t * {
+    const int kk = k0 + j;
+    const int dy = kk / p.S, k = kk - dy * p.S;
+    L = k == p.S - 1 ? Llast : kC;
+    return row0 + (int64_t)dy * p.pitch + k * kC;
   };
+  // ---- A: classify (8 chunks in flight per lane)
+  int ng = 0;
+  uint64_t cmask = 0;
+  for (int j0 = 0; j0 < cnt; j0 += 8) {
+    uint32_t px[8][4];
+    int Ls[8];
 #pragma unroll
-  for (int j = 0; j < kPrefetch - 1; ++j) issue(j);
-  int k = c0 % p.S;
-  int run = 0;
-  uint2 ent0 = make_uint2(0, 0), ent1 = make_uint2(0, 0);  // {run offset, plane sizes} of chunks lane, lane+32
-#pragma unroll 1
-  for (int j = 0; j < cnt; ++j) {
-    issue(j + kPrefetch - 1);
-    cp_async_wait<kPrefetch - 1>();
-    __syncwarp();
-    const uint4 v = sm.in[warp][j % kPrefetch][lane];
-    __syncwarp();
-    uint32_t px[4] = {v.x, v.y, v.z, v.w};
-    const int L = k == p.S - 1 ? Llast : kC;
-    uint32_t v0, psz;
-    int size;
-    if (chunk_is_constant(px, L, lane, v0)) {
-      emit_constant_record(scr + run, swz ? swizzle(v0) : v0, L, lane);
-      psz = 0x03030303u;
-      size = 12;
-    } else {
-      const EncodeOut eo = encode_chunk(px, L, lane, swz, sm.stage[warp], sm.toks[warp]);
-      store_record(scr + run, sm.stage[warp], eo.size, lane);
-      psz = eo.psizes;
-      size = eo.size;
+    for (int u = 0; u < 8; ++u) {
+      Ls[u] = 0;
+      if (j0 + u < cnt) {
+        const uint32_t *ptr = chunk_ptr(j0 + u, Ls[u]);
+        load_chunk(ptr, Ls[u], lane, p.vec != 0, px[u]);
+      }
     }
-    if (lane == (j & 31)) {
-      if (j < 32)
-        ent0 = make_uint2((uint32_t)run, psz);
-      else
-        ent1 = make_uint2((uint32_t)run, psz);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (j0 + u >= cnt) break;
+      uint32_t v0;
+      const bool cst = chunk_is_constant(px[u], Ls[u], lane, v0);
+      if (cst) {
+        cmask |= 1ull << (j0 + u);
+        if (lane == 0) {
+          W.cval[j0 + u] = swz ? swizzle(v0) : v0;
+          W.csize[j0 + u] = 12;
+          W.cps[j0 + u] = 0x03030303u;
+        }
+      } else {
+        if (lane == 0) W.gidx[ng] = (uint8_t)(j0 + u);
+        ++ng;
+      }
     }
-    run += size;
-    if (++k == p.S) k = 0;
   }
-  cp_async_wait<0>();
+  __syncwarp();
+  // ---- B: non-constant chunks, 8 per batch
+  int gen_bytes = 0;  // bytes of the non-constant records coded so far
+  uint8_t *ctl = W.ctl[lane];
+  uint8_t *pay = W.pay[lane];
+  for (int b0 = 0; b0 < ng; b0 += 8) {
+    const int nb = min(8, ng - b0);
+    // stage the batch plane-major (coalesced 128-bit loads from L2)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c < nb) {
+        int L;
+        const uint32_t *ptr = chunk_ptr(W.gidx[b0 + c], L);
+        uint32_t px[4];
+        load_chunk(ptr, L, lane, p.vec != 0, px);
+        if (swz) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) px[q] = swizzle(px[q]);
+        }
+        // 4x4 byte transpose: plane word q = byte q of px[0..3]
+        const uint32_t t01l = __byte_perm(px[0], px[1], 0x5140), t01h = __byte_perm(px[0], px[1], 0x7362);
+        const uint32_t t23l = __byte_perm(px[2], px[3], 0x5140), t23h = __byte_perm(px[2], px[3], 0x7362);
+        W.pm[4 * c + 0][lane] = __byte_perm(t01l, t23l, 0x5410);
+        W.pm[4 * c + 1][lane] = __byte_perm(t01l, t23l, 0x7632);
+        W.pm[4 * c + 2][lane] = __byte_perm(t01h, t23h, 0x5410);
+        W.pm[4 * c + 3][lane] = __byte_perm(t01h, t23h, 0x7632);
+      }
+    }
+    __syncwarp();
+    // serial coding: lane = plane (lane & 3) of chunk (lane >> 2)
+    const int mc = lane >> 2, mp = lane & 3;
+    const bool active = mc < nb;
+    int Lm = 0;
+    if (active) chunk_ptr(W.gidx[b0 + mc], Lm);
+    PlaneCoder pc;
+    pc.init();
+    if (active) {
+      const uint32_t *rowp = W.pm[lane];
+      const int nfull = Lm >> 2;
+      for (int k = 0; k < nfull; ++k) pc.word(rowp[k], 4 * k, ctl, pay);
+      if (Lm & 3) {
+        const uint32_t w = rowp[nfull];
+        for (int j = 0; j < (Lm & 3); ++j) pc.byte((w >> (8 * j)) & 0xFFu, 4 * nfull + j, ctl, pay);
+      }
+      pc.finish(Lm, ctl);
+    }
+    const int psize = active ? 1 + pc.ntok + pc.npay : 0;
+    // plane offsets inside the chunk record, chunk sizes
+    int pre = psize;
+    const int u1 = __shfl_up_sync(EQC_FULL, pre, 1);
+    if (mp >= 1) pre += u1;
+    const int u2 = __shfl_up_sync(EQC_FULL, pre, 2);
+    if (mp >= 2) pre += u2;
+    const int poff = pre - psize;                                   // plane offset in its record
+    const int csz = __shfl_sync(EQC_FULL, pre, (lane | 3));        // chunk record size
+    __syncwarp();  // all lanes are done reading pm: reuse it for assembly
+    uint8_t *asmb = reinterpret_cast<uint8_t *>(W.pm) + mc * kRecSlot + poff;
+    if (active) {
+      asmb[0] = (uint8_t)pc.ntok;
+      for (int q = 0; q < pc.ntok; ++q) asmb[1 + q] = ctl[q];
+      for (int q = 0; q < pc.npay; ++q) asmb[1 + pc.ntok + q] = pay[q];
+    }
+    const uint32_t ps_c = (uint32_t)psize << (8 * mp);
+    uint32_t ps_all = ps_c | __shfl_xor_sync(EQC_FULL, ps_c, 1);
+    ps_all |= __shfl_xor_sync(EQC_FULL, ps_all, 2);
+    __syncwarp();
+    // store the records at their offsets in the run
+#pragma unroll 1
+    for (int c = 0; c < nb; ++c) {
+      const int j = W.gidx[b0 + c];
+      const int sz = __shfl_sync(EQC_FULL, csz, 4 * c);
+      const int off = 12 * __popcll(cmask & ((1ull << j) - 1)) + gen_bytes;
+      store_record(scr + off, reinterpret_cast<uint8_t *>(W.pm) + c * kRecSlot, sz, lane);
+      if (lane == 0) W.csize[j] = (uint16_t)sz;
+      gen_bytes += sz;
+    }
+    if (mp == 0 && active) W.cps[W.gidx[b0 + mc]] = ps_all;
+    __syncwarp();
+  }
+  // ---- C: offsets of all chunks, constant records, table entries
+  const int j1 = lane, j2 = lane + 32;
+  const int s1 = j1 < cnt ? (int)W.csize[j1] : 0;
+  const int s2 = j2 < cnt ? (int)W.csize[j2] : 0;
+  const int i1 = (int)warp_incl_scan_add((uint32_t)s1, lane);
+  const int t1 = __shfl_sync(EQC_FULL, i1, 31);
+  const int i2 = (int)warp_incl_scan_add((uint32_t)s2, lane) + t1;
+  const int off1 = i1 - s1, off2 = i2 - s2;
+  const int run = __shfl_sync(EQC_FULL, i2, 31);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = h ? j2 : j1;
+    const int off = h ? off2 : off1;
+    if (j < cnt && ((cmask >> j) & 1ull)) {
+      int L;
+      chunk_ptr(j, L);
+      const uint32_t v = W.cval[j];
+      const uint8_t c = (uint8_t)(0x80 | (L - 1));
+      uint8_t *g = scr + off;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        g[3 * q] = 1;
+        g[3 * q + 1] = c;
+        g[3 * q + 2] = (uint8_t)(v >> (8 * q));
+      }
+    }
+  }
   if (lane == 0) sm.wsize[warp] = run;
   __syncthreads();
-  // offsets of the warp runs inside the super-tile
-  const int wv = lane < kWarps ? sm.wsize[lane] : 0;
+  const int wv = lane < kEncWarps ? sm.wsize[lane] : 0;
   const int winc = (int)warp_incl_scan_add((uint32_t)wv, lane);
   const int wexcl = __shfl_sync(EQC_FULL, winc - wv, warp);
   const int ttot = __shfl_sync(EQC_FULL, winc, 31);
   if (warp == 0) {
     int32_t *ti = p.tile_info + tile * kTileInfo;
     if (lane == 0) ti[0] = ttot;
-    if (lane < kWarps) ti[1 + lane] = winc - wv;
+    if (lane < kEncWarps) ti[1 + lane] = winc - wv;
   }
   if (cnt > 0) {
     // table entries relative to the super-tile (rebased by the compaction)
     uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
-    if (lane < cnt) table[lane] = make_uint2((uint32_t)(wexcl + ent0.x), ent0.y);
-    if (lane + 32 < cnt) table[lane + 32] = make_uint2((uint32_t)(wexcl + ent1.x), ent1.y);
+    if (j1 < cnt) table[j1] = make_uint2((uint32_t)(wexcl + off1), W.cps[j1]);
+    if (j2 < cnt) table[j2] = make_uint2((uint32_t)(wexcl + off2), W.cps[j2]);
   }
 }
 
@@ -253,7 +440,7 @@ struct CompactParams {
 // moves its run from the scratch to the stream, rebases its 64 table entries
 // and discards its scratch lines from L2; the last super-tile of an image
 // writes the header and the stream size.
-__global__ void __launch_bounds__(kWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
+__global__ void __launch_bounds__(kEncWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
   __shared__ int64_t s_off;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t tile = blockIdx.x;
@@ -291,9 +478,9 @@ __global__ void __launch_bounds__(kWarps * 32) rle_compact_kernel(const __grid_c
   if (cnt <= 0) return;
   const int32_t *ti = p.tile_info + tile * kTileInfo;
   const int64_t woff = __ldg(ti + 1 + warp);
-  const int64_t wend = warp + 1 < kWarps ? __ldg(ti + 2 + warp) : __ldg(ti);
+  const int64_t wend = warp + 1 < kEncWarps ? __ldg(ti + 2 + warp) : __ldg(ti);
   const int64_t run = wend - woff;
-  const uint8_t *scr = p.scratch + ((size_t)tile * kWarps + warp) * kScratchPerWarp;
+  const uint8_t *scr = p.scratch + ((size_t)tile * kEncWarps + warp) * kScratchPerWarp;
   uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
   for (int j = lane; j < cnt; j += 32) {
     uint2 e = table[j];
@@ -732,7 +919,7 @@ extern "C" int64_t image_rle_max_size(int w, int h) {
 extern "C" size_t image_rle_workspace_size_batch(int count, int w, int h) {
   if (count <= 0 || w <= 0 || h <= 0) return 0;
   const int64_t tiles = (int64_t)count * enc_tiles_per_image(w, h);
-  return enc_scratch_offset(tiles) + (size_t)tiles * kWarps * kScratchPerWarp;
+  return enc_scratch_offset(tiles) + (size_t)tiles * kEncWarps * kScratchPerWarp;
 }
 
 extern "C" size_t image_rle_workspace_size(int w, int h) { return image_rle_workspace_size_batch(1, w, h); }
@@ -781,7 +968,7 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
     configured = true;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  rle_encode_kernel<<<(unsigned)tiles, kWarps * 32, smem, st>>>(p);
+  rle_encode_kernel<<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
   CompactParams c;
   for (int i = 0; i < count; ++i) c.img[i] = p.img[i];
   c.tile_info = p.tile_info;
@@ -790,7 +977,7 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   c.w = w;
   c.h = h;
   c.tiles_per_image = p.tiles_per_image;
-  rle_compact_kernel<<<(unsigned)tiles, kWarps * 32, 0, st>>>(c);
+  rle_compact_kernel<<<(unsigned)tiles, kEncWarps * 32, 0, st>>>(c);
   return eqc_launch_status();
 }
 
