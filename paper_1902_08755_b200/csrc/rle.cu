@@ -29,11 +29,10 @@ namespace {
 constexpr int kWarps = 8;            // warps per CTA
 constexpr int kSTChunksPerWarp = 64; // encoder: consecutive chunks per warp in a super-tile
 static_assert(kSTChunksPerWarp <= 64, "two table-entry registers per lane");
-constexpr int kEncWarps = 4;                            // coder warps per CTA (encoder)
+constexpr int kEncWarps = 8;                            // coder warps per CTA (encoder)
 constexpr int kSTChunks = kEncWarps * kSTChunksPerWarp; // chunks per super-tile (CTA of the encoder)
 constexpr int kRecMax = 4 * (kC + 2);                  // worst-case chunk record bytes (520)
 constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 33280 = 260 x 128 B
-constexpr int kPrefetch = 4;         // chunks in flight per coder warp (cp.async ring)
 constexpr int kMaxBatch = 64;
 
 // workspace layout: tile_info[count * tiles_per_image][16] int32 (super-tile
@@ -72,16 +71,6 @@ __device__ __forceinline__ void load_chunk(const uint32_t *row, int L, int lane,
 #pragma unroll
     for (int j = 0; j < 4; ++j) px[j] = (i0 + j < L) ? ld_stream_u32(row + i0 + j) : 0u;
   }
-}
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 // Copy `size` bytes from a 16-byte aligned global source (the warp's record
@@ -141,110 +130,30 @@ __device__ __forceinline__ void discard_l2(const void *p) {
 
 // Per-warp shared memory of the encoder.
 struct WarpEnc {
-  uint32_t pm[32][33];   // batch of 8 chunks, plane-major: row 4c+p = plane p of chunk c (128 B + pad);
-                         // reused as the record assembly area (8 records x 528 B) after coding
-  uint8_t ctl[32][132];  // per-lane (= per plane) ctrl bytes
-  uint8_t pay[32][132];  // per-lane payload bytes
+  uint8_t stage[kStageBytes];        // one coded record
+  uint8_t toks[kTokBytes];           // token-start scratch of encode_chunk
   uint32_t cval[kSTChunksPerWarp];   // constant chunks: the (swizzled) value
   uint32_t cps[kSTChunksPerWarp];    // plane sizes of each chunk record
   uint16_t csize[kSTChunksPerWarp];  // record size of each chunk
   uint8_t gidx[kSTChunksPerWarp];    // positions of the non-constant chunks
 };
-constexpr int kRecSlot = 528;        // record assembly slot (>= 520)
 
 struct EncSmem {
   WarpEnc w[kEncWarps];
   int wsize[kEncWarps];
 };
 
-// Serial RLE of one byte plane (the lane's): bytes arrive 4 at a time as
-// little-endian words; tokens follow the rules of R-C8 exactly (the same
-// maximal runs the oracle finds): every byte is appended to the payload
-// tentatively; when a run reaches 3 the pending literal span (if any) is
-// closed and the run's second byte is dropped from the payload (its first
-// byte is the REPEAT value); when a REPEAT run ends its ctrl byte is written.
-// A word whose bytes all differ from their predecessors (literal noise) or
-// all continue a REPEAT takes a short path.
-struct PlaneCoder {
-  uint32_t prev;  // previous byte (0x100 = none)
-  int run, lit, ntok, npay;
-  bool inrep;
-  __device__ __forceinline__ void init() {
-    prev = 0x100u;
-    run = 0;
-    lit = 0;
-    ntok = 0;
-    npay = 0;
-    inrep = false;
-  }
-  __device__ __forceinline__ void byte(uint32_t b, int i, uint8_t *ctl, uint8_t *pay) {
-    const bool eq = b == prev;
-    const int runp = run;
-    run = eq ? run + 1 : 1;
-    if (!eq && inrep) {  // REPEAT ended at i - 1
-      ctl[ntok++] = (uint8_t)(0x80 | (runp - 1));
-      lit = i;
-      inrep = false;
-    }
-    if (eq && run == 3) {  // bytes i-2, i-1, i start a REPEAT
-      const int litlen = i - 2 - lit;
-      if (litlen > 0) ctl[ntok++] = (uint8_t)(litlen - 1);
-      npay -= 1;
-      inrep = true;
-    }
-    if (!inrep) pay[npay++] = (uint8_t)b;
-    prev = b;
-  }
-  // 4 bytes (positions i0..i0+3, all < L)
-  __device__ __forceinline__ void word(uint32_t w, int i0, uint8_t *ctl, uint8_t *pay) {
-    const uint32_t shifted = (w << 8) | (prev & 0xFFu);
-    uint32_t eqf = bytes_eq(w, shifted);
-    if (prev > 0xFFu) eqf &= ~0x80u;  // no predecessor for the first byte
-    if (eqf == 0) {
-      // fast literal: no byte equals its predecessor; a REPEAT in progress
-      // ends before the first byte
-      if (inrep) {
-        ctl[ntok++] = (uint8_t)(0x80 | (run - 1));
-        lit = i0;
-        inrep = false;
-      }
-      pay[npay] = (uint8_t)w;
-      pay[npay + 1] = (uint8_t)(w >> 8);
-      pay[npay + 2] = (uint8_t)(w >> 16);
-      pay[npay + 3] = (uint8_t)(w >> 24);
-      npay += 4;
-      run = 1;
-      prev = w >> 24;
-      return;
-    }
-    if (eqf == 0x80808080u && inrep) {  // the REPEAT continues through the word
-      run += 4;
-      return;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) byte((w >> (8 * j)) & 0xFFu, i0 + j, ctl, pay);
-  }
-  __device__ __forceinline__ void finish(int L, uint8_t *ctl) {
-    if (inrep) {
-      ctl[ntok++] = (uint8_t)(0x80 | (run - 1));
-    } else {
-      const int litlen = L - lit;
-      if (litlen > 0) ctl[ntok++] = (uint8_t)(litlen - 1);
-    }
-  }
-};
-
-// Encoder.  A CTA codes one super-tile of 256 consecutive chunks (4 warps x
-// 64).  Per warp:
+// Encoder.  A CTA codes one super-tile of kSTChunks consecutive chunks
+// (kEncWarps warps x 64).  Per warp:
 //  A. classify: stream the 64 chunks (coalesced 128-bit loads, 8 in flight
 //     per lane); a chunk whose pixels are all equal (76 % of the target
-//     workload) only records its value;
-//  B. code the other chunks in batches of 8: the warp stages a batch
-//     plane-major in shared memory (swizzled if colour) and lane 4c+p codes
-//     plane p of chunk c serially (PlaneCoder); the four plane records of a
-//     chunk are assembled into one record and stored to the record scratch at
-//     its offset in the warp's run;
-//  C. the constant chunks' 12-byte records are written lane-parallel.
+//     workload) only records its value -- about a dozen instructions;
+//  B. code every other chunk with encode_chunk (SIMD-within-a-word flags,
+//     packed-byte scans, per-plane classes) from a second, L2-resident read,
+//     the next chunk's load in flight, and store its record at its offset in
+//     the warp's run (the offsets of the constant chunks are known from A);
+//  C. write the constant chunks' 12-byte records lane-parallel and the
+//     table entries.
 // The compaction kernel then moves the runs to their final offsets.
 __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -263,7 +172,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid
   const int Llast = p.w - (p.S - 1) * kC;
   const int k0 = c0 % p.S;
   const uint32_t *row0 = im.src + (int64_t)(c0 / p.S) * p.pitch;
-  // chunk j of the run -> (row pointer, length)
+  // chunk j of the run -> (pointer, length)
   auto chunk_ptr = [&](int j, int &L) -> const uint32_t * {
     const int kk = k0 + j;
     const int dy = kk / p.S, k = kk - dy * p.S;
@@ -303,82 +212,25 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid
     }
   }
   __syncwarp();
-  // ---- B: non-constant chunks, 8 per batch
-  int gen_bytes = 0;  // bytes of the non-constant records coded so far
-  uint8_t *ctl = W.ctl[lane];
-  uint8_t *pay = W.pay[lane];
-  for (int b0 = 0; b0 < ng; b0 += 8) {
-    const int nb = min(8, ng - b0);
-    // stage the batch plane-major (coalesced 128-bit loads from L2)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (c < nb) {
-        int L;
-        const uint32_t *ptr = chunk_ptr(W.gidx[b0 + c], L);
-        uint32_t px[4];
-        load_chunk(ptr, L, lane, p.vec != 0, px);
-        if (swz) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) px[q] = swizzle(px[q]);
-        }
-        // 4x4 byte transpose: plane word q = byte q of px[0..3]
-        const uint32_t t01l = __byte_perm(px[0], px[1], 0x5140), t01h = __byte_perm(px[0], px[1], 0x7362);
-        const uint32_t t23l = __byte_perm(px[2], px[3], 0x5140), t23h = __byte_perm(px[2], px[3], 0x7362);
-        W.pm[4 * c + 0][lane] = __byte_perm(t01l, t23l, 0x5410);
-        W.pm[4 * c + 1][lane] = __byte_perm(t01l, t23l, 0x7632);
-        W.pm[4 * c + 2][lane] = __byte_perm(t01h, t23h, 0x5410);
-        W.pm[4 * c + 3][lane] = __byte_perm(t01h, t23h, 0x7632);
-      }
-    }
-    __syncwarp();
-    // serial coding: lane = plane (lane & 3) of chunk (lane >> 2)
-    const int mc = lane >> 2, mp = lane & 3;
-    const bool active = mc < nb;
-    int Lm = 0;
-    if (active) chunk_ptr(W.gidx[b0 + mc], Lm);
-    PlaneCoder pc;
-    pc.init();
-    if (active) {
-      const uint32_t *rowp = W.pm[lane];
-      const int nfull = Lm >> 2;
-      for (int k = 0; k < nfull; ++k) pc.word(rowp[k], 4 * k, ctl, pay);
-      if (Lm & 3) {
-        const uint32_t w = rowp[nfull];
-        for (int j = 0; j < (Lm & 3); ++j) pc.byte((w >> (8 * j)) & 0xFFu, 4 * nfull + j, ctl, pay);
-      }
-      pc.finish(Lm, ctl);
-    }
-    const int psize = active ? 1 + pc.ntok + pc.npay : 0;
-    // plane offsets inside the chunk record, chunk sizes
-    int pre = psize;
-    const int u1 = __shfl_up_sync(EQC_FULL, pre, 1);
-    if (mp >= 1) pre += u1;
-    const int u2 = __shfl_up_sync(EQC_FULL, pre, 2);
-    if (mp >= 2) pre += u2;
-    const int poff = pre - psize;                                   // plane offset in its record
-    const int csz = __shfl_sync(EQC_FULL, pre, (lane | 3));        // chunk record size
-    __syncwarp();  // all lanes are done reading pm: reuse it for assembly
-    uint8_t *asmb = reinterpret_cast<uint8_t *>(W.pm) + mc * kRecSlot + poff;
-    if (active) {
-      asmb[0] = (uint8_t)pc.ntok;
-      for (int q = 0; q < pc.ntok; ++q) asmb[1 + q] = ctl[q];
-      for (int q = 0; q < pc.npay; ++q) asmb[1 + pc.ntok + q] = pay[q];
-    }
-    const uint32_t ps_c = (uint32_t)psize << (8 * mp);
-    uint32_t ps_all = ps_c | __shfl_xor_sync(EQC_FULL, ps_c, 1);
-    ps_all |= __shfl_xor_sync(EQC_FULL, ps_all, 2);
-    __syncwarp();
-    // store the records at their offsets in the run
+  // ---- B: the other chunks, SIMD coder, next chunk's load in flight
+  int gen_bytes = 0;
+  uint32_t nxt[4] = {0, 0, 0, 0};
+  int Ln = 0;
+  if (ng > 0) load_chunk(chunk_ptr(W.gidx[0], Ln), Ln, lane, p.vec != 0, nxt);
 #pragma unroll 1
-    for (int c = 0; c < nb; ++c) {
-      const int j = W.gidx[b0 + c];
-      const int sz = __shfl_sync(EQC_FULL, csz, 4 * c);
-      const int off = 12 * __popcll(cmask & ((1ull << j) - 1)) + gen_bytes;
-      store_record(scr + off, reinterpret_cast<uint8_t *>(W.pm) + c * kRecSlot, sz, lane);
-      if (lane == 0) W.csize[j] = (uint16_t)sz;
-      gen_bytes += sz;
+  for (int g = 0; g < ng; ++g) {
+    uint32_t px[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
+    const int L = Ln;
+    const int j = W.gidx[g];
+    if (g + 1 < ng) load_chunk(chunk_ptr(W.gidx[g + 1], Ln), Ln, lane, p.vec != 0, nxt);
+    const EncodeOut eo = encode_chunk(px, L, lane, swz, W.stage, W.toks);
+    const int off = 12 * __popcll(cmask & ((1ull << j) - 1)) + gen_bytes;
+    store_record(scr + off, W.stage, eo.size, lane);
+    if (lane == 0) {
+      W.csize[j] = (uint16_t)eo.size;
+      W.cps[j] = eo.psizes;
     }
-    if (mp == 0 && active) W.cps[W.gidx[b0 + mc]] = ps_all;
+    gen_bytes += eo.size;
     __syncwarp();
   }
   // ---- C: offsets of all chunks, constant records, table entries
@@ -399,12 +251,12 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid
       chunk_ptr(j, L);
       const uint32_t v = W.cval[j];
       const uint8_t c = (uint8_t)(0x80 | (L - 1));
-      uint8_t *g = scr + off;
+      uint8_t *gp = scr + off;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        g[3 * q] = 1;
-        g[3 * q + 1] = c;
-        g[3 * q + 2] = (uint8_t)(v >> (8 * q));
+        gp[3 * q] = 1;
+        gp[3 * q + 1] = c;
+        gp[3 * q + 2] = (uint8_t)(v >> (8 * q));
       }
     }
   }
