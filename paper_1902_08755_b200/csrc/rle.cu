@@ -179,35 +179,40 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid
     L = k == p.S - 1 ? Llast : kC;
     return row0 + (int64_t)dy * p.pitch + k * kC;
   };
-  // ---- A: classify (8 chunks in flight per lane)
+  // ---- A: classify (4 chunks in flight per lane; row pointer advanced
+  // incrementally; the swizzle of constant values is deferred to C)
   int ng = 0;
   uint64_t cmask = 0;
-  for (int j0 = 0; j0 < cnt; j0 += 8) {
-    uint32_t px[8][4];
-    int Ls[8];
+  {
+    int ka = k0;
+    const uint32_t *rowa = row0;
+    for (int j0 = 0; j0 < cnt; j0 += 4) {
+      uint32_t px[4][4];
+      int Ls[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      Ls[u] = 0;
-      if (j0 + u < cnt) {
-        const uint32_t *ptr = chunk_ptr(j0 + u, Ls[u]);
-        load_chunk(ptr, Ls[u], lane, p.vec != 0, px[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (j0 + u >= cnt) break;
-      uint32_t v0;
-      const bool cst = chunk_is_constant(px[u], Ls[u], lane, v0);
-      if (cst) {
-        cmask |= 1ull << (j0 + u);
-        if (lane == 0) {
-          W.cval[j0 + u] = swz ? swizzle(v0) : v0;
-          W.csize[j0 + u] = 12;
-          W.cps[j0 + u] = 0x03030303u;
+      for (int u = 0; u < 4; ++u) {
+        Ls[u] = 0;
+        if (j0 + u < cnt) {
+          Ls[u] = ka == p.S - 1 ? Llast : kC;
+          load_chunk(rowa + ka * kC, Ls[u], lane, p.vec != 0, px[u]);
+          if (++ka == p.S) {
+            ka = 0;
+            rowa += p.pitch;
+          }
         }
-      } else {
-        if (lane == 0) W.gidx[ng] = (uint8_t)(j0 + u);
-        ++ng;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j0 + u >= cnt) break;
+        uint32_t v0;
+        const bool cst = chunk_is_constant(px[u], Ls[u], lane, v0);
+        if (cst) {
+          cmask |= 1ull << (j0 + u);
+          if (lane == 0) W.cval[j0 + u] = v0;
+        } else {
+          if (lane == 0) W.gidx[ng] = (uint8_t)(j0 + u);
+          ++ng;
+        }
       }
     }
   }
@@ -235,21 +240,24 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid
   }
   // ---- C: offsets of all chunks, constant records, table entries
   const int j1 = lane, j2 = lane + 32;
-  const int s1 = j1 < cnt ? (int)W.csize[j1] : 0;
-  const int s2 = j2 < cnt ? (int)W.csize[j2] : 0;
+  const bool cst1 = j1 < cnt && ((cmask >> j1) & 1ull), cst2 = j2 < cnt && ((cmask >> j2) & 1ull);
+  const int s1 = j1 < cnt ? (cst1 ? 12 : (int)W.csize[j1]) : 0;
+  const int s2 = j2 < cnt ? (cst2 ? 12 : (int)W.csize[j2]) : 0;
   const int i1 = (int)warp_incl_scan_add((uint32_t)s1, lane);
   const int t1 = __shfl_sync(EQC_FULL, i1, 31);
   const int i2 = (int)warp_incl_scan_add((uint32_t)s2, lane) + t1;
   const int off1 = i1 - s1, off2 = i2 - s2;
   const int run = __shfl_sync(EQC_FULL, i2, 31);
+  uint32_t ps1 = cst1 ? 0x03030303u : (j1 < cnt ? W.cps[j1] : 0u);
+  uint32_t ps2 = cst2 ? 0x03030303u : (j2 < cnt ? W.cps[j2] : 0u);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j = h ? j2 : j1;
     const int off = h ? off2 : off1;
-    if (j < cnt && ((cmask >> j) & 1ull)) {
+    if (h ? cst2 : cst1) {
       int L;
       chunk_ptr(j, L);
-      const uint32_t v = W.cval[j];
+      const uint32_t v = swz ? swizzle(W.cval[j]) : W.cval[j];
       const uint8_t c = (uint8_t)(0x80 | (L - 1));
       uint8_t *gp = scr + off;
 #pragma unroll
@@ -274,8 +282,8 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid
   if (cnt > 0) {
     // table entries relative to the super-tile (rebased by the compaction)
     uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
-    if (j1 < cnt) table[j1] = make_uint2((uint32_t)(wexcl + off1), W.cps[j1]);
-    if (j2 < cnt) table[j2] = make_uint2((uint32_t)(wexcl + off2), W.cps[j2]);
+    if (j1 < cnt) table[j1] = make_uint2((uint32_t)(wexcl + off1), ps1);
+    if (j2 < cnt) table[j2] = make_uint2((uint32_t)(wexcl + off2), ps2);
   }
 }
 
