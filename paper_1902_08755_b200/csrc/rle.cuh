@@ -271,8 +271,11 @@ __device__ __forceinline__ void store_record(uint8_t *g, const uint8_t *st, int 
 // Decode plane record r[0..size) (staging bytes) of a chunk of length L into
 // byte p of out[0..3] (positions 4*lane + j).  `info` is per-warp scratch of
 // 128 uint16.  Returns false if the record is malformed (warp-uniform).
-__device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, int lane, int p,
-                                             uint32_t out[4], uint16_t *info) {
+template <bool FULL>
+__device__ __forceinline__ bool decode_plane_t(const uint8_t *r, int size, int L_, int lane, int p,
+                                               uint32_t out[4], uint16_t *info) {
+  // FULL: a 128-pixel chunk (every lane's 4 positions are valid)
+  const int L = FULL ? kC : L_;
   const int i0 = 4 * lane;
   if (size < 2) return false;
   const int ntok = r[0];
@@ -290,7 +293,7 @@ __device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, 
       if (size != 2 + L) return false;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (i0 + j < L) out[j] |= (uint32_t)r[2 + i0 + j] << (8 * p);
+        if (FULL || i0 + j < L) out[j] |= (uint32_t)r[2 + i0 + j] << (8 * p);
     }
     return true;
   }
@@ -332,7 +335,7 @@ __device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, 
       run = max(run, (int)((w4 >> (8 * j)) & 0xFFu));
       const uint32_t ti = __shfl_sync(EQC_FULL, tinfo, max(run - 1, 0));
       const int i = i0 + j;
-      if (i < L) {
+      if (FULL || i < L) {
         const int pi = (int)((ti >> 8) & 0xFFFFu) + ((ti >> 31) ? 0 : i - (int)(ti & 0xFFu));
         out[j] |= (uint32_t)r[pi] << (8 * p);
       }
@@ -403,6 +406,12 @@ __device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, 
     }
   }
   return true;
+}
+
+__device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, int lane, int p, uint32_t out[4],
+                                             uint16_t *info) {
+  return L == kC ? decode_plane_t<true>(r, size, L, lane, p, out, info)
+                 : decode_plane_t<false>(r, size, L, lane, p, out, info);
 }
 
 }  // namespace eqc_rle
