@@ -12,3 +12,10 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --mas
 echo "bench $X rc=$?" >> gpurun_out/bench_n${N}_${X}.log
 done
 tail -5 gpurun_out/pytest_multi_n${N}.log; for f in gpurun_out/bench_n${N}_*.json; do python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[1], d['value'], d['ms_per_step'])" $f; done; for f in gpurun_out/bench_n${N}_*.log; do tail -n 3 $f; done
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29512 \
+  scripts/bench_compose.py > gpurun_out/compose_c4_n${N}.json 2> gpurun_out/compose_c4_n${N}.log
+echo "compose rc=$?" >> gpurun_out/compose_c4_n${N}.log
+cat gpurun_out/compose_c4_n${N}.json
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29513 \
+  scripts/bench_compose.py --w 3840 --h 2160 > gpurun_out/compose_4k_n${N}.json 2> gpurun_out/compose_4k_n${N}.log
+cat gpurun_out/compose_4k_n${N}.json
