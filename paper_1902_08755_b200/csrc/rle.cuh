@@ -297,6 +297,41 @@ __device__ __forceinline__ bool decode_plane_t(const uint8_t *r, int size, int L
     }
     return true;
   }
+  if (ntok <= 4) {
+    // few tokens (typical of mixed background/foreground chunks): the token
+    // boundaries are computed once (uniform), each position selects its token
+    // by comparison -- no scans, no shuffles, no scratch
+    int st[4], ps[4], rp[4];
+    int pos = 0, pay = 1 + ntok;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      st[t] = pos;
+      ps[t] = pay;
+      rp[t] = 1;
+      if (t < ntok) {
+        const int c = r[1 + t];
+        const int len = (c & 0x7F) + 1;
+        rp[t] = c >> 7;
+        pos += len;
+        pay += (c & 0x80) ? 1 : len;
+      } else {
+        st[t] = 0x7FFF;  // never selected
+      }
+    }
+    if (pos != L || pay != size) return false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j;
+      if (FULL || i < L) {
+        const int t = (i >= st[1]) + (i >= st[2]) + (i >= st[3]);
+        const int s0 = sel4(t, st[0], st[1], st[2], st[3]);
+        const int p0 = sel4(t, ps[0], ps[1], ps[2], ps[3]);
+        const int r0 = sel4(t, rp[0], rp[1], rp[2], rp[3]);
+        out[j] |= (uint32_t)r[p0 + (r0 ? 0 : i - s0)] << (8 * p);
+      }
+    }
+    return true;
+  }
   if (ntok <= 32) {
     // lane t holds token t: start positions and payload indices by one packed
     // warp scan; each position finds its token as the last start at or before
