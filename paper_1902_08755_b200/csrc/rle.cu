@@ -616,8 +616,11 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
   __shared__ int64_t s_pb[kMaxStreams];
   __shared__ uint8_t s_flags[kMaxStreams];
   __shared__ int s_bad;
+  // phase-A cache: per warp, per position, per stream {offset, plane sizes, value, constant}
+  extern __shared__ __align__(16) uint4 s_cache[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = p.n, ns = 2 * n;
+  uint4 *cache = s_cache + (size_t)warp * kPosPerWarp * ns;
   if (tid == 0) s_bad = 0;
   __syncthreads();
   for (int q = tid; q < ns; q += blockDim.x) {
@@ -642,7 +645,7 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
   const int y = has ? c / p.S : 0;
   const int k = has ? c - y * p.S : 0;
   const int L = has ? min(kC, p.w - k * kC) : 0;
-  // ---- phase A
+  // ---- phase A: every stream's entry validated and probed, results cached
   bool ok = true, allc = true;
   uint32_t sd = 0xFFFFFFFFu, sc = 0;  // lane-partial scalar composite
   int sidx = 0x7FFFFFFF;
@@ -654,15 +657,18 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
     uint32_t pd, pc;
     ok = entry_lane(p.src[n + ii], s_pb[n + ii], nch, c, hi, L, lane, od, pd, 4) && ok;
     ok = entry_lane(p.src[ii], s_pb[ii], nch, c, hi, L, lane, oc, pc, 4) && ok;
-    if (hi && ok && allc) {
-      uint32_t dv, cv;
+    if (hi && ok) {
+      uint32_t dv = 0, cv = 0;
       const bool dc = probe_const(p.src[n + ii] + payload0 + od, pd, L, dv);
-      const bool cc = dc && probe_const(p.src[ii] + payload0 + oc, pc, L, cv);
+      const bool cc = probe_const(p.src[ii] + payload0 + oc, pc, L, cv);
+      if (cc && (s_flags[ii] & EQC_FLAG_SWIZZLE)) cv = unswizzle(cv);
+      cache[pos * ns + n + ii] = make_uint4((uint32_t)od, pd, dv, dc ? 1u : 0u);
+      cache[pos * ns + ii] = make_uint4((uint32_t)oc, pc, cv, cc ? 1u : 0u);
       if (dc && cc) {
-        if (dv < sd) {  // sources visited in increasing index: strict < keeps the lower
+        if (allc && dv < sd) {  // sources visited in increasing index: strict < keeps the lower
           sd = dv;
           sidx = i;
-          sc = (s_flags[ii] & EQC_FLAG_SWIZZLE) ? unswizzle(cv) : cv;
+          sc = cv;
         }
       } else {
         allc = false;
@@ -687,6 +693,7 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
     if (lane == 0) set_corrupt(p.status);
     return;
   }
+  __syncwarp();
   const unsigned cmask = __ballot_sync(EQC_FULL, sub == 0 && has && allc);
   const unsigned gmask = __ballot_sync(EQC_FULL, sub == 0 && has && !allc);
   // ---- phase B1: all-constant positions (bit 4*pos set)
@@ -702,20 +709,19 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
   // ---- phase B2: positions with at least one non-constant chunk
   for (unsigned mm = gmask; mm; mm &= mm - 1) {
     const int ii = __ffs(mm) - 1;
-    const int64_t ci = cb + (ii >> 2);
+    const int pi = ii >> 2;
     const int yi = __shfl_sync(EQC_FULL, y, ii), ki = __shfl_sync(EQC_FULL, k, ii), Li = __shfl_sync(EQC_FULL, L, ii);
+    const uint4 *pc_ = cache + pi * ns;
     uint32_t bc[4] = {0, 0, 0, 0}, bd[4] = {0, 0, 0, 0};
     bool good = true;
     for (int i = 0; i < n && good; ++i) {
-      const int qd = n + i, qc = i;
-      // entries were validated in phase A; re-read them (uniform, cached)
-      const uint2 ted = __ldg(reinterpret_cast<const uint2 *>(p.src[qd] + 32 + 8 * ci));
-      const uint8_t *recd = p.src[qd] + payload0 + ted.x;
-      uint32_t d[4], v;
-      if (probe_const(recd, ted.y, Li, v)) {
+      const uint4 ed = pc_[n + i];
+      uint32_t d[4];
+      if (ed.w) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) d[j] = v;
-      } else if (!decode_record(p.src[qd], p.src_bytes[qd], recd, ted.y, Li, lane, stage[warp], info[warp], d)) {
+        for (int j = 0; j < 4; ++j) d[j] = ed.z;
+      } else if (!decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + ed.x, ed.y, Li, lane,
+                                stage[warp], info[warp], d)) {
         good = false;
         break;
       }
@@ -723,19 +729,21 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = (i == 0) || d[j] < bd[j];  // ties keep the lower index
       if (!__any_sync(EQC_FULL, t[0] || t[1] || t[2] || t[3])) continue;  // hidden: colour never read
-      const uint2 tec = __ldg(reinterpret_cast<const uint2 *>(p.src[qc] + 32 + 8 * ci));
-      const uint8_t *recc = p.src[qc] + payload0 + tec.x;
+      const uint4 ec = pc_[i];
       uint32_t col[4];
-      if (probe_const(recc, tec.y, Li, v)) {
+      if (ec.w) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) col[j] = v;
-      } else if (!decode_record(p.src[qc], p.src_bytes[qc], recc, tec.y, Li, lane, stage[warp], info[warp], col)) {
-        good = false;
-        break;
-      }
-      if (s_flags[qc] & EQC_FLAG_SWIZZLE) {
+        for (int j = 0; j < 4; ++j) col[j] = ec.z;  // already unswizzled
+      } else {
+        if (!decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + ec.x, ec.y, Li, lane, stage[warp],
+                           info[warp], col)) {
+          good = false;
+          break;
+        }
+        if (s_flags[i] & EQC_FLAG_SWIZZLE) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
+          for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -912,6 +920,14 @@ extern "C" int compositor_depth_rle(int n, const uint8_t *const *color_rle, cons
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
   const int64_t grid = ((int64_t)p.S * h + kFWarps * kPosPerWarp - 1) / (kFWarps * kPosPerWarp);
   if (grid > 0x7FFFFFFFll || (int64_t)p.S * h > 0x7FFFFFFFll) return EQC_E_INVALID;
-  depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
+  const size_t smem = (size_t)kFWarps * kPosPerWarp * 2 * n * sizeof(uint4);
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(depth_rle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((size_t)kFWarps * kPosPerWarp * 2 * EQC_MAX_SOURCES * sizeof(uint4))) != cudaSuccess)
+      return EQC_E_CUDA;
+    configured = true;
+  }
+  depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, smem, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
