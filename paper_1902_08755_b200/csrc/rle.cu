@@ -512,6 +512,24 @@ __device__ __forceinline__ bool entry_lane(const uint8_t *src, int64_t payload_b
   return ok;
 }
 
+// Lane-local variant: loads chunk c-1's entry itself (no warp collective).
+__device__ __forceinline__ bool entry_local(const uint8_t *src, int64_t payload_bytes, int64_t nchunks, int64_t c,
+                                            int L, int64_t &off, uint32_t &ps) {
+  const uint2 te = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * c));
+  off = te.x;
+  ps = te.y;
+  const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
+  const int64_t end = off + s0 + s1 + s2 + s3;
+  int64_t prev = 0;
+  if (c > 0) {
+    const uint2 tp = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * (c - 1)));
+    prev = (int64_t)tp.x + (tp.y & 0xFF) + ((tp.y >> 8) & 0xFF) + ((tp.y >> 16) & 0xFF) + (tp.y >> 24);
+  }
+  bool ok = off == prev && end <= payload_bytes && s0 <= L + 2 && s1 <= L + 2 && s2 <= L + 2 && s3 <= L + 2;
+  if (c == nchunks - 1) ok = ok && end == payload_bytes;
+  return ok;
+}
+
 // One warp per 32 x (128 / C) chunks: lane-parallel table validation and
 // constant-chunk classification, then constant chunks are filled with one
 // 128-bit store per lane and the others decoded warp-cooperatively.
@@ -597,8 +615,7 @@ struct FusedParams {
 };
 
 constexpr int kMaxStreams = 2 * EQC_MAX_SOURCES;
-constexpr int kPosPerWarp = 8;  // chunk positions per warp (4 lanes each in phase A)
-constexpr int kFWarps = 2;      // small CTAs: the per-warp work is uneven (mixed vs background chunks)
+constexpr int kFWarps = 4;      // fused kernel: one chunk position per warp, 4 warps per CTA
 
 // Warp per 8 consecutive chunk positions.
 //  Phase A (4 lanes per position, lane sub = lane & 3 takes sources
@@ -616,11 +633,8 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
   __shared__ int64_t s_pb[kMaxStreams];
   __shared__ uint8_t s_flags[kMaxStreams];
   __shared__ int s_bad;
-  // phase-A cache: per warp, per position, per stream {offset, plane sizes, value, constant}
-  extern __shared__ __align__(16) uint4 s_cache[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = p.n, ns = 2 * n;
-  uint4 *cache = s_cache + (size_t)warp * kPosPerWarp * ns;
   if (tid == 0) s_bad = 0;
   __syncthreads();
   for (int q = tid; q < ns; q += blockDim.x) {
@@ -637,128 +651,110 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
   }
   const int nch = p.S * p.h;
   const int64_t payload0 = 32 + 8 * (int64_t)nch;
-  const int cb = (blockIdx.x * kFWarps + warp) * kPosPerWarp;
-  if (cb >= nch) return;
-  const int pos = lane >> 2, sub = lane & 3;
-  const int c = cb + pos;
-  const bool has = c < nch;
-  const int y = has ? c / p.S : 0;
-  const int k = has ? c - y * p.S : 0;
-  const int L = has ? min(kC, p.w - k * kC) : 0;
-  // ---- phase A: every stream's entry validated and probed, results cached
-  bool ok = true, allc = true;
-  uint32_t sd = 0xFFFFFFFFu, sc = 0;  // lane-partial scalar composite
-  int sidx = 0x7FFFFFFF;
-  for (int i0 = 0; i0 < n; i0 += 4) {
-    const int i = i0 + sub;
-    const bool hi = has && i < n;
-    const int ii = min(i, n - 1);
-    int64_t od, oc;
-    uint32_t pd, pc;
-    ok = entry_lane(p.src[n + ii], s_pb[n + ii], nch, c, hi, L, lane, od, pd, 4) && ok;
-    ok = entry_lane(p.src[ii], s_pb[ii], nch, c, hi, L, lane, oc, pc, 4) && ok;
-    if (hi && ok) {
-      uint32_t dv = 0, cv = 0;
-      const bool dc = probe_const(p.src[n + ii] + payload0 + od, pd, L, dv);
-      const bool cc = probe_const(p.src[ii] + payload0 + oc, pc, L, cv);
-      if (cc && (s_flags[ii] & EQC_FLAG_SWIZZLE)) cv = unswizzle(cv);
-      cache[pos * ns + n + ii] = make_uint4((uint32_t)od, pd, dv, dc ? 1u : 0u);
-      cache[pos * ns + ii] = make_uint4((uint32_t)oc, pc, cv, cc ? 1u : 0u);
-      if (dc && cc) {
-        if (allc && dv < sd) {  // sources visited in increasing index: strict < keeps the lower
-          sd = dv;
-          sidx = i;
-          sc = cv;
-        }
-      } else {
-        allc = false;
-      }
-    }
-  }
-  // merge the four partial minima of a position by (depth, index)
+  const int c = blockIdx.x * kFWarps + warp;  // chunk position of this warp
+  if (c >= nch) return;
+  const int y = c / p.S, k = c - y * p.S;
+  const int L = min(kC, p.w - k * kC);
+  // ---- phase A: lane i < n validates and probes source i's depth and colour
+  // chunks (sources 32.. in further passes); results stay in registers
+  const int npass = (n + 31) >> 5;
+  uint4 ed[2], ec[2];  // {offset, plane sizes, value, constant} per pass
+  bool ok = true;
+  bool allc = true;
 #pragma unroll
-  for (int d = 1; d <= 2; d <<= 1) {
-    const uint32_t od = __shfl_xor_sync(EQC_FULL, sd, d), oc = __shfl_xor_sync(EQC_FULL, sc, d);
-    const int oi = __shfl_xor_sync(EQC_FULL, sidx, d);
-    if (od < sd || (od == sd && oi < sidx)) {
-      sd = od;
-      sc = oc;
-      sidx = oi;
+  for (int ps = 0; ps < 2; ++ps) {
+    ed[ps] = ec[ps] = make_uint4(0, 0, 0, 1);
+    if (ps >= npass) continue;
+    const int i = ps * 32 + lane;
+    if (i < n) {
+      int64_t od, oc;
+      uint32_t pd, pc;
+      ok = entry_local(p.src[n + i], s_pb[n + i], nch, c, L, od, pd) && ok;
+      ok = entry_local(p.src[i], s_pb[i], nch, c, L, oc, pc) && ok;
+      uint32_t dv = 0, cv = 0;
+      const bool dc = ok && probe_const(p.src[n + i] + payload0 + od, pd, L, dv);
+      const bool cc = ok && probe_const(p.src[i] + payload0 + oc, pc, L, cv);
+      if (cc && (s_flags[i] & EQC_FLAG_SWIZZLE)) cv = unswizzle(cv);
+      ed[ps] = make_uint4((uint32_t)od, pd, dv, dc ? 1u : 0u);
+      ec[ps] = make_uint4((uint32_t)oc, pc, cv, cc ? 1u : 0u);
+      allc = allc && dc && cc;
     }
-    allc = __shfl_xor_sync(EQC_FULL, (int)allc, d) && allc;
-    ok = __shfl_xor_sync(EQC_FULL, (int)ok, d) && ok;
   }
-  const unsigned bad = __ballot_sync(EQC_FULL, has && !ok);
-  if (bad) {
+  if (!__all_sync(EQC_FULL, ok)) {
     if (lane == 0) set_corrupt(p.status);
     return;
   }
-  __syncwarp();
-  const unsigned cmask = __ballot_sync(EQC_FULL, sub == 0 && has && allc);
-  const unsigned gmask = __ballot_sync(EQC_FULL, sub == 0 && has && !allc);
-  // ---- phase B1: all-constant positions (bit 4*pos set)
-  for (unsigned mm = cmask; mm; mm &= mm - 1) {
-    const int i = __ffs(mm) - 1;
-    const int yi = __shfl_sync(EQC_FULL, y, i), ki = __shfl_sync(EQC_FULL, k, i), Li = __shfl_sync(EQC_FULL, L, i);
-    const uint32_t ci = __shfl_sync(EQC_FULL, sc, i), di = __shfl_sync(EQC_FULL, sd, i);
-    const uint32_t pc[4] = {ci, ci, ci, ci}, pd[4] = {di, di, di, di};
-    const int64_t row = (int64_t)yi * p.out_pitch + (int64_t)ki * kC;
-    store_px(p.out_color + row, Li, lane, p.vec != 0, pc);
-    if (p.out_depth) store_px(p.out_depth + row, Li, lane, p.vec != 0, pd);
-  }
-  // ---- phase B2: positions with at least one non-constant chunk
-  for (unsigned mm = gmask; mm; mm &= mm - 1) {
-    const int ii = __ffs(mm) - 1;
-    const int pi = ii >> 2;
-    const int yi = __shfl_sync(EQC_FULL, y, ii), ki = __shfl_sync(EQC_FULL, k, ii), Li = __shfl_sync(EQC_FULL, L, ii);
-    const uint4 *pc_ = cache + pi * ns;
-    uint32_t bc[4] = {0, 0, 0, 0}, bd[4] = {0, 0, 0, 0};
-    bool good = true;
-    for (int i = 0; i < n && good; ++i) {
-      const uint4 ed = pc_[n + i];
-      uint32_t d[4];
-      if (ed.w) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) d[j] = ed.z;
-      } else if (!decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + ed.x, ed.y, Li, lane,
-                                stage[warp], info[warp], d)) {
-        good = false;
-        break;
-      }
-      bool t[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) t[j] = (i == 0) || d[j] < bd[j];  // ties keep the lower index
-      if (!__any_sync(EQC_FULL, t[0] || t[1] || t[2] || t[3])) continue;  // hidden: colour never read
-      const uint4 ec = pc_[i];
-      uint32_t col[4];
-      if (ec.w) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) col[j] = ec.z;  // already unswizzled
-      } else {
-        if (!decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + ec.x, ec.y, Li, lane, stage[warp],
-                           info[warp], col)) {
-          good = false;
-          break;
-        }
-        if (s_flags[i] & EQC_FLAG_SWIZZLE) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        bd[j] = t[j] ? d[j] : bd[j];
-        bc[j] = t[j] ? col[j] : bc[j];
+  const int64_t row = (int64_t)y * p.out_pitch + (int64_t)k * kC;
+  if (__all_sync(EQC_FULL, allc)) {
+    // every chunk of this position is one value: composite the scalars --
+    // minimum depth, ties to the lowest source index
+    uint32_t bdv = 0xFFFFFFFFu, bcv = 0;
+    int bi = 0x7FFFFFFF;
+    for (int ps = 0; ps < npass; ++ps) {
+      const int i = ps * 32 + lane;
+      const uint32_t dv = i < n ? ed[ps].z : 0xFFFFFFFFu;
+      const uint32_t m = __reduce_min_sync(EQC_FULL, dv);
+      const unsigned who = __ballot_sync(EQC_FULL, i < n && dv == m);
+      const int l0 = __ffs(who) - 1;
+      const int ii = ps * 32 + l0;
+      const uint32_t cv = __shfl_sync(EQC_FULL, ec[ps].z, l0);
+      if (who && (m < bdv || (m == bdv && ii < bi))) {
+        bdv = m;
+        bcv = cv;
+        bi = ii;
       }
     }
-    if (!good) {
+    const uint32_t pc[4] = {bcv, bcv, bcv, bcv}, pd[4] = {bdv, bdv, bdv, bdv};
+    store_px(p.out_color + row, L, lane, p.vec != 0, pc);
+    if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, pd);
+    return;
+  }
+  // ---- phase B: decode depth first; a source's colour only where it wins
+  uint32_t bc[4] = {0, 0, 0, 0}, bd[4] = {0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    const int ps = i >> 5, li = i & 31;
+    const uint4 e1 = ps ? ed[1] : ed[0];
+    const uint32_t dx = __shfl_sync(EQC_FULL, e1.x, li), dy = __shfl_sync(EQC_FULL, e1.y, li),
+                   dz = __shfl_sync(EQC_FULL, e1.z, li), dw = __shfl_sync(EQC_FULL, e1.w, li);
+    uint32_t d[4];
+    if (dw) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[j] = dz;
+    } else if (!decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane,
+                              stage[warp], info[warp], d)) {
       if (lane == 0) set_corrupt(p.status);
-      continue;
+      return;
     }
-    const int64_t row = (int64_t)yi * p.out_pitch + (int64_t)ki * kC;
-    store_px(p.out_color + row, Li, lane, p.vec != 0, bc);
-    if (p.out_depth) store_px(p.out_depth + row, Li, lane, p.vec != 0, bd);
+    bool t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t[j] = (i == 0) || d[j] < bd[j];  // ties keep the lower index
+    if (!__any_sync(EQC_FULL, t[0] || t[1] || t[2] || t[3])) continue;  // hidden: colour never read
+    const uint4 e2 = ps ? ec[1] : ec[0];
+    const uint32_t cx = __shfl_sync(EQC_FULL, e2.x, li), cy = __shfl_sync(EQC_FULL, e2.y, li),
+                   cz = __shfl_sync(EQC_FULL, e2.z, li), cw = __shfl_sync(EQC_FULL, e2.w, li);
+    uint32_t col[4];
+    if (cw) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) col[j] = cz;  // already unswizzled
+    } else {
+      if (!decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, L, lane, stage[warp], info[warp],
+                         col)) {
+        if (lane == 0) set_corrupt(p.status);
+        return;
+      }
+      if (s_flags[i] & EQC_FLAG_SWIZZLE) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bd[j] = t[j] ? d[j] : bd[j];
+      bc[j] = t[j] ? col[j] : bc[j];
+    }
   }
+  store_px(p.out_color + row, L, lane, p.vec != 0, bc);
+  if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, bd);
 }
 
 inline bool aligned(const void *q, uintptr_t a) { return ((uintptr_t)q & (a - 1)) == 0; }
@@ -918,16 +914,8 @@ extern "C" int compositor_depth_rle(int n, const uint8_t *const *color_rle, cons
   p.h = h;
   p.S = (w + kC - 1) / kC;
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
-  const int64_t grid = ((int64_t)p.S * h + kFWarps * kPosPerWarp - 1) / (kFWarps * kPosPerWarp);
+  const int64_t grid = ((int64_t)p.S * h + kFWarps - 1) / kFWarps;
   if (grid > 0x7FFFFFFFll || (int64_t)p.S * h > 0x7FFFFFFFll) return EQC_E_INVALID;
-  const size_t smem = (size_t)kFWarps * kPosPerWarp * 2 * n * sizeof(uint4);
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(depth_rle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((size_t)kFWarps * kPosPerWarp * 2 * EQC_MAX_SOURCES * sizeof(uint4))) != cudaSuccess)
-      return EQC_E_CUDA;
-    configured = true;
-  }
-  depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, smem, (cudaStream_t)stream>>>(p);
+  depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
