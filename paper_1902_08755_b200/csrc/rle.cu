@@ -27,12 +27,12 @@ using namespace eqc_rle;
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
-constexpr int kSTChunksPerWarp = 64; // encoder: consecutive chunks per warp in a super-tile
+constexpr int kSTChunksPerWarp = 16; // encoder: consecutive chunks per warp (small: balances uneven chunks)
 static_assert(kSTChunksPerWarp <= 64, "two table-entry registers per lane");
 constexpr int kEncWarps = 8;                            // coder warps per CTA (encoder)
 constexpr int kSTChunks = kEncWarps * kSTChunksPerWarp; // chunks per super-tile (CTA of the encoder)
 constexpr int kRecMax = 4 * (kC + 2);                  // worst-case chunk record bytes (520)
-constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 33280 = 260 x 128 B
+constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 8320 = 65 x 128 B
 constexpr int kMaxBatch = 64;
 
 // workspace layout: tile_info[count * tiles_per_image][16] int32 (super-tile
@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_compact_kernel(const __gri
   const EncImage im = p.img[m];
   if (warp == 0) {
     int64_t acc = 0;
+#pragma unroll 4
     for (int64_t q = lane; q < lt; q += 32) acc += __ldg(p.tile_info + (t0 + q) * kTileInfo);
     for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(EQC_FULL, acc, d);
     if (lane == 0) {
