@@ -301,6 +301,7 @@ struct CompactParams {
 // and discards its scratch lines from L2; the last super-tile of an image
 // writes the header and the stream size.
 __global__ void __launch_bounds__(kEncWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
+  __shared__ int64_t s_part[kEncWarps];
   __shared__ int64_t s_off;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t tile = blockIdx.x;
@@ -308,27 +309,32 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_compact_kernel(const __gri
   const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
   const int64_t t0 = (int64_t)m * p.tiles_per_image;
   const EncImage im = p.img[m];
-  if (warp == 0) {
+  {
+    // all warps sum a slice of the preceding super-tiles' totals
     int64_t acc = 0;
 #pragma unroll 4
-    for (int64_t q = lane; q < lt; q += 32) acc += __ldg(p.tile_info + (t0 + q) * kTileInfo);
+    for (int64_t q = tid; q < lt; q += kEncWarps * 32) acc += __ldg(p.tile_info + (t0 + q) * kTileInfo);
     for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(EQC_FULL, acc, d);
-    if (lane == 0) {
-      s_off = acc;
-      if (lt == p.tiles_per_image - 1) {
-        const int64_t payload = acc + __ldg(p.tile_info + tile * kTileInfo);
-        uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
-        h32[0] = kMagic;
-        h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
-                 ((uint32_t)kLog2C << 24);
-        h32[2] = (uint32_t)p.w;
-        h32[3] = (uint32_t)p.h;
-        h32[4] = (uint32_t)p.nchunks;
-        h32[5] = 0u;
-        h32[6] = (uint32_t)(uint64_t)payload;
-        h32[7] = (uint32_t)((uint64_t)payload >> 32);
-        *im.d_size = 32 + 8 * p.nchunks + payload;
-      }
+    if (lane == 0) s_part[warp] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int64_t acc = 0;
+    for (int w = 0; w < kEncWarps; ++w) acc += s_part[w];
+    s_off = acc;
+    if (lt == p.tiles_per_image - 1) {
+      const int64_t payload = acc + __ldg(p.tile_info + tile * kTileInfo);
+      uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
+      h32[0] = kMagic;
+      h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
+               ((uint32_t)kLog2C << 24);
+      h32[2] = (uint32_t)p.w;
+      h32[3] = (uint32_t)p.h;
+      h32[4] = (uint32_t)p.nchunks;
+      h32[5] = 0u;
+      h32[6] = (uint32_t)(uint64_t)payload;
+      h32[7] = (uint32_t)((uint64_t)payload >> 32);
+      *im.d_size = 32 + 8 * p.nchunks + payload;
     }
   }
   __syncthreads();
