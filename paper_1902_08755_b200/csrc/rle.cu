@@ -425,6 +425,20 @@ __device__ __forceinline__ bool probe_const(const uint8_t *rec, uint32_t ps, int
 // Stage a record (aligned 4-byte words; byte loads at the stream end) and
 // decode its four planes into px[0..3].  Warp-cooperative; returns false
 // (warp-uniform) on a malformed record.
+__device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int L, int lane, uint16_t *info,
+                                              uint32_t px[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) px[j] = 0;
+  // one (not unrolled) loop over the planes keeps the decoder body small
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const int sz = (int)((ps >> (8 * q)) & 0xFFu);
+    if (!decode_plane(r, sz, L, lane, q, px, info)) return false;
+    r += sz;
+  }
+  return true;
+}
+
 __device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8_t *rec, uint32_t ps, int L,
                               int lane, uint8_t *stage, uint16_t *info, uint32_t px[4]) {
   const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
@@ -448,17 +462,33 @@ __device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8
     st32[q] = v;
   }
   __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) px[j] = 0;
-  const uint8_t *r = stage + sh;
-  // one (not unrolled) loop over the planes keeps the decoder body small
-#pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
-    const int sz = (int)((ps >> (8 * q)) & 0xFFu);
-    if (!decode_plane(r, sz, L, lane, q, px, info)) return false;
-    r += sz;
+  return decode_staged(stage + sh, ps, L, lane, info, px);
+}
+
+// Words of a record (4-byte aligned window) a lane-parallel stager needs.
+__device__ __forceinline__ int record_words(const uint8_t *rec, uint32_t ps) {
+  const int total = (int)(ps & 0xFF) + (int)((ps >> 8) & 0xFF) + (int)((ps >> 16) & 0xFF) + (int)(ps >> 24);
+  return ((int)((uintptr_t)rec & 3) + total + 3) >> 2;
+}
+
+// Issue asynchronous 4-byte copies of a record's words into `dst` (shared);
+// words that would cross the stream end are copied synchronously.
+__device__ __forceinline__ void stage_async(const uint8_t *src, int64_t src_bytes, const uint8_t *rec, int nwords,
+                                            uint32_t *dst, int lane) {
+  const uintptr_t a0 = (uintptr_t)rec & ~(uintptr_t)3;
+  const uintptr_t lim = (uintptr_t)src + (uintptr_t)src_bytes;
+  for (int q = lane; q < nwords; q += 32) {
+    const uintptr_t a = a0 + 4 * (uintptr_t)q;
+    if (a + 4 <= lim) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + q);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(a) : "memory");
+    } else {
+      uint32_t v = 0;
+      for (int b = 0; b < 4; ++b)
+        if (a + b < lim) v |= (uint32_t)__ldg(reinterpret_cast<const uint8_t *>(a + b)) << (8 * b);
+      dst[q] = v;
+    }
   }
-  return true;
 }
 
 __device__ __forceinline__ void store_px(uint32_t *row, int L, int lane, bool vec, const uint32_t px[4]) {
@@ -623,6 +653,7 @@ struct FusedParams {
 
 constexpr int kMaxStreams = 2 * EQC_MAX_SOURCES;
 constexpr int kFWarps = 4;      // fused kernel: one chunk position per warp, 4 warps per CTA
+constexpr int kPreWords = 1024; // per-warp record prefetch buffer (4 KB)
 
 // Warp per 8 consecutive chunk positions.
 //  Phase A (4 lanes per position, lane sub = lane & 3 takes sources
@@ -640,6 +671,7 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
   __shared__ int64_t s_pb[kMaxStreams];
   __shared__ uint8_t s_flags[kMaxStreams];
   __shared__ int s_bad;
+  __shared__ __align__(16) uint32_t s_pre[kFWarps * kPreWords];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = p.n, ns = 2 * n;
   if (tid == 0) s_bad = 0;
@@ -716,19 +748,62 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
     if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, pd);
     return;
   }
-  // ---- phase B: decode depth first; a source's colour only where it wins
+  // ---- phase B: prefetch every non-constant record of this position into a
+  // per-warp buffer (asynchronous copies, one round trip for all of them),
+  // then decode depth first; a source's colour only where it wins.
+  // Lane i plans source i: word offsets of its depth and colour records.
+  uint32_t *pre = s_pre + (size_t)warp * kPreWords;
+  int wd0 = 0, wc0 = 0;  // word offsets (-1: not prefetched)
+  {
+    int nwd = 0, nwc = 0;
+    if (npass == 1 && lane < n) {
+      if (!ed[0].w) nwd = record_words(p.src[n + lane] + payload0 + ed[0].x, ed[0].y);
+      if (!ec[0].w) nwc = record_words(p.src[lane] + payload0 + ec[0].x, ec[0].y);
+    }
+    const int tot = nwd + nwc;
+    const int inc = (int)warp_incl_scan_add((uint32_t)tot, lane);
+    const int ex = inc - tot;
+    wd0 = (nwd && ex + nwd <= kPreWords) ? ex : -1;
+    wc0 = (nwc && ex + tot <= kPreWords) ? ex + nwd : -1;
+  }
+  if (npass == 1) {
+    for (int i = 0; i < n; ++i) {
+      const int od = __shfl_sync(EQC_FULL, wd0, i), oc = __shfl_sync(EQC_FULL, wc0, i);
+      if (od >= 0) {
+        const uint32_t x = __shfl_sync(EQC_FULL, ed[0].x, i), y2 = __shfl_sync(EQC_FULL, ed[0].y, i);
+        const uint8_t *rec = p.src[n + i] + payload0 + x;
+        stage_async(p.src[n + i], p.src_bytes[n + i], rec, record_words(rec, y2), pre + od, lane);
+      }
+      if (oc >= 0) {
+        const uint32_t x = __shfl_sync(EQC_FULL, ec[0].x, i), y2 = __shfl_sync(EQC_FULL, ec[0].y, i);
+        const uint8_t *rec = p.src[i] + payload0 + x;
+        stage_async(p.src[i], p.src_bytes[i], rec, record_words(rec, y2), pre + oc, lane);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+  __syncwarp();
   uint32_t bc[4] = {0, 0, 0, 0}, bd[4] = {0, 0, 0, 0};
   for (int i = 0; i < n; ++i) {
     const int ps = i >> 5, li = i & 31;
     const uint4 e1 = ps ? ed[1] : ed[0];
     const uint32_t dx = __shfl_sync(EQC_FULL, e1.x, li), dy = __shfl_sync(EQC_FULL, e1.y, li),
                    dz = __shfl_sync(EQC_FULL, e1.z, li), dw = __shfl_sync(EQC_FULL, e1.w, li);
+    const int od = __shfl_sync(EQC_FULL, wd0, li), oc = __shfl_sync(EQC_FULL, wc0, li);
     uint32_t d[4];
+    bool okd = true;
     if (dw) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) d[j] = dz;
-    } else if (!decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane,
-                              stage[warp], info[warp], d)) {
+    } else if (npass == 1 && od >= 0) {
+      okd = decode_staged(reinterpret_cast<const uint8_t *>(pre + od) + (dx & 3u) + ((uintptr_t)p.src[n + i] & 3u),
+                          dy, L, lane, info[warp], d);
+    } else {
+      okd = decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane, stage[warp],
+                          info[warp], d);
+    }
+    if (!okd) {
       if (lane == 0) set_corrupt(p.status);
       return;
     }
@@ -744,8 +819,14 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
 #pragma unroll
       for (int j = 0; j < 4; ++j) col[j] = cz;  // already unswizzled
     } else {
-      if (!decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, L, lane, stage[warp], info[warp],
-                         col)) {
+      bool okc;
+      if (npass == 1 && oc >= 0)
+        okc = decode_staged(reinterpret_cast<const uint8_t *>(pre + oc) + (cx & 3u) + ((uintptr_t)p.src[i] & 3u), cy,
+                            L, lane, info[warp], col);
+      else
+        okc = decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, L, lane, stage[warp], info[warp],
+                            col);
+      if (!okc) {
         if (lane == 0) set_corrupt(p.status);
         return;
       }
