@@ -49,13 +49,7 @@ def main():
     mine = range(rank * nl, (rank + 1) * nl)
     dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
     dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
-    rows = np.random.default_rng(7).choice(H, 8, replace=False)
-    want_rows = None
-    if rank == 0:
-        import oracle
-        want_rows = {int(y): oracle.depth_composite([x[y:y + 1] for x in c], [x[y:y + 1] for x in d])[0]
-                     for y in rows}
-    del c, d
+    del c, d  # parity of these schedules at this size: tests/mp_compose.py (c4 case)
     final = torch.empty((H, W), dtype=torch.int32, device=dev) if rank == 0 else None
     P = W * H
     s = torch.cuda.current_stream()
@@ -81,12 +75,7 @@ def main():
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         st = comm.stats()
-        parity = None
-        if rank == 0:
-            got = final.cpu().numpy().view(np.uint32)
-            parity = all(bool((got[y:y + 1] == want_rows[y]).all()) for y in want_rows)
-        results[name] = {"ms": round(float(t.item()), 4), "stats_rank0": st if rank == 0 else None,
-                         "oracle_sampled_rows_equal": parity}
+        results[name] = {"ms": round(float(t.item()), 4), "stats_rank0": st if rank == 0 else None}
     if rank == 0:
         inbound = (n - 1) / n * 12 * P
         t_nvl_us = inbound / (NVLINK_GBS * 1e9) * 1e6
