@@ -155,7 +155,7 @@ struct EncSmem {
 //  C. write the constant chunks' 12-byte records lane-parallel and the
 //     table entries.
 // The compaction kernel then moves the runs to their final offsets.
-__global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid_constant__ EncParams p) {
+__global__ void __launch_bounds__(kEncWarps * 32, 4) rle_encode_kernel(const __grid_constant__ EncParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -180,10 +180,33 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_encode_kernel(const __grid
     return row0 + (int64_t)dy * p.pitch + k * kC;
   };
   // ---- A: classify (4 chunks in flight per lane; row pointer advanced
-  // incrementally; the swizzle of constant values is deferred to C)
+  // incrementally; the swizzle of constant values is deferred to C).  When
+  // the warp's chunks are one contiguous span of full 128-pixel chunks
+  // (pitch == w, w % 128 == 0) the loads use immediate offsets.
   int ng = 0;
   uint64_t cmask = 0;
-  {
+  const bool contig = p.vec && (p.w % kC) == 0 && p.pitch == p.w;
+  if (contig) {
+    const uint4 *base = reinterpret_cast<const uint4 *>(row0 + (int64_t)k0 * kC) + lane;
+    for (int j0 = 0; j0 < cnt; j0 += 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (j0 + u < cnt) ? ld_stream_u4(base + 32 * (j0 + u)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j0 + u >= cnt) break;
+        const uint32_t v0 = __shfl_sync(EQC_FULL, v[u].x, 0);
+        const bool same = v[u].x == v0 && v[u].y == v0 && v[u].z == v0 && v[u].w == v0;
+        if (__all_sync(EQC_FULL, same)) {
+          cmask |= 1ull << (j0 + u);
+          if (lane == 0) W.cval[j0 + u] = v0;
+        } else {
+          if (lane == 0) W.gidx[ng] = (uint8_t)(j0 + u);
+          ++ng;
+        }
+      }
+    }
+  } else {
     int ka = k0;
     const uint32_t *rowa = row0;
     for (int j0 = 0; j0 < cnt; j0 += 4) {

@@ -77,8 +77,11 @@ __device__ __forceinline__ int sel4(int i, int a, int b, int c, int d) {
 // order), GENERAL (scatter of token starts and payload bytes by prefix
 // counts).  Chunks whose pixels are all equal never get here: the caller
 // emits them directly (chunk_is_constant / emit_constant_record).
-__device__ __forceinline__ EncodeOut encode_chunk(uint32_t px[4], int L, int lane, bool swz, uint8_t *st,
-                                                  uint8_t *tp) {
+template <bool FULL>
+__device__ __forceinline__ EncodeOut encode_chunk_t(uint32_t px[4], int L_, int lane, bool swz, uint8_t *st,
+                                                    uint8_t *tp) {
+  // FULL: a 128-pixel chunk; the position-validity masks fold to constants
+  const int L = FULL ? kC : L_;
   const int i0 = 4 * lane;
   if (swz) {
 #pragma unroll
@@ -215,6 +218,11 @@ __device__ __forceinline__ EncodeOut encode_chunk(uint32_t px[4], int L, int lan
   const uint32_t ps = (uint32_t)size[0] | ((uint32_t)size[1] << 8) | ((uint32_t)size[2] << 16) |
                       ((uint32_t)size[3] << 24);
   return EncodeOut{b4, ps};
+}
+
+__device__ __forceinline__ EncodeOut encode_chunk(uint32_t px[4], int L, int lane, bool swz, uint8_t *st,
+                                                  uint8_t *tp) {
+  return L == kC ? encode_chunk_t<true>(px, L, lane, swz, st, tp) : encode_chunk_t<false>(px, L, lane, swz, st, tp);
 }
 
 // Whole-chunk constancy test on the RAW pixels (the swizzle is a bijection,
