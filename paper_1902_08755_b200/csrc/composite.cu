@@ -102,22 +102,25 @@ struct Acc4 {
 };
 
 // x = s + x * (1 - a_s/255) per channel, all in units of 1/255 (fp32 FMAs).
+// Byte -> float conversions are split between the integer-convert pipe
+// (I2F.U8 with byte select, R and G) and the ALU/FMA pipes (PRMT + FADD,
+// B and A) so neither pipe limits the issue rate; the alpha float is shared
+// by the transparency factor and the alpha channel.
 __device__ __forceinline__ void over(Acc4 &x, uint32_t s) {
-  // 255 - a exactly: (2^23 + 255) - (2^23 + a)
-  const float t = 8388863.0f - __uint_as_float(__byte_perm(s, 0x4B000000u, 0x7443));
-  const float f = t * (1.0f / 255.0f);
-  x.r = fmaf(x.r, f, byte_f<0>(s));
-  x.g = fmaf(x.g, f, byte_f<1>(s));
+  const float a = byte_f<3>(s);
+  const float f = fmaf(a, -1.0f / 255.0f, 1.0f);  // 1 - a/255 (a = 255 -> |f| < 1e-8)
+  x.r = fmaf(x.r, f, __uint2float_rn(s & 0xFFu));
+  x.g = fmaf(x.g, f, __uint2float_rn((s >> 8) & 0xFFu));
   x.b = fmaf(x.b, f, byte_f<2>(s));
-  x.a = fmaf(x.a, f, byte_f<3>(s));
+  x.a = fmaf(x.a, f, a);
 }
 
 __device__ __forceinline__ uint32_t pack_round(const Acc4 &x) {
   // one rounding to RGBA8 (round-to-nearest), clamped to [0, 255]
-  uint32_t r = min(__float2uint_rn(x.r), 255u);
-  uint32_t g = min(__float2uint_rn(x.g), 255u);
-  uint32_t b = min(__float2uint_rn(x.b), 255u);
-  uint32_t a = min(__float2uint_rn(x.a), 255u);
+  uint32_t r = min(__float2uint_rn(fmaxf(x.r, 0.0f)), 255u);
+  uint32_t g = min(__float2uint_rn(fmaxf(x.g, 0.0f)), 255u);
+  uint32_t b = min(__float2uint_rn(fmaxf(x.b, 0.0f)), 255u);
+  uint32_t a = min(__float2uint_rn(fmaxf(x.a, 0.0f)), 255u);
   return r | (g << 8) | (b << 16) | (a << 24);
 }
 
