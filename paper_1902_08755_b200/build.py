@@ -57,17 +57,20 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile and link libeqc.  ``out``/``defines`` build tuning variants
+    (e.g. ``defines=["EQC_ENC_WARPS=4"]``) next to the default library."""
+    if out == LIB and not defines and not force and not needs_build():
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    obj_dir = OBJ if out == LIB else out + ".objs"
+    os.makedirs(obj_dir, exist_ok=True)
     inc, libdir = nccl_dirs()
     extra_inc = ["-I", INCLUDE] + (["-I", inc] if inc else [])
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *CFLAGS, *extra_inc, "-c", src, "-o", obj]
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *ARCH, *CFLAGS, *extra_inc, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if inc:
             cmd += ["-DEQC_HAVE_NCCL=1"]
         if verbose:
@@ -76,21 +79,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     failed = []
     for pr, src in procs:
-        out, _ = pr.communicate()
-        if out and (verbose or pr.returncode):
-            sys.stderr.write(out.decode(errors="replace"))
+        log, _ = pr.communicate()
+        if log and (verbose or pr.returncode):
+            sys.stderr.write(log.decode(errors="replace"))
         if pr.returncode:
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-cudart", "static"]
+    link = [NVCC, *ARCH, "-shared", "-o", out + ".tmp", *objs, "-cudart", "static"]
     if libdir:
         link += ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"]
     if verbose:
         print(" ".join(link))
     subprocess.check_call(link)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

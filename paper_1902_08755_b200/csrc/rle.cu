@@ -9,37 +9,42 @@
 //  compositor_depth_rle         stages (5) + (7) fused: decode in registers,
 //                               depth-composite, one HBM write
 //
-// Encoder: two kernels, no inter-CTA waiting.  rle_encode_kernel codes one
-// super-tile of 512 consecutive chunks per CTA: each warp streams its 64
-// chunks through a 4-deep cp.async ring, codes each in registers/shared
-// memory and appends the record to its slice of an (L2-resident) record
-// scratch, and writes its table entries relative to the super-tile.
-// rle_compact_kernel then gives every super-tile its payload offset (the sum
-// of the preceding super-tiles' sizes of the same image -- at most a few
-// hundred values, summed directly, no look-back chain), moves the records to
-// their final place, rebases the table entries and writes the header.
+// Encoder: two kernels, no inter-CTA waiting.  rle_encode_kernel: every warp
+// codes one run of 16 consecutive chunks (classify all, code the non-constant
+// ones in registers/shared memory), appends the records to its slice of an
+// (L2-resident) record scratch, and writes its run size and its table entries
+// relative to the run.  rle_compact_kernel then gives every run its payload
+// offset (the sum of the preceding runs' sizes of the same image -- a few
+// thousand values, summed directly, no look-back chain), moves the records
+// to their final place, rebases the table entries and writes the header.
 #include <algorithm>
 
 #include "rle.cuh"
+
+#ifndef EQC_ENC_WARPS
+#define EQC_ENC_WARPS 1
+#endif
+#ifndef EQC_CLS_BATCH
+#define EQC_CLS_BATCH 8
+#endif
 
 using namespace eqc_rle;
 
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
-constexpr int kSTChunksPerWarp = 16; // encoder: consecutive chunks per warp (small: balances uneven chunks)
+constexpr int kSTChunksPerWarp = 16; // encoder: consecutive chunks per warp run (small: balances uneven chunks)
 static_assert(kSTChunksPerWarp <= 64, "two table-entry registers per lane");
-constexpr int kEncWarps = 8;                            // coder warps per CTA (encoder)
-constexpr int kSTChunks = kEncWarps * kSTChunksPerWarp; // chunks per super-tile (CTA of the encoder)
+constexpr int kEncWarps = EQC_ENC_WARPS;  // coder warps per CTA (encoder); warps are independent
+constexpr int kCompactWarps = 8;          // runs per CTA of the compaction kernel
 constexpr int kRecMax = 4 * (kC + 2);                  // worst-case chunk record bytes (520)
 constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 8320 = 65 x 128 B
 constexpr int kMaxBatch = 64;
 
-// workspace layout: tile_info[count * tiles_per_image][16] int32 (super-tile
-// total, then the 8 warp-run offsets inside the super-tile), then (256-byte
-// aligned) the record scratch: kScratchPerWarp bytes per coder warp of every
-// super-tile.  No state survives between calls (no zeroing needed).
-constexpr int kTileInfo = 16;
+// workspace layout: run_size[count * runs_per_image] int32 (the coded bytes
+// of every run of kSTChunksPerWarp consecutive chunks), then (256-byte
+// aligned) the record scratch: kScratchPerWarp bytes per run.  No state
+// survives between calls (no zeroing needed).
 
 struct EncImage {
   const uint32_t *src;
@@ -50,12 +55,13 @@ struct EncImage {
 
 struct EncParams {
   EncImage img[kMaxBatch];
-  int32_t *tile_info;    // inside the workspace
+  int32_t *run_size;     // inside the workspace
   uint8_t *scratch;      // record scratch (inside the workspace)
   int64_t pitch;
   int64_t nchunks;       // per image
   int count, w, h, S;    // S = chunks per row
-  int tiles_per_image;
+  int tiles_per_image;   // encoder CTAs per image
+  int runs_per_image;
   int vec;               // 128-bit loads allowed
 };
 
@@ -140,13 +146,13 @@ struct WarpEnc {
 
 struct EncSmem {
   WarpEnc w[kEncWarps];
-  int wsize[kEncWarps];
 };
 
-// Encoder.  A CTA codes one super-tile of kSTChunks consecutive chunks
-// (kEncWarps warps x 64).  Per warp:
-//  A. classify: stream the 64 chunks (coalesced 128-bit loads, 8 in flight
-//     per lane); a chunk whose pixels are all equal (76 % of the target
+// Encoder.  Every warp codes one run of kSTChunksPerWarp consecutive chunks,
+// independently of the other warps of its (small) CTA -- no CTA barrier, so a
+// warp whose chunks are cheap never waits for a busy neighbour:
+//  A. classify: stream the run's chunks (coalesced 128-bit loads, several in
+//     flight per lane); a chunk whose pixels are all equal (76 % of the target
 //     workload) only records its value -- about a dozen instructions;
 //  B. code every other chunk with encode_chunk (SIMD-within-a-word flags,
 //     packed-byte scans, per-plane classes) from a second, L2-resident read,
@@ -155,25 +161,31 @@ struct EncSmem {
 //  C. write the constant chunks' 12-byte records lane-parallel and the
 //     table entries.
 // The compaction kernel then moves the runs to their final offsets.
-__global__ void __launch_bounds__(kEncWarps * 32, 4) rle_encode_kernel(const __grid_constant__ EncParams p) {
+__global__ void __launch_bounds__(kEncWarps * 32, 32 / kEncWarps) rle_encode_kernel(const __grid_constant__ EncParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   WarpEnc &W = sm.w[warp];
-  const int64_t tile = blockIdx.x;
-  const int m = (int)(tile / p.tiles_per_image);
-  const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
+  const int m = (int)(blockIdx.x / p.tiles_per_image);
+  const int lr = (int)(blockIdx.x - m * p.tiles_per_image) * kEncWarps + warp;  // run of image m
+  if (lr >= p.runs_per_image) return;  // no CTA-wide barrier below: warps are independent
+  const int64_t gr = (int64_t)m * p.runs_per_image + lr;
   const EncImage im = p.img[m];
   const int nch = (int)p.nchunks;
   const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
-  uint8_t *scr = p.scratch + ((size_t)tile * kEncWarps + warp) * kScratchPerWarp;
-  const int c0 = (int)(lt * kSTChunks) + warp * kSTChunksPerWarp;
-  const int cnt = max(0, min(kSTChunksPerWarp, nch - c0));
+  uint8_t *scr = p.scratch + (size_t)gr * kScratchPerWarp;
+  const int c0 = lr * kSTChunksPerWarp;
+  const int cnt = min(kSTChunksPerWarp, nch - c0);
   const int Llast = p.w - (p.S - 1) * kC;
   const int k0 = c0 % p.S;
   const uint32_t *row0 = im.src + (int64_t)(c0 / p.S) * p.pitch;
+  const bool contig = p.vec && (p.w % kC) == 0 && p.pitch == p.w;
   // chunk j of the run -> (pointer, length)
   auto chunk_ptr = [&](int j, int &L) -> const uint32_t * {
+    if (contig) {  // one contiguous span of full chunks
+      L = kC;
+      return row0 + (int64_t)(k0 + j) * kC;
+    }
     const int kk = k0 + j;
     const int dy = kk / p.S, k = kk - dy * p.S;
     L = k == p.S - 1 ? Llast : kC;
@@ -182,18 +194,18 @@ __global__ void __launch_bounds__(kEncWarps * 32, 4) rle_encode_kernel(const __g
   // ---- A: classify (4 chunks in flight per lane; row pointer advanced
   // incrementally; the swizzle of constant values is deferred to C).  When
   // the warp's chunks are one contiguous span of full 128-pixel chunks
-  // (pitch == w, w % 128 == 0) the loads use immediate offsets.
+  // (pitch == w, w % 128 == 0) the loads use immediate offsets, 8 in flight.
   int ng = 0;
   uint64_t cmask = 0;
-  const bool contig = p.vec && (p.w % kC) == 0 && p.pitch == p.w;
   if (contig) {
     const uint4 *base = reinterpret_cast<const uint4 *>(row0 + (int64_t)k0 * kC) + lane;
-    for (int j0 = 0; j0 < cnt; j0 += 4) {
-      uint4 v[4];
+    for (int j0 = 0; j0 < cnt; j0 += EQC_CLS_BATCH) {
+      uint4 v[EQC_CLS_BATCH];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = (j0 + u < cnt) ? ld_stream_u4(base + 32 * (j0 + u)) : make_uint4(0, 0, 0, 0);
+      for (int u = 0; u < EQC_CLS_BATCH; ++u)
+        v[u] = (j0 + u < cnt) ? ld_stream_u4(base + 32 * (j0 + u)) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < EQC_CLS_BATCH; ++u) {
         if (j0 + u >= cnt) break;
         const uint32_t v0 = __shfl_sync(EQC_FULL, v[u].x, 0);
         const bool same = v[u].x == v0 && v[u].y == v0 && v[u].z == v0 && v[u].w == v0;
@@ -291,62 +303,55 @@ __global__ void __launch_bounds__(kEncWarps * 32, 4) rle_encode_kernel(const __g
       }
     }
   }
-  if (lane == 0) sm.wsize[warp] = run;
-  __syncthreads();
-  const int wv = lane < kEncWarps ? sm.wsize[lane] : 0;
-  const int winc = (int)warp_incl_scan_add((uint32_t)wv, lane);
-  const int wexcl = __shfl_sync(EQC_FULL, winc - wv, warp);
-  const int ttot = __shfl_sync(EQC_FULL, winc, 31);
-  if (warp == 0) {
-    int32_t *ti = p.tile_info + tile * kTileInfo;
-    if (lane == 0) ti[0] = ttot;
-    if (lane < kEncWarps) ti[1 + lane] = winc - wv;
-  }
-  if (cnt > 0) {
-    // table entries relative to the super-tile (rebased by the compaction)
-    uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
-    if (j1 < cnt) table[j1] = make_uint2((uint32_t)(wexcl + off1), ps1);
-    if (j2 < cnt) table[j2] = make_uint2((uint32_t)(wexcl + off2), ps2);
-  }
+  if (lane == 0) p.run_size[gr] = run;
+  // table entries relative to the run (rebased by the compaction)
+  uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
+  if (j1 < cnt) table[j1] = make_uint2((uint32_t)off1, ps1);
+  if (j2 < cnt) table[j2] = make_uint2((uint32_t)off2, ps2);
 }
 
 struct CompactParams {
   EncImage img[kMaxBatch];
-  const int32_t *tile_info;
+  const int32_t *run_size;
   const uint8_t *scratch;
   int64_t nchunks;
-  int w, h, tiles_per_image;
+  int w, h, groups_per_image, runs_per_image;
 };
 
-// One CTA per super-tile: payload offset = sum of the preceding super-tiles'
-// totals of the same image (summed directly by warp 0), then every warp
-// moves its run from the scratch to the stream, rebases its 64 table entries
-// and discards its scratch lines from L2; the last super-tile of an image
-// writes the header and the stream size.
-__global__ void __launch_bounds__(kEncWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
-  __shared__ int64_t s_part[kEncWarps];
+// One CTA per group of kCompactWarps runs: payload offset = sum of the
+// preceding runs' sizes of the same image (summed directly by all threads,
+// no look-back chain), then every warp moves its run from the scratch to the
+// stream, rebases its table entries and discards its scratch lines from L2;
+// the last group of an image writes the header and the stream size.
+__global__ void __launch_bounds__(kCompactWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
+  __shared__ int64_t s_part[kCompactWarps];
   __shared__ int64_t s_off;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t tile = blockIdx.x;
-  const int m = (int)(tile / p.tiles_per_image);
-  const int64_t lt = tile - (int64_t)m * p.tiles_per_image;
-  const int64_t t0 = (int64_t)m * p.tiles_per_image;
+  const int m = (int)(blockIdx.x / p.groups_per_image);
+  const int r0 = (int)(blockIdx.x - m * p.groups_per_image) * kCompactWarps;  // first run of the group
+  const int32_t *rs = p.run_size + (int64_t)m * p.runs_per_image;
   const EncImage im = p.img[m];
   {
-    // all warps sum a slice of the preceding super-tiles' totals
     int64_t acc = 0;
 #pragma unroll 4
-    for (int64_t q = tid; q < lt; q += kEncWarps * 32) acc += __ldg(p.tile_info + (t0 + q) * kTileInfo);
+    for (int q = tid; q < r0; q += kCompactWarps * 32) acc += __ldg(rs + q);
     for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(EQC_FULL, acc, d);
     if (lane == 0) s_part[warp] = acc;
   }
+  // sizes of this group's runs: exclusive prefix for every warp
+  const int nr = min(kCompactWarps, p.runs_per_image - r0);
+  const int rv = lane < nr ? __ldg(rs + r0 + lane) : 0;
+  const int rinc = (int)warp_incl_scan_add((uint32_t)rv, lane);
+  const int64_t woff = __shfl_sync(EQC_FULL, rinc - rv, warp);
+  const int64_t run = __shfl_sync(EQC_FULL, rv, warp);
+  const int64_t group_bytes = __shfl_sync(EQC_FULL, rinc, 31);
   __syncthreads();
   if (tid == 0) {
     int64_t acc = 0;
-    for (int w = 0; w < kEncWarps; ++w) acc += s_part[w];
+    for (int w = 0; w < kCompactWarps; ++w) acc += s_part[w];
     s_off = acc;
-    if (lt == p.tiles_per_image - 1) {
-      const int64_t payload = acc + __ldg(p.tile_info + tile * kTileInfo);
+    if (r0 + nr == p.runs_per_image) {
+      const int64_t payload = acc + group_bytes;
       uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
       h32[0] = kMagic;
       h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
@@ -361,16 +366,12 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_compact_kernel(const __gri
     }
   }
   __syncthreads();
-  const int64_t base = s_off;
+  if (warp >= nr) return;
+  const int64_t base = s_off + woff;
   const int nch = (int)p.nchunks;
-  const int c0 = (int)(lt * kSTChunks) + warp * kSTChunksPerWarp;
-  const int cnt = max(0, min(kSTChunksPerWarp, nch - c0));
-  if (cnt <= 0) return;
-  const int32_t *ti = p.tile_info + tile * kTileInfo;
-  const int64_t woff = __ldg(ti + 1 + warp);
-  const int64_t wend = warp + 1 < kEncWarps ? __ldg(ti + 2 + warp) : __ldg(ti);
-  const int64_t run = wend - woff;
-  const uint8_t *scr = p.scratch + ((size_t)tile * kEncWarps + warp) * kScratchPerWarp;
+  const int c0 = (r0 + warp) * kSTChunksPerWarp;
+  const int cnt = min(kSTChunksPerWarp, nch - c0);
+  const uint8_t *scr = p.scratch + ((size_t)m * p.runs_per_image + r0 + warp) * kScratchPerWarp;
   uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
   for (int j = lane; j < cnt; j += 32) {
     uint2 e = table[j];
@@ -378,7 +379,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) rle_compact_kernel(const __gri
     table[j] = e;
   }
   if (run > 0) {
-    copy_run(im.dst + 32 + 8 * p.nchunks + base + woff, scr, run, lane);
+    copy_run(im.dst + 32 + 8 * p.nchunks + base, scr, run, lane);
     __syncwarp();
     for (int l = lane; (int64_t)l * 128 < run; l += 32) discard_l2(scr + 128 * l);
   }
@@ -875,13 +876,13 @@ inline int64_t rle_max_size(int w, int h) {
   return 32 + 16 * S * (int64_t)h + 4 * (int64_t)w * h;
 }
 
-inline int64_t enc_tiles_per_image(int w, int h) {
+inline int64_t enc_runs_per_image(int w, int h) {
   const int64_t S = (w + kC - 1) / kC;
-  return (S * h + kSTChunks - 1) / kSTChunks;
+  return (S * h + kSTChunksPerWarp - 1) / kSTChunksPerWarp;
 }
 
-inline size_t enc_scratch_offset(int64_t tiles) {
-  return (((size_t)tiles * kTileInfo * sizeof(int32_t)) + 255) & ~(size_t)255;
+inline size_t enc_scratch_offset(int64_t runs) {
+  return (((size_t)runs * sizeof(int32_t)) + 255) & ~(size_t)255;
 }
 
 }  // namespace
@@ -893,8 +894,8 @@ extern "C" int64_t image_rle_max_size(int w, int h) {
 
 extern "C" size_t image_rle_workspace_size_batch(int count, int w, int h) {
   if (count <= 0 || w <= 0 || h <= 0) return 0;
-  const int64_t tiles = (int64_t)count * enc_tiles_per_image(w, h);
-  return enc_scratch_offset(tiles) + (size_t)tiles * kEncWarps * kScratchPerWarp;
+  const int64_t runs = (int64_t)count * enc_runs_per_image(w, h);
+  return enc_scratch_offset(runs) + (size_t)runs * kScratchPerWarp;
 }
 
 extern "C" size_t image_rle_workspace_size(int w, int h) { return image_rle_workspace_size_batch(1, w, h); }
@@ -928,12 +929,14 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   p.count = count;
   p.w = w;
   p.h = h;
-  p.tiles_per_image = (int)enc_tiles_per_image(w, h);
+  p.runs_per_image = (int)enc_runs_per_image(w, h);
+  p.tiles_per_image = (p.runs_per_image + kEncWarps - 1) / kEncWarps;
   p.vec = vec ? 1 : 0;
+  const int64_t runs = (int64_t)count * p.runs_per_image;
   const int64_t tiles = (int64_t)count * p.tiles_per_image;
-  if (tiles > 0x7FFFFFFFll || p.nchunks > 0x7FFFFFFFll) return EQC_E_INVALID;
-  p.tile_info = reinterpret_cast<int32_t *>(workspace);
-  p.scratch = reinterpret_cast<uint8_t *>(workspace) + enc_scratch_offset(tiles);
+  if (runs > 0x7FFFFFFFll || p.nchunks > 0x7FFFFFFFll) return EQC_E_INVALID;
+  p.run_size = reinterpret_cast<int32_t *>(workspace);
+  p.scratch = reinterpret_cast<uint8_t *>(workspace) + enc_scratch_offset(runs);
   static bool configured = false;
   const size_t smem = sizeof(EncSmem);
   if (!configured) {
@@ -946,13 +949,14 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   rle_encode_kernel<<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
   CompactParams c;
   for (int i = 0; i < count; ++i) c.img[i] = p.img[i];
-  c.tile_info = p.tile_info;
+  c.run_size = p.run_size;
   c.scratch = p.scratch;
   c.nchunks = p.nchunks;
   c.w = w;
   c.h = h;
-  c.tiles_per_image = p.tiles_per_image;
-  rle_compact_kernel<<<(unsigned)tiles, kEncWarps * 32, 0, st>>>(c);
+  c.runs_per_image = p.runs_per_image;
+  c.groups_per_image = (p.runs_per_image + kCompactWarps - 1) / kCompactWarps;
+  rle_compact_kernel<<<(unsigned)(count * c.groups_per_image), kCompactWarps * 32, 0, st>>>(c);
   return eqc_launch_status();
 }
 

@@ -13,7 +13,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeqc.so")
+# EQC_LIB selects a tuning variant built by build.build(out=..., defines=...)
+LIB_PATH = os.environ.get("EQC_LIB") or os.path.join(_HERE, "libeqc.so")
 
 OK = 0
 E_INVALID, E_CAPACITY, E_CORRUPT, E_UNSUPPORTED, E_CUDA, E_NCCL = -1, -2, -3, -4, -5, -6
