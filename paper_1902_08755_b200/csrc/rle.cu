@@ -22,7 +22,7 @@
 #include "rle.cuh"
 
 #ifndef EQC_ENC_WARPS
-#define EQC_ENC_WARPS 1
+#define EQC_ENC_WARPS 2
 #endif
 #ifndef EQC_CLS_BATCH
 #define EQC_CLS_BATCH 8

@@ -61,12 +61,6 @@ struct EncodeOut {
   uint32_t psizes;    // byte p = plane p record size
 };
 
-// Select x[i] for a warp-uniform or lane-dependent i in [0, 4) without
-// dynamic register indexing (which would spill the array to local memory).
-__device__ __forceinline__ int sel4(int i, int a, int b, int c, int d) {
-  return i == 0 ? a : i == 1 ? b : i == 2 ? c : d;
-}
-
 // Encode one chunk.  Lane `lane` holds the RAW pixels px[0..3] (positions
 // 4*lane + j, valid while < L); `swz` applies the swizzle preconditioner.
 // Writes the chunk record (planes 0..3 concatenated) into `st` (any byte
@@ -202,16 +196,17 @@ __device__ __forceinline__ EncodeOut encode_chunk_t(uint32_t px[4], int L_, int 
     const int g2 = cls[2] == 2 ? (int)bytep(totT, 2) : 0;
     const int g3 = cls[3] == 2 ? (int)bytep(totT, 3) : 0;
     const int n0 = g0, n1 = n0 + g1, n2 = n1 + g2, n3 = n2 + g3;
+    // token q of the concatenated lists: plane = last p with q >= n_{p-1};
+    // per plane, tb = token scratch base - first q, sb = stage base - first q
     for (int q = lane; q < n3; q += 32) {
-      const int p = (q >= n0) + (q >= n1) + (q >= n2);
-      const int pb = sel4(p, 0, n0, n1, n2);
-      const int np = sel4(p, g0, g1, g2, g3);
-      const int t = q - pb;
-      const uint32_t a = tp[p * kC + t];
-      const int next = (t + 1 < np) ? (int)(tp[p * kC + t + 1] & 0x7Fu) : L;
+      int tb = 0, sb = b0 + 1, ne = n0;
+      if (q >= n0) tb = kC - n0, sb = b1 + 1 - n0, ne = n1;
+      if (q >= n1) tb = 2 * kC - n1, sb = b2 + 1 - n1, ne = n2;
+      if (q >= n2) tb = 3 * kC - n2, sb = b3 + 1 - n2, ne = n3;
+      const uint32_t a = tp[tb + q];
+      const int next = (q + 1 < ne) ? (int)(tp[tb + q + 1] & 0x7Fu) : L;
       const int len = next - (int)(a & 0x7Fu);
-      const int bp = sel4(p, b0, b1, b2, b3);
-      st[bp + 1 + t] = (uint8_t)((a & 0x80u) | (uint32_t)(len - 1));
+      st[sb + q] = (uint8_t)((a & 0x80u) | (uint32_t)(len - 1));
     }
   }
   __syncwarp();
@@ -309,21 +304,25 @@ __device__ __forceinline__ bool decode_plane_t(const uint8_t *r, int size, int L
     // few tokens (typical of mixed background/foreground chunks): the token
     // boundaries are computed once (uniform), each position selects its token
     // by comparison -- no scans, no shuffles, no scratch
-    int st[4], ps[4], rp[4];
+    // token t covers [st[t], st[t+1]); its byte for position i is
+    // r[bs[t] + lt[t] * i] (literal: bs = payload index - start, lt = 1;
+    // repeat: bs = payload index, lt = 0)
+    int st[4], bs[4], lt[4];
     int pos = 0, pay = 1 + ntok;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      st[t] = pos;
-      ps[t] = pay;
-      rp[t] = 1;
+      st[t] = 0x7FFF;  // never selected
+      bs[t] = 0;
+      lt[t] = 0;
       if (t < ntok) {
         const int c = r[1 + t];
         const int len = (c & 0x7F) + 1;
-        rp[t] = c >> 7;
+        const bool lit = !(c & 0x80);
+        st[t] = pos;
+        bs[t] = lit ? pay - pos : pay;
+        lt[t] = lit;
         pos += len;
-        pay += (c & 0x80) ? 1 : len;
-      } else {
-        st[t] = 0x7FFF;  // never selected
+        pay += lit ? len : 1;
       }
     }
     if (pos != L || pay != size) return false;
@@ -331,11 +330,15 @@ __device__ __forceinline__ bool decode_plane_t(const uint8_t *r, int size, int L
     for (int j = 0; j < 4; ++j) {
       const int i = i0 + j;
       if (FULL || i < L) {
-        const int t = (i >= st[1]) + (i >= st[2]) + (i >= st[3]);
-        const int s0 = sel4(t, st[0], st[1], st[2], st[3]);
-        const int p0 = sel4(t, ps[0], ps[1], ps[2], ps[3]);
-        const int r0 = sel4(t, rp[0], rp[1], rp[2], rp[3]);
-        out[j] |= (uint32_t)r[p0 + (r0 ? 0 : i - s0)] << (8 * p);
+        // the covering token is the last one starting at or before i
+        int b = bs[0], l = lt[0];
+#pragma unroll
+        for (int t = 1; t < 4; ++t) {
+          const bool in = i >= st[t];
+          b = in ? bs[t] : b;
+          l = in ? lt[t] : l;
+        }
+        out[j] |= (uint32_t)r[b + l * i] << (8 * p);
       }
     }
     return true;
