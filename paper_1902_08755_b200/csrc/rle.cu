@@ -687,8 +687,9 @@ constexpr int kPreWords = 1024; // per-warp record prefetch buffer (4 KB)
 //   values, then the four partial minima are merged by (depth, index).
 //  Phase B: all-constant positions are written with one 128-bit store per
 //   lane per output; every other position is decoded warp-cooperatively,
-//   depth first: a source's colour chunk is decoded only if the source wins
-//   at least one pixel of the chunk.
+//   depth first: all depth records give the winning source of every pixel,
+//   then a source's colour chunk is decoded only if it wins at least one
+//   pixel of the chunk in the final result.
 __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_constant__ FusedParams p) {
   __shared__ __align__(16) uint8_t stage[kFWarps][kStageBytes];
   __shared__ __align__(16) uint16_t info[kFWarps][kC];
@@ -808,13 +809,15 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   __syncwarp();
-  uint32_t bc[4] = {0, 0, 0, 0}, bd[4] = {0, 0, 0, 0};
+  // depth pass: running minimum and the index of the winning source per pixel
+  uint32_t bd[4] = {0, 0, 0, 0};
+  int bi[4] = {0, 0, 0, 0};
   for (int i = 0; i < n; ++i) {
     const int ps = i >> 5, li = i & 31;
     const uint4 e1 = ps ? ed[1] : ed[0];
     const uint32_t dx = __shfl_sync(EQC_FULL, e1.x, li), dy = __shfl_sync(EQC_FULL, e1.y, li),
                    dz = __shfl_sync(EQC_FULL, e1.z, li), dw = __shfl_sync(EQC_FULL, e1.w, li);
-    const int od = __shfl_sync(EQC_FULL, wd0, li), oc = __shfl_sync(EQC_FULL, wc0, li);
+    const int od = __shfl_sync(EQC_FULL, wd0, li);
     uint32_t d[4];
     bool okd = true;
     if (dw) {
@@ -831,13 +834,22 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
       if (lane == 0) set_corrupt(p.status);
       return;
     }
-    bool t[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) t[j] = (i == 0) || d[j] < bd[j];  // ties keep the lower index
-    if (!__any_sync(EQC_FULL, t[0] || t[1] || t[2] || t[3])) continue;  // hidden: colour never read
+    for (int j = 0; j < 4; ++j) {
+      const bool t = (i == 0) || d[j] < bd[j];  // ties keep the lower index
+      bd[j] = t ? d[j] : bd[j];
+      bi[j] = t ? i : bi[j];
+    }
+  }
+  // colour pass: only the sources that win at least one pixel of the chunk
+  uint32_t bc[4] = {0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    if (!__any_sync(EQC_FULL, bi[0] == i || bi[1] == i || bi[2] == i || bi[3] == i)) continue;
+    const int ps = i >> 5, li = i & 31;
     const uint4 e2 = ps ? ec[1] : ec[0];
     const uint32_t cx = __shfl_sync(EQC_FULL, e2.x, li), cy = __shfl_sync(EQC_FULL, e2.y, li),
                    cz = __shfl_sync(EQC_FULL, e2.z, li), cw = __shfl_sync(EQC_FULL, e2.w, li);
+    const int oc = __shfl_sync(EQC_FULL, wc0, li);
     uint32_t col[4];
     if (cw) {
 #pragma unroll
@@ -860,10 +872,7 @@ __global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_co
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      bd[j] = t[j] ? d[j] : bd[j];
-      bc[j] = t[j] ? col[j] : bc[j];
-    }
+    for (int j = 0; j < 4; ++j) bc[j] = bi[j] == i ? col[j] : bc[j];
   }
   store_px(p.out_color + row, L, lane, p.vec != 0, bc);
   if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, bd);
