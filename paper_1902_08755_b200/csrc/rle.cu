@@ -24,6 +24,12 @@
 #ifndef EQC_ENC_WARPS
 #define EQC_ENC_WARPS 2
 #endif
+#ifndef EQC_ENC_MINB
+#define EQC_ENC_MINB (32 / EQC_ENC_WARPS)  // 64 registers: 32 warps per SM
+#endif
+#ifndef EQC_FUSED_MINB
+#define EQC_FUSED_MINB 8  // 32 warps per SM (64 registers)
+#endif
 #ifndef EQC_CLS_BATCH
 #define EQC_CLS_BATCH 8
 #endif
@@ -161,7 +167,7 @@ struct EncSmem {
 //  C. write the constant chunks' 12-byte records lane-parallel and the
 //     table entries.
 // The compaction kernel then moves the runs to their final offsets.
-__global__ void __launch_bounds__(kEncWarps * 32, 32 / kEncWarps) rle_encode_kernel(const __grid_constant__ EncParams p) {
+__global__ void __launch_bounds__(kEncWarps * 32, EQC_ENC_MINB) rle_encode_kernel(const __grid_constant__ EncParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -690,7 +696,7 @@ constexpr int kPreWords = 1024; // per-warp record prefetch buffer (4 KB)
 //   depth first: all depth records give the winning source of every pixel,
 //   then a source's colour chunk is decoded only if it wins at least one
 //   pixel of the chunk in the final result.
-__global__ void __launch_bounds__(kFWarps * 32) depth_rle_kernel(const __grid_constant__ FusedParams p) {
+__global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel(const __grid_constant__ FusedParams p) {
   __shared__ __align__(16) uint8_t stage[kFWarps][kStageBytes];
   __shared__ __align__(16) uint16_t info[kFWarps][kC];
   __shared__ int64_t s_pb[kMaxStreams];
