@@ -63,6 +63,12 @@ def lib():
         L.or_rle_encode.restype = i64
         L.or_rle_decode.argtypes = [P, i64, P, i64, i32, i32]
         L.or_rle_decode.restype = i32
+        L.or_roi.argtypes = [P, i32, i32, i64, u32, P]
+        L.or_roi.restype = None
+        L.or_depth_composite_roi.argtypes = [i32, P, P, P, i32, i32, i64, P, P, i64]
+        L.or_depth_composite_roi.restype = i32
+        L.or_blend_ordered_roi.argtypes = [i32, P, P, P, i32, i32, i64, u32, P, i64]
+        L.or_blend_ordered_roi.restype = i32
         _lib = L
     return _lib
 
@@ -168,3 +174,53 @@ def rle_decode(stream: bytes, w: int, h: int):
     out = np.zeros((h, w), np.uint32)
     rc = lib().or_rle_decode(_ptr(buf), len(stream), _ptr(out), w, w, h)
     return rc, out
+
+
+def roi(frame: np.ndarray, background: int) -> tuple:
+    """Bounding box (x, y, w, h) of the pixels != background; (0, 0, 0, 0) if none."""
+    f = _as_u32_frames([frame])[0]
+    h, w = f.shape
+    out = np.zeros(4, np.int32)
+    lib().or_roi(_ptr(f), w, h, f.strides[0] // 4, int(background) & 0xFFFFFFFF, _ptr(out))
+    return tuple(int(v) for v in out)
+
+
+def _rois(rois, n):
+    r = np.ascontiguousarray(np.asarray(rois, dtype=np.int32).reshape(n, 4))
+    return r
+
+
+def depth_composite_roi(colors, depths, rois, want_depth: bool = True):
+    """O1 over sources that hold data only inside their ROI (x, y, w, h)."""
+    n = len(colors)
+    colors = _as_u32_frames(colors)
+    depths = _as_u32_frames(depths)
+    h, w = colors[0].shape
+    pitch = colors[0].strides[0] // 4
+    r = _rois(rois, n)
+    oc = np.empty((h, w), np.uint32)
+    od = np.empty((h, w), np.uint32) if want_depth else None
+    rc = lib().or_depth_composite_roi(n, _ptr_array(colors), _ptr_array(depths), _ptr(r), w, h, pitch,
+                                      _ptr(oc), _ptr(od) if od is not None else None, w)
+    if rc:
+        raise ValueError(f"or_depth_composite_roi: {rc}")
+    return oc, od
+
+
+def blend_ordered_roi(colors, rois, order=None, background: int = 0):
+    """O2 over layers that are transparent outside their ROI (x, y, w, h)."""
+    n = len(colors)
+    colors = _as_u32_frames(colors)
+    h, w = colors[0].shape
+    pitch = colors[0].strides[0] // 4
+    r = _rois(rois, n)
+    ordp = None
+    if order is not None:
+        order = np.ascontiguousarray(order, dtype=np.int32)
+        ordp = _ptr(order)
+    oc = np.empty((h, w), np.uint32)
+    rc = lib().or_blend_ordered_roi(n, _ptr_array(colors), ordp, _ptr(r), w, h, pitch,
+                                    int(background) & 0xFFFFFFFF, _ptr(oc), w)
+    if rc:
+        raise ValueError(f"or_blend_ordered_roi: {rc}")
+    return oc
