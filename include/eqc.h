@@ -100,6 +100,44 @@ EQC_API int compositor_blend_ordered(int n, const uint32_t *const *color, const 
                              uint32_t *out_color, int64_t out_pitch, void *stream);
 
 /*
+ * Region of interest.  "The ROI is the screen-space 2D
+ * bounding box fully enclosing the data rendered by a single resource"
+ * (P:2259-2263); it "is transmitted to all input frames together with the
+ * pixel data.  On the input frame, the compositing code respects this
+ * parameter to place the pixel data in the right position".
+ * A ROI is an int32 {x, y, w, h} in full-frame pixel coordinates; an empty
+ * ROI is {0, 0, 0, 0}.  Rectangles are clipped to the frame (R-C19).
+ *
+ * image_roi -- ROI of each of n frames computed on the GPU "by analysing the
+ *   framebuffer": the smallest rectangle containing every pixel
+ *   whose value differs from `background` (depth buffers: 0xFFFFFFFF; colour
+ *   of a blend layer: 0).
+ *   frames     host array of n device pointers, each [h][pitch] uint32.
+ *   d_roi      device int32[4 n], 16-byte aligned: receives the n ROIs.
+ *   Three launches on `stream` (init, scan, finalise); no host sync.
+ *
+ * compositor_depth_roi / compositor_blend_ordered_roi -- compositor_depth /
+ *   compositor_blend_ordered over sources that hold pixel data only inside
+ *   their ROI: outside d_roi[4i..4i+3] source i is background (depth
+ *   0xFFFFFFFF, colour 0) for depth compositing and transparent for blending,
+ *   and its buffers are never read there.  Buffers are indexed like full
+ *   frames ([h][pitch] from color[i]); a cropped buffer holding only the ROI
+ *   may be passed as `crop - (y * pitch + x)` (only in-ROI addresses are
+ *   dereferenced).  d_roi: DEVICE int32[4 n] (16-byte aligned), e.g. the
+ *   output of image_roi, indexed by source (not by draw position).
+ *   Results equal the full-frame calls on frames masked outside their ROIs.
+ */
+EQC_API int image_roi(int n, const uint32_t *const *frames, int w, int h, int64_t pitch, uint32_t background,
+                      int32_t *d_roi, void *stream);
+EQC_API int compositor_depth_roi(int n, const uint32_t *const *color, const uint32_t *const *depth,
+                                 const int32_t *d_roi, int w, int h, int64_t pitch, uint32_t *out_color,
+                                 uint32_t *out_depth, int64_t out_pitch, void *stream);
+EQC_API int compositor_blend_ordered_roi(int n, const uint32_t *const *color, const int32_t *order,
+                                         const int32_t *d_roi, int w, int h, int64_t pitch,
+                                         uint32_t background, uint32_t *out_color, int64_t out_pitch,
+                                         void *stream);
+
+/*
  * RLE-BP v1 codec: per-component (byte-plane) run-length encoding
  * with the optional bit-swizzle preconditioner, decomposed into
  * 128-pixel row chunks.  Wire format: DESIGN.md section 5 (R-C8).
@@ -107,9 +145,9 @@ EQC_API int compositor_blend_ordered(int n, const uint32_t *const *color, const 
  * image_rle_max_size -- upper bound of a stream: 32 + 16*ceil(w/128)*h + 4*w*h.
  *   Returns EQC_E_INVALID for w <= 0 or h <= 0.
  * image_rle_workspace_size -- bytes of device scratch image_compress_rle needs
- *   for ONE w x h image (chunk-offset look-back state).  The workspace must be
- *   zero-filled before its first use; every call leaves it reusable.  A
- *   workspace must not be shared by calls that may run concurrently.
+ *   for ONE w x h image (per-run sizes + an L2-resident record scratch).  No
+ *   state survives between calls, so no zero fill is needed.  A workspace
+ *   must not be shared by calls that may run concurrently.
  */
 EQC_API int64_t image_rle_max_size(int w, int h);
 EQC_API size_t image_rle_workspace_size(int w, int h);

@@ -399,9 +399,18 @@ void or_roi(const uint32_t *frame, int w, int h, int64_t pitch, uint32_t backgro
   out[3] = y1 - y0 + 1;
 }
 
-static int roi_valid(const int32_t *r, int w, int h) {
-  return r[0] >= 0 && r[1] >= 0 && r[2] >= 0 && r[3] >= 0 && (int64_t)r[0] + r[2] <= w &&
-         (int64_t)r[1] + r[3] <= h;
+/* R-C19: a rectangle is clipped to the frame; no pixel lies outside it. */
+static void roi_clip(const int32_t *r, int w, int h, int32_t *c) {
+  int64_t x0 = r[0], y0 = r[1], x1 = (int64_t)r[0] + r[2], y1 = (int64_t)r[1] + r[3];
+  if (x0 < 0) x0 = 0;
+  if (y0 < 0) y0 = 0;
+  if (x1 > w) x1 = w;
+  if (y1 > h) y1 = h;
+  if (r[2] <= 0 || r[3] <= 0 || x1 <= x0 || y1 <= y0) x0 = y0 = x1 = y1 = 0;
+  c[0] = (int32_t)x0;
+  c[1] = (int32_t)y0;
+  c[2] = (int32_t)(x1 - x0);
+  c[3] = (int32_t)(y1 - y0);
 }
 
 static int in_roi(const int32_t *r, int x, int y) {
@@ -415,21 +424,21 @@ static int in_roi(const int32_t *r, int x, int y) {
  * supplies pixel data only inside roi[4i..4i+3] = {x, y, w, h} (full-frame
  * coordinates, buffer indexed like a full frame); everywhere else it is
  * background (depth 0xFFFFFFFF, colour 0, R-C1).  The result is O1 over the
- * sources expanded that way.  Returns OR_E_INVALID for a rectangle that does
- * not lie inside the frame.
+ * sources expanded that way.  Rectangles are clipped to the frame (R-C19).
  */
 int or_depth_composite_roi(int n, const uint32_t *const *color, const uint32_t *const *depth,
                            const int32_t *roi, int w, int h, int64_t pitch, uint32_t *out_color,
                            uint32_t *out_depth, int64_t out_pitch) {
-  for (int i = 0; i < n; ++i)
-    if (!roi_valid(roi + 4 * i, w, h)) return OR_E_INVALID;
+  int32_t rc[4 * 64];
+  if (n < 1 || n > 64) return OR_E_INVALID;
+  for (int i = 0; i < n; ++i) roi_clip(roi + 4 * i, w, h, rc + 4 * i);
   for (int y = 0; y < h; ++y) {
     for (int x = 0; x < w; ++x) {
       int64_t p = (int64_t)y * pitch + x;
       int best = -1;
       uint32_t bd = 0, bc = 0;
       for (int i = 0; i < n; ++i) {
-        int inside = in_roi(roi + 4 * i, x, y);
+        int inside = in_roi(rc + 4 * i, x, y);
         uint32_t di = inside ? depth[i][p] : 0xFFFFFFFFu;
         uint32_t ci = inside ? color[i][p] : 0u;
         if (best < 0 || di < bd) { /* (depth, index) order: i > best */
@@ -453,8 +462,9 @@ int or_depth_composite_roi(int n, const uint32_t *const *color, const uint32_t *
 int or_blend_ordered_roi(int n, const uint32_t *const *color, const int32_t *order, const int32_t *roi,
                          int w, int h, int64_t pitch, uint32_t background, uint32_t *out_color,
                          int64_t out_pitch) {
-  for (int i = 0; i < n; ++i)
-    if (!roi_valid(roi + 4 * i, w, h)) return OR_E_INVALID;
+  int32_t rc[4 * 64];
+  if (n < 1 || n > 64) return OR_E_INVALID;
+  for (int i = 0; i < n; ++i) roi_clip(roi + 4 * i, w, h, rc + 4 * i);
   for (int y = 0; y < h; ++y) {
     for (int x = 0; x < w; ++x) {
       int64_t p = (int64_t)y * pitch + x;
@@ -462,7 +472,7 @@ int or_blend_ordered_roi(int n, const uint32_t *const *color, const int32_t *ord
       for (int c = 0; c < 4; ++c) xc[c] = (double)((background >> (8 * c)) & 0xFFu) / 255.0;
       for (int k = 0; k < n; ++k) {
         int src = order ? order[k] : k;
-        uint32_t s = in_roi(roi + 4 * src, x, y) ? color[src][p] : 0u;
+        uint32_t s = in_roi(rc + 4 * src, x, y) ? color[src][p] : 0u;
         double a = (double)(s >> 24) / 255.0;
         for (int c = 0; c < 4; ++c) {
           double sc = (double)((s >> (8 * c)) & 0xFFu) / 255.0;

@@ -170,6 +170,146 @@ __global__ void __launch_bounds__(256) blend_ordered_kernel(const __grid_constan
   }
 }
 
+// ---- region of interest --------------------------------
+// Source i holds pixel data only inside its rectangle d_roi[i] = {x, y, w, h}
+// (full-frame coordinates; the buffer is indexed like a full frame and is
+// dereferenced only inside the rectangle); elsewhere it is background
+// (depth 0xFFFFFFFF, colour 0; for blending: transparent) -- P:2268-2271.
+// Rectangles are read on the device (e.g. straight from image_roi), clipped
+// to the frame (R-C19), and staged in shared memory as {x0, y0, x1, y1}.
+struct Rect {
+  int x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ Rect load_rect(const int32_t *r, int w, int h) {
+  const int4 v = *reinterpret_cast<const int4 *>(r);
+  Rect q;
+  q.x0 = max(v.x, 0);
+  q.y0 = max(v.y, 0);
+  q.x1 = (v.z > 0 && v.x < w) ? (int)min((int64_t)v.x + v.z, (int64_t)w) : 0;
+  q.y1 = (v.w > 0 && v.y < h) ? (int)min((int64_t)v.y + v.w, (int64_t)h) : 0;
+  if (q.x1 <= q.x0 || q.y1 <= q.y0) q = Rect{0, 0, 0, 0};
+  return q;
+}
+
+struct DepthRoiParams {
+  const uint32_t *color[EQC_MAX_SOURCES];
+  const uint32_t *depth[EQC_MAX_SOURCES];
+  const int32_t *roi;  // device, n x {x, y, w, h}
+  uint32_t *out_color;
+  uint32_t *out_depth;
+  int64_t pitch, out_pitch;
+  int n, w, h, groups_per_row;
+  int vec;
+};
+
+// One thread per 4 consecutive pixels of a row, as depth_composite_kernel;
+// a source is read only where its rectangle covers the pixels.  Source 0 is
+// taken unconditionally where it is inside (argmin of (depth, index)).
+__global__ void __launch_bounds__(256) depth_composite_roi_kernel(const __grid_constant__ DepthRoiParams p) {
+  __shared__ Rect s_r[EQC_MAX_SOURCES];
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) s_r[i] = load_rect(p.roi + 4 * i, p.w, p.h);
+  __syncthreads();
+  const int64_t total = (int64_t)p.groups_per_row * p.h;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(g / p.groups_per_row);
+    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+    const int64_t off = (int64_t)y * p.pitch + x;
+    const int cnt = min(4, p.w - x);
+    uint32_t bd[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, bc[4] = {0, 0, 0, 0};
+    for (int i = 0; i < p.n; ++i) {
+      const Rect r = s_r[i];
+      if (y < r.y0 || y >= r.y1 || x + cnt <= r.x0 || x >= r.x1) continue;  // not covered
+      uint32_t d[4], c[4];
+      const bool full = x >= r.x0 && x + 4 <= r.x1;
+      if (p.vec && full) {
+        const uint4 dv = ld_stream_u4(p.depth[i] + off), cv = ld_stream_u4(p.color[i] + off);
+        d[0] = dv.x, d[1] = dv.y, d[2] = dv.z, d[3] = dv.w;
+        c[0] = cv.x, c[1] = cv.y, c[2] = cv.z, c[3] = cv.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool t = i == 0 || d[j] < bd[j];
+          bd[j] = t ? d[j] : bd[j];
+          bc[j] = t ? c[j] : bc[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < cnt && x + j >= r.x0 && x + j < r.x1) {
+            const uint32_t dj = ld_stream_u32(p.depth[i] + off + j), cj = ld_stream_u32(p.color[i] + off + j);
+            const bool t = i == 0 || dj < bd[j];
+            bd[j] = t ? dj : bd[j];
+            bc[j] = t ? cj : bc[j];
+          }
+        }
+      }
+    }
+    const int64_t ooff = (int64_t)y * p.out_pitch + x;
+    if (p.vec && cnt == 4) {
+      st_stream_u4(p.out_color + ooff, make_uint4(bc[0], bc[1], bc[2], bc[3]));
+      if (p.out_depth) st_stream_u4(p.out_depth + ooff, make_uint4(bd[0], bd[1], bd[2], bd[3]));
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        p.out_color[ooff + j] = bc[j];
+        if (p.out_depth) p.out_depth[ooff + j] = bd[j];
+      }
+    }
+  }
+}
+
+struct BlendRoiParams {
+  const uint32_t *color[EQC_MAX_SOURCES];  // already in draw order, back first
+  const int32_t *roi;                       // device, indexed by SOURCE
+  int src_of[EQC_MAX_SOURCES];              // draw position -> source index
+  uint32_t *out_color;
+  int64_t pitch, out_pitch;
+  int n, w, h, groups_per_row;
+  int vec;
+  float bg[4];
+};
+
+// Ordered blend over ROI-restricted layers: outside its rectangle a layer is
+// transparent and is skipped (over() with s = 0 is the identity).
+__global__ void __launch_bounds__(256) blend_ordered_roi_kernel(const __grid_constant__ BlendRoiParams p) {
+  __shared__ Rect s_r[EQC_MAX_SOURCES];
+  for (int k = threadIdx.x; k < p.n; k += blockDim.x) s_r[k] = load_rect(p.roi + 4 * p.src_of[k], p.w, p.h);
+  __syncthreads();
+  const int64_t total = (int64_t)p.groups_per_row * p.h;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(g / p.groups_per_row);
+    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+    const int64_t off = (int64_t)y * p.pitch + x;
+    const int cnt = min(4, p.w - x);
+    Acc4 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = Acc4{p.bg[0], p.bg[1], p.bg[2], p.bg[3]};
+    for (int k = 0; k < p.n; ++k) {
+      const Rect r = s_r[k];
+      if (y < r.y0 || y >= r.y1 || x + cnt <= r.x0 || x >= r.x1) continue;
+      if (p.vec && x >= r.x0 && x + 4 <= r.x1) {
+        const uint4 s = ld_stream_u4(p.color[k] + off);
+        over(acc[0], s.x);
+        over(acc[1], s.y);
+        over(acc[2], s.z);
+        over(acc[3], s.w);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < cnt && x + j >= r.x0 && x + j < r.x1) over(acc[j], ld_stream_u32(p.color[k] + off + j));
+      }
+    }
+    const int64_t ooff = (int64_t)y * p.out_pitch + x;
+    if (p.vec && cnt == 4) {
+      st_stream_u4(p.out_color + ooff,
+                   make_uint4(pack_round(acc[0]), pack_round(acc[1]), pack_round(acc[2]), pack_round(acc[3])));
+    } else {
+      for (int j = 0; j < cnt; ++j) p.out_color[ooff + j] = pack_round(acc[j]);
+    }
+  }
+}
+
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 inline int grid_for(int64_t items) {
@@ -243,5 +383,69 @@ extern "C" int compositor_blend_ordered(int n, const uint32_t *const *color, con
     blend_ordered_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
   else
     blend_ordered_kernel<false><<<grid_for(groups), 256, 0, s>>>(p);
+  return eqc_launch_status();
+}
+
+extern "C" int compositor_depth_roi(int n, const uint32_t *const *color, const uint32_t *const *depth,
+                                    const int32_t *d_roi, int w, int h, int64_t pitch, uint32_t *out_color,
+                                    uint32_t *out_depth, int64_t out_pitch, void *stream) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color || !depth || !d_roi || !out_color) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
+  if (((uintptr_t)d_roi & 15) != 0) return EQC_E_INVALID;
+  DepthRoiParams p;
+  bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) && aligned16(out_color) &&
+             (!out_depth || aligned16(out_depth));
+  for (int i = 0; i < n; ++i) {
+    if (!color[i] || !depth[i]) return EQC_E_INVALID;
+    p.color[i] = color[i];
+    p.depth[i] = depth[i];
+    vec = vec && aligned16(color[i]) && aligned16(depth[i]);
+  }
+  p.roi = d_roi;
+  p.out_color = out_color;
+  p.out_depth = out_depth;
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  p.vec = vec ? 1 : 0;
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  depth_composite_roi_kernel<<<grid_for(groups), 256, 0, (cudaStream_t)stream>>>(p);
+  return eqc_launch_status();
+}
+
+extern "C" int compositor_blend_ordered_roi(int n, const uint32_t *const *color, const int32_t *order,
+                                            const int32_t *d_roi, int w, int h, int64_t pitch,
+                                            uint32_t background, uint32_t *out_color, int64_t out_pitch,
+                                            void *stream) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color || !d_roi || !out_color) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
+  if (((uintptr_t)d_roi & 15) != 0) return EQC_E_INVALID;
+  BlendRoiParams p;
+  bool seen[EQC_MAX_SOURCES] = {false};
+  bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) && aligned16(out_color);
+  for (int k = 0; k < n; ++k) {
+    int src = order ? order[k] : k;
+    if (src < 0 || src >= n || seen[src]) return EQC_E_INVALID;  // not a permutation
+    seen[src] = true;
+    if (!color[src]) return EQC_E_INVALID;
+    p.color[k] = color[src];
+    p.src_of[k] = src;
+    vec = vec && aligned16(color[src]);
+  }
+  p.roi = d_roi;
+  p.out_color = out_color;
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  p.vec = vec ? 1 : 0;
+  for (int c = 0; c < 4; ++c) p.bg[c] = (float)((background >> (8 * c)) & 0xFFu);
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  blend_ordered_roi_kernel<<<grid_for(groups), 256, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }

@@ -45,6 +45,9 @@ def _load():
         "eqc_version": ([], i32),
         "compositor_depth": ([i32, P, P, i32, i32, i64, P, P, i64, P], i32),
         "compositor_blend_ordered": ([i32, P, P, i32, i32, i64, u32, P, i64, P], i32),
+        "image_roi": ([i32, P, i32, i32, i64, u32, P, P], i32),
+        "compositor_depth_roi": ([i32, P, P, P, i32, i32, i64, P, P, i64, P], i32),
+        "compositor_blend_ordered_roi": ([i32, P, P, P, i32, i32, i64, u32, P, i64, P], i32),
         "image_rle_max_size": ([i32, i32], i64),
         "image_rle_workspace_size": ([i32, i32], sz),
         "image_rle_workspace_size_batch": ([i32, i32, i32], sz),
@@ -140,6 +143,38 @@ def compositor_blend_ordered(colors, out_color, order=None, background: int = 0,
     rc = _lib.compositor_blend_ordered(n, _ptrs(colors), ordp, w, h, pitch, int(background) & 0xFFFFFFFF,
                                        _addr(out_color), opitch, _stream(stream))
     return _check(rc, "compositor_blend_ordered")
+
+
+def image_roi(frames, d_roi, background: int, stream=None):
+    """ROI {x, y, w, h} of each frame's pixels != background into the device
+    int32 tensor d_roi [n, 4]."""
+    n = len(frames)
+    w, h, pitch = _frame_geom(frames[0])
+    rc = _lib.image_roi(n, _ptrs(frames), w, h, pitch, int(background) & 0xFFFFFFFF, _addr(d_roi), _stream(stream))
+    return _check(rc, "image_roi")
+
+
+def compositor_depth_roi(colors, depths, d_roi, out_color, out_depth=None, stream=None):
+    """compositor_depth over sources holding data only inside their ROI
+    (device int32 [n, 4] {x, y, w, h})."""
+    n = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    _, _, opitch = _frame_geom(out_color)
+    rc = _lib.compositor_depth_roi(n, _ptrs(colors), _ptrs(depths), _addr(d_roi), w, h, pitch, _addr(out_color),
+                                   _addr(out_depth), opitch, _stream(stream))
+    return _check(rc, "compositor_depth_roi")
+
+
+def compositor_blend_ordered_roi(colors, d_roi, out_color, order=None, background: int = 0, stream=None):
+    n = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    _, _, opitch = _frame_geom(out_color)
+    ordp = None
+    if order is not None:
+        ordp = (ctypes.c_int32 * n)(*[int(v) for v in order])
+    rc = _lib.compositor_blend_ordered_roi(n, _ptrs(colors), ordp, _addr(d_roi), w, h, pitch,
+                                           int(background) & 0xFFFFFFFF, _addr(out_color), opitch, _stream(stream))
+    return _check(rc, "compositor_blend_ordered_roi")
 
 
 def image_rle_max_size(w: int, h: int) -> int:

@@ -70,9 +70,29 @@ def footprint(seed: int, w: int, h: int, F: float = 0.5) -> np.ndarray:
     return fp
 
 
+def kd_cells(n: int, x0: int, y0: int, x1: int, y1: int):
+    """Split the rectangle [x0, x1) x [y0, y1) into n cells by recursive
+    halving of the longer side (proportional to the cell counts)."""
+    if n == 1:
+        return [(x0, y0, x1, y1)]
+    a = n // 2
+    if x1 - x0 >= y1 - y0:
+        xm = x0 + (x1 - x0) * a // n
+        return kd_cells(a, x0, y0, xm, y1) + kd_cells(n - a, xm, y0, x1, y1)
+    ym = y0 + (y1 - y0) * a // n
+    return kd_cells(a, x0, y0, x1, ym) + kd_cells(n - a, x0, ym, x1, y1)
+
+
 def depth_sources(seed: int, n: int, w: int, h: int, F: float = 0.5,
-                  noise_bits: int = 1, ties: bool = False, pitch: int | None = None):
+                  noise_bits: int = 1, ties: bool = False, pitch: int | None = None,
+                  mode: str = "scattered"):
     """N sort-last source frames: (colors, depths), each a list of [H, W] uint32.
+
+    ``mode="scattered"`` (default): every source's fragments fall anywhere in
+    the footprint (round-robin allocation).  ``mode="compact"``:
+    source i's fragment centres fall in the i-th kD cell of the footprint's
+    bounding box (spatially compact allocation),
+    so each source covers a small screen region -- the case the ROI targets.
 
     If ``pitch`` > W the arrays are [H, pitch] buffers and the returned frames
     are [H, W] views into them (row pitch = ``pitch`` words); the padding holds
@@ -81,9 +101,23 @@ def depth_sources(seed: int, n: int, w: int, h: int, F: float = 0.5,
     fp = footprint(seed, w, h, F)
     fp_idx = np.flatnonzero(fp)
     fp_area = float(fp_idx.size)
+    cells = None
+    if mode == "compact":
+        ys, xs = np.nonzero(fp)
+        cells = kd_cells(n, int(xs.min()), int(ys.min()), int(xs.max()) + 1, int(ys.max()) + 1)
+    elif mode != "scattered":
+        raise ValueError(mode)
     colors, depths = [], []
     for i in range(n):
         rng = np.random.default_rng([seed, 1, i])
+        src_idx, src_area = fp_idx, fp_area
+        if cells is not None:
+            cx0, cy0, cx1, cy1 = cells[i]
+            sub = np.zeros_like(fp)
+            sub[cy0:cy1, cx0:cx1] = fp[cy0:cy1, cx0:cx1]
+            if sub.any():
+                src_idx = np.flatnonzero(sub)
+                src_area = float(src_idx.size)
         P = pitch if pitch is not None else w
         cbuf = np.full((h, P), 0xDEADBEEF, np.uint32)
         dbuf = np.full((h, P), 0x5A5A5A5A, np.uint32)
@@ -92,9 +126,9 @@ def depth_sources(seed: int, n: int, w: int, h: int, F: float = 0.5,
         col[:] = 0
         dep[:] = BG_DEPTH
         cover = float(rng.uniform(1.0 / math.sqrt(max(n, 1)), 1.0))
-        frag_area = cover * fp_area / 32.0 * 1.2
+        frag_area = cover * src_area / 32.0 * 1.2
         for _f in range(32):
-            c = int(fp_idx[int(rng.integers(0, fp_idx.size))])
+            c = int(src_idx[int(rng.integers(0, src_idx.size))])
             cy, cx = c // w + 0.5, c % w + 0.5
             aspect = float(rng.uniform(0.4, 2.5))
             rx = max(math.sqrt(frag_area * aspect / math.pi), 1.0)

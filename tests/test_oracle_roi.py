@@ -100,10 +100,15 @@ def test_blend_roi_reduces_to_o2_on_masked_layers():
     np.testing.assert_array_equal(oracle.blend_ordered_roi(bricks, exact), oracle.blend_ordered(bricks))
 
 
-def test_roi_rect_outside_frame_is_invalid():
-    c, d = synth.random_frames(1, 2, 8, 8)
-    for bad in [(-1, 0, 2, 2), (0, 0, 9, 1), (7, 7, 2, 1), (0, 0, -1, 3)]:
-        with pytest.raises(ValueError):
-            oracle.depth_composite_roi(c, d, [bad, (0, 0, 8, 8)])
-        with pytest.raises(ValueError):
-            oracle.blend_ordered_roi(c, [(0, 0, 8, 8), bad])
+def test_roi_rects_are_clipped_to_the_frame():
+    # R-C19: the part of a rectangle outside the frame holds no pixels
+    c, d = synth.random_frames(1, 2, 8, 8, depth_alphabet=[1, 2, BG])
+    for bad, clipped in [((-1, 0, 3, 2), (0, 0, 2, 2)), ((0, 0, 9, 1), (0, 0, 8, 1)),
+                         ((7, 7, 2, 1), (7, 7, 1, 1)), ((0, 0, -1, 3), (0, 0, 0, 0)),
+                         ((9, 2, 4, 4), (0, 0, 0, 0))]:
+        a = oracle.depth_composite_roi(c, d, [bad, (0, 0, 8, 8)])
+        b = oracle.depth_composite_roi(c, d, [clipped, (0, 0, 8, 8)])
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+        np.testing.assert_array_equal(oracle.blend_ordered_roi(c, [(0, 0, 8, 8), bad]),
+                                      oracle.blend_ordered_roi(c, [(0, 0, 8, 8), clipped]))
