@@ -12,6 +12,17 @@
 // No shared memory, no tensor cores: there is no reuse and no contraction.
 #include "eqc_common.cuh"
 
+// ROI kernels: one wave of resident CTAs (the rectangle staging is paid once
+// per CTA) unless EQC_ROI_GRID16 asks for the 16-CTAs/SM grid
+#ifdef EQC_ROI_GRID16
+#define EQC_ROI_GRID(k) (16 * eqc_num_sms())
+#else
+#define EQC_ROI_GRID(k) ([] { static const int c = eqc_resident_ctas(k, 256); return c; }())
+#endif
+#ifndef EQC_ROI_MINB
+#define EQC_ROI_MINB 3
+#endif
+
 namespace {
 
 struct DepthParams {
@@ -33,11 +44,11 @@ __device__ __forceinline__ void zmin(uint32_t &bd, uint32_t &bc, uint32_t d, uin
 
 template <bool VEC>
 __global__ void __launch_bounds__(256) depth_composite_kernel(const __grid_constant__ DepthParams p) {
-  const int64_t total = (int64_t)p.groups_per_row * p.h;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int y = (int)(g / p.groups_per_row);
-    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+  // 32-bit group index (the host guarantees groups_per_row * h < 2^31)
+  const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int y = (int)(g / (uint32_t)p.groups_per_row);
+    const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
     const int64_t off = (int64_t)y * p.pitch + x;
     const int64_t ooff = (int64_t)y * p.out_pitch + x;
     if (VEC && x + 4 <= p.w) {
@@ -125,12 +136,12 @@ __device__ __forceinline__ uint32_t pack_round(const Acc4 &x) {
 }
 
 template <bool VEC>
-__global__ void __launch_bounds__(256) blend_ordered_kernel(const __grid_constant__ BlendParams p) {
-  const int64_t total = (int64_t)p.groups_per_row * p.h;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int y = (int)(g / p.groups_per_row);
-    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+__global__ void __launch_bounds__(256, 4) blend_ordered_kernel(const __grid_constant__ BlendParams p) {
+  // 32-bit group index (the host guarantees groups_per_row * h < 2^31)
+  const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int y = (int)(g / (uint32_t)p.groups_per_row);
+    const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
     const int64_t off = (int64_t)y * p.pitch + x;
     const int64_t ooff = (int64_t)y * p.out_pitch + x;
     if (VEC && x + 4 <= p.w) {
@@ -192,6 +203,41 @@ __device__ __forceinline__ Rect load_rect(const int32_t *r, int w, int h) {
   return q;
 }
 
+// Union over the warp's active lanes of the sources (or draw positions)
+// whose rectangle covers one of the lanes' 4-pixel groups, as two 32-bit
+// masks.  When the warp's groups lie in one row (the common case: a row of
+// 4K is 30 full warps) lane i tests rectangle i against the warp's span --
+// one test per source instead of one per source per lane; otherwise every
+// lane tests every rectangle and the masks are OR-reduced.
+__device__ __forceinline__ void warp_cover_union(const Rect *rs, int n, int y, int x, int cnt, uint32_t wm[2]) {
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  const int l0 = __ffs(act) - 1, l1 = 31 - __clz(act);
+  const int ya = __shfl_sync(act, y, l0), yb = __shfl_sync(act, y, l1);
+  if (ya == yb) {
+    const int xa = __shfl_sync(act, x, l0), xb = __shfl_sync(act, x + cnt, l1);  // span [xa, xb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      bool c = false;
+      const int i = 32 * h + lane;
+      if (i < n) {
+        const Rect r = rs[i];
+        c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && xa < r.x1 && xb > r.x0;
+      }
+      wm[h] = __ballot_sync(act, c);
+    }
+  } else {
+    uint32_t m[2] = {0, 0};
+    for (int i = 0; i < n; ++i) {
+      const Rect r = rs[i];
+      const bool c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && x < r.x1 && x + cnt > r.x0;
+      if (i < 32) m[0] |= (uint32_t)c << i; else m[1] |= (uint32_t)c << (i - 32);
+    }
+    wm[0] = __reduce_or_sync(act, m[0]);
+    wm[1] = __reduce_or_sync(act, m[1]);
+  }
+}
+
 struct DepthRoiParams {
   const uint32_t *color[EQC_MAX_SOURCES];
   const uint32_t *depth[EQC_MAX_SOURCES];
@@ -206,41 +252,71 @@ struct DepthRoiParams {
 // One thread per 4 consecutive pixels of a row, as depth_composite_kernel;
 // a source is read only where its rectangle covers the pixels.  Source 0 is
 // taken unconditionally where it is inside (argmin of (depth, index)).
-__global__ void __launch_bounds__(256) depth_composite_roi_kernel(const __grid_constant__ DepthRoiParams p) {
+__global__ void __launch_bounds__(256, EQC_ROI_MINB) depth_composite_roi_kernel(const __grid_constant__ DepthRoiParams p) {
   __shared__ Rect s_r[EQC_MAX_SOURCES];
   for (int i = threadIdx.x; i < p.n; i += blockDim.x) s_r[i] = load_rect(p.roi + 4 * i, p.w, p.h);
   __syncthreads();
-  const int64_t total = (int64_t)p.groups_per_row * p.h;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int y = (int)(g / p.groups_per_row);
-    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+  // 32-bit group index (the host guarantees groups_per_row * h < 2^31)
+  const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int y = (int)(g / (uint32_t)p.groups_per_row);
+    const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
     const int64_t off = (int64_t)y * p.pitch + x;
     const int cnt = min(4, p.w - x);
     uint32_t bd[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, bc[4] = {0, 0, 0, 0};
-    for (int i = 0; i < p.n; ++i) {
-      const Rect r = s_r[i];
-      if (y < r.y0 || y >= r.y1 || x + cnt <= r.x0 || x >= r.x1) continue;  // not covered
-      uint32_t d[4], c[4];
-      const bool full = x >= r.x0 && x + 4 <= r.x1;
-      if (p.vec && full) {
-        const uint4 dv = ld_stream_u4(p.depth[i] + off), cv = ld_stream_u4(p.color[i] + off);
-        d[0] = dv.x, d[1] = dv.y, d[2] = dv.z, d[3] = dv.w;
-        c[0] = cv.x, c[1] = cv.y, c[2] = cv.z, c[3] = cv.w;
+    uint32_t wmask[2];
+    warp_cover_union(s_r, p.n, y, x, cnt, wmask);  // warp-uniform source set
+    for (int h = 0; h < 2; ++h) {
+      uint32_t wm = wmask[h];
+      while (wm) {
+        // up to 4 sources of the union per batch (ascending index), loads
+        // predicated per lane on full coverage of its 4 pixels
+        int src[4];
+        uint32_t fb = 0, cb = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const bool t = i == 0 || d[j] < bd[j];
-          bd[j] = t ? d[j] : bd[j];
-          bc[j] = t ? c[j] : bc[j];
+        for (int b = 0; b < 4; ++b) {
+          src[b] = -1;
+          if (wm) {
+            src[b] = 32 * h + __ffs(wm) - 1;
+            wm &= wm - 1;
+            const Rect r = s_r[src[b]];
+            const bool c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && x < r.x1 && x + cnt > r.x0;
+            const bool f = c && p.vec && x >= r.x0 && x + 4 <= r.x1;
+            cb |= (uint32_t)c << b;
+            fb |= (uint32_t)f << b;
+          }
         }
-      } else {
+        uint4 dv[4], cv[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j < cnt && x + j >= r.x0 && x + j < r.x1) {
-            const uint32_t dj = ld_stream_u32(p.depth[i] + off + j), cj = ld_stream_u32(p.color[i] + off + j);
-            const bool t = i == 0 || dj < bd[j];
-            bd[j] = t ? dj : bd[j];
-            bc[j] = t ? cj : bc[j];
+        for (int b = 0; b < 4; ++b) {
+          const int i = max(src[b], 0);
+          dv[b] = ld_stream_u4_if(p.depth[i] + off, (fb >> b) & 1u);
+          cv[b] = ld_stream_u4_if(p.color[i] + off, (fb >> b) & 1u);
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = src[b];
+          if (i < 0) break;
+          if ((fb >> b) & 1u) {
+            const uint32_t d[4] = {dv[b].x, dv[b].y, dv[b].z, dv[b].w};
+            const uint32_t c[4] = {cv[b].x, cv[b].y, cv[b].z, cv[b].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const bool t = i == 0 || d[j] < bd[j];  // ties keep the lower index
+              bd[j] = t ? d[j] : bd[j];
+              bc[j] = t ? c[j] : bc[j];
+            }
+          } else if ((cb >> b) & 1u) {  // rectangle edge: per pixel
+            const Rect r = s_r[i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (j < cnt && x + j >= r.x0 && x + j < r.x1) {
+                const uint32_t dj = ld_stream_u32(p.depth[i] + off + j), cj = ld_stream_u32(p.color[i] + off + j);
+                const bool t = i == 0 || dj < bd[j];
+                bd[j] = t ? dj : bd[j];
+                bc[j] = t ? cj : bc[j];
+              }
+            }
           }
         }
       }
@@ -271,33 +347,59 @@ struct BlendRoiParams {
 
 // Ordered blend over ROI-restricted layers: outside its rectangle a layer is
 // transparent and is skipped (over() with s = 0 is the identity).
-__global__ void __launch_bounds__(256) blend_ordered_roi_kernel(const __grid_constant__ BlendRoiParams p) {
+__global__ void __launch_bounds__(256, EQC_ROI_MINB) blend_ordered_roi_kernel(const __grid_constant__ BlendRoiParams p) {
   __shared__ Rect s_r[EQC_MAX_SOURCES];
   for (int k = threadIdx.x; k < p.n; k += blockDim.x) s_r[k] = load_rect(p.roi + 4 * p.src_of[k], p.w, p.h);
   __syncthreads();
-  const int64_t total = (int64_t)p.groups_per_row * p.h;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int y = (int)(g / p.groups_per_row);
-    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
+  // 32-bit group index (the host guarantees groups_per_row * h < 2^31)
+  const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int y = (int)(g / (uint32_t)p.groups_per_row);
+    const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
     const int64_t off = (int64_t)y * p.pitch + x;
     const int cnt = min(4, p.w - x);
     Acc4 acc[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = Acc4{p.bg[0], p.bg[1], p.bg[2], p.bg[3]};
-    for (int k = 0; k < p.n; ++k) {
-      const Rect r = s_r[k];
-      if (y < r.y0 || y >= r.y1 || x + cnt <= r.x0 || x >= r.x1) continue;
-      if (p.vec && x >= r.x0 && x + 4 <= r.x1) {
-        const uint4 s = ld_stream_u4(p.color[k] + off);
-        over(acc[0], s.x);
-        over(acc[1], s.y);
-        over(acc[2], s.z);
-        over(acc[3], s.w);
-      } else {
+    uint32_t wmask[2];
+    warp_cover_union(s_r, p.n, y, x, cnt, wmask);  // draw positions, warp-uniform
+    for (int h = 0; h < 2; ++h) {
+      uint32_t wm = wmask[h];  // ascending k = draw order
+      while (wm) {
+        int kk[4];
+        uint32_t fb = 0, cb = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < cnt && x + j >= r.x0 && x + j < r.x1) over(acc[j], ld_stream_u32(p.color[k] + off + j));
+        for (int b = 0; b < 4; ++b) {
+          kk[b] = -1;
+          if (wm) {
+            kk[b] = 32 * h + __ffs(wm) - 1;
+            wm &= wm - 1;
+            const Rect r = s_r[kk[b]];
+            const bool c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && x < r.x1 && x + cnt > r.x0;
+            const bool f = c && p.vec && x >= r.x0 && x + 4 <= r.x1;
+            cb |= (uint32_t)c << b;
+            fb |= (uint32_t)f << b;
+          }
+        }
+        uint4 sv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) sv[b] = ld_stream_u4_if(p.color[max(kk[b], 0)] + off, (fb >> b) & 1u);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int k = kk[b];
+          if (k < 0) break;
+          if ((fb >> b) & 1u) {
+            over(acc[0], sv[b].x);
+            over(acc[1], sv[b].y);
+            over(acc[2], sv[b].z);
+            over(acc[3], sv[b].w);
+          } else if ((cb >> b) & 1u) {
+            const Rect r = s_r[k];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < cnt && x + j >= r.x0 && x + j < r.x1) over(acc[j], ld_stream_u32(p.color[k] + off + j));
+          }
+        }
       }
     }
     const int64_t ooff = (int64_t)y * p.out_pitch + x;
@@ -312,9 +414,11 @@ __global__ void __launch_bounds__(256) blend_ordered_roi_kernel(const __grid_con
 
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
-inline int grid_for(int64_t items) {
+// Grid of a grid-stride kernel over `items` 4-pixel groups: one group per
+// thread, at most `cap` CTAs (16 per SM measured best for the streaming
+// kernels: several waves even out the per-thread iteration counts).
+inline int grid_for(int64_t items, int cap = 16 * eqc_num_sms()) {
   int64_t blocks = (items + 255) / 256;
-  int64_t cap = (int64_t)eqc_num_sms() * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return (int)blocks;
@@ -345,6 +449,7 @@ extern "C" int compositor_depth(int n, const uint32_t *const *color, const uint3
   p.h = h;
   p.groups_per_row = (w + 3) / 4;
   const int64_t groups = (int64_t)p.groups_per_row * h;
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   if (vec)
     depth_composite_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
@@ -378,6 +483,7 @@ extern "C" int compositor_blend_ordered(int n, const uint32_t *const *color, con
   p.groups_per_row = (w + 3) / 4;
   for (int c = 0; c < 4; ++c) p.bg[c] = (float)((background >> (8 * c)) & 0xFFu);
   const int64_t groups = (int64_t)p.groups_per_row * h;
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   if (vec)
     blend_ordered_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
@@ -412,7 +518,8 @@ extern "C" int compositor_depth_roi(int n, const uint32_t *const *color, const u
   p.groups_per_row = (w + 3) / 4;
   p.vec = vec ? 1 : 0;
   const int64_t groups = (int64_t)p.groups_per_row * h;
-  depth_composite_roi_kernel<<<grid_for(groups), 256, 0, (cudaStream_t)stream>>>(p);
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
+  depth_composite_roi_kernel<<<grid_for(groups, EQC_ROI_GRID(depth_composite_roi_kernel)), 256, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
 
@@ -446,6 +553,7 @@ extern "C" int compositor_blend_ordered_roi(int n, const uint32_t *const *color,
   p.vec = vec ? 1 : 0;
   for (int c = 0; c < 4; ++c) p.bg[c] = (float)((background >> (8 * c)) & 0xFFu);
   const int64_t groups = (int64_t)p.groups_per_row * h;
-  blend_ordered_roi_kernel<<<grid_for(groups), 256, 0, (cudaStream_t)stream>>>(p);
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
+  blend_ordered_roi_kernel<<<grid_for(groups, EQC_ROI_GRID(blend_ordered_roi_kernel)), 256, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }

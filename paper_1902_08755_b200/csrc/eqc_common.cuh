@@ -33,17 +33,42 @@ static inline int eqc_num_sms() {
   return n;
 }
 
+// CTAs of `kernel` (at `threads` per CTA) resident on the whole GPU at once:
+// grid-stride kernels launch at most this many, so there is no partial last
+// wave (a 1.33-wave grid leaves most SMs idle for its last third).
+template <typename K>
+inline int eqc_resident_ctas(K kernel, int threads, size_t smem = 0) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  return occ * eqc_num_sms();
+}
+
 // ---- streaming 128-bit global access (inputs are read exactly once) -------
+// The loads are not `volatile`: inputs are read-only for the kernel's lifetime,
+// and the scheduler must be free to hoist a batch of loads above the
+// arithmetic that consumes the previous ones (volatile asm pins their order
+// relative to each other and lets the compiler interleave load / use).
 __device__ __forceinline__ uint4 ld_stream_u4(const void *p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
 }
+// Predicated variant: no memory access (and zeros) when !pred.  Branch-free,
+// so a batch of them can all be in flight (a load under an `if` is not
+// hoisted above the branch of the next one).
+__device__ __forceinline__ uint4 ld_stream_u4_if(const void *p, bool pred) {
+  uint4 r = make_uint4(0, 0, 0, 0);
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+      : "l"(p), "r"((uint32_t)pred));
+  return r;
+}
 __device__ __forceinline__ uint32_t ld_stream_u32(const void *p) {
   uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ void st_stream_u4(void *p, uint4 v) {

@@ -42,23 +42,45 @@ __global__ void __launch_bounds__(256) roi_scan_kernel(const __grid_constant__ R
   const uint32_t *fr = p.frame[f];
   const uint32_t bg = p.background;
   int x0 = INT_MAX, y0 = INT_MAX, x1 = -1, y1 = -1;
-  const int64_t g0 = (int64_t)ya * p.groups_per_row, g1 = (int64_t)yb * p.groups_per_row;
-  for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x) {
-    const int y = (int)(g / p.groups_per_row);
-    const int x = (int)(g - (int64_t)y * p.groups_per_row) * 4;
-    const uint32_t *q = fr + (int64_t)y * p.pitch + x;
-    uint32_t m = 0;  // bit j: pixel x + j is rendered
-    if (p.vec && x + 4 <= p.w) {
-      const uint4 v = ld_stream_u4(q);
-      m = (v.x != bg) | ((v.y != bg) << 1) | ((v.z != bg) << 2) | ((v.w != bg) << 3);
-    } else {
-      for (int j = 0; j < 4 && x + j < p.w; ++j) m |= (uint32_t)(ld_stream_u32(q + j) != bg) << j;
+  const uint32_t gpr = (uint32_t)p.groups_per_row;
+  const uint32_t g0 = (uint32_t)ya * gpr, g1 = (uint32_t)yb * gpr;  // < 2^31 (host check)
+  const uint32_t stride = blockDim.x;
+  if (p.vec && (p.w & 3) == 0) {
+    // every group is 4 full pixels: 8 predicated 128-bit loads in flight per
+    // thread per step, no branches between them
+    for (uint32_t gb = g0 + threadIdx.x; gb < g1; gb += 8 * stride) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t g = min(gb + u * stride, g1 - 1);
+        const uint32_t y = g / gpr;
+        v[u] = ld_stream_u4_if(fr + (int64_t)y * p.pitch + (g - y * gpr) * 4, gb + u * stride < g1);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t g = gb + u * stride;
+        const uint32_t m = (v[u].x != bg) | ((v[u].y != bg) << 1) | ((v[u].z != bg) << 2) | ((v[u].w != bg) << 3);
+        if (g < g1 && m) {
+          const int y = (int)(g / gpr), x = (int)(g - (uint32_t)y * gpr) * 4;
+          x0 = min(x0, x + __ffs(m) - 1);
+          x1 = max(x1, x + 31 - __clz(m));
+          y0 = min(y0, y);
+          y1 = max(y1, y);
+        }
+      }
     }
-    if (m) {
-      x0 = min(x0, x + __ffs(m) - 1);
-      x1 = max(x1, x + 31 - __clz(m));
-      y0 = min(y0, y);
-      y1 = max(y1, y);
+  } else {
+    for (uint32_t g = g0 + threadIdx.x; g < g1; g += stride) {
+      const int y = (int)(g / gpr), x = (int)(g - (uint32_t)y * gpr) * 4;
+      const uint32_t *q = fr + (int64_t)y * p.pitch + x;
+      uint32_t m = 0;
+      for (int j = 0; j < 4 && x + j < p.w; ++j) m |= (uint32_t)(ld_stream_u32(q + j) != bg) << j;
+      if (m) {
+        x0 = min(x0, x + __ffs(m) - 1);
+        x1 = max(x1, x + 31 - __clz(m));
+        y0 = min(y0, y);
+        y1 = max(y1, y);
+      }
     }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -121,8 +143,10 @@ extern "C" int image_roi(int n, const uint32_t *const *frames, int w, int h, int
   p.background = background;
   p.vec = vec ? 1 : 0;
   p.groups_per_row = (w + 3) / 4;
-  // ~8 CTAs per SM over all frames, whole rows per CTA
-  p.ctas_per_frame = std::max(1, std::min(h, eqc_num_sms() * 8 / n));
+  if ((int64_t)p.groups_per_row * h > 0x7FFFFFFFll) return EQC_E_INVALID;
+  // one full wave of resident CTAs over all frames, whole rows per CTA
+  static const int resident = eqc_resident_ctas(roi_scan_kernel, 256);
+  p.ctas_per_frame = std::max(1, std::min(h, resident / n));
   cudaStream_t s = (cudaStream_t)stream;
   roi_init_kernel<<<1, 64, 0, s>>>(d_roi, n);
   roi_scan_kernel<<<n * p.ctas_per_frame, 256, 0, s>>>(p);

@@ -1,8 +1,8 @@
 """Region of interest on one B200: full-frame compositing
 against ROI compositing (image_roi on the device + compositor_*_roi), for
 compact and scattered sort-last scenes (8 x 3840x2160 colour + depth) and the
-c3 volume bricks (16 x 3840x2160 blend).  CUDA events, median of 20 after 3
-warm-ups; inputs > L2.  Prints one JSON line.
+c3 volume bricks (16 x 3840x2160 blend).  10 calls captured in a CUDA graph, replays
+timed with CUDA events (median of 20); inputs > L2.  Prints one JSON line.
 
     python scripts/bench_roi.py
 """
@@ -22,18 +22,31 @@ HBM = 6542.7
 BG = 0xFFFFFFFF
 
 
-def timed(fn, steps=20, warm=3):
-    for _ in range(warm):
-        fn()
+def timed(fn, steps=20, warm=3, reps=10):
+    """GPU time of one call: `reps` calls captured in a CUDA graph, replayed
+    `steps` times between events (median / reps).  The graph removes the
+    Python/ctypes launch overhead, which exceeds these kernels' run time."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(warm):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
     torch.cuda.synchronize()
     ts = []
     for _ in range(steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        g.replay()
         b.record()
         b.synchronize()
-        ts.append(a.elapsed_time(b))
+        ts.append(a.elapsed_time(b) / reps)
     return statistics.median(ts)
 
 
