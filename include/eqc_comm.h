@@ -33,6 +33,8 @@ typedef struct eqc_comm eqc_comm;
 #define EQC_OP_DEPTH 0      /* depth-sorted compositing (compositor_depth semantics) */
 #define EQC_FLAG_RLE 1      /* ship bands as RLE-BP streams (colour swizzled + depth) */
 #define EQC_FLAG_NCCL 2     /* direct send: force NCCL grouped send/recv instead of the NVLink peer-memory path */
+#define EQC_FLAG_ROI 4      /* region of interest: peer-memory direct send reads and composites
+                               only the ROI of every partial frame (computed on the device) */
 
 /* NCCL unique id of a new clique (rank 0 calls this and broadcasts the bytes). */
 EQC_API int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]);
@@ -87,6 +89,13 @@ EQC_API int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_ro
  * the steps; no staging, no NCCL on the data path).  Otherwise, or with
  * EQC_FLAG_NCCL, the bands move with NCCL grouped send/recv.  With
  * EQC_FLAG_RLE the call synchronises `stream` once (message sizes).
+ * EQC_FLAG_ROI (peer-memory path; other transports ignore it): the local
+ * pre-composite also reduces the bounding box of its rendered pixels (the
+ * ROI computed "by analysing the framebuffer", fused: no extra
+ * pass), publishes it in peer memory, and the band composite pulls only the
+ * peers' pixels inside their boxes (the ROI travels with the
+ * pixel data and places it).  Same result; fewer NVLink bytes when the
+ * partial frames cover compact regions.
  */
 EQC_API int compose_direct_send(eqc_comm *comm, int n_local, const uint32_t *const *color,
                                 const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,

@@ -22,6 +22,18 @@
 #include "../../include/eqc_comm.h"
 #include "eqc_common.cuh"
 
+// composite.cu: depth compositing over ROI-restricted sources (per-source ROI
+// pointers, band row offset, optional output rectangle)
+int eqc_depth_roi_launch(int n, const uint32_t *const *color, const uint32_t *const *depth,
+                         const int32_t *const *roi, int roi_dy, const int32_t *out_roi, int w, int h,
+                         int64_t pitch, uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
+                         cudaStream_t stream);
+// composite.cu: compositor_depth that also reduces the ROI of its output
+size_t eqc_depth_bbox_scratch_bytes();
+int eqc_depth_composite_bbox(int n, const uint32_t *const *color, const uint32_t *const *depth, int w, int h,
+                             int64_t pitch, uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
+                             void *scratch, int32_t *out_roi, cudaStream_t s);
+
 namespace {
 
 #define EQC_NCCL_TRY(expr)                 \
@@ -645,7 +657,7 @@ int validate(int nranks, int n_local, const void *color, const void *depth, int 
   if (nranks < 1 || n_local < 1 || n_local > EQC_MAX_SOURCES || nranks > EQC_MAX_SOURCES) return EQC_E_INVALID;
   if (!color || !depth || w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
   if (op != EQC_OP_DEPTH) return EQC_E_UNSUPPORTED;
-  if (flags & ~(EQC_FLAG_RLE | EQC_FLAG_NCCL)) return EQC_E_INVALID;
+  if (flags & ~(EQC_FLAG_RLE | EQC_FLAG_NCCL | EQC_FLAG_ROI)) return EQC_E_INVALID;
   if (dest < 0 || dest >= nranks) return EQC_E_INVALID;
   if (is_dest && (!out || out_pitch < w)) return EQC_E_INVALID;
   return EQC_OK;
@@ -689,10 +701,14 @@ __global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
   __syncthreads();
 }
 
+// The IPC-exposed `flags` allocation holds the barrier flags (EQC_MAX_SOURCES
+// ints) followed by the rank's partial-frame ROI {x, y, w, h} (kRoiSlot).
+constexpr int kRoiSlot = EQC_MAX_SOURCES;  // int offset, 16-byte aligned
+
 struct P2PState {
   int capable = -1;  // -1 unknown, 0 no (NCCL transport), 1 yes
   int64_t cap_px = 0;
-  DevBuf part_c, part_d, fin_c, flags, xfer;
+  DevBuf part_c, part_d, fin_c, flags, xfer, roi_local;
   std::vector<uint32_t *> peer_part_c, peer_part_d, peer_fin_c;
   std::vector<int *> peer_flags;
   int epoch = 0;
@@ -736,7 +752,7 @@ int p2p_setup(eqc_comm *c, int64_t px, cudaStream_t s) {
   EQC_TRY(P.part_d.ensure(bytes));
   EQC_TRY(P.fin_c.ensure(bytes));
   P.flags.release();
-  EQC_TRY(P.flags.ensure_zeroed(EQC_MAX_SOURCES * sizeof(int)));
+  EQC_TRY(P.flags.ensure_zeroed((kRoiSlot + 4) * sizeof(int)));
   P.epoch = 0;
   const int n = c->nranks;
   constexpr int kH = sizeof(cudaIpcMemHandle_t);
@@ -811,9 +827,21 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   for (int i = 0; i < 4; ++i) stats[i] = 0;
   std::vector<int> row0(n + 1);
   plan_bands(g.h, n, row0.data());
-  // (1) local pre-composite into the IPC-exposed partial frame
-  EQC_TRY(compositor_depth(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
-                           P.part_d.as<uint32_t>(), g.w, s));
+  const bool roi = (g.flags & EQC_FLAG_ROI) != 0;
+  int32_t *my_roi = P.flags.as<int32_t>() + kRoiSlot;
+  // (1) local pre-composite into the IPC-exposed partial frame.  With
+  // EQC_FLAG_ROI the same kernel reduces the bounding box of
+  // the partial's rendered pixels (the ROI "computed by analysing the
+  // framebuffer", at no extra pass) and publishes it in the
+  // peer-readable flags allocation; no host round trip.
+  if (roi) {
+    EQC_TRY(P.roi_local.ensure(eqc_depth_bbox_scratch_bytes()));
+    EQC_TRY(eqc_depth_composite_bbox(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
+                                     P.part_d.as<uint32_t>(), g.w, P.roi_local.p, my_roi, s));
+  } else {
+    EQC_TRY(compositor_depth(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
+                             P.part_d.as<uint32_t>(), g.w, s));
+  }
   EQC_TRY(p2p_barrier(c, s));
   // (2)+(3)+(4) band composite pulling every peer's band over NVLink, output
   // pushed into the destination's frame
@@ -830,7 +858,14 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
     }
     uint32_t *out = me == g.dest ? g.out + (size_t)y0 * g.out_pitch : P.peer_fin_c[g.dest] + (size_t)y0 * g.w;
     const int64_t opitch = me == g.dest ? g.out_pitch : g.w;
-    EQC_TRY(compositor_depth(n, cs.data(), ds.data(), g.w, rows, g.w, out, nullptr, opitch, s));
+    if (roi) {  // peers' partials are read only inside their ROIs (band-relative rows)
+      std::vector<const int32_t *> rp(n);
+      for (int q = 0; q < n; ++q) rp[q] = P.peer_flags[q] + kRoiSlot;
+      EQC_TRY(eqc_depth_roi_launch(n, cs.data(), ds.data(), rp.data(), y0, nullptr, g.w, rows, g.w, out, nullptr,
+                                   opitch, s));
+    } else {
+      EQC_TRY(compositor_depth(n, cs.data(), ds.data(), g.w, rows, g.w, out, nullptr, opitch, s));
+    }
     if (me != g.dest) {
       stats[1] += 1;
       stats[2] += (int64_t)rows * g.w * 4;

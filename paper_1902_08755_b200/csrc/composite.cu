@@ -30,9 +30,48 @@ struct DepthParams {
   const uint32_t *depth[EQC_MAX_SOURCES];
   uint32_t *out_color;
   uint32_t *out_depth;
+  int4 *cta_box;  // BBOX: per-CTA bounding box {x0, y0, x1, y1} (inclusive) of the rendered output
   int64_t pitch, out_pitch;
   int n, w, h, groups_per_row;
 };
+
+// Running bounding box of rendered pixels (output depth != background),
+// fused into the composite: the ROI of the composited frame
+// at no extra HBM pass.  `m` bit j: pixel x + j is rendered.
+struct BBox {
+  int x0 = 0x7FFFFFFF, y0 = 0x7FFFFFFF, x1 = -1, y1 = -1;
+  __device__ __forceinline__ void add(int x, int y, uint32_t m) {
+    if (m) {
+      x0 = min(x0, x + __ffs(m) - 1);
+      x1 = max(x1, x + 31 - __clz(m));
+      y0 = min(y0, y);
+      y1 = max(y1, y);
+    }
+  }
+  // CTA-wide reduction; thread 0 stores the CTA's box
+  __device__ __forceinline__ void store_cta(int4 *out) {
+    __shared__ int4 s_b[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int a = __reduce_min_sync(EQC_FULL, x0), b = __reduce_min_sync(EQC_FULL, y0);
+    int c = __reduce_max_sync(EQC_FULL, x1), d = __reduce_max_sync(EQC_FULL, y1);
+    if (lane == 0) s_b[warp] = make_int4(a, b, c, d);
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      const int4 v = lane < nw ? s_b[lane] : make_int4(0x7FFFFFFF, 0x7FFFFFFF, -1, -1);
+      a = __reduce_min_sync(EQC_FULL, v.x);
+      b = __reduce_min_sync(EQC_FULL, v.y);
+      c = __reduce_max_sync(EQC_FULL, v.z);
+      d = __reduce_max_sync(EQC_FULL, v.w);
+      if (lane == 0) out[blockIdx.x] = make_int4(a, b, c, d);
+    }
+  }
+};
+
+__device__ __forceinline__ uint32_t rendered4(uint4 d) {
+  return (d.x != 0xFFFFFFFFu) | ((d.y != 0xFFFFFFFFu) << 1) | ((d.z != 0xFFFFFFFFu) << 2) |
+         ((d.w != 0xFFFFFFFFu) << 3);
+}
 
 // One running (depth, colour) minimum step per lane: strictly smaller depth
 // replaces, so for equal depths the earlier (lower-index) source is kept.
@@ -42,8 +81,9 @@ __device__ __forceinline__ void zmin(uint32_t &bd, uint32_t &bc, uint32_t d, uin
   bc = t ? c : bc;
 }
 
-template <bool VEC>
+template <bool VEC, bool BBOX = false>
 __global__ void __launch_bounds__(256) depth_composite_kernel(const __grid_constant__ DepthParams p) {
+  BBox box;
   // 32-bit group index (the host guarantees groups_per_row * h < 2^31)
   const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
@@ -81,6 +121,7 @@ __global__ void __launch_bounds__(256) depth_composite_kernel(const __grid_const
       }
       st_stream_u4(p.out_color + ooff, bc);
       if (p.out_depth) st_stream_u4(p.out_depth + ooff, bd);
+      if (BBOX) box.add(x, y, rendered4(bd));
     } else {
       const int cnt = min(4, p.w - x);
       for (int k = 0; k < cnt; ++k) {
@@ -88,8 +129,38 @@ __global__ void __launch_bounds__(256) depth_composite_kernel(const __grid_const
         for (int i = 1; i < p.n; ++i) zmin(bd, bc, p.depth[i][off + k], p.color[i][off + k]);
         p.out_color[ooff + k] = bc;
         if (p.out_depth) p.out_depth[ooff + k] = bd;
+        if (BBOX) box.add(x + k, y, bd != 0xFFFFFFFFu);
       }
     }
+  }
+  if (BBOX) box.store_cta(p.cta_box);
+}
+
+// Reduce the per-CTA boxes into {x, y, w, h} ({0, 0, 0, 0} if nothing is rendered).
+__global__ void bbox_finalize_kernel(const int4 *cta, int ncta, int32_t *out) {
+  BBox b;
+  for (int i = threadIdx.x; i < ncta; i += blockDim.x) {
+    const int4 v = cta[i];
+    b.x0 = min(b.x0, v.x);
+    b.y0 = min(b.y0, v.y);
+    b.x1 = max(b.x1, v.z);
+    b.y1 = max(b.y1, v.w);
+  }
+  __shared__ int4 s_b[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int a = __reduce_min_sync(EQC_FULL, b.x0), c = __reduce_min_sync(EQC_FULL, b.y0);
+  int d = __reduce_max_sync(EQC_FULL, b.x1), e = __reduce_max_sync(EQC_FULL, b.y1);
+  if (lane == 0) s_b[warp] = make_int4(a, c, d, e);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int4 r = s_b[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      r.x = min(r.x, s_b[w].x);
+      r.y = min(r.y, s_b[w].y);
+      r.z = max(r.z, s_b[w].z);
+      r.w = max(r.w, s_b[w].w);
+    }
+    *reinterpret_cast<int4 *>(out) = r.z < 0 ? make_int4(0, 0, 0, 0) : make_int4(r.x, r.y, r.z - r.x + 1, r.w - r.y + 1);
   }
 }
 
@@ -209,29 +280,39 @@ __device__ __forceinline__ Rect load_rect(const int32_t *r, int w, int h) {
 // 4K is 30 full warps) lane i tests rectangle i against the warp's span --
 // one test per source instead of one per source per lane; otherwise every
 // lane tests every rectangle and the masks are OR-reduced.
-__device__ __forceinline__ void warp_cover_union(const Rect *rs, int n, int y, int x, int cnt, uint32_t wm[2]) {
+__device__ __forceinline__ void warp_cover_union(const Rect *rs, int n, int y, int x, int cnt, bool live,
+                                                 uint32_t wm[2]) {
   const unsigned act = __activemask();
+  const unsigned lv = __ballot_sync(act, live);  // lanes whose group is to be composited
+  wm[0] = wm[1] = 0;
+  if (!lv) return;
   const int lane = threadIdx.x & 31;
-  const int l0 = __ffs(act) - 1, l1 = 31 - __clz(act);
+  const int l0 = __ffs(lv) - 1, l1 = 31 - __clz(lv);
   const int ya = __shfl_sync(act, y, l0), yb = __shfl_sync(act, y, l1);
-  if (ya == yb) {
-    const int xa = __shfl_sync(act, x, l0), xb = __shfl_sync(act, x + cnt, l1);  // span [xa, xb)
+  const int xa = __shfl_sync(act, x, l0), xb = __shfl_sync(act, x + cnt, l1);
+  // fast path: every live lane lies on row ya inside the span [xa, xb) of the
+  // first and last live lanes; the union tested against the span is a
+  // superset of the lanes' union (extra sources are then masked per lane)
+  const bool one = ya == yb && __all_sync(act, !live || (y == ya && x >= xa && x + cnt <= xb));
+  if (one) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       bool c = false;
       const int i = 32 * h + lane;
       if (i < n) {
         const Rect r = rs[i];
-        c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && xa < r.x1 && xb > r.x0;
+        c = (unsigned)(ya - r.y0) < (unsigned)(r.y1 - r.y0) && xa < r.x1 && xb > r.x0;
       }
       wm[h] = __ballot_sync(act, c);
     }
   } else {
     uint32_t m[2] = {0, 0};
-    for (int i = 0; i < n; ++i) {
-      const Rect r = rs[i];
-      const bool c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && x < r.x1 && x + cnt > r.x0;
-      if (i < 32) m[0] |= (uint32_t)c << i; else m[1] |= (uint32_t)c << (i - 32);
+    if (live) {
+      for (int i = 0; i < n; ++i) {
+        const Rect r = rs[i];
+        const bool c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && x < r.x1 && x + cnt > r.x0;
+        if (i < 32) m[0] |= (uint32_t)c << i; else m[1] |= (uint32_t)c << (i - 32);
+      }
     }
     wm[0] = __reduce_or_sync(act, m[0]);
     wm[1] = __reduce_or_sync(act, m[1]);
@@ -241,7 +322,9 @@ __device__ __forceinline__ void warp_cover_union(const Rect *rs, int n, int y, i
 struct DepthRoiParams {
   const uint32_t *color[EQC_MAX_SOURCES];
   const uint32_t *depth[EQC_MAX_SOURCES];
-  const int32_t *roi;  // device, n x {x, y, w, h}
+  const int32_t *roi[EQC_MAX_SOURCES];  // device {x, y, w, h} of each source (may live on a peer GPU)
+  const int32_t *out_roi;               // nullable device {x, y, w, h}: only groups touching it are written
+  int roi_dy;                           // rectangles are in frame rows; this launch covers rows roi_dy..
   uint32_t *out_color;
   uint32_t *out_depth;
   int64_t pitch, out_pitch;
@@ -252,10 +335,19 @@ struct DepthRoiParams {
 // One thread per 4 consecutive pixels of a row, as depth_composite_kernel;
 // a source is read only where its rectangle covers the pixels.  Source 0 is
 // taken unconditionally where it is inside (argmin of (depth, index)).
+__device__ __forceinline__ Rect load_rect_dy(const int32_t *r, int dy, int w, int h) {
+  const int4 v = *reinterpret_cast<const int4 *>(r);
+  const int32_t q[4] = {v.x, v.y - dy, v.z, v.w};  // same clipping as load_rect, band-relative rows
+  return load_rect(q, w, h);
+}
+
 __global__ void __launch_bounds__(256, EQC_ROI_MINB) depth_composite_roi_kernel(const __grid_constant__ DepthRoiParams p) {
   __shared__ Rect s_r[EQC_MAX_SOURCES];
-  for (int i = threadIdx.x; i < p.n; i += blockDim.x) s_r[i] = load_rect(p.roi + 4 * i, p.w, p.h);
+  __shared__ Rect s_out;
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) s_r[i] = load_rect_dy(p.roi[i], p.roi_dy, p.w, p.h);
+  if (threadIdx.x == 0) s_out = p.out_roi ? load_rect_dy(p.out_roi, p.roi_dy, p.w, p.h) : Rect{0, 0, p.w, p.h};
   __syncthreads();
+  const Rect orr = s_out;
   // 32-bit group index (the host guarantees groups_per_row * h < 2^31)
   const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
@@ -263,9 +355,12 @@ __global__ void __launch_bounds__(256, EQC_ROI_MINB) depth_composite_roi_kernel(
     const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
     const int64_t off = (int64_t)y * p.pitch + x;
     const int cnt = min(4, p.w - x);
+    // outside the output rectangle nothing is read or written (the lane still
+    // takes part in the warp's collectives)
+    const bool live = (unsigned)(y - orr.y0) < (unsigned)(orr.y1 - orr.y0) && x < orr.x1 && x + cnt > orr.x0;
     uint32_t bd[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, bc[4] = {0, 0, 0, 0};
     uint32_t wmask[2];
-    warp_cover_union(s_r, p.n, y, x, cnt, wmask);  // warp-uniform source set
+    warp_cover_union(s_r, p.n, y, x, cnt, live, wmask);  // warp-uniform source set
     for (int h = 0; h < 2; ++h) {
       uint32_t wm = wmask[h];
       while (wm) {
@@ -280,7 +375,7 @@ __global__ void __launch_bounds__(256, EQC_ROI_MINB) depth_composite_roi_kernel(
             src[b] = 32 * h + __ffs(wm) - 1;
             wm &= wm - 1;
             const Rect r = s_r[src[b]];
-            const bool c = (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && x < r.x1 && x + cnt > r.x0;
+            const bool c = live && (unsigned)(y - r.y0) < (unsigned)(r.y1 - r.y0) && x < r.x1 && x + cnt > r.x0;
             const bool f = c && p.vec && x >= r.x0 && x + 4 <= r.x1;
             cb |= (uint32_t)c << b;
             fb |= (uint32_t)f << b;
@@ -321,6 +416,7 @@ __global__ void __launch_bounds__(256, EQC_ROI_MINB) depth_composite_roi_kernel(
         }
       }
     }
+    if (!live) continue;
     const int64_t ooff = (int64_t)y * p.out_pitch + x;
     if (p.vec && cnt == 4) {
       st_stream_u4(p.out_color + ooff, make_uint4(bc[0], bc[1], bc[2], bc[3]));
@@ -362,7 +458,7 @@ __global__ void __launch_bounds__(256, EQC_ROI_MINB) blend_ordered_roi_kernel(co
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = Acc4{p.bg[0], p.bg[1], p.bg[2], p.bg[3]};
     uint32_t wmask[2];
-    warp_cover_union(s_r, p.n, y, x, cnt, wmask);  // draw positions, warp-uniform
+    warp_cover_union(s_r, p.n, y, x, cnt, true, wmask);  // draw positions, warp-uniform
     for (int h = 0; h < 2; ++h) {
       uint32_t wm = wmask[h];  // ascending k = draw order
       while (wm) {
@@ -458,6 +554,46 @@ extern "C" int compositor_depth(int n, const uint32_t *const *color, const uint3
   return eqc_launch_status();
 }
 
+// Internal (compose.cu, EQC_FLAG_ROI): compositor_depth that also writes the
+// ROI {x, y, w, h} of its output (pixels with depth != 0xFFFFFFFF) to the
+// device int32[4] `out_roi`, reduced from per-CTA boxes in `scratch`
+// (>= eqc_depth_bbox_scratch_bytes()).
+size_t eqc_depth_bbox_scratch_bytes() { return (size_t)16 * eqc_num_sms() * sizeof(int4); }
+
+int eqc_depth_composite_bbox(int n, const uint32_t *const *color, const uint32_t *const *depth, int w, int h,
+                             int64_t pitch, uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
+                             void *scratch, int32_t *out_roi, cudaStream_t s) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color || !depth || !out_color || !out_depth || !scratch || !out_roi)
+    return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
+  DepthParams p;
+  bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) && aligned16(out_color) && aligned16(out_depth);
+  for (int i = 0; i < n; ++i) {
+    if (!color[i] || !depth[i]) return EQC_E_INVALID;
+    p.color[i] = color[i];
+    p.depth[i] = depth[i];
+    vec = vec && aligned16(color[i]) && aligned16(depth[i]);
+  }
+  p.out_color = out_color;
+  p.out_depth = out_depth;
+  p.cta_box = reinterpret_cast<int4 *>(scratch);
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
+  const int grid = grid_for(groups);
+  if (vec)
+    depth_composite_kernel<true, true><<<grid, 256, 0, s>>>(p);
+  else
+    depth_composite_kernel<false, true><<<grid, 256, 0, s>>>(p);
+  bbox_finalize_kernel<<<1, 256, 0, s>>>(p.cta_box, grid, out_roi);
+  return eqc_launch_status();
+}
+
 extern "C" int compositor_blend_ordered(int n, const uint32_t *const *color, const int32_t *order,
                                         int w, int h, int64_t pitch, uint32_t background,
                                         uint32_t *out_color, int64_t out_pitch, void *stream) {
@@ -492,22 +628,29 @@ extern "C" int compositor_blend_ordered(int n, const uint32_t *const *color, con
   return eqc_launch_status();
 }
 
-extern "C" int compositor_depth_roi(int n, const uint32_t *const *color, const uint32_t *const *depth,
-                                    const int32_t *d_roi, int w, int h, int64_t pitch, uint32_t *out_color,
-                                    uint32_t *out_depth, int64_t out_pitch, void *stream) {
-  if (n < 1 || n > EQC_MAX_SOURCES || !color || !depth || !d_roi || !out_color) return EQC_E_INVALID;
+// Internal launcher shared by compositor_depth_roi and the ROI direct send
+// (compose.cu): per-source ROI pointers (peer memory allowed), rectangles in
+// frame rows offset by roi_dy (a band starting at frame row roi_dy), and an
+// optional output rectangle outside which nothing is written.
+int eqc_depth_roi_launch(int n, const uint32_t *const *color, const uint32_t *const *depth,
+                         const int32_t *const *roi, int roi_dy, const int32_t *out_roi, int w, int h,
+                         int64_t pitch, uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
+                         cudaStream_t stream) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color || !depth || !roi || !out_color) return EQC_E_INVALID;
   if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
-  if (((uintptr_t)d_roi & 15) != 0) return EQC_E_INVALID;
+  if (out_roi && ((uintptr_t)out_roi & 15) != 0) return EQC_E_INVALID;
   DepthRoiParams p;
   bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) && aligned16(out_color) &&
              (!out_depth || aligned16(out_depth));
   for (int i = 0; i < n; ++i) {
-    if (!color[i] || !depth[i]) return EQC_E_INVALID;
+    if (!color[i] || !depth[i] || !roi[i] || ((uintptr_t)roi[i] & 15) != 0) return EQC_E_INVALID;
     p.color[i] = color[i];
     p.depth[i] = depth[i];
+    p.roi[i] = roi[i];
     vec = vec && aligned16(color[i]) && aligned16(depth[i]);
   }
-  p.roi = d_roi;
+  p.out_roi = out_roi;
+  p.roi_dy = roi_dy;
   p.out_color = out_color;
   p.out_depth = out_depth;
   p.pitch = pitch;
@@ -519,8 +662,18 @@ extern "C" int compositor_depth_roi(int n, const uint32_t *const *color, const u
   p.vec = vec ? 1 : 0;
   const int64_t groups = (int64_t)p.groups_per_row * h;
   if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
-  depth_composite_roi_kernel<<<grid_for(groups, EQC_ROI_GRID(depth_composite_roi_kernel)), 256, 0, (cudaStream_t)stream>>>(p);
+  depth_composite_roi_kernel<<<grid_for(groups, EQC_ROI_GRID(depth_composite_roi_kernel)), 256, 0, stream>>>(p);
   return eqc_launch_status();
+}
+
+extern "C" int compositor_depth_roi(int n, const uint32_t *const *color, const uint32_t *const *depth,
+                                    const int32_t *d_roi, int w, int h, int64_t pitch, uint32_t *out_color,
+                                    uint32_t *out_depth, int64_t out_pitch, void *stream) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !d_roi || ((uintptr_t)d_roi & 15) != 0) return EQC_E_INVALID;
+  const int32_t *roi[EQC_MAX_SOURCES];
+  for (int i = 0; i < n; ++i) roi[i] = d_roi + 4 * i;
+  return eqc_depth_roi_launch(n, color, depth, roi, 0, nullptr, w, h, pitch, out_color, out_depth, out_pitch,
+                              (cudaStream_t)stream);
 }
 
 extern "C" int compositor_blend_ordered_roi(int n, const uint32_t *const *color, const int32_t *order,

@@ -25,6 +25,7 @@ UNIQUE_ID_BYTES = 128
 OP_DEPTH = 0
 FLAG_RLE = 1
 FLAG_NCCL = 2
+FLAG_ROI = 4
 
 
 class EqcError(RuntimeError):

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--sources", type=int, default=8)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--scene", default="scattered", choices=["scattered", "compact"])
     a = ap.parse_args()
     json_fd = os.dup(1)
     os.dup2(2, 1)
@@ -45,7 +46,7 @@ def main():
     W, H, N = a.w, a.h, a.sources
     assert N % n == 0
     nl = N // n
-    c, d = synth.depth_sources(synth.SEED_BASE + 3, N, W, H)  # config index 3 (c4)
+    c, d = synth.depth_sources(synth.SEED_BASE + 3, N, W, H, mode=a.scene)  # config index 3 (c4)
     mine = range(rank * nl, (rank + 1) * nl)
     dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
     dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
@@ -55,6 +56,7 @@ def main():
     s = torch.cuda.current_stream()
     results = {}
     variants = [("direct_send_p2p", eqc.compose_direct_send, 0),
+                ("direct_send_p2p_roi", eqc.compose_direct_send, eqc.FLAG_ROI),
                 ("direct_send_nccl", eqc.compose_direct_send, eqc.FLAG_NCCL),
                 ("direct_send_rle", eqc.compose_direct_send, eqc.FLAG_RLE)]
     if n & (n - 1) == 0:
@@ -82,7 +84,7 @@ def main():
         for r in results.values():
             r["source_mpx_per_s"] = round(N * P / (r["ms"] * 1e-3) / 1e6, 1)
             r["frac_of_nvlink_roof"] = round(t_nvl_us / (r["ms"] * 1e3), 3) if n > 1 else None
-        line = {"config": f"c4: {N} sources {W}x{H}, {n} GPU(s), {nl} source(s) per GPU", "n_gpus": n,
+        line = {"config": f"c4: {N} sources {W}x{H} ({a.scene}), {n} GPU(s), {nl} source(s) per GPU", "n_gpus": n,
                 "nvlink_roof_us": round(t_nvl_us, 1), "nvlink_gbs_per_dir": NVLINK_GBS,
                 "dest_inbound_bytes": int(inbound), "results": results}
         out.write(json.dumps(line) + "\n")

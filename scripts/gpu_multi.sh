@@ -6,7 +6,7 @@ N=$(nvidia-smi -L | wc -l)
 nvidia-smi topo -m > gpurun_out/topo_n${N}.txt 2>&1
 timeout 900 python -m pytest tests/test_gpu_multi.py -q -k nccl > gpurun_out/pytest_multi_n${N}.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_multi_n${N}.log
-for X in raw nccl rle; do
+for X in ${BENCH_X-raw nccl rle}; do
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29511 \
   bench.py --gpus $N --steps 50 --warmup 5 --no-cpu-baseline --exchange $X > gpurun_out/bench_n${N}_${X}.json 2> gpurun_out/bench_n${N}_${X}.log
 echo "bench $X rc=$?" >> gpurun_out/bench_n${N}_${X}.log
@@ -19,3 +19,6 @@ cat gpurun_out/compose_c4_n${N}.json
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29513 \
   scripts/bench_compose.py --w 3840 --h 2160 > gpurun_out/compose_4k_n${N}.json 2> gpurun_out/compose_4k_n${N}.log
 cat gpurun_out/compose_4k_n${N}.json
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29514 \
+  scripts/bench_compose.py --scene compact > gpurun_out/compose_c4c_n${N}.json 2> gpurun_out/compose_c4c_n${N}.log
+cat gpurun_out/compose_c4c_n${N}.json

@@ -25,11 +25,15 @@ def main():
     comm = eqc.Comm.from_torch_distributed()
     dev = torch.device("cuda", local)
     failures = []
-    # (algo, n_local, w, h, dest, flags): flags 0 = NVLink peer-memory direct send,
-    # FLAG_NCCL = NCCL grouped send/recv, FLAG_RLE = RLE streams over NCCL
-    R, X = eqc.FLAG_RLE, eqc.FLAG_NCCL
+    # (algo, n_local, w, h, dest, flags[, scene]): flags 0 = NVLink peer-memory direct
+    # send, FLAG_NCCL = NCCL grouped send/recv, FLAG_RLE = RLE streams over NCCL,
+    # FLAG_ROI = peer-memory direct send restricted to each partial's ROI
+    R, X, O = eqc.FLAG_RLE, eqc.FLAG_NCCL, eqc.FLAG_ROI
     cases = [("ds", 2, 640, 361, 0, 0), ("ds", 1, 300, 41, world - 1, 0), ("ds", 2, 1920, 1080, 1 % world, 0),
-             ("ds", 2, 640, 361, 0, X), ("ds", 1, 300, 41, world - 1, R), ("ds", 2, 1920, 1080, 0, R)]
+             ("ds", 2, 640, 361, 0, X), ("ds", 1, 300, 41, world - 1, R), ("ds", 2, 1920, 1080, 0, R),
+             ("ds", 2, 640, 361, 0, O, "compact"), ("ds", 1, 301, 43, world - 1, O, "compact"),
+             ("ds", 3, 1920, 1080, 1 % world, O, "compact"), ("ds", 2, 640, 361, 0, O, "scattered"),
+             ("ds", 1, 64, 16, 0, O, "empty")]
     if world & (world - 1) == 0:
         cases += [("bs", 2, 640, 361, 0, 0), ("bs", 1, 300, 41, world - 1, R), ("bs", 2, 1920, 1080, 0, R)]
     # config c4 (8 sources of 7680x4320 over the ranks), checked on sampled rows
@@ -37,9 +41,14 @@ def main():
         cases += [("ds", 8 // world, 7680, 4320, 0, 0), ("ds", 8 // world, 7680, 4320, 0, R)]
         if world & (world - 1) == 0:
             cases += [("bs", 8 // world, 7680, 4320, 0, 0)]
-    for algo, nl, w, h, dest, rle in cases:
+    for algo, nl, w, h, dest, rle, *scene in cases:
         N = world * nl
-        c, d = synth.depth_sources(synth.SEED_BASE + 3 + N + w, N, w, h)
+        mode = scene[0] if scene else "scattered"
+        if mode == "empty":  # every source all background: ROIs are empty
+            c = [np.zeros((h, w), np.uint32) for _ in range(N)]
+            d = [np.full((h, w), 0xFFFFFFFF, np.uint32) for _ in range(N)]
+        else:
+            c, d = synth.depth_sources(synth.SEED_BASE + 3 + N + w, N, w, h, mode=mode)
         mine = range(rank * nl, (rank + 1) * nl)
         dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
         dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
