@@ -31,6 +31,9 @@ typedef struct eqc_comm eqc_comm;
 
 #define EQC_UNIQUE_ID_BYTES 128
 #define EQC_OP_DEPTH 0      /* depth-sorted compositing (compositor_depth semantics) */
+#define EQC_OP_BLEND 1      /* ordered back-to-front "over" (compositor_blend_ordered semantics, background 0):
+                               global layer order = rank-block order; depth may be NULL; partials cross
+                               GPUs as unorm16 RGBA (R-C6) and are rounded once to RGBA8 at the end */
 #define EQC_FLAG_RLE 1      /* ship bands as RLE-BP streams (colour swizzled + depth) */
 #define EQC_FLAG_NCCL 2     /* direct send: force NCCL grouped send/recv instead of the NVLink peer-memory path */
 #define EQC_FLAG_ROI 4      /* region of interest: peer-memory direct send reads and composites

@@ -33,6 +33,12 @@ size_t eqc_depth_bbox_scratch_bytes();
 int eqc_depth_composite_bbox(int n, const uint32_t *const *color, const uint32_t *const *depth, int w, int h,
                              int64_t pitch, uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
                              void *scratch, int32_t *out_roi, cudaStream_t s);
+// composite.cu: ordered blending through unorm16 partial planes (EQC_OP_BLEND)
+int eqc_blend_to_partial(int n, const uint32_t *const *color, int w, int h, int64_t pitch, uint32_t *out_rg,
+                         uint32_t *out_ba, int64_t out_pitch, cudaStream_t s);
+int eqc_blend_partials(int n, const uint32_t *const *rg, const uint32_t *const *ba, int w, int h, int64_t pitch,
+                       uint32_t background, uint32_t *out_c, uint32_t *out_rg, uint32_t *out_ba, int64_t out_pitch,
+                       cudaStream_t s);
 
 namespace {
 
@@ -110,6 +116,7 @@ struct Geometry {
   int n_local = 1;    // sources per rank
   int w = 0, h = 0;
   int64_t pitch = 0;  // of the source frames
+  int op = EQC_OP_DEPTH;  // per-pixel operator; EQC_OP_BLEND: the (c, d) planes carry unorm16 partials
   int flags = 0;
   int dest = 0;
   uint32_t *out = nullptr;
@@ -257,10 +264,32 @@ int alloc_common(RankState &r, const Geometry &g, size_t recv_rows, size_t band_
   return EQC_OK;
 }
 
+// The per-pixel operator of the schedules.  EQC_OP_DEPTH: (c, d) planes are
+// colour and depth, compositor_depth semantics.  EQC_OP_BLEND (SURVEY 8(f)
+// f4): the planes are a unorm16 "over" partial (rg, ba; R-C6) -- layers are in
+// draw order by rank blocks, so rank order (and the bit-0 group of a binary
+// swap round) is back-to-front.  Every step runs in the composite.cu kernels.
+int op_local(const Geometry &g, const uint32_t *const *color, const uint32_t *const *depth, uint32_t *out_c,
+             uint32_t *out_d, cudaStream_t s) {
+  if (g.op == EQC_OP_BLEND) return eqc_blend_to_partial(g.n_local, color, g.w, g.h, g.pitch, out_c, out_d, g.w, s);
+  return compositor_depth(g.n_local, color, depth, g.w, g.h, g.pitch, out_c, out_d, g.w, s);
+}
+// n partial (c, d) planes in rank order -> final colour (one rounding)
+int op_final(const Geometry &g, int n, const uint32_t *const *c, const uint32_t *const *d, int rows, uint32_t *out,
+             int64_t opitch, cudaStream_t s) {
+  if (g.op == EQC_OP_BLEND) return eqc_blend_partials(n, c, d, g.w, rows, g.w, 0u, out, nullptr, nullptr, opitch, s);
+  return compositor_depth(n, c, d, g.w, rows, g.w, out, nullptr, opitch, s);
+}
+// 2 partials (back/low first) -> 1 partial (binary-swap rounds)
+int op_merge(const Geometry &g, const uint32_t *const *c, const uint32_t *const *d, int rows, uint32_t *out_c,
+             uint32_t *out_d, cudaStream_t s) {
+  if (g.op == EQC_OP_BLEND) return eqc_blend_partials(2, c, d, g.w, rows, g.w, 0u, nullptr, out_c, out_d, g.w, s);
+  return compositor_depth(2, c, d, g.w, rows, g.w, out_c, out_d, g.w, s);
+}
+
 int local_precomposite(RankState &r, const Geometry &g, cudaStream_t s) {
   r.cur = 0;
-  return compositor_depth(g.n_local, r.color, r.depth, g.w, g.h, g.pitch, r.part_c[0].as<uint32_t>(),
-                          r.part_d[0].as<uint32_t>(), g.w, s);
+  return op_local(g, r.color, r.depth, r.part_c[0].as<uint32_t>(), r.part_d[0].as<uint32_t>(), s);
 }
 
 // Encode `count` (<= 2 per band) colour+depth bands: slot k of `enc`.
@@ -274,7 +303,7 @@ int encode_band(RankState &r, const Geometry &g, int slot, const uint32_t *c, co
                 int64_t cap, cudaStream_t s) {
   const uint32_t *src[2] = {c, d};
   int kinds[2] = {EQC_KIND_RGBA8, EQC_KIND_DEPTH32};
-  int flags[2] = {EQC_FLAG_SWIZZLE, 0};
+  int flags[2] = {g.op == EQC_OP_BLEND ? 0 : EQC_FLAG_SWIZZLE, 0};  // unorm16 planes: plain byte planes
   uint8_t *dst[2] = {r.enc.as<uint8_t>() + (size_t)(2 * slot) * cap,
                      r.enc.as<uint8_t>() + (size_t)(2 * slot + 1) * cap};
   return image_compress_rle_batch(2, src, g.w, rows, g.w, kinds, flags, dst, cap,
@@ -416,7 +445,7 @@ int ds_band_composite(RankState &r, const Geometry &g, int maxband, cudaStream_t
     out = r.fin_c.as<uint32_t>();
     opitch = g.w;
   }
-  return compositor_depth(g.n, c.data(), d.data(), g.w, rows, g.w, out, nullptr, opitch, s);
+  return op_final(g, g.n, c.data(), d.data(), rows, out, opitch, s);
 }
 
 // Phase (5): gather colour bands/regions to the destination.  rows_of(q)
@@ -521,7 +550,8 @@ int run_direct_send(std::vector<RankState *> &ranks, Geometry &g, Transport &T, 
 
 int bs_alloc(RankState &r, const Geometry &g) {
   const int half = (g.h + 1) / 2;
-  EQC_TRY(alloc_common(r, g, std::max(half, g.out_pitch != g.w && r.rank == g.dest ? g.h : 0), 1, 2));
+  EQC_TRY(alloc_common(r, g, std::max(half, g.out_pitch != g.w && r.rank == g.dest ? g.h : 0),
+                       g.op == EQC_OP_BLEND ? half : 1, 2));
   if (g.flags & EQC_FLAG_RLE) {
     const int64_t cap = band_cap(g, half);
     EQC_TRY(r.enc.ensure((size_t)2 * cap));
@@ -619,34 +649,47 @@ int run_binary_swap(std::vector<RankState *> &ranks, Geometry &g, Transport &T, 
       const uint32_t *c[2] = {b.low ? mine_c : their_c, b.low ? their_c : mine_c};
       const uint32_t *d[2] = {b.low ? mine_d : their_d, b.low ? their_d : mine_d};
       const int nxt = r.cur ^ 1;
-      EQC_TRY(compositor_depth(2, c, d, g.w, krows, g.w, r.part_c[nxt].as<uint32_t>() + off,
-                               r.part_d[nxt].as<uint32_t>() + off, g.w, s));
+      EQC_TRY(op_merge(g, c, d, krows, r.part_c[nxt].as<uint32_t>() + off, r.part_d[nxt].as<uint32_t>() + off, s));
       r.cur = nxt;
     }
   }
   // gather final regions (colour) to the destination
   auto region = [&](int q, int &y0, int &y1) { final_region_bs(g.h, g.n, q, y0, y1); };
+  // the final region's colour: the depth partial's colour plane, or the blend
+  // partial rounded once to RGBA8 (over a transparent background) in fin_c
+  auto final_colour = [&](RankState *r, int y0) -> const uint32_t * {
+    return g.op == EQC_OP_BLEND ? r->fin_c.as<uint32_t>() : r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w;
+  };
+  if (g.op == EQC_OP_BLEND) {
+    for (RankState *r : ranks) {
+      int y0, y1;
+      region(r->rank, y0, y1);
+      if (y1 <= y0) continue;
+      const size_t off = (size_t)y0 * g.w;
+      const uint32_t *c[1] = {r->part_c[r->cur].as<uint32_t>() + off}, *d[1] = {r->part_d[r->cur].as<uint32_t>() + off};
+      EQC_TRY(op_final(g, 1, c, d, y1 - y0, r->fin_c.as<uint32_t>(), g.w, s));
+    }
+  }
   for (RankState *r : ranks) {
     if (r->rank != g.dest) continue;
     int y0, y1;
     region(r->rank, y0, y1);
     if (y1 > y0)
-      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)y0 * g.out_pitch, g.out_pitch * 4,
-                                     r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w, (size_t)g.w * 4,
-                                     (size_t)g.w * 4, y1 - y0, cudaMemcpyDeviceToDevice, s));
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)y0 * g.out_pitch, g.out_pitch * 4, final_colour(r, y0),
+                                     (size_t)g.w * 4, (size_t)g.w * 4, y1 - y0, cudaMemcpyDeviceToDevice, s));
   }
   if (g.n > 1) {
     EQC_TRY(T.start());
     for (RankState *r : ranks) {
       int y0, y1;
       region(r->rank, y0, y1);
-      EQC_TRY(gather(*r, g, T, region, r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w, s, 0));
+      EQC_TRY(gather(*r, g, T, region, final_colour(r, y0), s, 0));
     }
     EQC_TRY(T.end());
     for (RankState *r : ranks) {
       int y0, y1;
       region(r->rank, y0, y1);
-      EQC_TRY(gather(*r, g, T, region, r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w, s, 1));
+      EQC_TRY(gather(*r, g, T, region, final_colour(r, y0), s, 1));
     }
   }
   return EQC_OK;
@@ -655,8 +698,8 @@ int run_binary_swap(std::vector<RankState *> &ranks, Geometry &g, Transport &T, 
 int validate(int nranks, int n_local, const void *color, const void *depth, int w, int h, int64_t pitch, int op,
              int flags, int dest, const void *out, int64_t out_pitch, bool is_dest) {
   if (nranks < 1 || n_local < 1 || n_local > EQC_MAX_SOURCES || nranks > EQC_MAX_SOURCES) return EQC_E_INVALID;
-  if (!color || !depth || w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
-  if (op != EQC_OP_DEPTH) return EQC_E_UNSUPPORTED;
+  if (op != EQC_OP_DEPTH && op != EQC_OP_BLEND) return EQC_E_UNSUPPORTED;
+  if (!color || (op == EQC_OP_DEPTH && !depth) || w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
   if (flags & ~(EQC_FLAG_RLE | EQC_FLAG_NCCL | EQC_FLAG_ROI)) return EQC_E_INVALID;
   if (dest < 0 || dest >= nranks) return EQC_E_INVALID;
   if (is_dest && (!out || out_pitch < w)) return EQC_E_INVALID;
@@ -827,7 +870,7 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   for (int i = 0; i < 4; ++i) stats[i] = 0;
   std::vector<int> row0(n + 1);
   plan_bands(g.h, n, row0.data());
-  const bool roi = (g.flags & EQC_FLAG_ROI) != 0;
+  const bool roi = (g.flags & EQC_FLAG_ROI) != 0 && g.op == EQC_OP_DEPTH;  // ROI: depth compositing only
   int32_t *my_roi = P.flags.as<int32_t>() + kRoiSlot;
   // (1) local pre-composite into the IPC-exposed partial frame.  With
   // EQC_FLAG_ROI the same kernel reduces the bounding box of
@@ -839,8 +882,7 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
     EQC_TRY(eqc_depth_composite_bbox(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
                                      P.part_d.as<uint32_t>(), g.w, P.roi_local.p, my_roi, s));
   } else {
-    EQC_TRY(compositor_depth(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
-                             P.part_d.as<uint32_t>(), g.w, s));
+    EQC_TRY(op_local(g, color, depth, P.part_c.as<uint32_t>(), P.part_d.as<uint32_t>(), s));
   }
   EQC_TRY(p2p_barrier(c, s));
   // (2)+(3)+(4) band composite pulling every peer's band over NVLink, output
@@ -864,7 +906,7 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
       EQC_TRY(eqc_depth_roi_launch(n, cs.data(), ds.data(), rp.data(), y0, nullptr, g.w, rows, g.w, out, nullptr,
                                    opitch, s));
     } else {
-      EQC_TRY(compositor_depth(n, cs.data(), ds.data(), g.w, rows, g.w, out, nullptr, opitch, s));
+      EQC_TRY(op_final(g, n, cs.data(), ds.data(), rows, out, opitch, s));
     }
     if (me != g.dest) {
       stats[1] += 1;
@@ -967,6 +1009,7 @@ static int compose_nccl(bool ds, eqc_comm *comm, int n_local, const uint32_t *co
   g.w = w;
   g.h = h;
   g.pitch = pitch;
+  g.op = op;
   g.flags = flags;
   g.dest = dest_rank;
   g.out = out_color;
@@ -1008,6 +1051,7 @@ static int compose_local(bool ds, int nranks, int n_local, const uint32_t *const
   g.w = w;
   g.h = h;
   g.pitch = pitch;
+  g.op = op;
   g.flags = flags;
   g.dest = dest_rank;
   g.out = out_color;
@@ -1018,7 +1062,7 @@ static int compose_local(bool ds, int nranks, int n_local, const uint32_t *const
   for (int q = 0; q < nranks; ++q) {
     states[q].rank = q;
     states[q].color = color + (size_t)q * n_local;
-    states[q].depth = depth + (size_t)q * n_local;
+    states[q].depth = depth ? depth + (size_t)q * n_local : nullptr;
     ranks.push_back(&states[q]);
   }
   LocalTransport T(s);

@@ -508,6 +508,111 @@ __global__ void __launch_bounds__(256, EQC_ROI_MINB) blend_ordered_roi_kernel(co
   }
 }
 
+// ---- blend partials for multi-GPU ordered compositing -----
+// A rank's partial image is its layers "over"-composited onto a transparent
+// background (premultiplied "over" is associative), carried in
+// unorm16 per channel (R-C6: an 8-bit intermediate would add up to 1/2 LSB per
+// partial) as two uint32 planes: rg = R16 | G16 << 16, ba = B16 | A16 << 16
+// (value16 = round(255-scale value * 257)).  The two planes travel through
+// the same band/RLE transport as colour and depth.
+
+__device__ __forceinline__ uint32_t u16_round(float v) {  // v in [0, 65535] (clamped)
+  return min(__float2uint_rn(fmaxf(v, 0.0f)), 65535u);
+}
+
+struct Part16 {
+  float r, g, b, a;  // 0..65535
+};
+
+__device__ __forceinline__ Part16 unpack16(uint32_t rg, uint32_t ba) {
+  return Part16{(float)(rg & 0xFFFFu), (float)(rg >> 16), (float)(ba & 0xFFFFu), (float)(ba >> 16)};
+}
+
+// x = s + x * (1 - a_s / 65535), all in unorm16 units
+__device__ __forceinline__ void over16(Part16 &x, const Part16 &s) {
+  const float f = fmaf(s.a, -1.0f / 65535.0f, 1.0f);
+  x.r = fmaf(x.r, f, s.r);
+  x.g = fmaf(x.g, f, s.g);
+  x.b = fmaf(x.b, f, s.b);
+  x.a = fmaf(x.a, f, s.a);
+}
+
+struct BlendPartialParams {
+  const uint32_t *color[EQC_MAX_SOURCES];  // RGBA8 layers in draw order (back first)
+  uint32_t *out_rg, *out_ba;
+  int64_t pitch, out_pitch;
+  int n, w, h, groups_per_row;
+};
+
+// n RGBA8 layers -> one unorm16 partial (transparent background)
+__global__ void __launch_bounds__(256) blend_partial_kernel(const __grid_constant__ BlendPartialParams p) {
+  const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int y = (int)(g / (uint32_t)p.groups_per_row);
+    const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
+    const int64_t off = (int64_t)y * p.pitch + x;
+    const int cnt = min(4, p.w - x);
+    Acc4 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = Acc4{0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k = 0; k < p.n; ++k) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < cnt) over(acc[j], ld_stream_u32(p.color[k] + off + j));
+    }
+    const int64_t ooff = (int64_t)y * p.out_pitch + x;
+    for (int j = 0; j < cnt; ++j) {
+      p.out_rg[ooff + j] = u16_round(acc[j].r * 257.0f) | (u16_round(acc[j].g * 257.0f) << 16);
+      p.out_ba[ooff + j] = u16_round(acc[j].b * 257.0f) | (u16_round(acc[j].a * 257.0f) << 16);
+    }
+  }
+}
+
+struct BlendPartialsParams {
+  const uint32_t *rg[EQC_MAX_SOURCES], *ba[EQC_MAX_SOURCES];  // partials, back first
+  uint32_t *out_c;           // FINAL: RGBA8 output
+  uint32_t *out_rg, *out_ba; // !FINAL: unorm16 partial output
+  int64_t pitch, out_pitch;
+  int n, w, h, groups_per_row;
+  float bg[4];               // FINAL: background in unorm16 units
+};
+
+// n unorm16 partials, back to front -> RGBA8 over `bg` (FINAL, one rounding
+// to 8 bits) or -> a unorm16 partial over transparent (binary-swap rounds)
+template <bool FINAL>
+__global__ void __launch_bounds__(256) blend_partials_kernel(const __grid_constant__ BlendPartialsParams p) {
+  const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int y = (int)(g / (uint32_t)p.groups_per_row);
+    const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
+    const int64_t off = (int64_t)y * p.pitch + x;
+    const int cnt = min(4, p.w - x);
+    Part16 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      acc[q] = FINAL ? Part16{p.bg[0], p.bg[1], p.bg[2], p.bg[3]} : Part16{0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k = 0; k < p.n; ++k) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < cnt) over16(acc[j], unpack16(ld_stream_u32(p.rg[k] + off + j), ld_stream_u32(p.ba[k] + off + j)));
+    }
+    const int64_t ooff = (int64_t)y * p.out_pitch + x;
+    for (int j = 0; j < cnt; ++j) {
+      if (FINAL) {
+        const float s = 1.0f / 257.0f;
+        const uint32_t r = min(__float2uint_rn(fmaxf(acc[j].r * s, 0.0f)), 255u);
+        const uint32_t gg = min(__float2uint_rn(fmaxf(acc[j].g * s, 0.0f)), 255u);
+        const uint32_t b = min(__float2uint_rn(fmaxf(acc[j].b * s, 0.0f)), 255u);
+        const uint32_t a = min(__float2uint_rn(fmaxf(acc[j].a * s, 0.0f)), 255u);
+        p.out_c[ooff + j] = r | (gg << 8) | (b << 16) | (a << 24);
+      } else {
+        p.out_rg[ooff + j] = u16_round(acc[j].r) | (u16_round(acc[j].g) << 16);
+        p.out_ba[ooff + j] = u16_round(acc[j].b) | (u16_round(acc[j].a) << 16);
+      }
+    }
+  }
+}
+
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 // Grid of a grid-stride kernel over `items` 4-pixel groups: one group per
@@ -591,6 +696,62 @@ int eqc_depth_composite_bbox(int n, const uint32_t *const *color, const uint32_t
   else
     depth_composite_kernel<false, true><<<grid, 256, 0, s>>>(p);
   bbox_finalize_kernel<<<1, 256, 0, s>>>(p.cta_box, grid, out_roi);
+  return eqc_launch_status();
+}
+
+// Internal (compose.cu, EQC_OP_BLEND): n RGBA8 layers -> unorm16 partial planes.
+int eqc_blend_to_partial(int n, const uint32_t *const *color, int w, int h, int64_t pitch, uint32_t *out_rg,
+                         uint32_t *out_ba, int64_t out_pitch, cudaStream_t s) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !color || !out_rg || !out_ba) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
+  BlendPartialParams p;
+  for (int k = 0; k < n; ++k) {
+    if (!color[k]) return EQC_E_INVALID;
+    p.color[k] = color[k];
+  }
+  p.out_rg = out_rg;
+  p.out_ba = out_ba;
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
+  blend_partial_kernel<<<grid_for(groups), 256, 0, s>>>(p);
+  return eqc_launch_status();
+}
+
+// Internal: n unorm16 partials (back first) -> RGBA8 over `background`
+// (out_c != NULL) or -> one unorm16 partial (out_rg/out_ba).
+int eqc_blend_partials(int n, const uint32_t *const *rg, const uint32_t *const *ba, int w, int h, int64_t pitch,
+                       uint32_t background, uint32_t *out_c, uint32_t *out_rg, uint32_t *out_ba, int64_t out_pitch,
+                       cudaStream_t s) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !rg || !ba || (!out_c && (!out_rg || !out_ba))) return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
+  BlendPartialsParams p;
+  for (int k = 0; k < n; ++k) {
+    if (!rg[k] || !ba[k]) return EQC_E_INVALID;
+    p.rg[k] = rg[k];
+    p.ba[k] = ba[k];
+  }
+  p.out_c = out_c;
+  p.out_rg = out_rg;
+  p.out_ba = out_ba;
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  for (int c = 0; c < 4; ++c) p.bg[c] = (float)((background >> (8 * c)) & 0xFFu) * 257.0f;
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
+  if (out_c)
+    blend_partials_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
+  else
+    blend_partials_kernel<false><<<grid_for(groups), 256, 0, s>>>(p);
   return eqc_launch_status();
 }
 

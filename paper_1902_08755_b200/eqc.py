@@ -23,6 +23,7 @@ KIND_RGBA8, KIND_DEPTH32 = 0, 1
 FLAG_SWIZZLE = 1
 UNIQUE_ID_BYTES = 128
 OP_DEPTH = 0
+OP_BLEND = 1
 FLAG_RLE = 1
 FLAG_NCCL = 2
 FLAG_ROI = 4
@@ -304,7 +305,8 @@ def _compose(fn, name, comm, colors, depths, out_color, dest_rank, flags, op, st
     n = len(colors)
     w, h, pitch = _frame_geom(colors[0])
     opitch = _frame_geom(out_color)[2] if out_color is not None else w
-    rc = fn(comm.handle, n, _ptrs(colors), _ptrs(depths), w, h, pitch, op, flags, dest_rank, _addr(out_color),
+    rc = fn(comm.handle, n, _ptrs(colors), _ptrs(depths) if depths is not None else None, w, h, pitch, op, flags,
+            dest_rank, _addr(out_color),
             opitch, _stream(stream))
     return _check(rc, name)
 
@@ -327,7 +329,8 @@ def _compose_local(fn, name, nranks, colors, depths, out_color, dest_rank, flags
     w, h, pitch = _frame_geom(colors[0])
     opitch = _frame_geom(out_color)[2]
     stats = (ctypes.c_int64 * 4)()
-    rc = fn(nranks, total // nranks, _ptrs(colors), _ptrs(depths), w, h, pitch, op, flags, dest_rank,
+    rc = fn(nranks, total // nranks, _ptrs(colors), _ptrs(depths) if depths is not None else None, w, h, pitch, op,
+            flags, dest_rank,
             _addr(out_color), opitch, stats, _stream(stream))
     _check(rc, name)
     return list(stats)

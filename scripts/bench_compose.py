@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--sources", type=int, default=8)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--scene", default="scattered", choices=["scattered", "compact"])
+    ap.add_argument("--scene", default="scattered", choices=["scattered", "compact", "bricks"])
     a = ap.parse_args()
     json_fd = os.dup(1)
     os.dup2(2, 1)
@@ -46,10 +46,14 @@ def main():
     W, H, N = a.w, a.h, a.sources
     assert N % n == 0
     nl = N // n
-    c, d = synth.depth_sources(synth.SEED_BASE + 3, N, W, H, mode=a.scene)  # config index 3 (c4)
+    blend = a.scene == "bricks"  # config c3: ordered blend of volume bricks (EQC_OP_BLEND)
+    if blend:
+        c, d = synth.volume_bricks(synth.SEED_BASE + 2, N, W, H), None
+    else:
+        c, d = synth.depth_sources(synth.SEED_BASE + 3, N, W, H, mode=a.scene)  # config index 3 (c4)
     mine = range(rank * nl, (rank + 1) * nl)
     dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
-    dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
+    dd = None if blend else [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
     del c, d  # parity of these schedules at this size: tests/mp_compose.py (c4 case)
     final = torch.empty((H, W), dtype=torch.int32, device=dev) if rank == 0 else None
     P = W * H
@@ -62,15 +66,18 @@ def main():
     if n & (n - 1) == 0:
         variants += [("binary_swap_nccl", eqc.compose_binary_swap, 0),
                      ("binary_swap_rle", eqc.compose_binary_swap, eqc.FLAG_RLE)]
+    op = eqc.OP_BLEND if blend else eqc.OP_DEPTH
+    if blend:
+        variants = [v for v in variants if "roi" not in v[0]]
     for name, fn, flags in variants:
         for _ in range(a.warmup):
-            fn(comm, dc, dd, final, dest_rank=0, flags=flags, stream=s)
+            fn(comm, dc, dd, final, dest_rank=0, flags=flags, op=op, stream=s)
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         for _ in range(a.steps):
-            fn(comm, dc, dd, final, dest_rank=0, flags=flags, stream=s)
+            fn(comm, dc, dd, final, dest_rank=0, flags=flags, op=op, stream=s)
         e1.record(s)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.steps
@@ -79,12 +86,13 @@ def main():
         st = comm.stats()
         results[name] = {"ms": round(float(t.item()), 4), "stats_rank0": st if rank == 0 else None}
     if rank == 0:
-        inbound = (n - 1) / n * 12 * P
+        inbound = (n - 1) / n * 12 * P  # blend: 8 B unorm16 partial + 4 B colour gather, the same
         t_nvl_us = inbound / (NVLINK_GBS * 1e9) * 1e6
         for r in results.values():
             r["source_mpx_per_s"] = round(N * P / (r["ms"] * 1e-3) / 1e6, 1)
             r["frac_of_nvlink_roof"] = round(t_nvl_us / (r["ms"] * 1e3), 3) if n > 1 else None
-        line = {"config": f"c4: {N} sources {W}x{H} ({a.scene}), {n} GPU(s), {nl} source(s) per GPU", "n_gpus": n,
+        tag = "c3 blend" if blend else "c4"
+        line = {"config": f"{tag}: {N} sources {W}x{H} ({a.scene}), {n} GPU(s), {nl} source(s) per GPU", "n_gpus": n,
                 "nvlink_roof_us": round(t_nvl_us, 1), "nvlink_gbs_per_dir": NVLINK_GBS,
                 "dest_inbound_bytes": int(inbound), "results": results}
         out.write(json.dumps(line) + "\n")

@@ -22,3 +22,6 @@ cat gpurun_out/compose_4k_n${N}.json
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29514 \
   scripts/bench_compose.py --scene compact > gpurun_out/compose_c4c_n${N}.json 2> gpurun_out/compose_c4c_n${N}.log
 cat gpurun_out/compose_c4c_n${N}.json
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29515 \
+  scripts/bench_compose.py --scene bricks --w 3840 --h 2160 --sources 16 > gpurun_out/compose_c3_n${N}.json 2> gpurun_out/compose_c3_n${N}.log
+cat gpurun_out/compose_c3_n${N}.json

@@ -73,6 +73,31 @@ def main():
         if algo == "ds" and st[0] != world - 1:
             failures.append(f"{algo}: rank {rank} sent {st[0]} band messages, want {world - 1}")
         dist.barrier()
+    # EQC_OP_BLEND: layers in rank-block draw order, result
+    # within 1/255 of O2 over all layers (unorm16 partials across GPUs, R-C6)
+    bcases = [("ds", 4, 640, 361, 0, 0), ("ds", 2, 300, 41, world - 1, X), ("ds", 3, 320, 181, 1 % world, R)]
+    if world & (world - 1) == 0:
+        bcases += [("bs", 4, 640, 361, 0, 0), ("bs", 2, 300, 41, world - 1, R)]
+    if 16 % world == 0:  # config c3: 16 bricks of 3840x2160, sampled rows
+        bcases += [("ds", 16 // world, 3840, 2160, 0, 0)]
+    for algo, nl, w, h, dest, fl in bcases:
+        N = world * nl
+        layers = synth.volume_bricks(synth.SEED_BASE + 2 if h == 2160 else synth.SEED_BASE + 80 + N, N, w, h)
+        mine = range(rank * nl, (rank + 1) * nl)
+        dl = [torch.from_numpy(layers[i].view(np.int32)).to(dev) for i in mine]
+        out = torch.zeros((h, w), dtype=torch.int32, device=dev)
+        fn = eqc.compose_direct_send if algo == "ds" else eqc.compose_binary_swap
+        for _ in range(2):
+            fn(comm, dl, None, out if rank == dest else None, dest_rank=dest, flags=fl, op=eqc.OP_BLEND)
+        torch.cuda.synchronize()
+        if rank == dest:
+            got = out.cpu().numpy().view(np.uint32)
+            rows = np.random.default_rng(h).choice(h, 8, replace=False) if h > 2000 else np.arange(h)
+            want = oracle.blend_ordered([x[rows] for x in layers])
+            diff = np.abs(got[rows].view(np.uint8).astype(int) - want.view(np.uint8).astype(int)).max()
+            if diff > 1:
+                failures.append(f"blend {algo} nl={nl} {w}x{h} flags={fl}: max error {diff} LSB")
+        dist.barrier()
     comm.destroy()
     t = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(t)

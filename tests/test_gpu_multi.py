@@ -76,6 +76,41 @@ def test_virtual_rank_schedule_equals_oracle(eqc, case):
     assert stats[2] == stats[3]  # every byte sent is received
 
 
+BLEND_CASES = [
+    # (algo, nranks, n_local, w, h, pitch, out_pitch, dest, rle, gen) -- EQC_OP_BLEND
+    ("ds", 1, 4, 64, 33, None, None, 0, 0, "bricks"),
+    ("ds", 2, 8, 320, 180, None, None, 0, 0, "bricks"),
+    ("ds", 4, 4, 257, 77, None, 264, 3, 0, "bricks"),
+    ("ds", 3, 2, 130, 31, 136, None, 1, 0, "noise"),
+    ("ds", 4, 2, 257, 77, None, None, 2, 1, "bricks"),
+    ("ds", 2, 3, 129, 20, 132, None, 1, 1, "noise"),
+    ("bs", 2, 8, 320, 180, None, None, 1, 0, "bricks"),
+    ("bs", 4, 2, 130, 37, 136, 140, 2, 0, "noise"),
+    ("bs", 8, 2, 128, 19, None, None, 7, 0, "bricks"),
+    ("bs", 4, 4, 257, 77, None, None, 0, 1, "bricks"),
+]
+
+
+@pytest.mark.parametrize("case", BLEND_CASES,
+                         ids=[f"{c[0]}_n{c[1]}x{c[2]}_{c[3]}x{c[4]}_rle{c[8]}" for c in BLEND_CASES])
+def test_virtual_rank_blend_within_one_lsb(eqc, case):
+    # global draw order = rank-block order (rank 0 holds the back-most layers);
+    # the result must match O2 over ALL layers within 1/255 (R-C4, R-C6)
+    algo, nr, nl, w, h, pitch, opitch, dest, rle, gen = case
+    N = nr * nl
+    layers = synth.volume_bricks(synth.SEED_BASE + 70 + N, N, w, h) if gen == "bricks" else \
+        synth.premultiplied_noise(synth.SEED_BASE + 71 + N, N, w, h)
+    want = oracle.blend_ordered(layers)
+    dl = [to_dev(x, pitch) for x in layers]
+    out = out_frame(h, w, opitch)
+    fn = eqc.compose_direct_send_local if algo == "ds" else eqc.compose_binary_swap_local
+    fn(nr, dl, None, out, dest_rank=dest, flags=eqc.FLAG_RLE if rle else 0, op=eqc.OP_BLEND)
+    torch.cuda.synchronize()
+    got = to_host(out)
+    diff = np.abs(got.view(np.uint8).astype(int) - want.view(np.uint8).astype(int))
+    assert diff.max() <= 1, f"max channel error {diff.max()} LSB"
+
+
 def test_binary_swap_rejects_non_power_of_two(eqc):
     c, d = synth.random_frames(1, 3, 8, 8)
     with pytest.raises(eqc.EqcError) as e:
