@@ -544,8 +544,10 @@ struct BlendPartialParams {
   int n, w, h, groups_per_row;
 };
 
-// n RGBA8 layers -> one unorm16 partial (transparent background)
-__global__ void __launch_bounds__(256) blend_partial_kernel(const __grid_constant__ BlendPartialParams p) {
+// n RGBA8 layers -> one unorm16 partial (transparent background).  VEC: one
+// 128-bit load per layer per thread, batches of 4 layers in flight.
+template <bool VEC>
+__global__ void __launch_bounds__(256, 4) blend_partial_kernel(const __grid_constant__ BlendPartialParams p) {
   const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
     const int y = (int)(g / (uint32_t)p.groups_per_row);
@@ -555,15 +557,49 @@ __global__ void __launch_bounds__(256) blend_partial_kernel(const __grid_constan
     Acc4 acc[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = Acc4{0.0f, 0.0f, 0.0f, 0.0f};
-    for (int k = 0; k < p.n; ++k) {
+    if (VEC && cnt == 4) {
+      int k = 0;
+      for (; k + 4 <= p.n; k += 4) {
+        uint4 v[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < cnt) over(acc[j], ld_stream_u32(p.color[k] + off + j));
+        for (int b = 0; b < 4; ++b) v[b] = ld_stream_u4(p.color[k + b] + off);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          over(acc[0], v[b].x);
+          over(acc[1], v[b].y);
+          over(acc[2], v[b].z);
+          over(acc[3], v[b].w);
+        }
+      }
+      for (; k < p.n; ++k) {
+        const uint4 v = ld_stream_u4(p.color[k] + off);
+        over(acc[0], v.x);
+        over(acc[1], v.y);
+        over(acc[2], v.z);
+        over(acc[3], v.w);
+      }
+    } else {
+      for (int k = 0; k < p.n; ++k) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < cnt) over(acc[j], ld_stream_u32(p.color[k] + off + j));
+      }
     }
     const int64_t ooff = (int64_t)y * p.out_pitch + x;
-    for (int j = 0; j < cnt; ++j) {
-      p.out_rg[ooff + j] = u16_round(acc[j].r * 257.0f) | (u16_round(acc[j].g * 257.0f) << 16);
-      p.out_ba[ooff + j] = u16_round(acc[j].b * 257.0f) | (u16_round(acc[j].a * 257.0f) << 16);
+    uint32_t rg[4], ba[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      rg[j] = u16_round(acc[j].r * 257.0f) | (u16_round(acc[j].g * 257.0f) << 16);
+      ba[j] = u16_round(acc[j].b * 257.0f) | (u16_round(acc[j].a * 257.0f) << 16);
+    }
+    if (VEC && cnt == 4) {
+      st_stream_u4(p.out_rg + ooff, make_uint4(rg[0], rg[1], rg[2], rg[3]));
+      st_stream_u4(p.out_ba + ooff, make_uint4(ba[0], ba[1], ba[2], ba[3]));
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        p.out_rg[ooff + j] = rg[j];
+        p.out_ba[ooff + j] = ba[j];
+      }
     }
   }
 }
@@ -578,9 +614,10 @@ struct BlendPartialsParams {
 };
 
 // n unorm16 partials, back to front -> RGBA8 over `bg` (FINAL, one rounding
-// to 8 bits) or -> a unorm16 partial over transparent (binary-swap rounds)
-template <bool FINAL>
-__global__ void __launch_bounds__(256) blend_partials_kernel(const __grid_constant__ BlendPartialsParams p) {
+// to 8 bits) or -> a unorm16 partial over transparent (binary-swap rounds).
+// VEC: two 128-bit loads (rg, ba) per partial, batches of 2 partials.
+template <bool FINAL, bool VEC>
+__global__ void __launch_bounds__(256, 4) blend_partials_kernel(const __grid_constant__ BlendPartialsParams p) {
   const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
     const int y = (int)(g / (uint32_t)p.groups_per_row);
@@ -591,23 +628,60 @@ __global__ void __launch_bounds__(256) blend_partials_kernel(const __grid_consta
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       acc[q] = FINAL ? Part16{p.bg[0], p.bg[1], p.bg[2], p.bg[3]} : Part16{0.0f, 0.0f, 0.0f, 0.0f};
-    for (int k = 0; k < p.n; ++k) {
+    if (VEC && cnt == 4) {
+      int k = 0;
+      for (; k + 2 <= p.n; k += 2) {
+        uint4 a[2], b[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < cnt) over16(acc[j], unpack16(ld_stream_u32(p.rg[k] + off + j), ld_stream_u32(p.ba[k] + off + j)));
+        for (int u = 0; u < 2; ++u) {
+          a[u] = ld_stream_u4(p.rg[k + u] + off);
+          b[u] = ld_stream_u4(p.ba[k + u] + off);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          over16(acc[0], unpack16(a[u].x, b[u].x));
+          over16(acc[1], unpack16(a[u].y, b[u].y));
+          over16(acc[2], unpack16(a[u].z, b[u].z));
+          over16(acc[3], unpack16(a[u].w, b[u].w));
+        }
+      }
+      for (; k < p.n; ++k) {
+        const uint4 a = ld_stream_u4(p.rg[k] + off), b = ld_stream_u4(p.ba[k] + off);
+        over16(acc[0], unpack16(a.x, b.x));
+        over16(acc[1], unpack16(a.y, b.y));
+        over16(acc[2], unpack16(a.z, b.z));
+        over16(acc[3], unpack16(a.w, b.w));
+      }
+    } else {
+      for (int k = 0; k < p.n; ++k) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < cnt) over16(acc[j], unpack16(ld_stream_u32(p.rg[k] + off + j), ld_stream_u32(p.ba[k] + off + j)));
+      }
     }
     const int64_t ooff = (int64_t)y * p.out_pitch + x;
-    for (int j = 0; j < cnt; ++j) {
+    uint32_t o0[4], o1[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
       if (FINAL) {
         const float s = 1.0f / 257.0f;
         const uint32_t r = min(__float2uint_rn(fmaxf(acc[j].r * s, 0.0f)), 255u);
         const uint32_t gg = min(__float2uint_rn(fmaxf(acc[j].g * s, 0.0f)), 255u);
         const uint32_t b = min(__float2uint_rn(fmaxf(acc[j].b * s, 0.0f)), 255u);
         const uint32_t a = min(__float2uint_rn(fmaxf(acc[j].a * s, 0.0f)), 255u);
-        p.out_c[ooff + j] = r | (gg << 8) | (b << 16) | (a << 24);
+        o0[j] = r | (gg << 8) | (b << 16) | (a << 24);
       } else {
-        p.out_rg[ooff + j] = u16_round(acc[j].r) | (u16_round(acc[j].g) << 16);
-        p.out_ba[ooff + j] = u16_round(acc[j].b) | (u16_round(acc[j].a) << 16);
+        o0[j] = u16_round(acc[j].r) | (u16_round(acc[j].g) << 16);
+        o1[j] = u16_round(acc[j].b) | (u16_round(acc[j].a) << 16);
+      }
+    }
+    if (VEC && cnt == 4) {
+      st_stream_u4((FINAL ? p.out_c : p.out_rg) + ooff, make_uint4(o0[0], o0[1], o0[2], o0[3]));
+      if (!FINAL) st_stream_u4(p.out_ba + ooff, make_uint4(o1[0], o1[1], o1[2], o1[3]));
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        (FINAL ? p.out_c : p.out_rg)[ooff + j] = o0[j];
+        if (!FINAL) p.out_ba[ooff + j] = o1[j];
       }
     }
   }
@@ -705,9 +779,11 @@ int eqc_blend_to_partial(int n, const uint32_t *const *color, int w, int h, int6
   if (n < 1 || n > EQC_MAX_SOURCES || !color || !out_rg || !out_ba) return EQC_E_INVALID;
   if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
   BlendPartialParams p;
+  bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) && aligned16(out_rg) && aligned16(out_ba);
   for (int k = 0; k < n; ++k) {
     if (!color[k]) return EQC_E_INVALID;
     p.color[k] = color[k];
+    vec = vec && aligned16(color[k]);
   }
   p.out_rg = out_rg;
   p.out_ba = out_ba;
@@ -719,7 +795,10 @@ int eqc_blend_to_partial(int n, const uint32_t *const *color, int w, int h, int6
   p.groups_per_row = (w + 3) / 4;
   const int64_t groups = (int64_t)p.groups_per_row * h;
   if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
-  blend_partial_kernel<<<grid_for(groups), 256, 0, s>>>(p);
+  if (vec)
+    blend_partial_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
+  else
+    blend_partial_kernel<false><<<grid_for(groups), 256, 0, s>>>(p);
   return eqc_launch_status();
 }
 
@@ -731,10 +810,13 @@ int eqc_blend_partials(int n, const uint32_t *const *rg, const uint32_t *const *
   if (n < 1 || n > EQC_MAX_SOURCES || !rg || !ba || (!out_c && (!out_rg || !out_ba))) return EQC_E_INVALID;
   if (w <= 0 || h <= 0 || pitch < w || out_pitch < w) return EQC_E_INVALID;
   BlendPartialsParams p;
+  bool vec = (pitch % 4 == 0) && (out_pitch % 4 == 0) &&
+             (out_c ? aligned16(out_c) : (aligned16(out_rg) && aligned16(out_ba)));
   for (int k = 0; k < n; ++k) {
     if (!rg[k] || !ba[k]) return EQC_E_INVALID;
     p.rg[k] = rg[k];
     p.ba[k] = ba[k];
+    vec = vec && aligned16(rg[k]) && aligned16(ba[k]);
   }
   p.out_c = out_c;
   p.out_rg = out_rg;
@@ -748,10 +830,17 @@ int eqc_blend_partials(int n, const uint32_t *const *rg, const uint32_t *const *
   for (int c = 0; c < 4; ++c) p.bg[c] = (float)((background >> (8 * c)) & 0xFFu) * 257.0f;
   const int64_t groups = (int64_t)p.groups_per_row * h;
   if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
-  if (out_c)
-    blend_partials_kernel<true><<<grid_for(groups), 256, 0, s>>>(p);
-  else
-    blend_partials_kernel<false><<<grid_for(groups), 256, 0, s>>>(p);
+  if (out_c) {
+    if (vec)
+      blend_partials_kernel<true, true><<<grid_for(groups), 256, 0, s>>>(p);
+    else
+      blend_partials_kernel<true, false><<<grid_for(groups), 256, 0, s>>>(p);
+  } else {
+    if (vec)
+      blend_partials_kernel<false, true><<<grid_for(groups), 256, 0, s>>>(p);
+    else
+      blend_partials_kernel<false, false><<<grid_for(groups), 256, 0, s>>>(p);
+  }
   return eqc_launch_status();
 }
 
