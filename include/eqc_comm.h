@@ -134,6 +134,32 @@ EQC_API int compose_binary_swap_local(int nranks, int n_local, const uint32_t *c
                                       int flags, int dest_rank, uint32_t *out_color, int64_t out_pitch,
                                       int64_t *out_stats, void *stream);
 
+/*
+ * compose_swap23 -- the same contract with the 2-3 swap schedule (P:2193-2195:
+ * binary swap extended to any number of ranks "by exchanging compositions
+ * between groups of two or three nodes"), reading R-C21: with m the largest
+ * 2^a 3^b <= nranks, ranks (2i, 2i+1), i < nranks - m, first fold (2i+1's
+ * whole partial to 2i); the m remaining ranks then run mixed-radix swap
+ * rounds, radix 2 rounds first then radix 3: a group = the ranks whose active
+ * index differs only in the round's digit; the current row region splits into
+ * k parts at y0 + floor(u (y1 - y0) / k); digit t keeps part t, receives it
+ * from the k - 1 other members and composites the k partials in rank order.
+ * For a power of two this is binary swap.  Final regions are gathered on
+ * dest_rank.  All ops and flags of compose_direct_send except the
+ * peer-memory path (NCCL transport).
+ * eqc_plan_swap23 -- the plan of `rank` as ints: {fold_role (0 none, 1
+ *   receiver, 2 sender), fold_partner, k rounds, final_y0, final_y1}, then per
+ *   round {radix, digit, member[3] (-1 padded), bound[4]}; returns k.
+ */
+EQC_API int compose_swap23(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                           const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                           int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream);
+EQC_API int compose_swap23_local(int nranks, int n_local, const uint32_t *const *color,
+                                 const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                 int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                 void *stream);
+EQC_API int eqc_plan_swap23(int h, int n, int rank, int *out, int max_ints);
+
 #ifdef __cplusplus
 }
 #endif

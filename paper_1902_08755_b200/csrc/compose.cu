@@ -695,6 +695,285 @@ int run_binary_swap(std::vector<RankState *> &ranks, Geometry &g, Transport &T, 
   return EQC_OK;
 }
 
+// ---- 2-3 swap ------------------------------------
+// "an extension to binary swap, which overcomes the power-of-two source
+// channel requirement by exchanging compositions between groups of two or
+// three nodes in the compositing tree".  Reading R-C21: with m = the largest
+// 2^a 3^b <= n and r = n - m, a fold step first pairs ranks (2i, 2i+1), i < r
+// (group of two: 2i+1 sends its whole partial, 2i composites, lower ranks
+// first); the m active ranks (in rank order: 0, 2, .., 2r-2, 2r, .., n-1)
+// then run a mixed-radix swap with group sizes 2 (first) then 3: in a round of
+// radix k, the active ranks whose active index differs only in that digit form
+// a group, the current row region [y0, y1) splits into k parts at
+// y0 + floor(u (y1 - y0) / k), the member with digit t keeps part t and
+// receives it from the other members, and the k partials are composited in
+// member (= rank = source) order.  For n = 2^a this is exactly binary swap.
+struct S23Round {
+  int k = 0, t = 0;
+  int members[3] = {-1, -1, -1};
+  int bnd[4] = {0, 0, 0, 0};  // part u = rows [bnd[u], bnd[u + 1])
+};
+struct S23Plan {
+  int fold_role = 0;      // 0 none, 1 receives the partner's frame, 2 sends its frame (then idle)
+  int fold_partner = -1;
+  std::vector<S23Round> rounds;
+  int fy0 = 0, fy1 = 0;   // final region (empty for a folded sender)
+};
+
+int plan_swap23(int h, int n, int rank, S23Plan &P) {
+  if (n < 1 || rank < 0 || rank >= n || h < 1) return EQC_E_INVALID;
+  P = S23Plan();
+  int m = 1;
+  for (int p2 = 1; p2 <= n; p2 *= 2)
+    for (int v = p2; v <= n; v *= 3) m = std::max(m, v);
+  std::vector<int> radix;
+  for (int v = m; v % 2 == 0; v /= 2) radix.push_back(2);
+  for (int v = m; v % 3 == 0; v /= 3) radix.push_back(3);
+  const int r = n - m;
+  std::vector<int> act;
+  for (int i = 0; i < r; ++i) act.push_back(2 * i);
+  for (int q = 2 * r; q < n; ++q) act.push_back(q);
+  int a = -1;
+  if (rank < 2 * r) {
+    P.fold_role = (rank % 2 == 0) ? 1 : 2;
+    P.fold_partner = rank ^ 1;
+    if (P.fold_role == 2) return 0;  // contributes through its partner only
+    a = rank / 2;
+  } else {
+    a = rank - r;
+  }
+  int y0 = 0, y1 = h, stride = 1;
+  for (int k : radix) {
+    S23Round rd;
+    rd.k = k;
+    rd.t = (a / stride) % k;
+    const int base = a - rd.t * stride;
+    for (int u = 0; u < k; ++u) rd.members[u] = act[base + u * stride];
+    for (int u = 0; u <= k; ++u) rd.bnd[u] = y0 + (int)((int64_t)u * (y1 - y0) / k);
+    P.rounds.push_back(rd);
+    y0 = rd.bnd[rd.t];
+    y1 = rd.bnd[rd.t + 1];
+    stride *= k;
+  }
+  P.fy0 = y0;
+  P.fy1 = y1;
+  return (int)P.rounds.size();
+}
+
+int s23_alloc(RankState &r, const Geometry &g) {
+  // part ping-pong buffers (full frame), two receive slots of up to h rows
+  // (the fold moves a whole frame), final colour region of up to h rows
+  EQC_TRY(alloc_common(r, g, (size_t)2 * g.h, g.op == EQC_OP_BLEND ? g.h : 1, 2));
+  if (g.flags & EQC_FLAG_RLE) {
+    const int64_t cap = band_cap(g, g.h);
+    EQC_TRY(r.enc.ensure((size_t)4 * cap));  // 2 outgoing parts x (c, d) streams
+    EQC_TRY(r.dec.ensure((size_t)4 * cap));
+    EQC_TRY(r.sizes.ensure((size_t)8 * sizeof(int64_t)));  // [0..3] sent, [4..7] received
+    EQC_TRY(r.ws.ensure_zeroed(image_rle_workspace_size_batch(2, g.w, g.h)));
+  }
+  return EQC_OK;
+}
+
+// One exchange step of the 2-3 swap: every rank sends rows [y0, y1) of its
+// live partial (both planes) to each peer in `sends` and receives `rows`
+// rows from each peer in `recvs` into receive slot i (raw, or RLE streams
+// after one size exchange).
+struct S23Msg {
+  int peer, y0, y1;
+};
+int s23_exchange(std::vector<RankState *> &ranks, const Geometry &g, Transport &T,
+                 const std::vector<std::vector<S23Msg>> &sends, const std::vector<std::vector<S23Msg>> &recvs,
+                 cudaStream_t s) {
+  const bool rle = (g.flags & EQC_FLAG_RLE) != 0;
+  const int64_t cap = band_cap(g, g.h);
+  const size_t slot = (size_t)g.h * g.w;
+  if (rle) {
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      RankState &r = *ranks[i];
+      for (size_t j = 0; j < sends[i].size(); ++j) {
+        const S23Msg &m = sends[i][j];
+        if (m.y1 <= m.y0) continue;
+        const size_t off = (size_t)m.y0 * g.w;
+        EQC_TRY(encode_band(r, g, (int)j, r.part_c[r.cur].as<uint32_t>() + off, r.part_d[r.cur].as<uint32_t>() + off,
+                            m.y1 - m.y0, cap, s));
+      }
+    }
+    EQC_TRY(T.start());
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      RankState &r = *ranks[i];
+      int64_t *sz = r.sizes.as<int64_t>();
+      for (size_t j = 0; j < sends[i].size(); ++j)
+        if (sends[i][j].y1 > sends[i][j].y0) EQC_TRY(T.send(r, sends[i][j].peer, sz + 2 * j, 2 * sizeof(int64_t)));
+      for (size_t j = 0; j < recvs[i].size(); ++j)
+        if (recvs[i][j].y1 > recvs[i][j].y0) EQC_TRY(T.recv(r, recvs[i][j].peer, sz + 4 + 2 * j, 2 * sizeof(int64_t)));
+    }
+    EQC_TRY(T.end());
+    for (RankState *r : ranks)
+      EQC_CUDA_TRY(cudaMemcpyAsync(r->h_sizes, r->sizes.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  EQC_TRY(T.start());
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    RankState &r = *ranks[i];
+    for (size_t j = 0; j < sends[i].size(); ++j) {
+      const S23Msg &m = sends[i][j];
+      if (m.y1 <= m.y0) continue;
+      if (rle) {
+        EQC_TRY(T.send(r, m.peer, r.enc.as<uint8_t>() + (size_t)(2 * j) * cap, (size_t)r.h_sizes[2 * j]));
+        EQC_TRY(T.send(r, m.peer, r.enc.as<uint8_t>() + (size_t)(2 * j + 1) * cap, (size_t)r.h_sizes[2 * j + 1]));
+      } else {
+        const size_t off = (size_t)m.y0 * g.w;
+        EQC_TRY(T.send(r, m.peer, r.part_c[r.cur].as<uint32_t>() + off, frame_bytes(g, m.y1 - m.y0)));
+        EQC_TRY(T.send(r, m.peer, r.part_d[r.cur].as<uint32_t>() + off, frame_bytes(g, m.y1 - m.y0)));
+      }
+      r.stats[0] += 1;
+    }
+    for (size_t j = 0; j < recvs[i].size(); ++j) {
+      const S23Msg &m = recvs[i][j];
+      if (m.y1 <= m.y0) continue;
+      if (rle) {
+        EQC_TRY(T.recv(r, m.peer, r.dec.as<uint8_t>() + (size_t)(2 * j) * cap, (size_t)r.h_sizes[4 + 2 * j]));
+        EQC_TRY(T.recv(r, m.peer, r.dec.as<uint8_t>() + (size_t)(2 * j + 1) * cap, (size_t)r.h_sizes[5 + 2 * j]));
+      } else {
+        EQC_TRY(T.recv(r, m.peer, r.recv_c.as<uint32_t>() + j * slot, frame_bytes(g, m.y1 - m.y0)));
+        EQC_TRY(T.recv(r, m.peer, r.recv_d.as<uint32_t>() + j * slot, frame_bytes(g, m.y1 - m.y0)));
+      }
+    }
+  }
+  EQC_TRY(T.end());
+  if (rle) {
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      RankState &r = *ranks[i];
+      for (size_t j = 0; j < recvs[i].size(); ++j) {
+        const S23Msg &m = recvs[i][j];
+        if (m.y1 <= m.y0) continue;
+        const uint8_t *src[2] = {r.dec.as<uint8_t>() + (size_t)(2 * j) * cap,
+                                 r.dec.as<uint8_t>() + (size_t)(2 * j + 1) * cap};
+        uint32_t *dst[2] = {r.recv_c.as<uint32_t>() + j * slot, r.recv_d.as<uint32_t>() + j * slot};
+        const int64_t caps[2] = {cap, cap};
+        EQC_TRY(image_decompress_rle_batch(2, src, caps, dst, g.w, g.w, m.y1 - m.y0, r.status.as<int32_t>(), s));
+      }
+    }
+  }
+  return EQC_OK;
+}
+
+int run_swap23(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaStream_t s) {
+  std::vector<S23Plan> plans(ranks.size());
+  for (size_t i = 0; i < ranks.size(); ++i) EQC_TRY(plan_swap23(g.h, g.n, ranks[i]->rank, plans[i]) < 0 ? EQC_E_INVALID : EQC_OK);
+  for (RankState *r : ranks) {
+    for (int i = 0; i < 4; ++i) r->stats[i] = 0;
+    EQC_TRY(s23_alloc(*r, g));
+    EQC_TRY(local_precomposite(*r, g, s));
+  }
+  const size_t slot = (size_t)g.h * g.w;
+  // fold: groups of two, whole frames
+  {
+    std::vector<std::vector<S23Msg>> snd(ranks.size()), rcv(ranks.size());
+    bool any = false;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      if (plans[i].fold_role == 2) snd[i].push_back(S23Msg{plans[i].fold_partner, 0, g.h});
+      if (plans[i].fold_role == 1) rcv[i].push_back(S23Msg{plans[i].fold_partner, 0, g.h});
+      any = any || plans[i].fold_role != 0;
+    }
+    if (any) {
+      EQC_TRY(s23_exchange(ranks, g, T, snd, rcv, s));
+      for (size_t i = 0; i < ranks.size(); ++i) {
+        if (plans[i].fold_role != 1) continue;
+        RankState &r = *ranks[i];
+        const uint32_t *c[2] = {r.part_c[r.cur].as<uint32_t>(), r.recv_c.as<uint32_t>()};
+        const uint32_t *d[2] = {r.part_d[r.cur].as<uint32_t>(), r.recv_d.as<uint32_t>()};
+        const int nxt = r.cur ^ 1;
+        EQC_TRY(op_merge(g, c, d, g.h, r.part_c[nxt].as<uint32_t>(), r.part_d[nxt].as<uint32_t>(), s));
+        r.cur = nxt;
+      }
+    }
+  }
+  size_t nrounds = 0;
+  for (auto &P : plans) nrounds = std::max(nrounds, P.rounds.size());
+  for (size_t rd = 0; rd < nrounds; ++rd) {
+    std::vector<std::vector<S23Msg>> snd(ranks.size()), rcv(ranks.size());
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      if (rd >= plans[i].rounds.size()) continue;
+      const S23Round &R = plans[i].rounds[rd];
+      for (int u = 0; u < R.k; ++u) {
+        if (u == R.t) continue;
+        snd[i].push_back(S23Msg{R.members[u], R.bnd[u], R.bnd[u + 1]});
+        rcv[i].push_back(S23Msg{R.members[u], R.bnd[R.t], R.bnd[R.t + 1]});
+      }
+    }
+    EQC_TRY(s23_exchange(ranks, g, T, snd, rcv, s));
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      if (rd >= plans[i].rounds.size()) continue;
+      RankState &r = *ranks[i];
+      const S23Round &R = plans[i].rounds[rd];
+      const int ky0 = R.bnd[R.t], rows = R.bnd[R.t + 1] - ky0;
+      const int nxt = r.cur ^ 1;
+      if (rows <= 0) {
+        r.cur = nxt;
+        continue;
+      }
+      const size_t off = (size_t)ky0 * g.w;
+      // members in rank order; slot j holds the j-th other member's part
+      const uint32_t *c[3], *d[3];
+      for (int u = 0, j = 0; u < R.k; ++u) {
+        if (u == R.t) {
+          c[u] = r.part_c[r.cur].as<uint32_t>() + off;
+          d[u] = r.part_d[r.cur].as<uint32_t>() + off;
+        } else {
+          c[u] = r.recv_c.as<uint32_t>() + (size_t)j * slot;
+          d[u] = r.recv_d.as<uint32_t>() + (size_t)j * slot;
+          ++j;
+        }
+      }
+      uint32_t *oc = r.part_c[nxt].as<uint32_t>() + off, *od = r.part_d[nxt].as<uint32_t>() + off;
+      if (g.op == EQC_OP_BLEND)
+        EQC_TRY(eqc_blend_partials(R.k, c, d, g.w, rows, g.w, 0u, nullptr, oc, od, g.w, s));
+      else
+        EQC_TRY(compositor_depth(R.k, c, d, g.w, rows, g.w, oc, od, g.w, s));
+      r.cur = nxt;
+    }
+  }
+  // final regions -> colour -> destination
+  auto region = [&](int q, int &y0, int &y1) {
+    S23Plan P;
+    plan_swap23(g.h, g.n, q, P);
+    y0 = P.fy0;
+    y1 = P.fy1;
+  };
+  auto final_colour = [&](RankState *r, int y0) -> const uint32_t * {
+    return g.op == EQC_OP_BLEND ? r->fin_c.as<uint32_t>() : r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w;
+  };
+  for (RankState *r : ranks) {
+    int y0, y1;
+    region(r->rank, y0, y1);
+    if (y1 <= y0) continue;
+    if (g.op == EQC_OP_BLEND) {
+      const size_t off = (size_t)y0 * g.w;
+      const uint32_t *c[1] = {r->part_c[r->cur].as<uint32_t>() + off}, *d[1] = {r->part_d[r->cur].as<uint32_t>() + off};
+      EQC_TRY(op_final(g, 1, c, d, y1 - y0, r->fin_c.as<uint32_t>(), g.w, s));
+    }
+    if (r->rank == g.dest)
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)y0 * g.out_pitch, g.out_pitch * 4, final_colour(r, y0),
+                                     (size_t)g.w * 4, (size_t)g.w * 4, y1 - y0, cudaMemcpyDeviceToDevice, s));
+  }
+  if (g.n > 1) {
+    EQC_TRY(T.start());
+    for (RankState *r : ranks) {
+      int y0, y1;
+      region(r->rank, y0, y1);
+      EQC_TRY(gather(*r, g, T, region, final_colour(r, y0), s, 0));
+    }
+    EQC_TRY(T.end());
+    for (RankState *r : ranks) {
+      int y0, y1;
+      region(r->rank, y0, y1);
+      EQC_TRY(gather(*r, g, T, region, final_colour(r, y0), s, 1));
+    }
+  }
+  return EQC_OK;
+}
+
 int validate(int nranks, int n_local, const void *color, const void *depth, int w, int h, int64_t pitch, int op,
              int flags, int dest, const void *out, int64_t out_pitch, bool is_dest) {
   if (nranks < 1 || n_local < 1 || n_local > EQC_MAX_SOURCES || nranks > EQC_MAX_SOURCES) return EQC_E_INVALID;
@@ -996,13 +1275,16 @@ extern "C" int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max
   return k;
 }
 
-static int compose_nccl(bool ds, eqc_comm *comm, int n_local, const uint32_t *const *color,
+enum Algo { kDirectSend, kBinarySwap, kSwap23 };
+
+static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *const *color,
                         const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags, int dest_rank,
                         uint32_t *out_color, int64_t out_pitch, void *stream) {
   if (!comm) return EQC_E_INVALID;
   EQC_TRY(validate(comm->nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
                    comm->rank == dest_rank));
-  if (!ds && (comm->nranks & (comm->nranks - 1))) return EQC_E_UNSUPPORTED;
+  if (algo == kBinarySwap && (comm->nranks & (comm->nranks - 1))) return EQC_E_UNSUPPORTED;
+  const bool ds = algo == kDirectSend;
   Geometry g;
   g.n = comm->nranks;
   g.n_local = n_local;
@@ -1023,28 +1305,29 @@ static int compose_nccl(bool ds, eqc_comm *comm, int n_local, const uint32_t *co
   }
   NcclTransport T(comm->nccl, s);
   std::vector<RankState *> ranks{&comm->st};
-  return ds ? run_direct_send(ranks, g, T, s) : run_binary_swap(ranks, g, T, s);
+  return ds ? run_direct_send(ranks, g, T, s)
+            : algo == kBinarySwap ? run_binary_swap(ranks, g, T, s) : run_swap23(ranks, g, T, s);
 }
 
 extern "C" int compose_direct_send(eqc_comm *comm, int n_local, const uint32_t *const *color,
                                    const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
                                    int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream) {
-  return compose_nccl(true, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+  return compose_nccl(kDirectSend, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
                       stream);
 }
 
 extern "C" int compose_binary_swap(eqc_comm *comm, int n_local, const uint32_t *const *color,
                                    const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
                                    int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream) {
-  return compose_nccl(false, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+  return compose_nccl(kBinarySwap, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
                       stream);
 }
 
-static int compose_local(bool ds, int nranks, int n_local, const uint32_t *const *color,
+static int compose_local(Algo algo, int nranks, int n_local, const uint32_t *const *color,
                          const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags, int dest_rank,
                          uint32_t *out_color, int64_t out_pitch, int64_t *out_stats, void *stream) {
   EQC_TRY(validate(nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch, true));
-  if (!ds && (nranks & (nranks - 1))) return EQC_E_UNSUPPORTED;
+  if (algo == kBinarySwap && (nranks & (nranks - 1))) return EQC_E_UNSUPPORTED;
   Geometry g;
   g.n = nranks;
   g.n_local = n_local;
@@ -1066,7 +1349,8 @@ static int compose_local(bool ds, int nranks, int n_local, const uint32_t *const
     ranks.push_back(&states[q]);
   }
   LocalTransport T(s);
-  int rc = ds ? run_direct_send(ranks, g, T, s) : run_binary_swap(ranks, g, T, s);
+  int rc = algo == kDirectSend ? run_direct_send(ranks, g, T, s)
+           : algo == kBinarySwap ? run_binary_swap(ranks, g, T, s) : run_swap23(ranks, g, T, s);
   cudaStreamSynchronize(s);  // scratch is freed below
   if (out_stats) {
     for (int i = 0; i < 4; ++i) out_stats[i] = 0;
@@ -1081,7 +1365,7 @@ extern "C" int compose_direct_send_local(int nranks, int n_local, const uint32_t
                                          const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
                                          int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
                                          void *stream) {
-  return compose_local(true, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+  return compose_local(kDirectSend, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
                        out_stats, stream);
 }
 
@@ -1089,6 +1373,44 @@ extern "C" int compose_binary_swap_local(int nranks, int n_local, const uint32_t
                                          const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
                                          int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
                                          void *stream) {
-  return compose_local(false, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+  return compose_local(kBinarySwap, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
                        out_stats, stream);
+}
+
+extern "C" int compose_swap23(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                              const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                              int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream) {
+  return compose_nccl(kSwap23, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+                      stream);
+}
+
+extern "C" int compose_swap23_local(int nranks, int n_local, const uint32_t *const *color,
+                                    const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                    int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                    void *stream) {
+  return compose_local(kSwap23, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color,
+                       out_pitch, out_stats, stream);
+}
+
+extern "C" int eqc_plan_swap23(int h, int n, int rank, int *out, int max_ints) {
+  if (h <= 0 || n < 1 || rank < 0 || rank >= n || !out) return EQC_E_INVALID;
+  S23Plan P;
+  const int k = plan_swap23(h, n, rank, P);
+  if (k < 0) return k;
+  const int need = 5 + 9 * k;
+  if (need > max_ints) return EQC_E_CAPACITY;
+  out[0] = P.fold_role;
+  out[1] = P.fold_partner;
+  out[2] = k;
+  out[3] = P.fy0;
+  out[4] = P.fy1;
+  for (int i = 0; i < k; ++i) {
+    const S23Round &R = P.rounds[i];
+    int *o = out + 5 + 9 * i;
+    o[0] = R.k;
+    o[1] = R.t;
+    for (int u = 0; u < 3; ++u) o[2 + u] = R.members[u];
+    for (int u = 0; u < 4; ++u) o[5 + u] = R.bnd[u];
+  }
+  return k;
 }

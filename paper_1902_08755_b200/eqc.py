@@ -69,6 +69,9 @@ def _load():
         "compose_binary_swap": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
         "compose_direct_send_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
         "compose_binary_swap_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
+        "compose_swap23": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
+        "compose_swap23_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
+        "eqc_plan_swap23": ([i32, i32, i32, P, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -347,3 +350,29 @@ def compose_binary_swap_local(nranks, colors, depths, out_color, dest_rank: int 
                               op: int = OP_DEPTH, stream=None):
     return _compose_local(_lib.compose_binary_swap_local, "compose_binary_swap_local", nranks, colors, depths,
                           out_color, dest_rank, flags, op, stream)
+
+
+def compose_swap23(comm, colors, depths, out_color=None, dest_rank: int = 0, flags: int = 0,
+                   op: int = OP_DEPTH, stream=None):
+    """2-3 swap (any number of ranks; R-C21)."""
+    return _compose(_lib.compose_swap23, "compose_swap23", comm, colors, depths, out_color, dest_rank,
+                    flags, op, stream)
+
+
+def compose_swap23_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
+                         op: int = OP_DEPTH, stream=None):
+    return _compose_local(_lib.compose_swap23_local, "compose_swap23_local", nranks, colors, depths,
+                          out_color, dest_rank, flags, op, stream)
+
+
+def eqc_plan_swap23(h: int, n: int, rank: int):
+    """Plan of `rank`: dict(fold_role, fold_partner, final=(y0, y1), rounds=[dict(k, t, members, bounds)])."""
+    buf = (ctypes.c_int * (5 + 9 * 64))()
+    k = _check(_lib.eqc_plan_swap23(h, n, rank, buf, len(buf)), "eqc_plan_swap23")
+    v = list(buf)
+    rounds = []
+    for i in range(k):
+        o = v[5 + 9 * i: 14 + 9 * i]
+        rounds.append({"k": o[0], "t": o[1], "members": [m for m in o[2:5] if m >= 0][:o[0]],
+                       "bounds": o[5:6 + o[0]]})
+    return {"fold_role": v[0], "fold_partner": v[1], "final": (v[3], v[4]), "rounds": rounds}

@@ -66,6 +66,7 @@ def main():
     if n & (n - 1) == 0:
         variants += [("binary_swap_nccl", eqc.compose_binary_swap, 0),
                      ("binary_swap_rle", eqc.compose_binary_swap, eqc.FLAG_RLE)]
+    variants += [("swap23_nccl", eqc.compose_swap23, 0), ("swap23_rle", eqc.compose_swap23, eqc.FLAG_RLE)]
     op = eqc.OP_BLEND if blend else eqc.OP_DEPTH
     if blend:
         variants = [v for v in variants if "roi" not in v[0]]

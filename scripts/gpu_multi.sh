@@ -25,3 +25,8 @@ cat gpurun_out/compose_c4c_n${N}.json
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29515 \
   scripts/bench_compose.py --scene bricks --w 3840 --h 2160 --sources 16 > gpurun_out/compose_c3_n${N}.json 2> gpurun_out/compose_c3_n${N}.log
 cat gpurun_out/compose_c3_n${N}.json
+if [ "$N" -ge 3 ]; then
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=3 --master-addr=127.0.0.1 --master-port=29516 \
+  scripts/bench_compose.py --sources 6 > gpurun_out/compose_c4s6_n3.json 2> gpurun_out/compose_c4s6_n3.log
+cat gpurun_out/compose_c4s6_n3.json
+fi

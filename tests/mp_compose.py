@@ -36,6 +36,8 @@ def main():
              ("ds", 1, 64, 16, 0, O, "empty")]
     if world & (world - 1) == 0:
         cases += [("bs", 2, 640, 361, 0, 0), ("bs", 1, 300, 41, world - 1, R), ("bs", 2, 1920, 1080, 0, R)]
+    # 2-3 swap (any rank count, R-C21)
+    cases += [("s23", 2, 640, 361, 0, 0), ("s23", 1, 300, 41, world - 1, R), ("s23", 2, 1920, 1080, 1 % world, 0)]
     # config c4 (8 sources of 7680x4320 over the ranks), checked on sampled rows
     if 8 % world == 0:
         cases += [("ds", 8 // world, 7680, 4320, 0, 0), ("ds", 8 // world, 7680, 4320, 0, R)]
@@ -53,7 +55,7 @@ def main():
         dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
         dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
         out = torch.zeros((h, w), dtype=torch.int32, device=dev)
-        fn = eqc.compose_direct_send if algo == "ds" else eqc.compose_binary_swap
+        fn = {"ds": eqc.compose_direct_send, "bs": eqc.compose_binary_swap, "s23": eqc.compose_swap23}[algo]
         for _ in range(2):  # the second call reuses the communicator's scratch
             fn(comm, dc, dd, out if rank == dest else None, dest_rank=dest, flags=rle)
         torch.cuda.synchronize()
@@ -78,6 +80,7 @@ def main():
     bcases = [("ds", 4, 640, 361, 0, 0), ("ds", 2, 300, 41, world - 1, X), ("ds", 3, 320, 181, 1 % world, R)]
     if world & (world - 1) == 0:
         bcases += [("bs", 4, 640, 361, 0, 0), ("bs", 2, 300, 41, world - 1, R)]
+    bcases += [("s23", 3, 640, 361, 0, 0), ("s23", 2, 300, 41, world - 1, R)]
     if 16 % world == 0:  # config c3: 16 bricks of 3840x2160, sampled rows
         bcases += [("ds", 16 // world, 3840, 2160, 0, 0)]
     for algo, nl, w, h, dest, fl in bcases:
@@ -86,7 +89,7 @@ def main():
         mine = range(rank * nl, (rank + 1) * nl)
         dl = [torch.from_numpy(layers[i].view(np.int32)).to(dev) for i in mine]
         out = torch.zeros((h, w), dtype=torch.int32, device=dev)
-        fn = eqc.compose_direct_send if algo == "ds" else eqc.compose_binary_swap
+        fn = {"ds": eqc.compose_direct_send, "bs": eqc.compose_binary_swap, "s23": eqc.compose_swap23}[algo]
         for _ in range(2):
             fn(comm, dl, None, out if rank == dest else None, dest_rank=dest, flags=fl, op=eqc.OP_BLEND)
         torch.cuda.synchronize()

@@ -91,6 +91,40 @@ def _worker(rank, world, port, algo, n_local, w, h, dest, tie_alphabet, result_q
                     bands_d.append(recv_map[q][1])
             fin = oracle.depth_composite(bands_c, bands_d)[0] if y1 > y0 else np.zeros((0, w), np.uint32)
             regions = [(row0[q], row0[q + 1]) for q in range(world)]
+        elif algo == "s23":
+            # 2-3 swap (R-C21): fold pairs, then mixed-radix groups of 2 / 3
+            plan = eqc.eqc_plan_swap23(h, world, rank)
+            cur_c, cur_d = pc.copy(), pd.copy()
+            if plan["fold_role"] == 2:
+                _exchange([(cur_c, plan["fold_partner"]), (cur_d, plan["fold_partner"])], [])
+                msgs += 1
+            elif plan["fold_role"] == 1:
+                tc, td = _exchange([], [((h, w), plan["fold_partner"])] * 2)
+                cur_c, cur_d = oracle.depth_composite([cur_c, tc], [cur_d, td])  # lower rank first
+            for rd in plan["rounds"]:
+                k, t, mem, bnd = rd["k"], rd["t"], rd["members"], rd["bounds"]
+                ky0, ky1 = bnd[t], bnd[t + 1]
+                sends, recvs, others = [], [], []
+                for u in range(k):
+                    if u == t:
+                        continue
+                    if bnd[u + 1] > bnd[u]:
+                        sends += [(cur_c[bnd[u]:bnd[u + 1]], mem[u]), (cur_d[bnd[u]:bnd[u + 1]], mem[u])]
+                        msgs += 1
+                    if ky1 > ky0:
+                        recvs += [((ky1 - ky0, w), mem[u])] * 2
+                        others.append(u)
+                got = _exchange(sends, recvs)
+                if ky1 > ky0:
+                    parts = {t: (cur_c[ky0:ky1].copy(), cur_d[ky0:ky1].copy())}
+                    for i, u in enumerate(others):
+                        parts[u] = (got[2 * i], got[2 * i + 1])
+                    oc, od = oracle.depth_composite([parts[u][0] for u in range(k)], [parts[u][1] for u in range(k)])
+                    cur_c[ky0:ky1] = oc
+                    cur_d[ky0:ky1] = od
+            regions = [eqc.eqc_plan_swap23(h, world, q)["final"] for q in range(world)]
+            y0, y1 = regions[rank]
+            fin = cur_c[y0:y1]
         else:
             plan = eqc.eqc_plan_binary_swap(h, world, rank)
             cur_c, cur_d = pc.copy(), pd.copy()
@@ -138,6 +172,9 @@ def _worker(rank, world, port, algo, n_local, w, h, dest, tie_alphabet, result_q
     ("bs", 2, 3, 40, 33, 1, True),
     ("bs", 4, 1, 64, 37, 0, False),
     ("bs", 4, 2, 16, 5, 3, True),
+    ("s23", 3, 2, 40, 31, 1, True),
+    ("s23", 5, 1, 24, 17, 4, True),
+    ("s23", 6, 1, 33, 12, 0, False),
 ])
 def test_schedule_equals_oracle_over_all_sources(algo, world, n_local, w, h, dest, ties):
     ctx = mp.get_context("spawn")
@@ -156,5 +193,5 @@ def test_schedule_equals_oracle_over_all_sources(algo, world, n_local, w, h, des
     msgs = sum(r[1] for r in res)
     if algo == "ds":
         assert msgs == world * (world - 1)  # n(n-1) band messages
-    else:
+    elif algo == "bs":
         assert msgs == world * (world.bit_length() - 1)  # n log2 n swaps

@@ -111,6 +111,46 @@ def test_virtual_rank_blend_within_one_lsb(eqc, case):
     assert diff.max() <= 1, f"max channel error {diff.max()} LSB"
 
 
+S23_CASES = [
+    # (nranks, n_local, w, h, pitch, out_pitch, dest, rle, op) -- 2-3 swap (R-C21)
+    (1, 2, 64, 16, None, None, 0, 0, "depth"),
+    (3, 2, 300, 41, None, None, 1, 0, "depth"),
+    (5, 1, 130, 37, 136, 140, 4, 0, "depth"),
+    (6, 1, 128, 19, None, None, 2, 1, "depth"),
+    (7, 2, 257, 77, None, 264, 3, 0, "depth"),
+    (12, 1, 96, 50, None, None, 11, 1, "depth"),
+    (3, 3, 320, 90, None, None, 0, 0, "blend"),
+    (5, 2, 130, 37, 136, None, 2, 1, "blend"),
+    (6, 2, 128, 19, None, None, 5, 0, "blend"),
+]
+
+
+@pytest.mark.parametrize("case", S23_CASES,
+                         ids=[f"n{c[0]}x{c[1]}_{c[2]}x{c[3]}_rle{c[7]}_{c[8]}" for c in S23_CASES])
+def test_virtual_rank_swap23(eqc, case):
+    nr, nl, w, h, pitch, opitch, dest, rle, op = case
+    N = nr * nl
+    out = out_frame(h, w, opitch)
+    flags = eqc.FLAG_RLE if rle else 0
+    if op == "depth":
+        c, d = synth.random_frames(N + w + 1, N, w, h, depth_alphabet=[0, 2, 0xFFFFFFFF]) if nr % 2 else \
+            synth.depth_sources(synth.SEED_BASE + 3 + N, N, w, h)
+        dc = [to_dev(x, pitch) for x in c]
+        dd = [to_dev(x, pitch) for x in d]
+        stats = eqc.compose_swap23_local(nr, dc, dd, out, dest_rank=dest, flags=flags)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(to_host(out), oracle.depth_composite(c, d)[0])
+        assert stats[2] == stats[3]
+    else:
+        layers = synth.volume_bricks(synth.SEED_BASE + 90 + N, N, w, h)
+        dl = [to_dev(x, pitch) for x in layers]
+        eqc.compose_swap23_local(nr, dl, None, out, dest_rank=dest, flags=flags, op=eqc.OP_BLEND)
+        torch.cuda.synchronize()
+        want = oracle.blend_ordered(layers)
+        diff = np.abs(to_host(out).view(np.uint8).astype(int) - want.view(np.uint8).astype(int))
+        assert diff.max() <= 1
+
+
 def test_binary_swap_rejects_non_power_of_two(eqc):
     c, d = synth.random_frames(1, 3, 8, 8)
     with pytest.raises(eqc.EqcError) as e:
@@ -118,7 +158,7 @@ def test_binary_swap_rejects_non_power_of_two(eqc):
     assert e.value.code == eqc.E_UNSUPPORTED
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("nproc", [2, 3, 4])
 def test_nccl_multi_gpu(eqc, nproc):
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")

@@ -7,6 +7,7 @@ i.e. n(n-1) + (n-1) messages.  Binary swap: log2 n
 rounds with partner rank ^ 2^r; final regions partition the frame in
 bit-reversed order; non-power-of-two n is unsupported.
 """
+import numpy as np
 import pytest
 
 from paper_1902_08755_b200 import eqc
@@ -74,3 +75,83 @@ def test_direct_send_message_count(n):
     gathers = sum(1 for q in range(n) if q != 0 and row0[q + 1] > row0[q])
     assert band_msgs == n * (n - 1)
     assert gathers == n - 1
+
+
+# ---- 2-3 swap plans (R-C21) ----------------------------------
+def _s23_plans(h, n):
+    return [eqc.eqc_plan_swap23(h, n, r) for r in range(n)]
+
+
+@pytest.mark.parametrize("n", list(range(1, 21)) + [24, 27, 36])
+def test_swap23_final_regions_partition_the_frame(n):
+    for h in (1, 7, 100, 1081):
+        plans = _s23_plans(h, n)
+        covered = np.zeros(h, int)
+        for p in plans:
+            y0, y1 = p["final"]
+            if p["fold_role"] == 2:
+                assert (y0, y1) == (0, 0) and not p["rounds"]
+            covered[y0:y1] += 1
+        assert (covered == 1).all()  # every row owned by exactly one rank
+
+
+@pytest.mark.parametrize("n", list(range(1, 21)) + [24, 27, 36])
+def test_swap23_groups_of_two_or_three_consistent(n):
+    h = 720
+    plans = _s23_plans(h, n)
+    for p in plans:
+        for r, rd in enumerate(p["rounds"]):
+            assert rd["k"] in (2, 3) and len(rd["members"]) == rd["k"]
+            assert rd["members"] == sorted(rd["members"])
+            for u, q in enumerate(rd["members"]):  # every member agrees on the group
+                other = plans[q]["rounds"][r]
+                assert other["members"] == rd["members"] and other["bounds"] == rd["bounds"]
+                assert other["t"] == u
+    folds = [p for p in plans if p["fold_role"]]
+    for r, p in enumerate(plans):
+        if p["fold_role"]:
+            assert plans[p["fold_partner"]]["fold_partner"] == r
+            assert {p["fold_role"], plans[p["fold_partner"]]["fold_role"]} == {1, 2}
+    assert len(folds) % 2 == 0
+
+
+@pytest.mark.parametrize("n", list(range(1, 21)) + [24, 27, 36])
+def test_swap23_symbolic_execution_reaches_all_sources_in_order(n):
+    # track, per rank and row, the ordered list of source ranks composited so
+    # far: every final row must hold ALL ranks, merged in ascending order
+    h = 97
+    plans = _s23_plans(h, n)
+    held = {r: [[r] for _ in range(h)] for r in range(n)}
+    for r, p in enumerate(plans):
+        if p["fold_role"] == 1:
+            q = p["fold_partner"]
+            held[r] = [a + b for a, b in zip(held[r], held[q])]
+    nr = max(len(p["rounds"]) for p in plans)
+    for rd in range(nr):
+        new = {r: [list(x) for x in held[r]] for r in range(n)}
+        for r, p in enumerate(plans):
+            if rd >= len(p["rounds"]):
+                continue
+            R = p["rounds"][rd]
+            y0, y1 = R["bounds"][R["t"]], R["bounds"][R["t"] + 1]
+            for y in range(y0, y1):
+                new[r][y] = sum((held[q][y] for q in R["members"]), [])
+        held = new
+    for r, p in enumerate(plans):
+        y0, y1 = p["final"]
+        for y in range(y0, y1):
+            assert held[r][y] == list(range(n)), (n, r, y)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 16])
+def test_swap23_is_binary_swap_for_powers_of_two(n):
+    h = 1081
+    for r in range(n):
+        p = eqc.eqc_plan_swap23(h, n, r)
+        bs = eqc.eqc_plan_binary_swap(h, n, r)
+        assert p["fold_role"] == 0 and len(p["rounds"]) == len(bs)
+        for rd, b in zip(p["rounds"], bs):
+            partner, low, ky0, ky1, sy0, sy1 = b
+            assert rd["k"] == 2 and partner in rd["members"]
+            assert (rd["bounds"][rd["t"]], rd["bounds"][rd["t"] + 1]) == (ky0, ky1)
+            assert (rd["t"] == 0) == bool(low)
