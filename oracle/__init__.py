@@ -69,6 +69,8 @@ def lib():
         L.or_depth_composite_roi.restype = i32
         L.or_blend_ordered_roi.argtypes = [i32, P, P, P, i32, i32, i64, u32, P, i64]
         L.or_blend_ordered_roi.restype = i32
+        L.or_average.argtypes = [i32, P, i32, i32, i64, P, i64]
+        L.or_average.restype = None
         _lib = L
     return _lib
 
@@ -223,4 +225,15 @@ def blend_ordered_roi(colors, rois, order=None, background: int = 0):
                                     int(background) & 0xFFFFFFFF, _ptr(oc), w)
     if rc:
         raise ValueError(f"or_blend_ordered_roi: {rc}")
+    return oc
+
+
+def average(colors):
+    """Subpixel accumulation + averaging: per channel round-half-up mean."""
+    n = len(colors)
+    colors = _as_u32_frames(colors)
+    h, w = colors[0].shape
+    pitch = colors[0].strides[0] // 4
+    oc = np.empty((h, w), np.uint32)
+    lib().or_average(n, _ptr_array(colors), w, h, pitch, _ptr(oc), w)
     return oc

@@ -26,6 +26,9 @@
  *                        dataset is unavailable).
  *   or_roi               pinned: numpy nonzero bounding boxes, empty / single
  *                        pixel / full frames.
+ *   or_average           pinned: numpy integer mean with explicit half-up
+ *                        rounding, n = 1 identity, equal sources, permutation
+ *                        invariance, exact .5 ties rounding up.
  *   or_*_roi             pinned: reduction to O1 / O2 on frames masked outside
  *                        the rectangle (the definition of ROI placement), and
  *                        invariance under cropping to the exact bounding box.
@@ -490,4 +493,30 @@ int or_blend_ordered_roi(int n, const uint32_t *const *color, const int32_t *ord
     }
   }
   return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Subpixel compositing: accumulation and averaging      */
+/* ------------------------------------------------------------------------ */
+/*
+ * subpixel compounds' "default compositing algorithm uses
+ * accumulation and averaging of all computed fragments for a pixel".  Plain
+ * definition per channel c: out_c = the mean of the n source values rounded
+ * half up, i.e. floor((2 * sum_i s_ic + n) / (2 n)) in integers (R-C22).
+ */
+void or_average(int n, const uint32_t *const *color, int w, int h, int64_t pitch, uint32_t *out_color,
+                int64_t out_pitch) {
+  for (int y = 0; y < h; ++y) {
+    for (int x = 0; x < w; ++x) {
+      int64_t p = (int64_t)y * pitch + x;
+      uint32_t o = 0;
+      for (int c = 0; c < 4; ++c) {
+        uint64_t sum = 0;
+        for (int i = 0; i < n; ++i) sum += (color[i][p] >> (8 * c)) & 0xFFu;
+        uint64_t v = (2 * sum + (uint64_t)n) / (2 * (uint64_t)n);
+        o |= (uint32_t)v << (8 * c);
+      }
+      out_color[(int64_t)y * out_pitch + x] = o;
+    }
+  }
 }
