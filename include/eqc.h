@@ -100,6 +100,16 @@ EQC_API int compositor_blend_ordered(int n, const uint32_t *const *color, const 
                              uint32_t *out_color, int64_t out_pitch, void *stream);
 
 /*
+ * compositor_average -- subpixel compositing: "accumulation and averaging of
+ * all computed fragments for a pixel".  Per channel
+ *   out_c = floor((2 * sum_i s_ic + n) / (2 n))   (mean rounded half up, R-C22)
+ *   n          1 <= n <= EQC_MAX_SOURCES; color: host array of n device
+ *              pointers to RGBA8 [h][pitch].  Bit-exact.
+ */
+EQC_API int compositor_average(int n, const uint32_t *const *color, int w, int h, int64_t pitch,
+                               uint32_t *out_color, int64_t out_pitch, void *stream);
+
+/*
  * Region of interest.  "The ROI is the screen-space 2D
  * bounding box fully enclosing the data rendered by a single resource"
  * (P:2259-2263); it "is transmitted to all input frames together with the

@@ -34,6 +34,9 @@ typedef struct eqc_comm eqc_comm;
 #define EQC_OP_BLEND 1      /* ordered back-to-front "over" (compositor_blend_ordered semantics, background 0):
                                global layer order = rank-block order; depth may be NULL; partials cross
                                GPUs as unorm16 RGBA (R-C6) and are rounded once to RGBA8 at the end */
+#define EQC_OP_AVERAGE 2    /* subpixel accumulation + averaging (compositor_average semantics):
+                               depth may be NULL; partial channel sums cross GPUs exactly as packed 16-bit
+                               sums (<= 256 sources in total); bit-exact */
 #define EQC_FLAG_RLE 1      /* ship bands as RLE-BP streams (colour swizzled + depth) */
 #define EQC_FLAG_NCCL 2     /* direct send: force NCCL grouped send/recv instead of the NVLink peer-memory path */
 #define EQC_FLAG_ROI 4      /* region of interest: peer-memory direct send reads and composites
@@ -159,6 +162,22 @@ EQC_API int compose_swap23_local(int nranks, int n_local, const uint32_t *const 
                                  int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
                                  void *stream);
 EQC_API int eqc_plan_swap23(int h, int n, int rank, int *out, int max_ints);
+
+/*
+ * compose_stream -- the streaming sort-last chain: rank k
+ * receives the whole partial frame of ranks 0..k-1 from rank k-1 (raw or
+ * EQC_FLAG_RLE streams), composites it under / before its own partial and
+ * passes it to rank k+1; rank n-1 completes the frame and sends the colour to
+ * dest_rank.  Latency t_local + (n - 1) (t_transfer + t_merge).
+ * All ops; NCCL transport.  compose_stream_local: virtual ranks on one GPU.
+ */
+EQC_API int compose_stream(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                           const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                           int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream);
+EQC_API int compose_stream_local(int nranks, int n_local, const uint32_t *const *color,
+                                 const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                 int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                 void *stream);
 
 #ifdef __cplusplus
 }

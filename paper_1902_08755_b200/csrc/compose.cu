@@ -39,6 +39,10 @@ int eqc_blend_to_partial(int n, const uint32_t *const *color, int w, int h, int6
 int eqc_blend_partials(int n, const uint32_t *const *rg, const uint32_t *const *ba, int w, int h, int64_t pitch,
                        uint32_t background, uint32_t *out_c, uint32_t *out_rg, uint32_t *out_ba, int64_t out_pitch,
                        cudaStream_t s);
+// composite.cu: subpixel accumulation + averaging through packed sum planes (EQC_OP_AVERAGE)
+int eqc_average(bool local, int n, const uint32_t *const *src, const uint32_t *const *src_ba, int w, int h,
+                int64_t pitch, int total, uint32_t *out_c, uint32_t *out_rg, uint32_t *out_ba, int64_t out_pitch,
+                cudaStream_t s);
 
 namespace {
 
@@ -272,19 +276,26 @@ int alloc_common(RankState &r, const Geometry &g, size_t recv_rows, size_t band_
 int op_local(const Geometry &g, const uint32_t *const *color, const uint32_t *const *depth, uint32_t *out_c,
              uint32_t *out_d, cudaStream_t s) {
   if (g.op == EQC_OP_BLEND) return eqc_blend_to_partial(g.n_local, color, g.w, g.h, g.pitch, out_c, out_d, g.w, s);
+  if (g.op == EQC_OP_AVERAGE)
+    return eqc_average(true, g.n_local, color, nullptr, g.w, g.h, g.pitch, g.n * g.n_local, nullptr, out_c, out_d,
+                       g.w, s);
   return compositor_depth(g.n_local, color, depth, g.w, g.h, g.pitch, out_c, out_d, g.w, s);
 }
 // n partial (c, d) planes in rank order -> final colour (one rounding)
 int op_final(const Geometry &g, int n, const uint32_t *const *c, const uint32_t *const *d, int rows, uint32_t *out,
              int64_t opitch, cudaStream_t s) {
   if (g.op == EQC_OP_BLEND) return eqc_blend_partials(n, c, d, g.w, rows, g.w, 0u, out, nullptr, nullptr, opitch, s);
+  if (g.op == EQC_OP_AVERAGE)
+    return eqc_average(false, n, c, d, g.w, rows, g.w, g.n * g.n_local, out, nullptr, nullptr, opitch, s);
   return compositor_depth(n, c, d, g.w, rows, g.w, out, nullptr, opitch, s);
 }
-// 2 partials (back/low first) -> 1 partial (binary-swap rounds)
-int op_merge(const Geometry &g, const uint32_t *const *c, const uint32_t *const *d, int rows, uint32_t *out_c,
-             uint32_t *out_d, cudaStream_t s) {
-  if (g.op == EQC_OP_BLEND) return eqc_blend_partials(2, c, d, g.w, rows, g.w, 0u, nullptr, out_c, out_d, g.w, s);
-  return compositor_depth(2, c, d, g.w, rows, g.w, out_c, out_d, g.w, s);
+// k partials (back / lower ranks first) -> 1 partial (swap rounds, folds)
+int op_merge(const Geometry &g, int k, const uint32_t *const *c, const uint32_t *const *d, int rows,
+             uint32_t *out_c, uint32_t *out_d, cudaStream_t s) {
+  if (g.op == EQC_OP_BLEND) return eqc_blend_partials(k, c, d, g.w, rows, g.w, 0u, nullptr, out_c, out_d, g.w, s);
+  if (g.op == EQC_OP_AVERAGE)
+    return eqc_average(false, k, c, d, g.w, rows, g.w, g.n * g.n_local, nullptr, out_c, out_d, g.w, s);
+  return compositor_depth(k, c, d, g.w, rows, g.w, out_c, out_d, g.w, s);
 }
 
 int local_precomposite(RankState &r, const Geometry &g, cudaStream_t s) {
@@ -303,7 +314,7 @@ int encode_band(RankState &r, const Geometry &g, int slot, const uint32_t *c, co
                 int64_t cap, cudaStream_t s) {
   const uint32_t *src[2] = {c, d};
   int kinds[2] = {EQC_KIND_RGBA8, EQC_KIND_DEPTH32};
-  int flags[2] = {g.op == EQC_OP_BLEND ? 0 : EQC_FLAG_SWIZZLE, 0};  // unorm16 planes: plain byte planes
+  int flags[2] = {g.op != EQC_OP_DEPTH ? 0 : EQC_FLAG_SWIZZLE, 0};  // 16-bit planes: plain byte planes
   uint8_t *dst[2] = {r.enc.as<uint8_t>() + (size_t)(2 * slot) * cap,
                      r.enc.as<uint8_t>() + (size_t)(2 * slot + 1) * cap};
   return image_compress_rle_batch(2, src, g.w, rows, g.w, kinds, flags, dst, cap,
@@ -551,7 +562,7 @@ int run_direct_send(std::vector<RankState *> &ranks, Geometry &g, Transport &T, 
 int bs_alloc(RankState &r, const Geometry &g) {
   const int half = (g.h + 1) / 2;
   EQC_TRY(alloc_common(r, g, std::max(half, g.out_pitch != g.w && r.rank == g.dest ? g.h : 0),
-                       g.op == EQC_OP_BLEND ? half : 1, 2));
+                       g.op != EQC_OP_DEPTH ? half : 1, 2));
   if (g.flags & EQC_FLAG_RLE) {
     const int64_t cap = band_cap(g, half);
     EQC_TRY(r.enc.ensure((size_t)2 * cap));
@@ -649,7 +660,7 @@ int run_binary_swap(std::vector<RankState *> &ranks, Geometry &g, Transport &T, 
       const uint32_t *c[2] = {b.low ? mine_c : their_c, b.low ? their_c : mine_c};
       const uint32_t *d[2] = {b.low ? mine_d : their_d, b.low ? their_d : mine_d};
       const int nxt = r.cur ^ 1;
-      EQC_TRY(op_merge(g, c, d, krows, r.part_c[nxt].as<uint32_t>() + off, r.part_d[nxt].as<uint32_t>() + off, s));
+      EQC_TRY(op_merge(g, 2, c, d, krows, r.part_c[nxt].as<uint32_t>() + off, r.part_d[nxt].as<uint32_t>() + off, s));
       r.cur = nxt;
     }
   }
@@ -658,9 +669,9 @@ int run_binary_swap(std::vector<RankState *> &ranks, Geometry &g, Transport &T, 
   // the final region's colour: the depth partial's colour plane, or the blend
   // partial rounded once to RGBA8 (over a transparent background) in fin_c
   auto final_colour = [&](RankState *r, int y0) -> const uint32_t * {
-    return g.op == EQC_OP_BLEND ? r->fin_c.as<uint32_t>() : r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w;
+    return g.op != EQC_OP_DEPTH ? r->fin_c.as<uint32_t>() : r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w;
   };
-  if (g.op == EQC_OP_BLEND) {
+  if (g.op != EQC_OP_DEPTH) {
     for (RankState *r : ranks) {
       int y0, y1;
       region(r->rank, y0, y1);
@@ -763,7 +774,7 @@ int plan_swap23(int h, int n, int rank, S23Plan &P) {
 int s23_alloc(RankState &r, const Geometry &g) {
   // part ping-pong buffers (full frame), two receive slots of up to h rows
   // (the fold moves a whole frame), final colour region of up to h rows
-  EQC_TRY(alloc_common(r, g, (size_t)2 * g.h, g.op == EQC_OP_BLEND ? g.h : 1, 2));
+  EQC_TRY(alloc_common(r, g, (size_t)2 * g.h, g.op != EQC_OP_DEPTH ? g.h : 1, 2));
   if (g.flags & EQC_FLAG_RLE) {
     const int64_t cap = band_cap(g, g.h);
     EQC_TRY(r.enc.ensure((size_t)4 * cap));  // 2 outgoing parts x (c, d) streams
@@ -884,7 +895,7 @@ int run_swap23(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaS
         const uint32_t *c[2] = {r.part_c[r.cur].as<uint32_t>(), r.recv_c.as<uint32_t>()};
         const uint32_t *d[2] = {r.part_d[r.cur].as<uint32_t>(), r.recv_d.as<uint32_t>()};
         const int nxt = r.cur ^ 1;
-        EQC_TRY(op_merge(g, c, d, g.h, r.part_c[nxt].as<uint32_t>(), r.part_d[nxt].as<uint32_t>(), s));
+        EQC_TRY(op_merge(g, 2, c, d, g.h, r.part_c[nxt].as<uint32_t>(), r.part_d[nxt].as<uint32_t>(), s));
         r.cur = nxt;
       }
     }
@@ -927,10 +938,7 @@ int run_swap23(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaS
         }
       }
       uint32_t *oc = r.part_c[nxt].as<uint32_t>() + off, *od = r.part_d[nxt].as<uint32_t>() + off;
-      if (g.op == EQC_OP_BLEND)
-        EQC_TRY(eqc_blend_partials(R.k, c, d, g.w, rows, g.w, 0u, nullptr, oc, od, g.w, s));
-      else
-        EQC_TRY(compositor_depth(R.k, c, d, g.w, rows, g.w, oc, od, g.w, s));
+      EQC_TRY(op_merge(g, R.k, c, d, rows, oc, od, s));
       r.cur = nxt;
     }
   }
@@ -942,13 +950,13 @@ int run_swap23(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaS
     y1 = P.fy1;
   };
   auto final_colour = [&](RankState *r, int y0) -> const uint32_t * {
-    return g.op == EQC_OP_BLEND ? r->fin_c.as<uint32_t>() : r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w;
+    return g.op != EQC_OP_DEPTH ? r->fin_c.as<uint32_t>() : r->part_c[r->cur].as<uint32_t>() + (size_t)y0 * g.w;
   };
   for (RankState *r : ranks) {
     int y0, y1;
     region(r->rank, y0, y1);
     if (y1 <= y0) continue;
-    if (g.op == EQC_OP_BLEND) {
+    if (g.op != EQC_OP_DEPTH) {
       const size_t off = (size_t)y0 * g.w;
       const uint32_t *c[1] = {r->part_c[r->cur].as<uint32_t>() + off}, *d[1] = {r->part_d[r->cur].as<uint32_t>() + off};
       EQC_TRY(op_final(g, 1, c, d, y1 - y0, r->fin_c.as<uint32_t>(), g.w, s));
@@ -974,10 +982,75 @@ int run_swap23(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaS
   return EQC_OK;
 }
 
+// ---- streaming sort-last chain --------------------
+// "The output of one source channel is copied to the next channel in the
+// chain, which then composites it on top of its own rendering, streaming the
+// combined frame on to the next source.  At the end of the chain, the
+// destination channel completes the input frame".  Rank k receives the
+// partial of ranks 0..k-1 (whole frame; raw or RLE), merges it with its own
+// partial (received = lower ranks = back first) and passes it on; rank n-1
+// finishes the frame and sends the colour to dest_rank.  Latency
+// t_local + (n - 1) (t_transfer + t_merge).
+int run_stream(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaStream_t s) {
+  for (RankState *r : ranks) {
+    for (int i = 0; i < 4; ++i) r->stats[i] = 0;
+    EQC_TRY(s23_alloc(*r, g));
+    EQC_TRY(r->fin_c.ensure(frame_bytes(g, g.h)));
+    EQC_TRY(local_precomposite(*r, g, s));
+  }
+  for (int hop = 0; hop + 1 < g.n; ++hop) {
+    std::vector<std::vector<S23Msg>> snd(ranks.size()), rcv(ranks.size());
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      if (ranks[i]->rank == hop) snd[i].push_back(S23Msg{hop + 1, 0, g.h});
+      if (ranks[i]->rank == hop + 1) rcv[i].push_back(S23Msg{hop, 0, g.h});
+    }
+    EQC_TRY(s23_exchange(ranks, g, T, snd, rcv, s));
+    for (RankState *r : ranks) {
+      if (r->rank != hop + 1) continue;
+      const uint32_t *c[2] = {r->recv_c.as<uint32_t>(), r->part_c[r->cur].as<uint32_t>()};
+      const uint32_t *d[2] = {r->recv_d.as<uint32_t>(), r->part_d[r->cur].as<uint32_t>()};
+      const int nxt = r->cur ^ 1;
+      EQC_TRY(op_merge(g, 2, c, d, g.h, r->part_c[nxt].as<uint32_t>(), r->part_d[nxt].as<uint32_t>(), s));
+      r->cur = nxt;
+    }
+  }
+  // the end of the chain completes the frame; its colour goes to the destination
+  const int last = g.n - 1;
+  const uint32_t *col_last = nullptr;
+  for (RankState *r : ranks) {
+    if (r->rank != last) continue;
+    col_last = r->part_c[r->cur].as<uint32_t>();
+    if (g.op != EQC_OP_DEPTH) {
+      const uint32_t *c[1] = {r->part_c[r->cur].as<uint32_t>()}, *d[1] = {r->part_d[r->cur].as<uint32_t>()};
+      EQC_TRY(op_final(g, 1, c, d, g.h, r->fin_c.as<uint32_t>(), g.w, s));
+      col_last = r->fin_c.as<uint32_t>();
+    }
+  }
+  if (last != g.dest) {  // every rank takes part in the (possibly empty) message group
+    EQC_TRY(T.start());
+    for (RankState *r : ranks) {
+      if (r->rank == last) {
+        EQC_TRY(T.send(*r, g.dest, col_last, frame_bytes(g, g.h)));
+        r->stats[1] += 1;
+      }
+      if (r->rank == g.dest) EQC_TRY(T.recv(*r, last, r->fin_c.as<uint32_t>(), frame_bytes(g, g.h)));
+    }
+    EQC_TRY(T.end());
+  }
+  for (RankState *r : ranks) {
+    if (r->rank != g.dest) continue;
+    const uint32_t *col = last == g.dest ? col_last : r->fin_c.as<uint32_t>();
+    EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out, g.out_pitch * 4, col, (size_t)g.w * 4, (size_t)g.w * 4, g.h,
+                                   cudaMemcpyDeviceToDevice, s));
+  }
+  return EQC_OK;
+}
+
 int validate(int nranks, int n_local, const void *color, const void *depth, int w, int h, int64_t pitch, int op,
              int flags, int dest, const void *out, int64_t out_pitch, bool is_dest) {
   if (nranks < 1 || n_local < 1 || n_local > EQC_MAX_SOURCES || nranks > EQC_MAX_SOURCES) return EQC_E_INVALID;
-  if (op != EQC_OP_DEPTH && op != EQC_OP_BLEND) return EQC_E_UNSUPPORTED;
+  if (op != EQC_OP_DEPTH && op != EQC_OP_BLEND && op != EQC_OP_AVERAGE) return EQC_E_UNSUPPORTED;
+  if (op == EQC_OP_AVERAGE && (int64_t)nranks * n_local > 256) return EQC_E_UNSUPPORTED;  // 16-bit sums
   if (!color || (op == EQC_OP_DEPTH && !depth) || w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
   if (flags & ~(EQC_FLAG_RLE | EQC_FLAG_NCCL | EQC_FLAG_ROI)) return EQC_E_INVALID;
   if (dest < 0 || dest >= nranks) return EQC_E_INVALID;
@@ -1275,7 +1348,7 @@ extern "C" int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max
   return k;
 }
 
-enum Algo { kDirectSend, kBinarySwap, kSwap23 };
+enum Algo { kDirectSend, kBinarySwap, kSwap23, kStream };
 
 static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *const *color,
                         const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags, int dest_rank,
@@ -1306,7 +1379,9 @@ static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *
   NcclTransport T(comm->nccl, s);
   std::vector<RankState *> ranks{&comm->st};
   return ds ? run_direct_send(ranks, g, T, s)
-            : algo == kBinarySwap ? run_binary_swap(ranks, g, T, s) : run_swap23(ranks, g, T, s);
+         : algo == kBinarySwap ? run_binary_swap(ranks, g, T, s)
+         : algo == kSwap23     ? run_swap23(ranks, g, T, s)
+                               : run_stream(ranks, g, T, s);
 }
 
 extern "C" int compose_direct_send(eqc_comm *comm, int n_local, const uint32_t *const *color,
@@ -1350,7 +1425,9 @@ static int compose_local(Algo algo, int nranks, int n_local, const uint32_t *con
   }
   LocalTransport T(s);
   int rc = algo == kDirectSend ? run_direct_send(ranks, g, T, s)
-           : algo == kBinarySwap ? run_binary_swap(ranks, g, T, s) : run_swap23(ranks, g, T, s);
+           : algo == kBinarySwap ? run_binary_swap(ranks, g, T, s)
+           : algo == kSwap23     ? run_swap23(ranks, g, T, s)
+                                 : run_stream(ranks, g, T, s);
   cudaStreamSynchronize(s);  // scratch is freed below
   if (out_stats) {
     for (int i = 0; i < 4; ++i) out_stats[i] = 0;
@@ -1413,4 +1490,19 @@ extern "C" int eqc_plan_swap23(int h, int n, int rank, int *out, int max_ints) {
     for (int u = 0; u < 4; ++u) o[5 + u] = R.bnd[u];
   }
   return k;
+}
+
+extern "C" int compose_stream(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                              const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                              int dest_rank, uint32_t *out_color, int64_t out_pitch, void *stream) {
+  return compose_nccl(kStream, comm, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
+                      stream);
+}
+
+extern "C" int compose_stream_local(int nranks, int n_local, const uint32_t *const *color,
+                                    const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                    int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                    void *stream) {
+  return compose_local(kStream, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color,
+                       out_pitch, out_stats, stream);
 }

@@ -687,6 +687,70 @@ __global__ void __launch_bounds__(256, 4) blend_partials_kernel(const __grid_con
   }
 }
 
+// ---- subpixel accumulation + averaging --------
+// Channel sums of RGBA8 sources held as two packed planes rg = R16 | G16 << 16,
+// ba = B16 | A16 << 16 (a sum of <= 64 bytes is <= 16320, so 32-bit adds of
+// packed planes never carry between halves: merging partial sums is a plain
+// add).  Final: per channel floor((2 sum + N) / (2 N)) (mean rounded half up,
+// R-C22), N = the total number of sources.
+struct AvgParams {
+  const uint32_t *src[EQC_MAX_SOURCES];  // RGBA8 layers (LOCAL) or rg planes (partials)
+  const uint32_t *src_ba[EQC_MAX_SOURCES];
+  uint32_t *out_c;            // FINAL
+  uint32_t *out_rg, *out_ba;  // !FINAL
+  int64_t pitch, out_pitch;
+  int n, w, h, groups_per_row;
+  uint32_t total;             // FINAL: N
+  float inv2n;                // 1 / (2 N)
+};
+
+// floor((2 sum + N) / (2 N)) without an integer divide: a = 2 sum + N < 2^24
+// is exact in fp32, a / 2N is either an integer k (the product may land a few
+// ulp below k) or at least 1/(2N) >= 1/512 below the next integer, so adding
+// 1e-4 before truncation is exact (fp32 error at <= 255 is ~1.5e-5).
+__device__ __forceinline__ uint32_t avg_round(uint32_t sum, uint32_t n, float inv2n) {
+  return (uint32_t)fmaf((float)(2 * sum + n), inv2n, 1e-4f);
+}
+
+// LOCAL: inputs are RGBA8 layers; else packed partial-sum planes.
+template <bool LOCAL, bool FINAL>
+__global__ void __launch_bounds__(256) average_kernel(const __grid_constant__ AvgParams p) {
+  const uint32_t total = (uint32_t)p.groups_per_row * (uint32_t)p.h;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int y = (int)(g / (uint32_t)p.groups_per_row);
+    const int x = (int)(g - (uint32_t)y * (uint32_t)p.groups_per_row) * 4;
+    const int64_t off = (int64_t)y * p.pitch + x;
+    const int cnt = min(4, p.w - x);
+    uint32_t rg[4] = {0, 0, 0, 0}, ba[4] = {0, 0, 0, 0};
+    for (int k = 0; k < p.n; ++k) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= cnt) continue;
+        if (LOCAL) {
+          const uint32_t v = ld_stream_u32(p.src[k] + off + j);
+          rg[j] += __byte_perm(v, 0u, 0x4140);  // [R, 0, G, 0]
+          ba[j] += __byte_perm(v, 0u, 0x4342);  // [B, 0, A, 0]
+        } else {
+          rg[j] += ld_stream_u32(p.src[k] + off + j);
+          ba[j] += ld_stream_u32(p.src_ba[k] + off + j);
+        }
+      }
+    }
+    const int64_t ooff = (int64_t)y * p.out_pitch + x;
+    for (int j = 0; j < cnt; ++j) {
+      if (FINAL) {
+        p.out_c[ooff + j] = avg_round(rg[j] & 0xFFFFu, p.total, p.inv2n) |
+                            (avg_round(rg[j] >> 16, p.total, p.inv2n) << 8) |
+                            (avg_round(ba[j] & 0xFFFFu, p.total, p.inv2n) << 16) |
+                            (avg_round(ba[j] >> 16, p.total, p.inv2n) << 24);
+      } else {
+        p.out_rg[ooff + j] = rg[j];
+        p.out_ba[ooff + j] = ba[j];
+      }
+    }
+  }
+}
+
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 // Grid of a grid-stride kernel over `items` 4-pixel groups: one group per
@@ -842,6 +906,53 @@ int eqc_blend_partials(int n, const uint32_t *const *rg, const uint32_t *const *
       blend_partials_kernel<false, false><<<grid_for(groups), 256, 0, s>>>(p);
   }
   return eqc_launch_status();
+}
+
+// Internal (compose.cu, EQC_OP_AVERAGE) and compositor_average: `local`:
+// src = n RGBA8 layers, else n partial-sum plane pairs (src, src_ba).  FINAL
+// (out_c != NULL): mean over `total` sources, else partial-sum planes out.
+int eqc_average(bool local, int n, const uint32_t *const *src, const uint32_t *const *src_ba, int w, int h,
+                int64_t pitch, int total, uint32_t *out_c, uint32_t *out_rg, uint32_t *out_ba, int64_t out_pitch,
+                cudaStream_t s) {
+  if (n < 1 || n > EQC_MAX_SOURCES || !src || (!local && !src_ba) || (!out_c && (!out_rg || !out_ba)))
+    return EQC_E_INVALID;
+  if (w <= 0 || h <= 0 || pitch < w || out_pitch < w || total < 1 || total > 256) return EQC_E_INVALID;
+  AvgParams p;
+  for (int k = 0; k < n; ++k) {
+    if (!src[k] || (!local && !src_ba[k])) return EQC_E_INVALID;
+    p.src[k] = src[k];
+    p.src_ba[k] = local ? nullptr : src_ba[k];
+  }
+  p.out_c = out_c;
+  p.out_rg = out_rg;
+  p.out_ba = out_ba;
+  p.pitch = pitch;
+  p.out_pitch = out_pitch;
+  p.n = n;
+  p.w = w;
+  p.h = h;
+  p.groups_per_row = (w + 3) / 4;
+  p.total = (uint32_t)total;
+  p.inv2n = 1.0f / (2.0f * (float)total);
+  const int64_t groups = (int64_t)p.groups_per_row * h;
+  if (groups > 0x7FFFFFFFll) return EQC_E_INVALID;
+  const int grid = grid_for(groups);
+  if (local && out_c)
+    average_kernel<true, true><<<grid, 256, 0, s>>>(p);
+  else if (local)
+    average_kernel<true, false><<<grid, 256, 0, s>>>(p);
+  else if (out_c)
+    average_kernel<false, true><<<grid, 256, 0, s>>>(p);
+  else
+    average_kernel<false, false><<<grid, 256, 0, s>>>(p);
+  return eqc_launch_status();
+}
+
+extern "C" int compositor_average(int n, const uint32_t *const *color, int w, int h, int64_t pitch,
+                                  uint32_t *out_color, int64_t out_pitch, void *stream) {
+  if (!out_color) return EQC_E_INVALID;
+  return eqc_average(true, n, color, nullptr, w, h, pitch, n, out_color, nullptr, nullptr, out_pitch,
+                     (cudaStream_t)stream);
 }
 
 extern "C" int compositor_blend_ordered(int n, const uint32_t *const *color, const int32_t *order,

@@ -24,6 +24,7 @@ FLAG_SWIZZLE = 1
 UNIQUE_ID_BYTES = 128
 OP_DEPTH = 0
 OP_BLEND = 1
+OP_AVERAGE = 2
 FLAG_RLE = 1
 FLAG_NCCL = 2
 FLAG_ROI = 4
@@ -48,6 +49,7 @@ def _load():
         "compositor_depth": ([i32, P, P, i32, i32, i64, P, P, i64, P], i32),
         "compositor_blend_ordered": ([i32, P, P, i32, i32, i64, u32, P, i64, P], i32),
         "image_roi": ([i32, P, i32, i32, i64, u32, P, P], i32),
+        "compositor_average": ([i32, P, i32, i32, i64, P, i64, P], i32),
         "compositor_depth_roi": ([i32, P, P, P, i32, i32, i64, P, P, i64, P], i32),
         "compositor_blend_ordered_roi": ([i32, P, P, P, i32, i32, i64, u32, P, i64, P], i32),
         "image_rle_max_size": ([i32, i32], i64),
@@ -72,6 +74,8 @@ def _load():
         "compose_swap23": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
         "compose_swap23_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
         "eqc_plan_swap23": ([i32, i32, i32, P, i32], i32),
+        "compose_stream": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
+        "compose_stream_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -148,6 +152,15 @@ def compositor_blend_ordered(colors, out_color, order=None, background: int = 0,
     rc = _lib.compositor_blend_ordered(n, _ptrs(colors), ordp, w, h, pitch, int(background) & 0xFFFFFFFF,
                                        _addr(out_color), opitch, _stream(stream))
     return _check(rc, "compositor_blend_ordered")
+
+
+def compositor_average(colors, out_color, stream=None):
+    """Subpixel accumulation + averaging: per-channel mean, rounded half up."""
+    n = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    _, _, opitch = _frame_geom(out_color)
+    rc = _lib.compositor_average(n, _ptrs(colors), w, h, pitch, _addr(out_color), opitch, _stream(stream))
+    return _check(rc, "compositor_average")
 
 
 def image_roi(frames, d_roi, background: int, stream=None):
@@ -376,3 +389,16 @@ def eqc_plan_swap23(h: int, n: int, rank: int):
         rounds.append({"k": o[0], "t": o[1], "members": [m for m in o[2:5] if m >= 0][:o[0]],
                        "bounds": o[5:6 + o[0]]})
     return {"fold_role": v[0], "fold_partner": v[1], "final": (v[3], v[4]), "rounds": rounds}
+
+
+def compose_stream(comm, colors, depths, out_color=None, dest_rank: int = 0, flags: int = 0,
+                   op: int = OP_DEPTH, stream=None):
+    """Streaming sort-last chain 0 -> 1 -> ... -> n-1."""
+    return _compose(_lib.compose_stream, "compose_stream", comm, colors, depths, out_color, dest_rank,
+                    flags, op, stream)
+
+
+def compose_stream_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
+                         op: int = OP_DEPTH, stream=None):
+    return _compose_local(_lib.compose_stream_local, "compose_stream_local", nranks, colors, depths,
+                          out_color, dest_rank, flags, op, stream)

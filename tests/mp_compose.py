@@ -38,6 +38,8 @@ def main():
         cases += [("bs", 2, 640, 361, 0, 0), ("bs", 1, 300, 41, world - 1, R), ("bs", 2, 1920, 1080, 0, R)]
     # 2-3 swap (any rank count, R-C21)
     cases += [("s23", 2, 640, 361, 0, 0), ("s23", 1, 300, 41, world - 1, R), ("s23", 2, 1920, 1080, 1 % world, 0)]
+    # streaming chain
+    cases += [("st", 2, 640, 361, 0, 0), ("st", 1, 300, 41, world - 1, R)]
     # config c4 (8 sources of 7680x4320 over the ranks), checked on sampled rows
     if 8 % world == 0:
         cases += [("ds", 8 // world, 7680, 4320, 0, 0), ("ds", 8 // world, 7680, 4320, 0, R)]
@@ -55,7 +57,8 @@ def main():
         dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
         dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
         out = torch.zeros((h, w), dtype=torch.int32, device=dev)
-        fn = {"ds": eqc.compose_direct_send, "bs": eqc.compose_binary_swap, "s23": eqc.compose_swap23}[algo]
+        fn = {"ds": eqc.compose_direct_send, "bs": eqc.compose_binary_swap, "s23": eqc.compose_swap23,
+              "st": eqc.compose_stream}[algo]
         for _ in range(2):  # the second call reuses the communicator's scratch
             fn(comm, dc, dd, out if rank == dest else None, dest_rank=dest, flags=rle)
         torch.cuda.synchronize()
@@ -80,7 +83,7 @@ def main():
     bcases = [("ds", 4, 640, 361, 0, 0), ("ds", 2, 300, 41, world - 1, X), ("ds", 3, 320, 181, 1 % world, R)]
     if world & (world - 1) == 0:
         bcases += [("bs", 4, 640, 361, 0, 0), ("bs", 2, 300, 41, world - 1, R)]
-    bcases += [("s23", 3, 640, 361, 0, 0), ("s23", 2, 300, 41, world - 1, R)]
+    bcases += [("s23", 3, 640, 361, 0, 0), ("s23", 2, 300, 41, world - 1, R), ("st", 2, 320, 181, 0, 0)]
     if 16 % world == 0:  # config c3: 16 bricks of 3840x2160, sampled rows
         bcases += [("ds", 16 // world, 3840, 2160, 0, 0)]
     for algo, nl, w, h, dest, fl in bcases:
@@ -89,7 +92,8 @@ def main():
         mine = range(rank * nl, (rank + 1) * nl)
         dl = [torch.from_numpy(layers[i].view(np.int32)).to(dev) for i in mine]
         out = torch.zeros((h, w), dtype=torch.int32, device=dev)
-        fn = {"ds": eqc.compose_direct_send, "bs": eqc.compose_binary_swap, "s23": eqc.compose_swap23}[algo]
+        fn = {"ds": eqc.compose_direct_send, "bs": eqc.compose_binary_swap, "s23": eqc.compose_swap23,
+              "st": eqc.compose_stream}[algo]
         for _ in range(2):
             fn(comm, dl, None, out if rank == dest else None, dest_rank=dest, flags=fl, op=eqc.OP_BLEND)
         torch.cuda.synchronize()
@@ -100,6 +104,21 @@ def main():
             diff = np.abs(got[rows].view(np.uint8).astype(int) - want.view(np.uint8).astype(int)).max()
             if diff > 1:
                 failures.append(f"blend {algo} nl={nl} {w}x{h} flags={fl}: max error {diff} LSB")
+        dist.barrier()
+    # EQC_OP_AVERAGE (subpixel accumulation + averaging): bit-exact
+    for algo, nl, w, h, dest, fl in [("ds", 2, 640, 361, 0, 0), ("ds", 3, 300, 41, world - 1, R),
+                                     ("s23", 2, 320, 181, 0, 0), ("st", 2, 320, 181, 1 % world, R)]:
+        N = world * nl
+        c, _ = synth.random_frames(600 + N + w, N, w, h)
+        mine = range(rank * nl, (rank + 1) * nl)
+        dl = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
+        out = torch.zeros((h, w), dtype=torch.int32, device=dev)
+        fn = {"ds": eqc.compose_direct_send, "s23": eqc.compose_swap23, "st": eqc.compose_stream}[algo]
+        for _ in range(2):
+            fn(comm, dl, None, out if rank == dest else None, dest_rank=dest, flags=fl, op=eqc.OP_AVERAGE)
+        torch.cuda.synchronize()
+        if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.average(c)).all():
+            failures.append(f"average {algo} nl={nl} {w}x{h} flags={fl}: mismatch")
         dist.barrier()
     comm.destroy()
     t = torch.tensor([len(failures)], device=dev)
