@@ -66,7 +66,8 @@ def main():
     if n & (n - 1) == 0:
         variants += [("binary_swap_nccl", eqc.compose_binary_swap, 0),
                      ("binary_swap_rle", eqc.compose_binary_swap, eqc.FLAG_RLE)]
-    variants += [("swap23_nccl", eqc.compose_swap23, 0), ("swap23_rle", eqc.compose_swap23, eqc.FLAG_RLE)]
+    variants += [("swap23_nccl", eqc.compose_swap23, 0), ("swap23_rle", eqc.compose_swap23, eqc.FLAG_RLE),
+                 ("stream_nccl", eqc.compose_stream, 0)]
     op = eqc.OP_BLEND if blend else eqc.OP_DEPTH
     if blend:
         variants = [v for v in variants if "roi" not in v[0]]

@@ -30,3 +30,6 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=3 --mast
   scripts/bench_compose.py --sources 6 > gpurun_out/compose_c4s6_n3.json 2> gpurun_out/compose_c4s6_n3.log
 cat gpurun_out/compose_c4s6_n3.json
 fi
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29517 \
+  scripts/bench_stream.py > gpurun_out/stream_n${N}.json 2> gpurun_out/stream_n${N}.log
+cat gpurun_out/stream_n${N}.json
