@@ -71,6 +71,12 @@ def lib():
         L.or_blend_ordered_roi.restype = i32
         L.or_average.argtypes = [i32, P, i32, i32, i64, P, i64]
         L.or_average.restype = None
+        L.or_rle64_encode_chunk.argtypes = [P, i32, P]
+        L.or_rle64_encode_chunk.restype = i32
+        L.or_rle64_encode.argtypes = [P, i32, i32, i64, i32, P, i64]
+        L.or_rle64_encode.restype = i64
+        L.or_rle64_decode.argtypes = [P, i64, P, i64, i32, i32]
+        L.or_rle64_decode.restype = i32
         _lib = L
     return _lib
 
@@ -237,3 +243,32 @@ def average(colors):
     oc = np.empty((h, w), np.uint32)
     lib().or_average(n, _ptr_array(colors), w, h, pitch, _ptr(oc), w)
     return oc
+
+
+FLAG_RLE64 = 2
+
+
+def rle64_encode_chunk(pixels) -> bytes:
+    """RLE-64 record of one chunk of L <= 128 uint32 pixels (R-C17)."""
+    px = np.ascontiguousarray(np.asarray(pixels, dtype=np.uint32))
+    out = np.zeros(1 + 64 + 8 * 64, np.uint8)
+    n = lib().or_rle64_encode_chunk(_ptr(px), len(px), _ptr(out))
+    return out[:n].tobytes()
+
+
+def rle64_encode(img: np.ndarray, kind: int = KIND_RGBA8) -> bytes:
+    assert img.dtype == np.uint32 and img.ndim == 2 and img.strides[1] == 4
+    h, w = img.shape
+    cap = rle_max_size(w, h, 7)
+    out = np.empty(cap, np.uint8)
+    n = lib().or_rle64_encode(_ptr(img), w, h, img.strides[0] // 4, kind, _ptr(out), cap)
+    if n < 0:
+        raise ValueError(f"or_rle64_encode failed: {n}")
+    return out[:n].tobytes()
+
+
+def rle64_decode(stream: bytes, w: int, h: int):
+    buf = np.frombuffer(bytes(stream), np.uint8).copy() if len(stream) else np.zeros(1, np.uint8)
+    out = np.zeros((h, w), np.uint32)
+    rc = lib().or_rle64_decode(_ptr(buf), len(stream), _ptr(out), w, w, h)
+    return rc, out

@@ -26,6 +26,10 @@
  *                        dataset is unavailable).
  *   or_roi               pinned: numpy nonzero bounding boxes, empty / single
  *                        pixel / full frames.
+ *   or_rle64_*           pinned: hand-derived record bytes (tests/golden),
+ *                        round trips, canonical-form checker (maximal runs,
+ *                        literal spans never hold a run of 2), size bound,
+ *                        corrupt-stream rejection.
  *   or_average           pinned: numpy integer mean with explicit half-up
  *                        rounding, n = 1 identity, equal sources, permutation
  *                        invariance, exact .5 ties rounding up.
@@ -519,4 +523,153 @@ void or_average(int n, const uint32_t *const *color, int w, int h, int64_t pitch
       out_color[(int64_t)y * out_pitch + x] = o;
     }
   }
+}
+
+/* ------------------------------------------------------------------------ */
+/* RLE-64: the basic 64-bit token codec (reading R-C17)   */
+/* ------------------------------------------------------------------------ */
+/*
+ * "a fast 64-bit version comparing two pixels at the same time
+ * (8 bit per channel RGBA format) ... it can only compress adjacent pixels of
+ * the same colour".  Reading R-C17 (wire format in DESIGN.md section 5): the
+ * stream is RLE-BP v1's (same header, chunking and table) with header flags
+ * = EQC_FLAG_RLE64 (2).  A chunk of L pixels is U = ceil(L / 2) 64-bit units,
+ * unit u = pixel 2u | pixel 2u+1 << 32 (for odd L the last unit's high half
+ * is 0).  Maximal runs of >= 2 equal units become REPEAT tokens (ctrl = 0x80 |
+ * (len - 1), payload = the unit, 8 bytes little-endian); each maximal span of
+ * other units becomes one LITERAL token (ctrl = len - 1, payload = the
+ * units).  Record = [ntok u8][ctrl x ntok][payloads]; the table entry's
+ * second word is the record size (u32) instead of four plane sizes.
+ */
+static uint64_t unit64(const uint32_t *row, int L, int u) {
+  uint64_t lo = row[2 * u];
+  uint64_t hi = (2 * u + 1 < L) ? row[2 * u + 1] : 0u;
+  return lo | (hi << 32);
+}
+
+static void put_u64le(uint8_t *d, uint64_t v) {
+  for (int b = 0; b < 8; ++b) d[b] = (uint8_t)(v >> (8 * b));
+}
+
+/* Encode one chunk (row pointer, L pixels); returns the record size. */
+int or_rle64_encode_chunk(const uint32_t *row, int L, uint8_t *out) {
+  int U = (L + 1) / 2;
+  uint8_t ctrl[64];
+  uint8_t pay[8 * 64];
+  int ntok = 0, np = 0, i = 0;
+  while (i < U) {
+    uint64_t v = unit64(row, L, i);
+    int j = i + 1;
+    while (j < U && unit64(row, L, j) == v) ++j;
+    if (j - i >= 2) { /* REPEAT */
+      ctrl[ntok++] = (uint8_t)(0x80 | (j - i - 1));
+      put_u64le(pay + np, v);
+      np += 8;
+      i = j;
+    } else { /* LITERAL: up to the start of the next run of >= 2 */
+      int s = i;
+      while (i < U && !(i + 1 < U && unit64(row, L, i + 1) == unit64(row, L, i))) {
+        put_u64le(pay + np, unit64(row, L, i));
+        np += 8;
+        ++i;
+      }
+      ctrl[ntok++] = (uint8_t)(i - s - 1);
+    }
+  }
+  out[0] = (uint8_t)ntok;
+  memcpy(out + 1, ctrl, (size_t)ntok);
+  memcpy(out + 1 + ntok, pay, (size_t)np);
+  return 1 + ntok + np;
+}
+
+int64_t or_rle64_encode(const uint32_t *src, int w, int h, int64_t pitch, int kind, uint8_t *dst, int64_t cap) {
+  if (!src || !dst || w <= 0 || h <= 0 || pitch < w) return OR_E_INVALID;
+  if (kind != 0 && kind != 1) return OR_E_INVALID;
+  const int C = 128, log2c = 7;
+  int S = (w + C - 1) / C;
+  int64_t nchunks = (int64_t)S * h;
+  int64_t payload0 = 32 + 8 * nchunks;
+  if (cap < payload0) return OR_E_CAPACITY;
+  uint8_t rec[1 + 64 + 8 * 64];
+  int64_t off = 0;
+  for (int y = 0; y < h; ++y) {
+    for (int k = 0; k < S; ++k) {
+      int x0 = k * C;
+      int L = (w - x0 < C) ? (w - x0) : C;
+      int sz = or_rle64_encode_chunk(src + (int64_t)y * pitch + x0, L, rec);
+      int64_t chunk_id = (int64_t)y * S + k;
+      if (off > 0xFFFFFFFFll) return OR_E_INVALID;
+      if (payload0 + off + sz > cap) return OR_E_CAPACITY;
+      put_u32(dst + 32 + 8 * chunk_id, (uint32_t)off);
+      put_u32(dst + 32 + 8 * chunk_id + 4, (uint32_t)sz);
+      memcpy(dst + payload0 + off, rec, (size_t)sz);
+      off += sz;
+    }
+  }
+  put_u32(dst + 0, RLE_MAGIC);
+  dst[4] = RLE_VERSION;
+  dst[5] = (uint8_t)kind;
+  dst[6] = 2; /* EQC_FLAG_RLE64 */
+  dst[7] = (uint8_t)log2c;
+  put_u32(dst + 8, (uint32_t)w);
+  put_u32(dst + 12, (uint32_t)h);
+  put_u32(dst + 16, (uint32_t)nchunks);
+  put_u32(dst + 20, 0);
+  put_u64(dst + 24, (uint64_t)off);
+  return payload0 + off;
+}
+
+/* Exact inverse with validation (OR_E_CORRUPT on any inconsistency). */
+int or_rle64_decode(const uint8_t *src, int64_t src_bytes, uint32_t *dst, int64_t pitch, int w, int h) {
+  if (!src || !dst || w <= 0 || h <= 0 || pitch < w) return OR_E_INVALID;
+  if (src_bytes < 32) return OR_E_CORRUPT;
+  if (get_u32(src) != RLE_MAGIC || src[4] != RLE_VERSION || src[5] > 1 || src[6] != 2 || src[7] != 7)
+    return OR_E_CORRUPT;
+  if ((int64_t)get_u32(src + 8) != w || (int64_t)get_u32(src + 12) != h) return OR_E_CORRUPT;
+  const int C = 128;
+  int S = (w + C - 1) / C;
+  int64_t nchunks = (int64_t)S * h;
+  if ((int64_t)get_u32(src + 16) != nchunks || get_u32(src + 20) != 0) return OR_E_CORRUPT;
+  uint64_t pbytes = get_u64(src + 24);
+  int64_t payload0 = 32 + 8 * nchunks;
+  if (src_bytes < payload0 || (uint64_t)(src_bytes - payload0) < pbytes) return OR_E_CORRUPT;
+  uint64_t expect = 0;
+  for (int y = 0; y < h; ++y) {
+    for (int k = 0; k < S; ++k) {
+      int x0 = k * C;
+      int L = (w - x0 < C) ? (w - x0) : C;
+      int U = (L + 1) / 2;
+      int64_t chunk_id = (int64_t)y * S + k;
+      uint64_t off = get_u32(src + 32 + 8 * chunk_id);
+      uint64_t size = get_u32(src + 32 + 8 * chunk_id + 4);
+      if (off != expect || size < 2 || off + size > pbytes) return OR_E_CORRUPT;
+      const uint8_t *r = src + payload0 + off;
+      int ntok = r[0];
+      if (ntok < 1 || (uint64_t)(1 + ntok) > size) return OR_E_CORRUPT;
+      uint64_t p = 1 + (uint64_t)ntok;
+      int u = 0;
+      uint32_t *row = dst + (int64_t)y * pitch + x0;
+      for (int t = 0; t < ntok; ++t) {
+        int c = r[1 + t];
+        int len = (c & 0x7F) + 1;
+        if (u + len > U) return OR_E_CORRUPT;
+        for (int q = 0; q < len; ++q) {
+          uint64_t pp = p + ((c & 0x80) ? 0 : 8 * (uint64_t)q);
+          if (pp + 8 > size) return OR_E_CORRUPT;
+          uint64_t v = 0;
+          for (int b = 0; b < 8; ++b) v |= (uint64_t)r[pp + b] << (8 * b);
+          int px = 2 * (u + q);
+          row[px] = (uint32_t)v;
+          if (px + 1 < L) row[px + 1] = (uint32_t)(v >> 32);
+          else if ((v >> 32) != 0) return OR_E_CORRUPT; /* canonical padding */
+        }
+        p += (c & 0x80) ? 8 : 8 * (uint64_t)len;
+        u += len;
+      }
+      if (u != U || p != size) return OR_E_CORRUPT;
+      expect = off + size;
+    }
+  }
+  if (expect != pbytes) return OR_E_CORRUPT;
+  return OR_OK;
 }
