@@ -60,6 +60,8 @@ extern "C" {
 #define EQC_KIND_RGBA8 0       /* RLE kind: colour */
 #define EQC_KIND_DEPTH32 1     /* RLE kind: depth */
 #define EQC_FLAG_SWIZZLE 1     /* RLE flag: bit-swizzle preconditioner (colour only, R-C11) */
+#define EQC_FLAG_RLE64 2       /* RLE flag: the basic 64-bit token codec (pixel pairs, R-C17);
+                                  exclusive with EQC_FLAG_SWIZZLE; one codec per encode batch */
 
 /* Human-readable name of an EQC_* code (static string, never NULL). */
 EQC_API const char *eqc_strerror(int code);

@@ -167,7 +167,11 @@ struct EncSmem {
 //  C. write the constant chunks' 12-byte records lane-parallel and the
 //     table entries.
 // The compaction kernel then moves the runs to their final offsets.
+// R64: the RLE-64 codec (R-C17); constant chunks (all 128 pixels equal) get a
+// 10-byte record [1][0x80 | 63][v v] instead of four 3-byte planes.
+template <bool R64>
 __global__ void __launch_bounds__(kEncWarps * 32, EQC_ENC_MINB) rle_encode_kernel(const __grid_constant__ EncParams p) {
+  constexpr int kCRec = R64 ? 10 : 12;  // record bytes of a constant chunk
   extern __shared__ __align__(16) uint8_t smem_raw[];
   EncSmem &sm = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(kEncWarps * 32, EQC_ENC_MINB) rle_encode_kerne
       for (int u = 0; u < 4; ++u) {
         if (j0 + u >= cnt) break;
         uint32_t v0;
-        const bool cst = chunk_is_constant(px[u], Ls[u], lane, v0);
+        const bool cst = chunk_is_constant(px[u], Ls[u], lane, v0) && (!R64 || (Ls[u] & 1) == 0);
         if (cst) {
           cmask |= 1ull << (j0 + u);
           if (lane == 0) W.cval[j0 + u] = v0;
@@ -269,8 +273,9 @@ __global__ void __launch_bounds__(kEncWarps * 32, EQC_ENC_MINB) rle_encode_kerne
     const int L = Ln;
     const int j = W.gidx[g];
     if (g + 1 < ng) load_chunk(chunk_ptr(W.gidx[g + 1], Ln), Ln, lane, p.vec != 0, nxt);
-    const EncodeOut eo = encode_chunk(px, L, lane, swz, W.stage, W.toks);
-    const int off = 12 * __popcll(cmask & ((1ull << j) - 1)) + gen_bytes;
+    const EncodeOut eo = R64 ? encode_chunk64(px, L, lane, W.stage, W.toks)
+                             : encode_chunk(px, L, lane, swz, W.stage, W.toks);
+    const int off = kCRec * __popcll(cmask & ((1ull << j) - 1)) + gen_bytes;
     store_record(scr + off, W.stage, eo.size, lane);
     if (lane == 0) {
       W.csize[j] = (uint16_t)eo.size;
@@ -282,15 +287,16 @@ __global__ void __launch_bounds__(kEncWarps * 32, EQC_ENC_MINB) rle_encode_kerne
   // ---- C: offsets of all chunks, constant records, table entries
   const int j1 = lane, j2 = lane + 32;
   const bool cst1 = j1 < cnt && ((cmask >> j1) & 1ull), cst2 = j2 < cnt && ((cmask >> j2) & 1ull);
-  const int s1 = j1 < cnt ? (cst1 ? 12 : (int)W.csize[j1]) : 0;
-  const int s2 = j2 < cnt ? (cst2 ? 12 : (int)W.csize[j2]) : 0;
+  const int s1 = j1 < cnt ? (cst1 ? kCRec : (int)W.csize[j1]) : 0;
+  const int s2 = j2 < cnt ? (cst2 ? kCRec : (int)W.csize[j2]) : 0;
   const int i1 = (int)warp_incl_scan_add((uint32_t)s1, lane);
   const int t1 = __shfl_sync(EQC_FULL, i1, 31);
   const int i2 = (int)warp_incl_scan_add((uint32_t)s2, lane) + t1;
   const int off1 = i1 - s1, off2 = i2 - s2;
   const int run = __shfl_sync(EQC_FULL, i2, 31);
-  uint32_t ps1 = cst1 ? 0x03030303u : (j1 < cnt ? W.cps[j1] : 0u);
-  uint32_t ps2 = cst2 ? 0x03030303u : (j2 < cnt ? W.cps[j2] : 0u);
+  const uint32_t cps = R64 ? (uint32_t)kCRec : 0x03030303u;  // RLE-64: the table holds the record size
+  uint32_t ps1 = cst1 ? cps : (j1 < cnt ? W.cps[j1] : 0u);
+  uint32_t ps2 = cst2 ? cps : (j2 < cnt ? W.cps[j2] : 0u);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j = h ? j2 : j1;
@@ -298,14 +304,22 @@ __global__ void __launch_bounds__(kEncWarps * 32, EQC_ENC_MINB) rle_encode_kerne
     if (h ? cst2 : cst1) {
       int L;
       chunk_ptr(j, L);
-      const uint32_t v = swz ? swizzle(W.cval[j]) : W.cval[j];
-      const uint8_t c = (uint8_t)(0x80 | (L - 1));
       uint8_t *gp = scr + off;
+      if (R64) {  // [1][0x80 | (L/2 - 1)][v v], L even
+        const uint32_t v = W.cval[j];
+        gp[0] = 1;
+        gp[1] = (uint8_t)(0x80 | (L / 2 - 1));
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        gp[3 * q] = 1;
-        gp[3 * q + 1] = c;
-        gp[3 * q + 2] = (uint8_t)(v >> (8 * q));
+        for (int q = 0; q < 8; ++q) gp[2 + q] = (uint8_t)(v >> (8 * (q & 3)));
+      } else {
+        const uint32_t v = swz ? swizzle(W.cval[j]) : W.cval[j];
+        const uint8_t c = (uint8_t)(0x80 | (L - 1));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          gp[3 * q] = 1;
+          gp[3 * q + 1] = c;
+          gp[3 * q + 2] = (uint8_t)(v >> (8 * q));
+        }
       }
     }
   }
@@ -402,15 +416,17 @@ struct StreamHdr {
 };
 
 // Validate a stream header against the expected w x h.
-__device__ StreamHdr read_header(const uint8_t *src, int64_t src_bytes, int w, int h) {
+// allow64: also accept RLE-64 streams (flags == EQC_FLAG_RLE64, 128-pixel chunks)
+__device__ StreamHdr read_header(const uint8_t *src, int64_t src_bytes, int w, int h, bool allow64 = false) {
   StreamHdr hd{};
   hd.ok = 0;
   if (src_bytes < 32) return hd;
   const uint32_t *h32 = reinterpret_cast<const uint32_t *>(src);
   const uint32_t w0 = h32[0], w1 = h32[1];
   const int ver = w1 & 0xFF, kind = (w1 >> 8) & 0xFF, flags = (w1 >> 16) & 0xFF, log2c = w1 >> 24;
-  if (w0 != kMagic || ver != kVersion || kind > 1 || (flags & ~1) || (kind == 1 && flags) || log2c < 5 ||
-      log2c > 7)
+  const bool r64 = allow64 && flags == EQC_FLAG_RLE64 && log2c == kLog2C;
+  if (w0 != kMagic || ver != kVersion || kind > 1 || ((flags & ~1) && !r64) || (kind == 1 && (flags & 1)) ||
+      log2c < 5 || log2c > 7)
     return hd;
   if ((int64_t)h32[2] != w || (int64_t)h32[3] != h || h32[5] != 0u) return hd;
   const int C = 1 << log2c;
@@ -600,6 +616,112 @@ __device__ __forceinline__ bool entry_local(const uint8_t *src, int64_t payload_
 // One warp per 32 x (128 / C) chunks: lane-parallel table validation and
 // constant-chunk classification, then constant chunks are filled with one
 // 128-bit store per lane and the others decoded warp-cooperatively.
+// ---- RLE-64 decode (R-C17): a warp decodes its group of chunks one by one --
+// Lane l expands units 2l and 2l+1 (pixels 4l..4l+3).  Tokens t and t + 32
+// live in lane t; their start units and payload units come from two packed
+// warp scans; each unit finds its token by start markers + a running max.
+__device__ __forceinline__ void rle64_decode_group(const DecImage im, const StreamHdr hd, int64_t cb, int w,
+                                                int64_t pitch, bool vec, int32_t *status, uint8_t *mark) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = cb + lane;
+  const bool has = c < hd.nchunks;
+  const uint8_t *tab = im.src + 32;
+  uint32_t off = 0, size = 0;
+  if (has) {
+    const uint2 e = __ldg(reinterpret_cast<const uint2 *>(tab + 8 * c));
+    off = e.x;
+    size = e.y;
+  }
+  // contiguity: chunk c starts where chunk c-1 ends; the last one ends the payload
+  uint64_t prev = __shfl_up_sync(EQC_FULL, (uint64_t)off + size, 1);
+  if (lane == 0) {
+    prev = 0;
+    if (cb > 0) {
+      const uint2 e = __ldg(reinterpret_cast<const uint2 *>(tab + 8 * (cb - 1)));
+      prev = (uint64_t)e.x + e.y;
+    }
+  }
+  bool ok = !has || (off == prev && size >= 2 && (uint64_t)off + size <= (uint64_t)hd.payload_bytes &&
+                     (c != hd.nchunks - 1 || (uint64_t)off + size == (uint64_t)hd.payload_bytes));
+  const unsigned bad = __ballot_sync(EQC_FULL, !ok);
+  if (bad) {
+    if (lane == 0) set_corrupt(status);
+    return;
+  }
+  const int nhere = (int)min((int64_t)32, hd.nchunks - cb);
+  for (int i = 0; i < nhere; ++i) {
+    const int64_t ci = cb + i;
+    const int y = (int)(ci / hd.S), k = (int)(ci - (int64_t)y * hd.S);
+    const int L = min(kC, w - k * kC), U = (L + 1) >> 1;
+    const uint32_t oi = __shfl_sync(EQC_FULL, off, i), si = __shfl_sync(EQC_FULL, size, i);
+    const uint8_t *rec = im.src + hd.payload0 + oi;
+    const int ntok = __ldg(rec);
+    bool good = ntok >= 1 && ntok <= U && (uint32_t)(1 + ntok) <= si;
+    const int t0 = lane, t1 = lane + 32;
+    const int c0 = (good && t0 < ntok) ? __ldg(rec + 1 + t0) : 0;
+    const int c1 = (good && t1 < ntok) ? __ldg(rec + 1 + t1) : 0;
+    const uint32_t l0 = (good && t0 < ntok) ? (c0 & 0x7F) + 1 : 0, l1 = (good && t1 < ntok) ? (c1 & 0x7F) + 1 : 0;
+    const uint32_t v0 = l0 | ((c0 & 0x80 ? (l0 ? 1u : 0u) : l0) << 16);
+    const uint32_t v1 = l1 | ((c1 & 0x80 ? (l1 ? 1u : 0u) : l1) << 16);
+    const uint32_t inc0 = warp_incl_scan_add(v0, lane), inc1 = warp_incl_scan_add(v1, lane);
+    const uint32_t tot0 = __shfl_sync(EQC_FULL, inc0, 31), tot1 = __shfl_sync(EQC_FULL, inc1, 31);
+    const uint32_t ex0 = inc0 - v0, ex1 = inc1 - v1 + tot0, tot = tot0 + tot1;
+    good = good && (int)(tot & 0xFFFFu) == U && 1u + (uint32_t)ntok + 8u * (tot >> 16) == si;
+    if (!good) {  // warp-uniform
+      if (lane == 0) set_corrupt(status);
+      continue;
+    }
+    // token info: start unit | payload unit << 8 | literal << 16
+    const uint32_t info0 = (ex0 & 0xFFFFu) | ((ex0 >> 16) << 8) | ((uint32_t)!(c0 & 0x80) << 16);
+    const uint32_t info1 = (ex1 & 0xFFFFu) | ((ex1 >> 16) << 8) | ((uint32_t)!(c1 & 0x80) << 16);
+    __syncwarp();
+    reinterpret_cast<uint16_t *>(mark)[lane] = 0;
+    __syncwarp();
+    if (t0 < ntok) mark[ex0 & 0xFFFFu] = (uint8_t)(t0 + 1);
+    if (t1 < ntok) mark[ex1 & 0xFFFFu] = (uint8_t)(t1 + 1);
+    __syncwarp();
+    const uint32_t mm = reinterpret_cast<const uint16_t *>(mark)[lane];
+    const int ma = (int)(mm & 0xFFu), mb = (int)(mm >> 8);
+    int run = max(ma, mb);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(EQC_FULL, run, d);
+      if (lane >= d) run = max(run, o);
+    }
+    int pre = __shfl_up_sync(EQC_FULL, run, 1);
+    if (lane == 0) pre = 0;
+    const int ta = max(pre, ma) - 1, tb = max(pre, max(ma, mb)) - 1;
+    const uint32_t ia0 = __shfl_sync(EQC_FULL, info0, ta & 31), ia1 = __shfl_sync(EQC_FULL, info1, ta & 31);
+    const uint32_t ib0 = __shfl_sync(EQC_FULL, info0, tb & 31), ib1 = __shfl_sync(EQC_FULL, info1, tb & 31);
+    const uint32_t ia = ta >= 32 ? ia1 : ia0, ib = tb >= 32 ? ib1 : ib0;
+    uint32_t px[4] = {0, 0, 0, 0};
+    bool pad_ok = true;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = 2 * lane + h;
+      if (u >= U) continue;
+      const uint32_t inf = h ? ib : ia;
+      const int su = (int)(inf & 0xFFu), sp = (int)((inf >> 8) & 0xFFu);
+      const int idx = sp + ((inf >> 16) ? u - su : 0);
+      const uint8_t *q = rec + 1 + ntok + 8 * idx;
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        lo |= (uint32_t)__ldg(q + b) << (8 * b);
+        hi |= (uint32_t)__ldg(q + 4 + b) << (8 * b);
+      }
+      px[2 * h] = lo;
+      px[2 * h + 1] = hi;
+      if (2 * u + 1 >= L && hi != 0) pad_ok = false;  // canonical zero padding
+    }
+    if (!__all_sync(EQC_FULL, pad_ok)) {
+      if (lane == 0) set_corrupt(status);
+      continue;
+    }
+    store_px(im.dst + (int64_t)y * pitch + (int64_t)k * kC, L, lane, vec, px);
+  }
+}
+
 __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_constant__ DecParams p) {
   __shared__ __align__(16) uint8_t stage[kWarps][kStageBytes];
   __shared__ __align__(16) uint16_t info[kWarps][kC];
@@ -608,13 +730,19 @@ __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_co
   const int m = (int)(blockIdx.x / p.tiles_per_image);
   const int64_t lt = blockIdx.x - (int64_t)m * p.tiles_per_image;
   const DecImage im = p.img[m];
+  __shared__ __align__(4) uint8_t s_mark[kWarps][64];
   if (tid == 0) {
-    s_hd = read_header(im.src, im.src_bytes, p.w, p.h);
+    s_hd = read_header(im.src, im.src_bytes, p.w, p.h, true);
     if (!s_hd.ok) set_corrupt(p.status);
   }
   __syncthreads();
   const StreamHdr hd = s_hd;
   if (!hd.ok) return;
+  if (hd.flags == EQC_FLAG_RLE64) {  // the 64-bit token codec (R-C17)
+    const int64_t cb = (lt * kWarps + warp) * kGroup;
+    if (cb < hd.nchunks) rle64_decode_group(im, hd, cb, p.w, p.pitch, p.vec != 0, p.status, s_mark[warp]);
+    return;
+  }
   const int C = 1 << hd.log2c;
   const int r = kC / C;
   const bool swz = (hd.flags & EQC_FLAG_SWIZZLE) != 0;
@@ -929,11 +1057,13 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   if (!aligned(workspace, 8)) return EQC_E_INVALID;
   EncParams p;
   bool vec = (pitch % 4) == 0;
+  const bool r64 = (flags[0] & EQC_FLAG_RLE64) != 0;  // one codec per batch
   for (int i = 0; i < count; ++i) {
     if (!src[i] || !dst[i]) return EQC_E_INVALID;
     if (kind[i] != EQC_KIND_RGBA8 && kind[i] != EQC_KIND_DEPTH32) return EQC_E_INVALID;
-    if (flags[i] & ~EQC_FLAG_SWIZZLE) return EQC_E_INVALID;
-    if (kind[i] == EQC_KIND_DEPTH32 && flags[i]) return EQC_E_UNSUPPORTED;
+    if (flags[i] & ~(EQC_FLAG_SWIZZLE | EQC_FLAG_RLE64)) return EQC_E_INVALID;
+    if (((flags[i] & EQC_FLAG_RLE64) != 0) != r64) return EQC_E_INVALID;
+    if ((flags[i] & EQC_FLAG_SWIZZLE) && (kind[i] == EQC_KIND_DEPTH32 || r64)) return EQC_E_UNSUPPORTED;
     if (!aligned(dst[i], 8) || !aligned(src[i], 4)) return EQC_E_INVALID;
     vec = vec && aligned(src[i], 16);
     p.img[i] = EncImage{src[i], dst[i], d_sizes + i, kind[i], flags[i]};
@@ -955,13 +1085,18 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   static bool configured = false;
   const size_t smem = sizeof(EncSmem);
   if (!configured) {
-    if (cudaFuncSetAttribute(rle_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(rle_encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(rle_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
       return EQC_E_CUDA;
     configured = true;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  rle_encode_kernel<<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
+  if (r64)
+    rle_encode_kernel<true><<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
+  else
+    rle_encode_kernel<false><<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
   CompactParams c;
   for (int i = 0; i < count; ++i) c.img[i] = p.img[i];
   c.run_size = p.run_size;

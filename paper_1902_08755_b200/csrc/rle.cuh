@@ -215,6 +215,61 @@ __device__ __forceinline__ EncodeOut encode_chunk_t(uint32_t px[4], int L_, int 
   return EncodeOut{b4, ps};
 }
 
+// ---- RLE-64 (reading R-C17): 64-bit units = pixel pairs -------
+// Lane l holds units a = 2l (px0, px1) and b = 2l + 1 (px2, px3); positions at
+// or beyond L hold 0 (the odd tail unit's high half is 0 by definition).
+// Maximal runs of >= 2 equal units -> REPEAT (ctrl 0x80 | (len - 1), one
+// 8-byte unit), other maximal spans -> LITERAL (ctrl len - 1, the units).
+// Record = [ntok][ctrl x ntok][payload]; returns {size, size}.
+__device__ __forceinline__ bool u64eq(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+  return a0 == b0 && a1 == b1;
+}
+
+__device__ __forceinline__ EncodeOut encode_chunk64(const uint32_t px[4], int L, int lane, uint8_t *st, uint8_t *tp) {
+  const int U = (L + 1) >> 1;
+  const int ua = 2 * lane, ub = ua + 1;
+  const bool va = ua < U, vb = ub < U;
+  // neighbours: unit a-1 (previous lane's b), unit b+1 (next lane's a)
+  const uint32_t pm0 = __shfl_up_sync(EQC_FULL, px[2], 1), pm1 = __shfl_up_sync(EQC_FULL, px[3], 1);
+  const uint32_t pn0 = __shfl_down_sync(EQC_FULL, px[0], 1), pn1 = __shfl_down_sync(EQC_FULL, px[1], 1);
+  const bool ea = va && ua >= 1 && u64eq(px[0], px[1], pm0, pm1);    // a == a-1
+  const bool eb = vb && u64eq(px[2], px[3], px[0], px[1]);           // b == a
+  const bool en = (ub + 1 < U) && u64eq(pn0, pn1, px[2], px[3]);     // b+1 == b
+  const bool Ra = va && (ea || eb), Rb = vb && (eb || en);           // inside a run of >= 2
+  bool Rp = __shfl_up_sync(EQC_FULL, Rb, 1);                          // R of unit a-1
+  if (lane == 0) Rp = false;
+  const bool Ta = va && (ua == 0 || Ra != Rp || (Ra && Rp && !ea));
+  const bool Tb = vb && (Rb != Ra || (Rb && Ra && !eb));
+  const bool Ea = va && (!Ra || Ta), Eb = vb && (!Rb || Tb);
+  const uint32_t cnt = (uint32_t)Ta + (uint32_t)Tb + (((uint32_t)Ea + (uint32_t)Eb) << 16);
+  const uint32_t inc = warp_incl_scan_add(cnt, lane);
+  const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
+  const uint32_t ex = inc - cnt;
+  const int ntok = (int)(tot & 0xFFFFu), npay = (int)(tot >> 16);
+  int tk = (int)(ex & 0xFFFFu), ek = 1 + ntok + 8 * (int)(ex >> 16);
+  if (Ta) tp[tk++] = (uint8_t)(ua | ((uint32_t)Ra << 7));
+  if (Tb) tp[tk] = (uint8_t)(ub | ((uint32_t)Rb << 7));
+  if (Ea) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) st[ek + q] = (uint8_t)((q < 4 ? px[0] : px[1]) >> (8 * (q & 3)));
+    ek += 8;
+  }
+  if (Eb) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) st[ek + q] = (uint8_t)((q < 4 ? px[2] : px[3]) >> (8 * (q & 3)));
+  }
+  if (lane == 0) st[0] = (uint8_t)ntok;
+  __syncwarp();
+  for (int q = lane; q < ntok; q += 32) {
+    const uint32_t a = tp[q];
+    const int next = q + 1 < ntok ? (int)(tp[q + 1] & 0x7Fu) : U;
+    st[1 + q] = (uint8_t)((a & 0x80u) | (uint32_t)(next - (int)(a & 0x7Fu) - 1));
+  }
+  __syncwarp();
+  const int size = 1 + ntok + 8 * npay;
+  return EncodeOut{size, (uint32_t)size};
+}
+
 __device__ __forceinline__ EncodeOut encode_chunk(uint32_t px[4], int L, int lane, bool swz, uint8_t *st,
                                                   uint8_t *tp) {
   return L == kC ? encode_chunk_t<true>(px, L, lane, swz, st, tp) : encode_chunk_t<false>(px, L, lane, swz, st, tp);

@@ -21,6 +21,7 @@ E_INVALID, E_CAPACITY, E_CORRUPT, E_UNSUPPORTED, E_CUDA, E_NCCL = -1, -2, -3, -4
 MAX_SOURCES = 64
 KIND_RGBA8, KIND_DEPTH32 = 0, 1
 FLAG_SWIZZLE = 1
+FLAG_RLE64 = 2
 UNIQUE_ID_BYTES = 128
 OP_DEPTH = 0
 OP_BLEND = 1
