@@ -511,28 +511,28 @@ __device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8
   return decode_staged(stage + sh, ps, L, lane, info, px);
 }
 
-// Words of a record (4-byte aligned window) a lane-parallel stager needs.
-__device__ __forceinline__ int record_words(const uint8_t *rec, uint32_t ps) {
+// 16-byte units of the aligned window covering a record.
+__device__ __forceinline__ int record_quads(const uint8_t *rec, uint32_t ps) {
   const int total = (int)(ps & 0xFF) + (int)((ps >> 8) & 0xFF) + (int)((ps >> 16) & 0xFF) + (int)(ps >> 24);
-  return ((int)((uintptr_t)rec & 3) + total + 3) >> 2;
+  return ((int)((uintptr_t)rec & 15) + total + 15) >> 4;
 }
 
-// Issue asynchronous 4-byte copies of a record's words into `dst` (shared);
-// words that would cross the stream end are copied synchronously.
-__device__ __forceinline__ void stage_async(const uint8_t *src, int64_t src_bytes, const uint8_t *rec, int nwords,
-                                            uint32_t *dst, int lane) {
-  const uintptr_t a0 = (uintptr_t)rec & ~(uintptr_t)3;
+// Issue asynchronous 16-byte copies of the aligned window covering a record
+// into `dst` (shared; the record starts at byte rec & 15 of dst).  The window
+// never starts before the stream (records follow the header and table); a
+// quad that would cross the stream end is copied byte by byte.
+__device__ __forceinline__ void stage_async16(const uint8_t *src, int64_t src_bytes, const uint8_t *rec, int nquads,
+                                              uint4 *dst, int lane) {
+  const uintptr_t a0 = (uintptr_t)rec & ~(uintptr_t)15;
   const uintptr_t lim = (uintptr_t)src + (uintptr_t)src_bytes;
-  for (int q = lane; q < nwords; q += 32) {
-    const uintptr_t a = a0 + 4 * (uintptr_t)q;
-    if (a + 4 <= lim) {
+  for (int q = lane; q < nquads; q += 32) {
+    const uintptr_t a = a0 + 16 * (uintptr_t)q;
+    if (a + 16 <= lim) {
       const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + q);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(a) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(a) : "memory");
     } else {
-      uint32_t v = 0;
-      for (int b = 0; b < 4; ++b)
-        if (a + b < lim) v |= (uint32_t)__ldg(reinterpret_cast<const uint8_t *>(a + b)) << (8 * b);
-      dst[q] = v;
+      uint8_t *d = reinterpret_cast<uint8_t *>(dst + q);
+      for (int b = 0; b < 16; ++b) d[b] = a + b < lim ? __ldg(reinterpret_cast<const uint8_t *>(a + b)) : 0;
     }
   }
 }
@@ -911,19 +911,20 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   // per-warp buffer (asynchronous copies, one round trip for all of them),
   // then decode depth first; a source's colour only where it wins.
   // Lane i plans source i: word offsets of its depth and colour records.
-  uint32_t *pre = s_pre + (size_t)warp * kPreWords;
-  int wd0 = 0, wc0 = 0;  // word offsets (-1: not prefetched)
+  uint4 *pre = reinterpret_cast<uint4 *>(s_pre + (size_t)warp * kPreWords);
+  constexpr int kPreQuads = kPreWords / 4;
+  int wd0 = 0, wc0 = 0;  // 16-byte slot offsets (-1: not prefetched)
   {
     int nwd = 0, nwc = 0;
     if (npass == 1 && lane < n) {
-      if (!ed[0].w) nwd = record_words(p.src[n + lane] + payload0 + ed[0].x, ed[0].y);
-      if (!ec[0].w) nwc = record_words(p.src[lane] + payload0 + ec[0].x, ec[0].y);
+      if (!ed[0].w) nwd = record_quads(p.src[n + lane] + payload0 + ed[0].x, ed[0].y);
+      if (!ec[0].w) nwc = record_quads(p.src[lane] + payload0 + ec[0].x, ec[0].y);
     }
     const int tot = nwd + nwc;
     const int inc = (int)warp_incl_scan_add((uint32_t)tot, lane);
     const int ex = inc - tot;
-    wd0 = (nwd && ex + nwd <= kPreWords) ? ex : -1;
-    wc0 = (nwc && ex + tot <= kPreWords) ? ex + nwd : -1;
+    wd0 = (nwd && ex + nwd <= kPreQuads) ? ex : -1;
+    wc0 = (nwc && ex + tot <= kPreQuads) ? ex + nwd : -1;
   }
   if (npass == 1) {
     for (int i = 0; i < n; ++i) {
@@ -931,12 +932,12 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
       if (od >= 0) {
         const uint32_t x = __shfl_sync(EQC_FULL, ed[0].x, i), y2 = __shfl_sync(EQC_FULL, ed[0].y, i);
         const uint8_t *rec = p.src[n + i] + payload0 + x;
-        stage_async(p.src[n + i], p.src_bytes[n + i], rec, record_words(rec, y2), pre + od, lane);
+        stage_async16(p.src[n + i], p.src_bytes[n + i], rec, record_quads(rec, y2), pre + od, lane);
       }
       if (oc >= 0) {
         const uint32_t x = __shfl_sync(EQC_FULL, ec[0].x, i), y2 = __shfl_sync(EQC_FULL, ec[0].y, i);
         const uint8_t *rec = p.src[i] + payload0 + x;
-        stage_async(p.src[i], p.src_bytes[i], rec, record_words(rec, y2), pre + oc, lane);
+        stage_async16(p.src[i], p.src_bytes[i], rec, record_quads(rec, y2), pre + oc, lane);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -958,7 +959,8 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
 #pragma unroll
       for (int j = 0; j < 4; ++j) d[j] = dz;
     } else if (npass == 1 && od >= 0) {
-      okd = decode_staged(reinterpret_cast<const uint8_t *>(pre + od) + (dx & 3u) + ((uintptr_t)p.src[n + i] & 3u),
+      okd = decode_staged(reinterpret_cast<const uint8_t *>(pre + od) +
+                              ((uintptr_t)(p.src[n + i] + payload0 + dx) & 15u),
                           dy, L, lane, info[warp], d);
     } else {
       okd = decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane, stage[warp],
@@ -991,8 +993,9 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
     } else {
       bool okc;
       if (npass == 1 && oc >= 0)
-        okc = decode_staged(reinterpret_cast<const uint8_t *>(pre + oc) + (cx & 3u) + ((uintptr_t)p.src[i] & 3u), cy,
-                            L, lane, info[warp], col);
+        okc = decode_staged(reinterpret_cast<const uint8_t *>(pre + oc) +
+                                ((uintptr_t)(p.src[i] + payload0 + cx) & 15u),
+                            cy, L, lane, info[warp], col);
       else
         okc = decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, L, lane, stage[warp], info[warp],
                             col);
