@@ -140,11 +140,11 @@ def make_inputs(seed, n, w, h):
 
 def launches_per_compose(n, exchange):
     """Our kernels per compose_direct_send call: local pre-composite + band
-    composite (+ n-1 band encodes of 2 kernels each and one decode batch with
+    composite (+ n-1 band encodes of 3 kernels each and one decode batch with
     RLE).  NCCL's own kernels are not counted."""
     if exchange == "raw":  # pre-composite, 2 flag barriers, fused pull+composite
         return 4
-    return 2 + (2 * (n - 1) + 1 if exchange == "rle" else 0)
+    return 2 + (3 * (n - 1) + 1 if exchange == "rle" else 0)
 
 
 def run_eqc(args):
@@ -385,8 +385,8 @@ def run_eqc(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(world * NSRC * P / (e2e_ms * 1e-3) / 1e6, 1), "unit": UNIT,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        # per step: encode batch (encode + compaction kernels) + fused decode/composite
-        "gpu_launches": (3 + (launches_per_compose(world, args.exchange) if world > 1 else 0)) * args.steps,
+        # per step: encode batch (encode, run scan, compaction kernels) + fused decode/composite
+        "gpu_launches": (4 + (launches_per_compose(world, args.exchange) if world > 1 else 0)) * args.steps,
         "clocks": clocks,
     }
     emit(line)

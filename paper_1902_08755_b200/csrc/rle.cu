@@ -333,65 +333,72 @@ __global__ void __launch_bounds__(kEncWarps * 32, EQC_ENC_MINB) rle_encode_kerne
 struct CompactParams {
   EncImage img[kMaxBatch];
   const int32_t *run_size;
+  const uint32_t *run_off;  // per image: exclusive prefix of run sizes, then the total
   const uint8_t *scratch;
   int64_t nchunks;
   int w, h, groups_per_image, runs_per_image;
 };
 
-// One CTA per group of kCompactWarps runs: payload offset = sum of the
-// preceding runs' sizes of the same image (summed directly by all threads,
-// no look-back chain), then every warp moves its run from the scratch to the
-// stream, rebases its table entries and discards its scratch lines from L2;
-// the last group of an image writes the header and the stream size.
-__global__ void __launch_bounds__(kCompactWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
-  __shared__ int64_t s_part[kCompactWarps];
-  __shared__ int64_t s_off;
+// One CTA per image: exclusive prefix of the image's run sizes (the payload
+// offset of every run) and the payload total, so the compaction needs no
+// per-CTA summation of all preceding runs.
+__global__ void __launch_bounds__(1024) rle_runscan_kernel(const int32_t *run_size, uint32_t *run_off, int runs) {
+  __shared__ uint32_t s_w[32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int32_t *rs = run_size + (int64_t)blockIdx.x * runs;
+  uint32_t *ro = run_off + (int64_t)blockIdx.x * (runs + 1);
+  const int per = (runs + blockDim.x - 1) / blockDim.x;  // consecutive runs per thread
+  const int q0 = tid * per, q1 = min(runs, q0 + per);
+  uint32_t local = 0;
+  for (int q = q0; q < q1; ++q) local += (uint32_t)__ldg(rs + q);
+  const uint32_t inc = warp_incl_scan_add(local, lane);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0u;
+    const uint32_t wi = warp_incl_scan_add(v, lane);
+    s_w[lane] = wi - v;
+  }
+  __syncthreads();
+  uint32_t acc = s_w[warp] + inc - local;
+  for (int q = q0; q < q1; ++q) {
+    ro[q] = acc;
+    acc += (uint32_t)__ldg(rs + q);
+  }
+  if (q1 == runs && q0 < q1) ro[runs] = acc;
+  if (runs == 0 && tid == 0) ro[0] = 0;
+}
+
+// One warp per run (kCompactWarps per CTA, independent): moves the run from
+// the scratch to its payload offset, rebases its table entries and discards
+// its scratch lines from L2; the warp of an image's last run writes the
+// header and the stream size.
+__global__ void __launch_bounds__(kCompactWarps * 32) rle_compact_kernel(const __grid_constant__ CompactParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = (int)(blockIdx.x / p.groups_per_image);
-  const int r0 = (int)(blockIdx.x - m * p.groups_per_image) * kCompactWarps;  // first run of the group
-  const int32_t *rs = p.run_size + (int64_t)m * p.runs_per_image;
+  const int r = (int)(blockIdx.x - m * p.groups_per_image) * kCompactWarps + warp;  // run of image m
+  if (r >= p.runs_per_image) return;
   const EncImage im = p.img[m];
-  {
-    int64_t acc = 0;
-#pragma unroll 4
-    for (int q = tid; q < r0; q += kCompactWarps * 32) acc += __ldg(rs + q);
-    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(EQC_FULL, acc, d);
-    if (lane == 0) s_part[warp] = acc;
+  const uint32_t *ro = p.run_off + (int64_t)m * (p.runs_per_image + 1);
+  const int64_t base = __ldg(ro + r);
+  const int64_t run = __ldg(p.run_size + (int64_t)m * p.runs_per_image + r);
+  if (r == p.runs_per_image - 1 && lane == 0) {
+    const int64_t payload = __ldg(ro + p.runs_per_image);
+    uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
+    h32[0] = kMagic;
+    h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) | ((uint32_t)kLog2C << 24);
+    h32[2] = (uint32_t)p.w;
+    h32[3] = (uint32_t)p.h;
+    h32[4] = (uint32_t)p.nchunks;
+    h32[5] = 0u;
+    h32[6] = (uint32_t)(uint64_t)payload;
+    h32[7] = (uint32_t)((uint64_t)payload >> 32);
+    *im.d_size = 32 + 8 * p.nchunks + payload;
   }
-  // sizes of this group's runs: exclusive prefix for every warp
-  const int nr = min(kCompactWarps, p.runs_per_image - r0);
-  const int rv = lane < nr ? __ldg(rs + r0 + lane) : 0;
-  const int rinc = (int)warp_incl_scan_add((uint32_t)rv, lane);
-  const int64_t woff = __shfl_sync(EQC_FULL, rinc - rv, warp);
-  const int64_t run = __shfl_sync(EQC_FULL, rv, warp);
-  const int64_t group_bytes = __shfl_sync(EQC_FULL, rinc, 31);
-  __syncthreads();
-  if (tid == 0) {
-    int64_t acc = 0;
-    for (int w = 0; w < kCompactWarps; ++w) acc += s_part[w];
-    s_off = acc;
-    if (r0 + nr == p.runs_per_image) {
-      const int64_t payload = acc + group_bytes;
-      uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
-      h32[0] = kMagic;
-      h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) |
-               ((uint32_t)kLog2C << 24);
-      h32[2] = (uint32_t)p.w;
-      h32[3] = (uint32_t)p.h;
-      h32[4] = (uint32_t)p.nchunks;
-      h32[5] = 0u;
-      h32[6] = (uint32_t)(uint64_t)payload;
-      h32[7] = (uint32_t)((uint64_t)payload >> 32);
-      *im.d_size = 32 + 8 * p.nchunks + payload;
-    }
-  }
-  __syncthreads();
-  if (warp >= nr) return;
-  const int64_t base = s_off + woff;
   const int nch = (int)p.nchunks;
-  const int c0 = (r0 + warp) * kSTChunksPerWarp;
+  const int c0 = r * kSTChunksPerWarp;
   const int cnt = min(kSTChunksPerWarp, nch - c0);
-  const uint8_t *scr = p.scratch + ((size_t)m * p.runs_per_image + r0 + warp) * kScratchPerWarp;
+  const uint8_t *scr = p.scratch + ((size_t)m * p.runs_per_image + r) * kScratchPerWarp;
   uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
   for (int j = lane; j < cnt; j += 32) {
     uint2 e = table[j];
@@ -1027,8 +1034,11 @@ inline int64_t enc_runs_per_image(int w, int h) {
   return (S * h + kSTChunksPerWarp - 1) / kSTChunksPerWarp;
 }
 
-inline size_t enc_scratch_offset(int64_t runs) {
-  return (((size_t)runs * sizeof(int32_t)) + 255) & ~(size_t)255;
+// workspace: run_size[runs] int32, run_off[runs + count] uint32, then (256-byte
+// aligned) the record scratch
+inline size_t enc_runoff_offset(int64_t runs) { return (size_t)runs * sizeof(int32_t); }
+inline size_t enc_scratch_offset(int64_t runs, int count) {
+  return (enc_runoff_offset(runs) + ((size_t)runs + count) * sizeof(uint32_t) + 255) & ~(size_t)255;
 }
 
 }  // namespace
@@ -1041,7 +1051,7 @@ extern "C" int64_t image_rle_max_size(int w, int h) {
 extern "C" size_t image_rle_workspace_size_batch(int count, int w, int h) {
   if (count <= 0 || w <= 0 || h <= 0) return 0;
   const int64_t runs = (int64_t)count * enc_runs_per_image(w, h);
-  return enc_scratch_offset(runs) + (size_t)runs * kScratchPerWarp;
+  return enc_scratch_offset(runs, count) + (size_t)runs * kScratchPerWarp;
 }
 
 extern "C" size_t image_rle_workspace_size(int w, int h) { return image_rle_workspace_size_batch(1, w, h); }
@@ -1084,7 +1094,8 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   const int64_t tiles = (int64_t)count * p.tiles_per_image;
   if (runs > 0x7FFFFFFFll || p.nchunks > 0x7FFFFFFFll) return EQC_E_INVALID;
   p.run_size = reinterpret_cast<int32_t *>(workspace);
-  p.scratch = reinterpret_cast<uint8_t *>(workspace) + enc_scratch_offset(runs);
+  p.scratch = reinterpret_cast<uint8_t *>(workspace) + enc_scratch_offset(runs, count);
+  uint32_t *run_off = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(workspace) + enc_runoff_offset(runs));
   static bool configured = false;
   const size_t smem = sizeof(EncSmem);
   if (!configured) {
@@ -1102,7 +1113,9 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
     rle_encode_kernel<false><<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
   CompactParams c;
   for (int i = 0; i < count; ++i) c.img[i] = p.img[i];
+  rle_runscan_kernel<<<count, 1024, 0, st>>>(p.run_size, run_off, p.runs_per_image);
   c.run_size = p.run_size;
+  c.run_off = run_off;
   c.scratch = p.scratch;
   c.nchunks = p.nchunks;
   c.w = w;
