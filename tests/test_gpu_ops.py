@@ -102,3 +102,18 @@ def test_average_rejects_too_many_sources(eqc):
     c, _ = synth.random_frames(1, 64, 8, 4)
     with pytest.raises(eqc.EqcError):  # 5 x 64 = 320 sources exceed the exact 16-bit sums
         eqc.compose_direct_send_local(5, [to_dev(x) for x in c] * 5, None, out_frame(4, 8), op=eqc.OP_AVERAGE)
+
+
+@pytest.mark.parametrize("algo,nr,h", [("s23", 6, 2), ("s23", 5, 1), ("stream", 4, 1), ("ds", 5, 3), ("bs", 8, 3)])
+def test_schedules_with_fewer_rows_than_parts(eqc, algo, nr, h):
+    # more ranks / parts than rows: empty bands and regions must be handled
+    w = 70
+    c, d = synth.random_frames(700 + nr + h, nr, w, h, depth_alphabet=[0, 1, 0xFFFFFFFF])
+    out = out_frame(h, w)
+    _fn(eqc, algo)(nr, [to_dev(x) for x in c], [to_dev(x) for x in d], out, dest_rank=nr - 1)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(to_host(out), oracle.depth_composite(c, d)[0])
+    out2 = out_frame(h, w)
+    _fn(eqc, algo)(nr, [to_dev(x) for x in c], None, out2, dest_rank=0, flags=eqc.FLAG_RLE, op=eqc.OP_AVERAGE)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(to_host(out2), oracle.average(c))
