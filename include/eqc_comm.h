@@ -76,9 +76,19 @@ EQC_API int eqc_plan_bands(int h, int n, int *row0);
 EQC_API int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_rounds);
 
 /*
- * compose_direct_send -- sort-last depth compositing of all ranks' sources
- * with the direct-send schedule.  Rank g holds the n_local sources with
- * global indices [g*n_local, (g+1)*n_local) (contiguous blocks, R-C5).
+ * compose_direct_send -- sort-last compositing of all ranks' sources with the
+ * direct-send schedule.  Rank g holds the n_local sources with global indices
+ * [g*n_local, (g+1)*n_local) (contiguous blocks, R-C5).
+ *   comm       this rank's communicator (collective call: every rank calls it
+ *              with the same w, h, op, flags, dest_rank).
+ *   color, depth  host arrays of n_local device pointers [h][pitch]; depth is
+ *              ignored (may be NULL) for EQC_OP_BLEND / EQC_OP_AVERAGE.
+ *   op         EQC_OP_DEPTH (below), EQC_OP_BLEND or EQC_OP_AVERAGE (the
+ *              same schedule with the operator's partial format, see above).
+ *   out_color  device [h][out_pitch] on dest_rank (NULL elsewhere).
+ *   Scratch lives in `comm` (allocated at the first call, reused).
+ *   Errors: EQC_E_INVALID (arguments), EQC_E_UNSUPPORTED (unknown op, more
+ *   than 256 sources for EQC_OP_AVERAGE), EQC_E_CUDA, EQC_E_NCCL.
  *   (1) local pre-composite of the rank's sources (compositor_depth);
  *   (2) [EQC_FLAG_RLE: encode each outgoing band, exchange sizes];
  *   (3) every rank sends band j (colour + depth) to rank j (NCCL grouped
