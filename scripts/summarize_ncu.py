@@ -115,14 +115,18 @@ def main():
     if traffic:
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         old = json.load(open(tpath)) if os.path.exists(tpath) else {}
-        # bench names its kernels by the C-ABI call; map the encode pair and the fused kernel
-        m = {"rle_encode_kernel": "image_compress_rle_batch", "depth_rle_kernel": "compositor_depth_rle"}
+        # bench names its kernels by the C-ABI call: the encode batch is the
+        # encoder + run scan + compaction kernels, the fused call one kernel
+        base = {k.split("<")[0]: v for k, v in traffic.items()}
         for k, v in traffic.items():
             if k.startswith("at::"):
                 continue  # torch setup kernels (workspace zero-fill), not timed
-            old[m.get(k, k)] = v
-        if "rle_compact_kernel" in traffic and "rle_encode_kernel" in traffic:
-            old["image_compress_rle_batch"] = traffic["rle_encode_kernel"] + traffic["rle_compact_kernel"]
+            old[k] = v
+        if "rle_encode_kernel" in base:
+            old["image_compress_rle_batch"] = sum(base.get(k, 0) for k in
+                                                  ("rle_encode_kernel", "rle_runscan_kernel", "rle_compact_kernel"))
+        if "depth_rle_kernel" in base:
+            old["compositor_depth_rle"] = base["depth_rle_kernel"]
         old["_source"] = f"profiles/ncu_{a.tag}.md (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
         json.dump(old, open(tpath, "w"), indent=1)
     print("\n".join(lines[:60]))
