@@ -189,6 +189,30 @@ EQC_API int compose_stream_local(int nranks, int n_local, const uint32_t *const 
                                  int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
                                  void *stream);
 
+/*
+ * compose_direct_send_roi -- compose_direct_send (EQC_OP_DEPTH) with
+ * application-provided regions of interest: "Equalizer provides an API for
+ * the programmer to provide the ROI ... the screen-space 2D bounding box fully
+ * enclosing the data rendered by a single resource".
+ *   d_src_roi  DEVICE int32[4 n_local] (16-byte aligned): {x, y, w, h} of each
+ *              local source (full-frame coordinates, clipped to the frame,
+ *              R-C19); outside it a source is background and never read.
+ * The pre-composite reads only inside these ROIs; on the peer-memory path the
+ * partial frame is written only inside their union box, which is published
+ * and bounds the peers' pulls (as EQC_FLAG_ROI, without analysing the
+ * frame).  Same result as compose_direct_send when every ROI encloses its
+ * source's rendered pixels.  compose_direct_send_roi_local: virtual ranks
+ * (d_src_roi holds nranks * n_local ROIs, rank-major).
+ */
+EQC_API int compose_direct_send_roi(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                                    const uint32_t *const *depth, const int32_t *d_src_roi, int w, int h,
+                                    int64_t pitch, int flags, int dest_rank, uint32_t *out_color,
+                                    int64_t out_pitch, void *stream);
+EQC_API int compose_direct_send_roi_local(int nranks, int n_local, const uint32_t *const *color,
+                                          const uint32_t *const *depth, const int32_t *d_src_roi, int w, int h,
+                                          int64_t pitch, int flags, int dest_rank, uint32_t *out_color,
+                                          int64_t out_pitch, int64_t *out_stats, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,8 @@
 // stream, NVLink 5 / NVSwitch).
 #include <nccl.h>
 
+#include <climits>
+#include <cstdint>
 #include <cstring>
 #include <vector>
 
@@ -121,6 +123,8 @@ struct Geometry {
   int w = 0, h = 0;
   int64_t pitch = 0;  // of the source frames
   int op = EQC_OP_DEPTH;  // per-pixel operator; EQC_OP_BLEND: the (c, d) planes carry unorm16 partials
+  const int32_t *src_roi = nullptr;  // application source ROIs (device, x 4 ints) or NULL
+  bool src_roi_all_ranks = false;    // virtual ranks: src_roi holds every rank's ROIs (rank-major)
   int flags = 0;
   int dest = 0;
   uint32_t *out = nullptr;
@@ -300,6 +304,13 @@ int op_merge(const Geometry &g, int k, const uint32_t *const *c, const uint32_t 
 
 int local_precomposite(RankState &r, const Geometry &g, cudaStream_t s) {
   r.cur = 0;
+  if (g.src_roi && g.op == EQC_OP_DEPTH) {  // application ROIs: sources read only inside them
+    std::vector<const int32_t *> rp(g.n_local);
+    const size_t first = g.src_roi_all_ranks ? (size_t)r.rank * g.n_local : 0;
+    for (int i = 0; i < g.n_local; ++i) rp[i] = g.src_roi + 4 * (first + i);
+    return eqc_depth_roi_launch(g.n_local, r.color, r.depth, rp.data(), 0, nullptr, g.w, g.h, g.pitch,
+                                r.part_c[0].as<uint32_t>(), r.part_d[0].as<uint32_t>(), g.w, s);
+  }
   return op_local(g, r.color, r.depth, r.part_c[0].as<uint32_t>(), r.part_d[0].as<uint32_t>(), s);
 }
 
@@ -1100,6 +1111,27 @@ __global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
 // ints) followed by the rank's partial-frame ROI {x, y, w, h} (kRoiSlot).
 constexpr int kRoiSlot = EQC_MAX_SOURCES;  // int offset, 16-byte aligned
 
+// Bounding box of the union of n ROIs {x, y, w, h} (empty ones ignored),
+// clipped by the consumer: the ROI of a partial frame whose sources hold data
+// only inside their (application-provided) ROIs.
+__global__ void roi_union_kernel(const int32_t *in, int n, int32_t *out) {
+  if (threadIdx.x != 0) return;
+  int64_t x0 = INT64_MAX, y0 = INT64_MAX, x1 = INT64_MIN, y1 = INT64_MIN;
+  for (int i = 0; i < n; ++i) {
+    const int4 r = reinterpret_cast<const int4 *>(in)[i];
+    if (r.z <= 0 || r.w <= 0) continue;
+    x0 = min(x0, (int64_t)r.x);
+    y0 = min(y0, (int64_t)r.y);
+    x1 = max(x1, (int64_t)r.x + r.z);
+    y1 = max(y1, (int64_t)r.y + r.w);
+  }
+  x0 = max(x0, (int64_t)INT32_MIN);
+  y0 = max(y0, (int64_t)INT32_MIN);
+  *reinterpret_cast<int4 *>(out) = x1 == INT64_MIN ? make_int4(0, 0, 0, 0)
+                                                  : make_int4((int)x0, (int)y0, (int)min(x1 - x0, (int64_t)INT32_MAX),
+                                                              (int)min(y1 - y0, (int64_t)INT32_MAX));
+}
+
 struct P2PState {
   int capable = -1;  // -1 unknown, 0 no (NCCL transport), 1 yes
   int64_t cap_px = 0;
@@ -1222,14 +1254,25 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   for (int i = 0; i < 4; ++i) stats[i] = 0;
   std::vector<int> row0(n + 1);
   plan_bands(g.h, n, row0.data());
-  const bool roi = (g.flags & EQC_FLAG_ROI) != 0 && g.op == EQC_OP_DEPTH;  // ROI: depth compositing only
+  // ROI (depth compositing only): computed (EQC_FLAG_ROI) or application-provided
+  const bool roi = ((g.flags & EQC_FLAG_ROI) != 0 || g.src_roi) && g.op == EQC_OP_DEPTH;
   int32_t *my_roi = P.flags.as<int32_t>() + kRoiSlot;
   // (1) local pre-composite into the IPC-exposed partial frame.  With
   // EQC_FLAG_ROI the same kernel reduces the bounding box of
   // the partial's rendered pixels (the ROI "computed by analysing the
   // framebuffer", at no extra pass) and publishes it in the
   // peer-readable flags allocation; no host round trip.
-  if (roi) {
+  if (g.src_roi && g.op == EQC_OP_DEPTH) {
+    // application-provided ROIs: sources are read only inside
+    // them, the partial is written only inside their union box, which is
+    // published as the partial's ROI
+    roi_union_kernel<<<1, 32, 0, s>>>(g.src_roi, g.n_local, my_roi);
+    EQC_TRY(eqc_launch_status());
+    std::vector<const int32_t *> rp(g.n_local);
+    for (int i = 0; i < g.n_local; ++i) rp[i] = g.src_roi + 4 * i;
+    EQC_TRY(eqc_depth_roi_launch(g.n_local, color, depth, rp.data(), 0, my_roi, g.w, g.h, g.pitch,
+                                 P.part_c.as<uint32_t>(), P.part_d.as<uint32_t>(), g.w, s));
+  } else if (roi) {
     EQC_TRY(P.roi_local.ensure(eqc_depth_bbox_scratch_bytes()));
     EQC_TRY(eqc_depth_composite_bbox(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
                                      P.part_d.as<uint32_t>(), g.w, P.roi_local.p, my_roi, s));
@@ -1352,7 +1395,7 @@ enum Algo { kDirectSend, kBinarySwap, kSwap23, kStream };
 
 static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *const *color,
                         const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags, int dest_rank,
-                        uint32_t *out_color, int64_t out_pitch, void *stream) {
+                        uint32_t *out_color, int64_t out_pitch, void *stream, const int32_t *src_roi = nullptr) {
   if (!comm) return EQC_E_INVALID;
   EQC_TRY(validate(comm->nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch,
                    comm->rank == dest_rank));
@@ -1371,6 +1414,7 @@ static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *
   g.out_pitch = comm->rank == dest_rank ? out_pitch : w;
   comm->st.color = color;
   comm->st.depth = depth;
+  g.src_roi = src_roi;
   cudaStream_t s = (cudaStream_t)stream;
   if (ds && comm->nranks > 1 && !(flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) {
     EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
@@ -1400,7 +1444,8 @@ extern "C" int compose_binary_swap(eqc_comm *comm, int n_local, const uint32_t *
 
 static int compose_local(Algo algo, int nranks, int n_local, const uint32_t *const *color,
                          const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags, int dest_rank,
-                         uint32_t *out_color, int64_t out_pitch, int64_t *out_stats, void *stream) {
+                         uint32_t *out_color, int64_t out_pitch, int64_t *out_stats, void *stream,
+                         const int32_t *src_roi = nullptr) {
   EQC_TRY(validate(nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch, true));
   if (algo == kBinarySwap && (nranks & (nranks - 1))) return EQC_E_UNSUPPORTED;
   Geometry g;
@@ -1414,6 +1459,8 @@ static int compose_local(Algo algo, int nranks, int n_local, const uint32_t *con
   g.dest = dest_rank;
   g.out = out_color;
   g.out_pitch = out_pitch;
+  g.src_roi = src_roi;
+  g.src_roi_all_ranks = true;
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<RankState> states(nranks);
   std::vector<RankState *> ranks;
@@ -1505,4 +1552,22 @@ extern "C" int compose_stream_local(int nranks, int n_local, const uint32_t *con
                                     void *stream) {
   return compose_local(kStream, nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color,
                        out_pitch, out_stats, stream);
+}
+
+extern "C" int compose_direct_send_roi(eqc_comm *comm, int n_local, const uint32_t *const *color,
+                                       const uint32_t *const *depth, const int32_t *d_src_roi, int w, int h,
+                                       int64_t pitch, int flags, int dest_rank, uint32_t *out_color,
+                                       int64_t out_pitch, void *stream) {
+  if (!d_src_roi || ((uintptr_t)d_src_roi & 15) != 0) return EQC_E_INVALID;
+  return compose_nccl(kDirectSend, comm, n_local, color, depth, w, h, pitch, EQC_OP_DEPTH, flags, dest_rank,
+                      out_color, out_pitch, stream, d_src_roi);
+}
+
+extern "C" int compose_direct_send_roi_local(int nranks, int n_local, const uint32_t *const *color,
+                                             const uint32_t *const *depth, const int32_t *d_src_roi, int w, int h,
+                                             int64_t pitch, int flags, int dest_rank, uint32_t *out_color,
+                                             int64_t out_pitch, int64_t *out_stats, void *stream) {
+  if (!d_src_roi || ((uintptr_t)d_src_roi & 15) != 0) return EQC_E_INVALID;
+  return compose_local(kDirectSend, nranks, n_local, color, depth, w, h, pitch, EQC_OP_DEPTH, flags, dest_rank,
+                       out_color, out_pitch, out_stats, stream, d_src_roi);
 }

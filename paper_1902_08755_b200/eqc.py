@@ -76,6 +76,8 @@ def _load():
         "compose_swap23_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
         "eqc_plan_swap23": ([i32, i32, i32, P, i32], i32),
         "compose_stream": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
+        "compose_direct_send_roi": ([P, i32, P, P, P, i32, i32, i64, i32, i32, P, i64, P], i32),
+        "compose_direct_send_roi_local": ([i32, i32, P, P, P, i32, i32, i64, i32, i32, P, i64, P, P], i32),
         "compose_stream_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
     }
     for name, (args, res) in sig.items():
@@ -403,3 +405,27 @@ def compose_stream_local(nranks, colors, depths, out_color, dest_rank: int = 0, 
                          op: int = OP_DEPTH, stream=None):
     return _compose_local(_lib.compose_stream_local, "compose_stream_local", nranks, colors, depths,
                           out_color, dest_rank, flags, op, stream)
+
+
+def compose_direct_send_roi(comm, colors, depths, d_src_roi, out_color=None, dest_rank: int = 0, flags: int = 0,
+                            stream=None):
+    """Direct send with application-provided source ROIs (device int32 [n_local, 4])."""
+    n = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    opitch = _frame_geom(out_color)[2] if out_color is not None else w
+    rc = _lib.compose_direct_send_roi(comm.handle, n, _ptrs(colors), _ptrs(depths), _addr(d_src_roi), w, h, pitch,
+                                      flags, dest_rank, _addr(out_color), opitch, _stream(stream))
+    return _check(rc, "compose_direct_send_roi")
+
+
+def compose_direct_send_roi_local(nranks, colors, depths, d_src_roi, out_color, dest_rank: int = 0, flags: int = 0,
+                                  stream=None):
+    total = len(colors)
+    w, h, pitch = _frame_geom(colors[0])
+    opitch = _frame_geom(out_color)[2]
+    stats = (ctypes.c_int64 * 4)()
+    rc = _lib.compose_direct_send_roi_local(nranks, total // nranks, _ptrs(colors), _ptrs(depths), _addr(d_src_roi),
+                                            w, h, pitch, flags, dest_rank, _addr(out_color), opitch, stats,
+                                            _stream(stream))
+    _check(rc, "compose_direct_send_roi_local")
+    return list(stats)

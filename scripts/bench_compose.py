@@ -69,6 +69,15 @@ def main():
     variants += [("swap23_nccl", eqc.compose_swap23, 0), ("swap23_rle", eqc.compose_swap23, eqc.FLAG_RLE),
                  ("stream_nccl", eqc.compose_stream, 0)]
     op = eqc.OP_BLEND if blend else eqc.OP_DEPTH
+    if not blend:  # application-provided ROIs: here the sources' exact boxes, from image_roi
+        app_roi = torch.zeros((len(dd), 4), dtype=torch.int32, device=dev)
+        eqc.image_roi(dd, app_roi, 0xFFFFFFFF)
+        torch.cuda.synchronize()
+
+        def ds_app_roi(comm_, dc_, dd_, final_, dest_rank=0, flags=0, op=0, stream=None):
+            return eqc.compose_direct_send_roi(comm_, dc_, dd_, app_roi, final_, dest_rank=dest_rank, flags=flags,
+                                               stream=stream)
+        variants.insert(2, ("direct_send_p2p_app_roi", ds_app_roi, 0))
     if blend:
         variants = [v for v in variants if "roi" not in v[0]]
     for name, fn, flags in variants:

@@ -78,6 +78,21 @@ def main():
         if algo == "ds" and st[0] != world - 1:
             failures.append(f"{algo}: rank {rank} sent {st[0]} band messages, want {world - 1}")
         dist.barrier()
+    # application-provided source ROIs, P2P and NCCL transports
+    for nl, w, h, dest, fl in [(2, 640, 361, 0, 0), (1, 300, 41, world - 1, X), (2, 1920, 1080, 1 % world, 0)]:
+        N = world * nl
+        c, d = synth.depth_sources(synth.SEED_BASE + 90 + N + w, N, w, h, mode="compact")
+        mine = range(rank * nl, (rank + 1) * nl)
+        dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
+        dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
+        r = torch.tensor([list(oracle.roi(d[i], 0xFFFFFFFF)) for i in mine], dtype=torch.int32, device=dev)
+        out = torch.zeros((h, w), dtype=torch.int32, device=dev)
+        for _ in range(2):
+            eqc.compose_direct_send_roi(comm, dc, dd, r, out if rank == dest else None, dest_rank=dest, flags=fl)
+        torch.cuda.synchronize()
+        if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.depth_composite(c, d)[0]).all():
+            failures.append(f"app-roi nl={nl} {w}x{h} flags={fl}: mismatch")
+        dist.barrier()
     # EQC_OP_BLEND: layers in rank-block draw order, result
     # within 1/255 of O2 over all layers (unorm16 partials across GPUs, R-C6)
     bcases = [("ds", 4, 640, 361, 0, 0), ("ds", 2, 300, 41, world - 1, X), ("ds", 3, 320, 181, 1 % world, R)]

@@ -168,3 +168,21 @@ def test_roi_host_validation(eqc):
     with pytest.raises(eqc.EqcError):
         eqc.compositor_blend_ordered_roi(c * 2, torch.zeros((2, 4), dtype=torch.int32, device="cuda"), out,
                                          order=[0, 0])  # not a permutation
+
+
+@pytest.mark.parametrize("nr,nl,w,h,loose,dest", [(2, 2, 640, 360, 0, 0), (3, 1, 300, 41, 5, 2), (4, 2, 257, 77, 0, 1)])
+def test_direct_send_with_application_rois_virtual_ranks(eqc, nr, nl, w, h, loose, dest):
+    # application-provided ROIs: exact or loose boxes around each
+    # source's rendered pixels; the result equals the full composite
+    N = nr * nl
+    c, d = synth.depth_sources(synth.SEED_BASE + 68 + N, N, w, h, mode="compact")
+    rois = []
+    for x in d:
+        rx, ry, rw, rh = oracle.roi(x, BG)
+        rois.append((rx - loose, ry - loose, rw + 2 * loose, rh + 2 * loose) if rw else (0, 0, 0, 0))
+    out = out_frame(h, w)
+    for flags in (0, eqc.FLAG_RLE):
+        eqc.compose_direct_send_roi_local(nr, [to_dev(x) for x in c], [to_dev(x) for x in d], roi_tensor(rois), out,
+                                          dest_rank=dest, flags=flags)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(to_host(out), oracle.depth_composite(c, d)[0])
