@@ -17,6 +17,8 @@
 #include <nccl.h>
 
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -1110,6 +1112,45 @@ __global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
 // The IPC-exposed `flags` allocation holds the barrier flags (EQC_MAX_SOURCES
 // ints) followed by the rank's partial-frame ROI {x, y, w, h} (kRoiSlot).
 constexpr int kRoiSlot = EQC_MAX_SOURCES;  // int offset, 16-byte aligned
+constexpr int kProgSlot = kRoiSlot + 4;    // progress counter of the rank's pipelined pre-composite
+constexpr int kFlagInts = kProgSlot + 4;
+#ifndef EQC_P2P_PIECES
+#define EQC_P2P_PIECES 2  // pieces per band of the pipelined peer-memory direct send
+#endif
+#ifndef EQC_P2P_AUX_PRIO
+#define EQC_P2P_AUX_PRIO 0  // 1: pulling stream at the highest priority (measured no better)
+#endif
+
+// Pipelined direct send: the owner publishes "pieces 0..k of every band of my
+// partial frame are complete" as a monotonic counter in its own flags page
+// (release, system scope) ...
+__global__ void p2p_signal_kernel(int *my_flags, int value) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(my_flags + kProgSlot), "r"(value) : "memory");
+  }
+}
+
+struct WaitArgs {
+  const int *peer_flags[EQC_MAX_SOURCES];
+  int n, target;
+};
+
+// ... and a puller waits until every rank's counter reached the piece
+// (acquire, system scope, polling peer memory over NVLink).
+__global__ void p2p_wait_kernel(const __grid_constant__ WaitArgs a) {
+  const int i = threadIdx.x;
+  if (i < a.n) {
+    const int *f = a.peer_flags[i] + kProgSlot;
+    int v;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v - a.target >= 0) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
 
 // Bounding box of the union of n ROIs {x, y, w, h} (empty ones ignored),
 // clipped by the consumer: the ROI of a partial frame whose sources hold data
@@ -1135,6 +1176,9 @@ __global__ void roi_union_kernel(const int32_t *in, int n, int32_t *out) {
 struct P2PState {
   int capable = -1;  // -1 unknown, 0 no (NCCL transport), 1 yes
   int64_t cap_px = 0;
+  int prog = 0;                    // this rank's published progress counter
+  cudaStream_t aux = nullptr;      // pulling stream of the pipelined direct send
+  cudaEvent_t ev_start = nullptr, ev_pulled = nullptr;
   DevBuf part_c, part_d, fin_c, flags, xfer, roi_local;
   std::vector<uint32_t *> peer_part_c, peer_part_d, peer_fin_c;
   std::vector<int *> peer_flags;
@@ -1179,8 +1223,9 @@ int p2p_setup(eqc_comm *c, int64_t px, cudaStream_t s) {
   EQC_TRY(P.part_d.ensure(bytes));
   EQC_TRY(P.fin_c.ensure(bytes));
   P.flags.release();
-  EQC_TRY(P.flags.ensure_zeroed((kRoiSlot + 4) * sizeof(int)));
+  EQC_TRY(P.flags.ensure_zeroed(kFlagInts * sizeof(int)));
   P.epoch = 0;
+  P.prog = 0;
   const int n = c->nranks;
   constexpr int kH = sizeof(cudaIpcMemHandle_t);
   std::vector<uint8_t> mine(4 * kH), all((size_t)n * 4 * kH);
@@ -1243,6 +1288,158 @@ int p2p_barrier(eqc_comm *c, cudaStream_t s) {
   a.epoch = ++P.epoch;
   p2p_barrier_kernel<<<1, 64, 0, s>>>(a);
   return eqc_launch_status();
+}
+
+// Pipelined peer-memory direct send ("chunked out-of-order
+// assembly overlapped with the exchange"): every
+// band is cut into K pieces; the owner pre-composites piece k of every band
+// and publishes its progress, while (on a second stream) each rank pulls
+// piece k of its band from every peer as soon as all of them have published
+// it -- the HBM-bound pre-composite of piece k+1 overlaps the NVLink-bound
+// pull + composite of piece k.  Used without EQC_FLAG_ROI (a computed ROI is
+// only known after the whole pre-composite); application ROIs are fine.
+int direct_send_p2p_pipelined(eqc_comm *c, const Geometry &g, const uint32_t *const *color,
+                              const uint32_t *const *depth, cudaStream_t s) {
+  P2PState &P = c->p2p;
+  const int n = c->nranks, me = c->rank, K = EQC_P2P_PIECES;
+  int64_t *stats = c->st.stats;
+  for (int i = 0; i < 4; ++i) stats[i] = 0;
+  std::vector<int> row0(n + 1);
+  plan_bands(g.h, n, row0.data());
+  auto piece = [&](int j, int k, int &y0, int &y1) {
+    const int len = row0[j + 1] - row0[j];
+    y0 = row0[j] + (int)((int64_t)k * len / K);
+    y1 = row0[j] + (int)((int64_t)(k + 1) * len / K);
+  };
+  if (!P.aux) {
+    // highest priority: the pulls are NVLink-bound and should take SMs as soon
+    // as a piece is published, ahead of the pending CTAs of the next piece's
+    // (HBM-bound) pre-composite
+    int lo = 0, hi = 0;
+    EQC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    EQC_CUDA_TRY(cudaStreamCreateWithPriority(&P.aux, cudaStreamNonBlocking, EQC_P2P_AUX_PRIO ? hi : lo));
+    EQC_CUDA_TRY(cudaEventCreateWithFlags(&P.ev_start, cudaEventDisableTiming));
+    EQC_CUDA_TRY(cudaEventCreateWithFlags(&P.ev_pulled, cudaEventDisableTiming));
+  }
+  const bool app_roi = g.src_roi && g.op == EQC_OP_DEPTH;
+  int32_t *my_roi = P.flags.as<int32_t>() + kRoiSlot;
+  std::vector<const int32_t *> src_rp(g.n_local);
+  if (app_roi) {
+    roi_union_kernel<<<1, 32, 0, s>>>(g.src_roi, g.n_local, my_roi);
+    EQC_TRY(eqc_launch_status());
+    for (int i = 0; i < g.n_local; ++i) src_rp[i] = g.src_roi + 4 * i;
+  }
+  // the pulls write the caller's frame (on dest): order them after its prior work
+  EQC_CUDA_TRY(cudaEventRecord(P.ev_start, s));
+  EQC_CUDA_TRY(cudaStreamWaitEvent(P.aux, P.ev_start, 0));
+  const int base = P.prog;
+  std::vector<const uint32_t *> cs(g.n_local), ds(g.n_local);
+  // EQC_P2P_TRACE=1: per-phase GPU times of this call on stderr (debug; syncs)
+  static const bool trace = getenv("EQC_P2P_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  mark(s);
+  for (int k = 0; k < K; ++k) {
+    // (1) piece k of every band of my partial frame
+    for (int j = 0; j < n; ++j) {
+      int y0, y1;
+      piece(j, k, y0, y1);
+      if (y1 <= y0) continue;
+      const size_t so = (size_t)y0 * g.pitch, po = (size_t)y0 * g.w;
+      for (int i = 0; i < g.n_local; ++i) {
+        cs[i] = color[i] + so;
+        ds[i] = depth ? depth[i] + so : nullptr;
+      }
+      uint32_t *pc = P.part_c.as<uint32_t>() + po, *pd = P.part_d.as<uint32_t>() + po;
+      if (app_roi) {
+        EQC_TRY(eqc_depth_roi_launch(g.n_local, cs.data(), ds.data(), src_rp.data(), y0, my_roi, g.w, y1 - y0,
+                                     g.pitch, pc, pd, g.w, s));
+      } else if (g.op == EQC_OP_BLEND) {
+        EQC_TRY(eqc_blend_to_partial(g.n_local, cs.data(), g.w, y1 - y0, g.pitch, pc, pd, g.w, s));
+      } else if (g.op == EQC_OP_AVERAGE) {
+        EQC_TRY(eqc_average(true, g.n_local, cs.data(), nullptr, g.w, y1 - y0, g.pitch, g.n * g.n_local, nullptr,
+                            pc, pd, g.w, s));
+      } else {
+        EQC_TRY(compositor_depth(g.n_local, cs.data(), ds.data(), g.w, y1 - y0, g.pitch, pc, pd, g.w, s));
+      }
+    }
+    p2p_signal_kernel<<<1, 32, 0, s>>>(P.flags.as<int>(), base + k + 1);
+    EQC_TRY(eqc_launch_status());
+    mark(s);
+    // (2)-(4) on the pulling stream: wait for piece k everywhere, pull + composite it
+    WaitArgs wa;
+    for (int q = 0; q < n; ++q) wa.peer_flags[q] = P.peer_flags[q];
+    wa.n = n;
+    wa.target = base + k + 1;
+    p2p_wait_kernel<<<1, 64, 0, P.aux>>>(wa);
+    EQC_TRY(eqc_launch_status());
+    mark(P.aux);
+    int y0, y1;
+    piece(me, k, y0, y1);
+    if (y1 <= y0) continue;
+    std::vector<const uint32_t *> pc(n), pd(n);
+    for (int q = 0; q < n; ++q) {
+      pc[q] = P.peer_part_c[q] + (size_t)y0 * g.w;
+      pd[q] = P.peer_part_d[q] + (size_t)y0 * g.w;
+    }
+    uint32_t *out = me == g.dest ? g.out + (size_t)y0 * g.out_pitch : P.peer_fin_c[g.dest] + (size_t)y0 * g.w;
+    const int64_t opitch = me == g.dest ? g.out_pitch : g.w;
+    if (app_roi) {
+      std::vector<const int32_t *> rp(n);
+      for (int q = 0; q < n; ++q) rp[q] = P.peer_flags[q] + kRoiSlot;
+      EQC_TRY(eqc_depth_roi_launch(n, pc.data(), pd.data(), rp.data(), y0, nullptr, g.w, y1 - y0, g.w, out,
+                                   nullptr, opitch, P.aux));
+    } else {
+      EQC_TRY(op_final(g, n, pc.data(), pd.data(), y1 - y0, out, opitch, P.aux));
+    }
+  }
+  mark(P.aux);
+  P.prog = base + K;
+  {
+    const int y0 = row0[me], rows = row0[me + 1] - row0[me];
+    for (int q = 0; q < n && rows > 0; ++q)
+      if (q != me) {
+        stats[0] += 1;
+        stats[3] += (int64_t)rows * g.w * 8;
+      }
+    if (me != g.dest && rows > 0) {
+      stats[1] += 1;
+      stats[2] += (int64_t)rows * g.w * 4;
+    }
+    (void)y0;
+  }
+  EQC_CUDA_TRY(cudaEventRecord(P.ev_pulled, P.aux));
+  EQC_CUDA_TRY(cudaStreamWaitEvent(s, P.ev_pulled, 0));
+  // every band is complete on the destination (and nobody reads partials)
+  EQC_TRY(p2p_barrier(c, s));
+  if (me == g.dest) {
+    for (int q = 0; q < n; ++q) {
+      const int qy0 = row0[q], qrows = row0[q + 1] - row0[q];
+      if (q == me || qrows == 0) continue;
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)qy0 * g.out_pitch, g.out_pitch * 4,
+                                     P.fin_c.as<uint32_t>() + (size_t)qy0 * g.w, (size_t)g.w * 4, (size_t)g.w * 4,
+                                     qrows, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  mark(s);
+  if (trace) {
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[eqc p2p rank %d] us since start:", me);
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      fprintf(stderr, " %.1f", ms * 1e3);
+    }
+    fprintf(stderr, "  (pre k, wait k, ..., pulls done, end)\n");
+    for (auto e : tev) cudaEventDestroy(e);
+  }
+  return EQC_OK;
 }
 
 int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *color, const uint32_t *const *depth,
@@ -1353,6 +1550,9 @@ extern "C" int eqc_comm_destroy(eqc_comm *comm) {
   if (!comm) return EQC_E_INVALID;
   cudaDeviceSynchronize();
   comm->p2p.close_peers(comm->rank);
+  if (comm->p2p.aux) cudaStreamDestroy(comm->p2p.aux);
+  if (comm->p2p.ev_start) cudaEventDestroy(comm->p2p.ev_start);
+  if (comm->p2p.ev_pulled) cudaEventDestroy(comm->p2p.ev_pulled);
   comm->p2p.part_c.release();
   comm->p2p.part_d.release();
   comm->p2p.fin_c.release();
@@ -1418,7 +1618,9 @@ static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *
   cudaStream_t s = (cudaStream_t)stream;
   if (ds && comm->nranks > 1 && !(flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) {
     EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
-    if (comm->p2p.capable == 1) return direct_send_p2p(comm, g, color, depth, s);
+    if (comm->p2p.capable == 1)
+      return (flags & EQC_FLAG_ROI) ? direct_send_p2p(comm, g, color, depth, s)
+                                    : direct_send_p2p_pipelined(comm, g, color, depth, s);
   }
   NcclTransport T(comm->nccl, s);
   std::vector<RankState *> ranks{&comm->st};
