@@ -1618,9 +1618,14 @@ static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *
   cudaStream_t s = (cudaStream_t)stream;
   if (ds && comm->nranks > 1 && !(flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) {
     EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
-    if (comm->p2p.capable == 1)
-      return (flags & EQC_FLAG_ROI) ? direct_send_p2p(comm, g, color, depth, s)
-                                    : direct_send_p2p_pipelined(comm, g, color, depth, s);
+    if (comm->p2p.capable == 1) {
+      // pieces pay off only when each rank's pre-composite is substantial
+      // (measured: >= 2 sources and >= 6 Mpx per band; below that the extra
+      // launches and flag round trips cost more than the overlap gains)
+      const bool big = n_local >= 2 && (int64_t)w * (h / comm->nranks) >= (int64_t)6 << 20;
+      return (!(flags & EQC_FLAG_ROI) && big) ? direct_send_p2p_pipelined(comm, g, color, depth, s)
+                                              : direct_send_p2p(comm, g, color, depth, s);
+    }
   }
   NcclTransport T(comm->nccl, s);
   std::vector<RankState *> ranks{&comm->st};
