@@ -140,11 +140,11 @@ def make_inputs(seed, n, w, h):
 
 def launches_per_compose(n, exchange):
     """Our kernels per compose_direct_send call: local pre-composite + band
-    composite (+ n-1 band encodes of 3 kernels each and one decode batch with
+    composite (+ n-1 band encodes of 3 kernels each and one decode batch (2 kernels) with
     RLE).  NCCL's own kernels are not counted."""
     if exchange == "raw":  # pre-composite, 2 flag barriers, fused pull+composite
         return 4
-    return 2 + (3 * (n - 1) + 1 if exchange == "rle" else 0)
+    return 2 + (3 * (n - 1) + 2 if exchange == "rle" else 0)
 
 
 def run_eqc(args):

@@ -27,6 +27,9 @@
 #ifndef EQC_ENC_MINB
 #define EQC_ENC_MINB (32 / EQC_ENC_WARPS)  // 64 registers: 32 warps per SM
 #endif
+#ifndef EQC_DEC_MINB
+#define EQC_DEC_MINB 3  // 80 registers (measured best for the v1 decoder)
+#endif
 #ifndef EQC_FUSED_MINB
 #define EQC_FUSED_MINB 8  // 32 warps per SM (64 registers)
 #endif
@@ -729,15 +732,34 @@ __device__ __forceinline__ void rle64_decode_group(const DecImage im, const Stre
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_constant__ DecParams p) {
-  __shared__ __align__(16) uint8_t stage[kWarps][kStageBytes];
+// RLE-64 streams of a batch (R-C17): launched with the same geometry as
+// rle_decode_kernel, each kernel skips the other codec's streams, so each
+// keeps its own register allocation.
+__global__ void __launch_bounds__(kWarps * 32) rle64_decode_kernel(const __grid_constant__ DecParams p) {
+  __shared__ StreamHdr s_hd;
+  __shared__ __align__(4) uint8_t s_mark[kWarps][64];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int m = (int)(blockIdx.x / p.tiles_per_image);
+  const int64_t lt = blockIdx.x - (int64_t)m * p.tiles_per_image;
+  const DecImage im = p.img[m];
+  if (tid == 0) s_hd = read_header(im.src, im.src_bytes, p.w, p.h, true);  // rle_decode_kernel flags bad headers
+  __syncthreads();
+  const StreamHdr hd = s_hd;
+  if (!hd.ok || hd.flags != EQC_FLAG_RLE64) return;
+  const int64_t cb = (lt * kWarps + warp) * kGroup;
+  if (cb < hd.nchunks) rle64_decode_group(im, hd, cb, p.w, p.pitch, p.vec != 0, p.status, s_mark[warp]);
+}
+
+constexpr int kStage2 = 560;  // >= 15 + 520 record bytes, multiple of 16
+
+__global__ void __launch_bounds__(kWarps * 32, EQC_DEC_MINB) rle_decode_kernel(const __grid_constant__ DecParams p) {
+  __shared__ __align__(16) uint8_t stage[kWarps][2][kStage2];  // double buffer: next record in flight
   __shared__ __align__(16) uint16_t info[kWarps][kC];
   __shared__ StreamHdr s_hd;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = (int)(blockIdx.x / p.tiles_per_image);
   const int64_t lt = blockIdx.x - (int64_t)m * p.tiles_per_image;
   const DecImage im = p.img[m];
-  __shared__ __align__(4) uint8_t s_mark[kWarps][64];
   if (tid == 0) {
     s_hd = read_header(im.src, im.src_bytes, p.w, p.h, true);
     if (!s_hd.ok) set_corrupt(p.status);
@@ -745,11 +767,7 @@ __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_co
   __syncthreads();
   const StreamHdr hd = s_hd;
   if (!hd.ok) return;
-  if (hd.flags == EQC_FLAG_RLE64) {  // the 64-bit token codec (R-C17)
-    const int64_t cb = (lt * kWarps + warp) * kGroup;
-    if (cb < hd.nchunks) rle64_decode_group(im, hd, cb, p.w, p.pitch, p.vec != 0, p.status, s_mark[warp]);
-    return;
-  }
+  if (hd.flags == EQC_FLAG_RLE64) return;  // decoded by rle64_decode_kernel (same launch geometry)
   const int C = 1 << hd.log2c;
   const int r = kC / C;
   const bool swz = (hd.flags & EQC_FLAG_SWIZZLE) != 0;
@@ -773,6 +791,19 @@ __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_co
     const unsigned bad = __ballot_sync(EQC_FULL, has && !ok);
     if (bad && lane == 0) set_corrupt(p.status);
     const int nhere = (int)min((int64_t)kGroup, hd.nchunks - cb);
+    // non-constant, valid chunks: their records are staged with 16-byte
+    // cp.async, the next one in flight while the current one is decoded
+    const unsigned live = nhere == 32 ? EQC_FULL : ((1u << nhere) - 1u);
+    unsigned todo = __ballot_sync(EQC_FULL, has && ok && !cst) & ~bad & live;
+    auto issue = [&](int j, int b) {
+      const int64_t offj = __shfl_sync(EQC_FULL, off, j);
+      const uint32_t psj = __shfl_sync(EQC_FULL, ps, j);
+      const uint8_t *rec = im.src + hd.payload0 + offj;
+      stage_async16(im.src, im.src_bytes, rec, record_quads(rec, psj), reinterpret_cast<uint4 *>(stage[warp][b]), lane);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int buf = 0;
+    if (todo) issue(__ffs(todo) - 1, 0);
     for (int i = 0; i < nhere; ++i) {
       if ((bad >> i) & 1u) continue;
       const int yi = __shfl_sync(EQC_FULL, y, i);
@@ -787,8 +818,19 @@ __global__ void __launch_bounds__(kWarps * 32) rle_decode_kernel(const __grid_co
       } else {
         const int64_t offi = __shfl_sync(EQC_FULL, off, i);
         const uint32_t psi = __shfl_sync(EQC_FULL, ps, i);
-        if (!decode_record(im.src, im.src_bytes, im.src + hd.payload0 + offi, psi, Li, lane, stage[warp],
-                           info[warp], px)) {
+        todo &= ~(1u << i);
+        if (todo) {  // the next record streams in while this one is decoded
+          issue(__ffs(todo) - 1, buf ^ 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        const uint8_t *rec = im.src + hd.payload0 + offi;
+        const bool okr = decode_staged(stage[warp][buf] + ((uintptr_t)rec & 15u), psi, Li, lane, info[warp], px);
+        __syncwarp();  // the buffer is refilled two records later
+        buf ^= 1;
+        if (!okr) {
           if (lane == 0) set_corrupt(p.status);
           continue;
         }
@@ -1158,6 +1200,7 @@ extern "C" int image_decompress_rle_batch(int count, const uint8_t *const *src, 
   const int64_t grid = (int64_t)count * p.tiles_per_image;
   if (grid > 0x7FFFFFFFll) return EQC_E_INVALID;
   rle_decode_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
+  rle64_decode_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
 
