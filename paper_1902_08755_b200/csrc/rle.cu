@@ -31,7 +31,7 @@
 #define EQC_DEC_MINB 3  // 80 registers (measured best for the v1 decoder)
 #endif
 #ifndef EQC_FUSED_MINB
-#define EQC_FUSED_MINB 8  // 32 warps per SM (64 registers)
+#define EQC_FUSED_MINB (32 / EQC_FWARPS)  // 32 warps per SM (64 registers)
 #endif
 #ifndef EQC_CLS_BATCH
 #define EQC_CLS_BATCH 8
@@ -859,7 +859,10 @@ struct FusedParams {
 };
 
 constexpr int kMaxStreams = 2 * EQC_MAX_SOURCES;
-constexpr int kFWarps = 4;      // fused kernel: one chunk position per warp, 4 warps per CTA
+#ifndef EQC_FWARPS
+#define EQC_FWARPS 4
+#endif
+constexpr int kFWarps = EQC_FWARPS;  // fused kernel: one chunk position per warp, EQC_FWARPS warps per CTA
 constexpr int kPreWords = 1024; // per-warp record prefetch buffer (4 KB)
 
 // Warp per 8 consecutive chunk positions.
