@@ -22,10 +22,10 @@
 #include "rle.cuh"
 
 #ifndef EQC_ENC_WARPS
-#define EQC_ENC_WARPS 2
+#define EQC_ENC_WARPS 1
 #endif
 #ifndef EQC_ENC_MINB
-#define EQC_ENC_MINB (32 / EQC_ENC_WARPS)  // 64 registers: 32 warps per SM
+#define EQC_ENC_MINB 28  // 1-warp CTAs at 72 registers (measured best: no spills, no intra-CTA imbalance)
 #endif
 #ifndef EQC_DEC_MINB
 #define EQC_DEC_MINB 3  // 80 registers (measured best for the v1 decoder)
