@@ -735,19 +735,29 @@ __device__ __forceinline__ void rle64_decode_group(const DecImage im, const Stre
 // RLE-64 streams of a batch (R-C17): launched with the same geometry as
 // rle_decode_kernel, each kernel skips the other codec's streams, so each
 // keeps its own register allocation.
+// Grid-stride over (image, tile): images of the other codec are skipped
+// whole after one header read, so a batch without RLE-64 streams costs a
+// couple of microseconds.
 __global__ void __launch_bounds__(kWarps * 32) rle64_decode_kernel(const __grid_constant__ DecParams p) {
   __shared__ StreamHdr s_hd;
   __shared__ __align__(4) uint8_t s_mark[kWarps][64];
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int m = (int)(blockIdx.x / p.tiles_per_image);
-  const int64_t lt = blockIdx.x - (int64_t)m * p.tiles_per_image;
-  const DecImage im = p.img[m];
-  if (tid == 0) s_hd = read_header(im.src, im.src_bytes, p.w, p.h, true);  // rle_decode_kernel flags bad headers
-  __syncthreads();
-  const StreamHdr hd = s_hd;
-  if (!hd.ok || hd.flags != EQC_FLAG_RLE64) return;
-  const int64_t cb = (lt * kWarps + warp) * kGroup;
-  if (cb < hd.nchunks) rle64_decode_group(im, hd, cb, p.w, p.pitch, p.vec != 0, p.status, s_mark[warp]);
+  const int64_t ntiles = (int64_t)p.count * p.tiles_per_image;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int m = (int)(t / p.tiles_per_image);
+    const int64_t lt = t - (int64_t)m * p.tiles_per_image;
+    const DecImage im = p.img[m];
+    __syncthreads();  // s_hd of the previous tile is no longer read
+    if (tid == 0) s_hd = read_header(im.src, im.src_bytes, p.w, p.h, true);  // rle_decode_kernel flags bad ones
+    __syncthreads();
+    const StreamHdr hd = s_hd;
+    if (!hd.ok || hd.flags != EQC_FLAG_RLE64) {
+      t += (p.tiles_per_image - 1 - lt) / gridDim.x * gridDim.x;  // skip this image's remaining tiles
+      continue;
+    }
+    const int64_t cb = (lt * kWarps + warp) * kGroup;
+    if (cb < hd.nchunks) rle64_decode_group(im, hd, cb, p.w, p.pitch, p.vec != 0, p.status, s_mark[warp]);
+  }
 }
 
 constexpr int kStage2 = 560;  // >= 15 + 520 record bytes, multiple of 16
@@ -1203,7 +1213,8 @@ extern "C" int image_decompress_rle_batch(int count, const uint8_t *const *src, 
   const int64_t grid = (int64_t)count * p.tiles_per_image;
   if (grid > 0x7FFFFFFFll) return EQC_E_INVALID;
   rle_decode_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
-  rle64_decode_kernel<<<(unsigned)grid, kWarps * 32, 0, (cudaStream_t)stream>>>(p);
+  rle64_decode_kernel<<<(unsigned)std::min<int64_t>(grid, (int64_t)eqc_num_sms() * 32), kWarps * 32, 0,
+                        (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
 
