@@ -57,10 +57,10 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=(), extra=()) -> str:
     """Compile and link libeqc.  ``out``/``defines`` build tuning variants
     (e.g. ``defines=["EQC_ENC_WARPS=4"]``) next to the default library."""
-    if out == LIB and not defines and not force and not needs_build():
+    if out == LIB and not defines and not extra and not force and not needs_build():
         return LIB
     obj_dir = OBJ if out == LIB else out + ".objs"
     os.makedirs(obj_dir, exist_ok=True)
@@ -70,7 +70,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     procs = []
     for src in sources():
         obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *CFLAGS, *extra_inc, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *CFLAGS, *extra, *extra_inc, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if inc:
             cmd += ["-DEQC_HAVE_NCCL=1"]
         if verbose:
