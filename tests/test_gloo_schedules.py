@@ -195,3 +195,111 @@ def test_schedule_equals_oracle_over_all_sources(algo, world, n_local, w, h, des
         assert msgs == world * (world - 1)  # n(n-1) band messages
     elif algo == "bs":
         assert msgs == world * (world.bit_length() - 1)  # n log2 n swaps
+
+
+# ---- ordered blending through the schedules ---------
+# The schedule must merge partials in rank (= draw) order: "over" is not
+# commutative.  Partials are exact float64 premultiplied (rgb, a) planes here
+# (test-side arithmetic: the plain definition x = s + x (1 - a_s)); the final
+# band is rounded once and compared with O2 over all layers.
+def _over(back, front):
+    return front + back * (1.0 - front[..., 3:4])
+
+
+def _partial(layers):
+    acc = np.zeros(layers[0].shape + (4,))
+    for l in layers:
+        acc = _over(acc, l.view(np.uint8).reshape(l.shape + (4,)).astype(np.float64) / 255.0)
+    return acc
+
+
+def _blend_worker(rank, world, port, algo, n_local, w, h, dest, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def xchg(sends, recvs):
+        reqs, outs = [], []
+        for arr, dst in sends:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(arr)), dst))
+        for shape, src in recvs:
+            t = torch.empty(shape, dtype=torch.float64)
+            reqs.append(dist.irecv(t, src))
+            outs.append(t)
+        for r in reqs:
+            r.wait()
+        return [o.numpy() for o in outs]
+
+    try:
+        n = world * n_local
+        layers = synth.premultiplied_noise(900 + n, n, w, h)
+        part = _partial(layers[rank * n_local:(rank + 1) * n_local])
+        if algo == "ds":
+            row0 = eqc.eqc_plan_bands(h, world)
+            y0, y1 = row0[rank], row0[rank + 1]
+            sends = [(part[row0[j]:row0[j + 1]], j) for j in range(world) if j != rank and row0[j + 1] > row0[j]]
+            srcs = [q for q in range(world) if q != rank and y1 > y0]
+            got = dict(zip(srcs, xchg(sends, [((y1 - y0, w, 4), q) for q in srcs])))
+            band = np.zeros((y1 - y0, w, 4))
+            for q in range(world):  # rank order = draw order
+                band = _over(band, part[y0:y1] if q == rank else got[q]) if y1 > y0 else band
+            regions = [(row0[q], row0[q + 1]) for q in range(world)]
+            fin = band
+        else:  # 2-3 swap
+            plan = eqc.eqc_plan_swap23(h, world, rank)
+            cur = part.copy()
+            if plan["fold_role"] == 2:
+                xchg([(cur, plan["fold_partner"])], [])
+            elif plan["fold_role"] == 1:
+                (their,) = xchg([], [((h, w, 4), plan["fold_partner"])])
+                cur = _over(cur, their)  # the partner holds the next (front) layers
+            for rd in plan["rounds"]:
+                k, t, mem, bnd = rd["k"], rd["t"], rd["members"], rd["bounds"]
+                ky0, ky1 = bnd[t], bnd[t + 1]
+                sends = [(cur[bnd[u]:bnd[u + 1]], mem[u]) for u in range(k) if u != t and bnd[u + 1] > bnd[u]]
+                others = [u for u in range(k) if u != t] if ky1 > ky0 else []
+                got = xchg(sends, [((ky1 - ky0, w, 4), mem[u]) for u in others])
+                if ky1 > ky0:
+                    parts = {t: cur[ky0:ky1].copy(), **{u: g for u, g in zip(others, got)}}
+                    acc = np.zeros((ky1 - ky0, w, 4))
+                    for u in range(k):
+                        acc = _over(acc, parts[u])
+                    cur[ky0:ky1] = acc
+            regions = [eqc.eqc_plan_swap23(h, world, q)["final"] for q in range(world)]
+            y0, y1 = regions[rank]
+            fin = cur[y0:y1]
+        if rank != dest:
+            if y1 > y0:
+                xchg([(fin, dest)], [])
+            result_q.put((rank, None))
+        else:
+            out = np.zeros((h, w, 4))
+            out[y0:y1] = fin
+            for q in range(world):
+                qy0, qy1 = regions[q]
+                if q != dest and qy1 > qy0:
+                    (out[qy0:qy1],) = xchg([], [((qy1 - qy0, w, 4), q)])
+            got8 = np.clip(np.floor(255.0 * out + 0.5), 0, 255).astype(np.uint8)
+            want = oracle.blend_ordered(layers).view(np.uint8).reshape(h, w, 4)
+            result_q.put((rank, int(np.abs(got8.astype(int) - want.astype(int)).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("algo,world,n_local,w,h,dest", [
+    ("ds", 2, 3, 40, 21, 0), ("ds", 3, 2, 33, 17, 2), ("s23", 3, 2, 24, 19, 1), ("s23", 5, 1, 20, 11, 4),
+])
+def test_blend_schedule_keeps_draw_order(algo, world, n_local, w, h, dest):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blend_worker, args=(r, world, port, algo, n_local, w, h, dest, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    err = [r[1] for r in res if r[0] == dest]
+    assert err[0] <= 1  # float64 partials: the exact chain, rounded once (R-C4)
