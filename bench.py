@@ -138,12 +138,12 @@ def make_inputs(seed, n, w, h):
     return c, d
 
 
-def launches_per_compose(n, exchange):
+def launches_per_compose(n, exchange, slots=False):
     """Our kernels per compose_direct_send call: local pre-composite + band
     composite (+ n-1 band encodes of 3 kernels each and one decode batch (2 kernels) with
     RLE).  NCCL's own kernels are not counted."""
-    if exchange == "raw":  # pre-composite, 2 flag barriers, fused pull+composite
-        return 4
+    if exchange == "raw":  # pre-composite (not with frame slots), 2 flag barriers, fused pull+composite
+        return 3 if slots else 4
     return 2 + (3 * (n - 1) + 2 if exchange == "rle" else 0)
 
 
@@ -184,6 +184,19 @@ def run_eqc(args):
         comm = eqc.Comm.from_torch_distributed()
         final = torch.empty((H, W), dtype=torch.int32, device=dev) if rank == 0 else None
     xflags = {"raw": 0, "rle": eqc.FLAG_RLE, "nccl": eqc.FLAG_NCCL}[args.exchange]
+    slots = False
+    if comm is not None and args.exchange == "raw" and args.frame_slots:
+        # decode the partial frames straight into the comm's peer-mapped slots:
+        # the direct send reads them in place (no pre-composite copy) and the
+        # peers' bands land in rank 0's final frame directly.  Opt-in: it cuts
+        # the compose latency by ~30 % (scripts/bench_compose.py, 1 partial per
+        # GPU) but measured 2-4 % LOWER pipelined throughput
+        fb = [comm.frame_buffers(W, H, i) for i in range(2)]
+        if all(x is not None for x in fb):
+            slots = True
+            outs = [(x[0], x[1]) for x in fb]
+            out_c, out_d = outs[0]
+            final = fb[0][2] if rank == 0 else None
     # asynchronous compositing pipeline: the multi-GPU exchange +
     # composite of frame k runs on its own stream while frame k+1 is encoded
     pipelined = world > 1 and not args.no_pipeline
@@ -372,7 +385,9 @@ def run_eqc(args):
             "l2": f"inputs larger than L2 ({len(imgs) * 4 * P / 1e6:.0f} MB of source frames per step > 126 MB L2)",
             "parallelism": (f"screen-partition direct send ({args.exchange}) over {world} GPU(s)" +
                             (", compose of frame k overlapped with frame k+1 (async compositing pipeline, "
-                             "P:2302-2310)" if pipelined else "")) if world > 1 else "single GPU",
+                             "P:2302-2310)" if pipelined else "") +
+                            (", partial frames decoded into peer-mapped frame slots (zero-copy)" if slots else "")
+                            ) if world > 1 else "single GPU",
         },
         "output_mpx_per_s": round(world * P / (ms * 1e-3) / 1e6, 1),
         "compose_direct_send_latency_ms_rank0": round(comp_ms, 4) if world > 1 else None,
@@ -396,7 +411,7 @@ def run_eqc(args):
         "e2e": {"value": round(world * NSRC * P / (e2e_ms * 1e-3) / 1e6, 1), "unit": UNIT,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         # per step: encode batch (encode, run scan, compaction kernels) + fused decode/composite
-        "gpu_launches": (4 + (launches_per_compose(world, args.exchange) if world > 1 else 0)) * args.steps,
+        "gpu_launches": (4 + (launches_per_compose(world, args.exchange, slots) if world > 1 else 0)) * args.steps,
         "clocks": clocks,
     }
     emit(line)
@@ -483,6 +498,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="rows of the frame in one CPU-oracle sample (0 = calibrate to a time budget)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--frame-slots", action="store_true",
+                    help="N>1: decode into the comm's peer-mapped frame slots (zero-copy direct send)")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N > 1: run the multi-GPU compose of frame k before encoding frame k+1")
     ap.add_argument("--exchange", default="raw", choices=["raw", "rle", "nccl"],

@@ -63,6 +63,37 @@ EQC_API int eqc_comm_destroy(eqc_comm *comm);
 EQC_API int eqc_comm_stats(const eqc_comm *comm, int64_t out[4]);
 
 /*
+ * eqc_comm_frame_buffers -- zero-copy partial frames for the peer-memory
+ * direct send (collective: every rank calls it with the same w, h; the first
+ * call for a size allocates and maps, later calls are host-only lookups).
+ * The asynchronous pipeline renders / decodes frame k into a buffer while
+ * frame k-1 is composited; when that buffer is one the peers
+ * have mapped, the pre-composite copy of step (1) disappears: the band
+ * composite reads it in place over NVLink.
+ *   slot        0 or 1 (two slots: one being composited, one being filled).
+ *   *color, *depth  receive slot `slot`'s device buffers, [h][w] u32 each
+ *               (pitch w).  Pass them (n_local = 1, pitch = w, EQC_OP_DEPTH,
+ *               no ROI) to compose_direct_send and it skips the local copy;
+ *               EVERY rank must then pass its own slot-`slot` buffers (like
+ *               the matching calls of a collective).
+ *   *final_color  receives the comm's gather buffer [h][w]: passed as
+ *               out_color (out_pitch = w) on dest_rank, the peers' bands land
+ *               in it directly and the final band copy is skipped.
+ *   stream      orders the collective setup (the call synchronises it on the
+ *               first use of a size).
+ * Ownership: the buffers belong to `comm` and stay valid until
+ * eqc_comm_destroy, a larger eqc_comm_frame_buffers call, or (final_color
+ * only) a compose call on a larger frame.  Reuse of a slot must wait for the
+ * compose that read it (stream order / an event): peers read it until that
+ * compose's closing barrier.
+ * Errors: EQC_E_INVALID (arguments), EQC_E_UNSUPPORTED (one rank, or the
+ * ranks cannot map each other's memory: use your own buffers, the NCCL
+ * transport takes them), EQC_E_CUDA, EQC_E_NCCL.
+ */
+EQC_API int eqc_comm_frame_buffers(eqc_comm *comm, int w, int h, int slot, uint32_t **color, uint32_t **depth,
+                                   uint32_t **final_color, void *stream);
+
+/*
  * Host-side schedule plans (no GPU needed; used by the executors below and
  * by the tests).
  * eqc_plan_bands: row0[j] = floor(j*h/n), j = 0..n (band j = rows

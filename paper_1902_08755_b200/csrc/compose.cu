@@ -1183,6 +1183,31 @@ struct P2PState {
   std::vector<uint32_t *> peer_part_c, peer_part_d, peer_fin_c;
   std::vector<int *> peer_flags;
   int epoch = 0;
+  // caller-visible, peer-mapped frame slots (eqc_comm_frame_buffers): a
+  // partial frame rendered / decoded straight into slot i is read by the
+  // peers in place (no pre-composite copy)
+  static constexpr int kSlots = 2;
+  int64_t slot_px = 0;
+  DevBuf slot_c[kSlots], slot_d[kSlots];
+  std::vector<uint32_t *> peer_slot_c[kSlots], peer_slot_d[kSlots];
+
+  // slot of (color, depth) when they are exactly slot i's buffers, else -1
+  int slot_of(const uint32_t *color, const uint32_t *depth) const {
+    for (int i = 0; i < kSlots; ++i)
+      if (slot_c[i].p && color == slot_c[i].as<uint32_t>() && depth == slot_d[i].as<uint32_t>()) return i;
+    return -1;
+  }
+  void close_slots(int rank) {
+    for (int i = 0; i < kSlots; ++i) {
+      for (size_t q = 0; q < peer_slot_c[i].size(); ++q) {
+        if ((int)q == rank) continue;
+        if (peer_slot_c[i][q]) cudaIpcCloseMemHandle(peer_slot_c[i][q]);
+        if (peer_slot_d[i][q]) cudaIpcCloseMemHandle(peer_slot_d[i][q]);
+      }
+      peer_slot_c[i].clear();
+      peer_slot_d[i].clear();
+    }
+  }
 
   void close_peers(int rank) {
     for (size_t q = 0; q < peer_part_c.size(); ++q) {
@@ -1211,6 +1236,52 @@ struct eqc_comm {
 
 namespace {
 
+// Exchange the IPC handles of this rank's k allocations `ptrs` with every
+// rank and open the peers' (collective).  out[i][q] = rank q's allocation i
+// as mapped here (this rank's own pointer at q == rank).  `ok` is the
+// all-rank AND of "every handle was created and opened".
+int ipc_exchange(eqc_comm *c, void *const *ptrs, int k, std::vector<std::vector<void *>> &out, int &ok,
+                 cudaStream_t s) {
+  P2PState &P = c->p2p;
+  const int n = c->nranks;
+  constexpr int kH = sizeof(cudaIpcMemHandle_t);
+  std::vector<uint8_t> mine((size_t)k * kH), all((size_t)n * k * kH);
+  ok = 1;
+  for (int i = 0; i < k; ++i) {
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, ptrs[i]) != cudaSuccess) ok = 0;
+    std::memcpy(mine.data() + (size_t)i * kH, &h, kH);
+  }
+  EQC_TRY(P.xfer.ensure((size_t)(n + 1) * k * kH + 64));
+  uint8_t *dx = P.xfer.as<uint8_t>();
+  EQC_CUDA_TRY(cudaMemcpyAsync(dx, mine.data(), mine.size(), cudaMemcpyHostToDevice, s));
+  EQC_NCCL_TRY(ncclAllGather(dx, dx + mine.size(), mine.size(), ncclUint8, c->nccl, s));
+  EQC_CUDA_TRY(cudaMemcpyAsync(all.data(), dx + mine.size(), all.size(), cudaMemcpyDeviceToHost, s));
+  EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  out.assign(k, std::vector<void *>(n, nullptr));
+  for (int q = 0; q < n && ok; ++q)
+    for (int i = 0; i < k && ok; ++i) {
+      if (q == c->rank) {
+        out[i][q] = ptrs[i];
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, all.data() + ((size_t)q * k + i) * kH, kH);
+      if (cudaIpcOpenMemHandle(&out[i][q], h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        out[i][q] = nullptr;
+        ok = 0;
+      }
+    }
+  cudaGetLastError();  // a failed open is reported through `ok`
+  // agree on the transport: P2P only if every rank mapped every peer
+  int *dok = reinterpret_cast<int *>(dx);
+  EQC_CUDA_TRY(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+  EQC_NCCL_TRY(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->nccl, s));
+  EQC_CUDA_TRY(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  return EQC_OK;
+}
+
 // (Re)build the IPC mappings for frames of `px` pixels.  Collective.
 int p2p_setup(eqc_comm *c, int64_t px, cudaStream_t s) {
   P2PState &P = c->p2p;
@@ -1226,55 +1297,57 @@ int p2p_setup(eqc_comm *c, int64_t px, cudaStream_t s) {
   EQC_TRY(P.flags.ensure_zeroed(kFlagInts * sizeof(int)));
   P.epoch = 0;
   P.prog = 0;
-  const int n = c->nranks;
-  constexpr int kH = sizeof(cudaIpcMemHandle_t);
-  std::vector<uint8_t> mine(4 * kH), all((size_t)n * 4 * kH);
-  int ok = 1;
   void *ptrs[4] = {P.part_c.p, P.part_d.p, P.fin_c.p, P.flags.p};
-  for (int i = 0; i < 4; ++i) {
-    cudaIpcMemHandle_t h;
-    if (cudaIpcGetMemHandle(&h, ptrs[i]) != cudaSuccess) ok = 0;
-    std::memcpy(mine.data() + i * kH, &h, kH);
-  }
-  EQC_TRY(P.xfer.ensure((size_t)(n + 1) * 4 * kH + 64));
-  uint8_t *dx = P.xfer.as<uint8_t>();
-  EQC_CUDA_TRY(cudaMemcpyAsync(dx, mine.data(), 4 * kH, cudaMemcpyHostToDevice, s));
-  EQC_NCCL_TRY(ncclAllGather(dx, dx + 4 * kH, 4 * kH, ncclUint8, c->nccl, s));
-  EQC_CUDA_TRY(cudaMemcpyAsync(all.data(), dx + 4 * kH, all.size(), cudaMemcpyDeviceToHost, s));
-  EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<std::vector<void *>> m;
+  int ok = 0;
+  EQC_TRY(ipc_exchange(c, ptrs, 4, m, ok, s));
+  const int n = c->nranks;
   P.peer_part_c.assign(n, nullptr);
   P.peer_part_d.assign(n, nullptr);
   P.peer_fin_c.assign(n, nullptr);
   P.peer_flags.assign(n, nullptr);
-  for (int q = 0; q < n && ok; ++q) {
-    if (q == c->rank) {
-      P.peer_part_c[q] = P.part_c.as<uint32_t>();
-      P.peer_part_d[q] = P.part_d.as<uint32_t>();
-      P.peer_fin_c[q] = P.fin_c.as<uint32_t>();
-      P.peer_flags[q] = P.flags.as<int>();
-      continue;
-    }
-    void *o[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (int i = 0; i < 4 && ok; ++i) {
-      cudaIpcMemHandle_t h;
-      std::memcpy(&h, all.data() + ((size_t)q * 4 + i) * kH, kH);
-      if (cudaIpcOpenMemHandle(&o[i], h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
-    }
-    P.peer_part_c[q] = (uint32_t *)o[0];
-    P.peer_part_d[q] = (uint32_t *)o[1];
-    P.peer_fin_c[q] = (uint32_t *)o[2];
-    P.peer_flags[q] = (int *)o[3];
+  for (int q = 0; q < n; ++q) {
+    P.peer_part_c[q] = (uint32_t *)m[0][q];
+    P.peer_part_d[q] = (uint32_t *)m[1][q];
+    P.peer_fin_c[q] = (uint32_t *)m[2][q];
+    P.peer_flags[q] = (int *)m[3][q];
   }
-  cudaGetLastError();  // a failed open is reported through `ok`
-  // agree on the transport: P2P only if every rank mapped every peer
-  int *dok = reinterpret_cast<int *>(dx);
-  EQC_CUDA_TRY(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
-  EQC_NCCL_TRY(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->nccl, s));
-  EQC_CUDA_TRY(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
-  EQC_CUDA_TRY(cudaStreamSynchronize(s));
   P.capable = ok ? 1 : 0;
   P.cap_px = ok ? px : 0;
   if (!ok) P.close_peers(c->rank);
+  return EQC_OK;
+}
+
+// Caller-visible frame slots of >= px pixels, peer-mapped.  Collective.
+int p2p_slots(eqc_comm *c, int64_t px, cudaStream_t s) {
+  P2PState &P = c->p2p;
+  if (px <= P.slot_px) return EQC_OK;
+  cudaStreamSynchronize(s);
+  P.close_slots(c->rank);
+  P.slot_px = 0;
+  void *ptrs[2 * P2PState::kSlots];
+  for (int i = 0; i < P2PState::kSlots; ++i) {
+    EQC_TRY(P.slot_c[i].ensure((size_t)px * 4));
+    EQC_TRY(P.slot_d[i].ensure((size_t)px * 4));
+    ptrs[2 * i] = P.slot_c[i].p;
+    ptrs[2 * i + 1] = P.slot_d[i].p;
+  }
+  std::vector<std::vector<void *>> m;
+  int ok = 0;
+  EQC_TRY(ipc_exchange(c, ptrs, 2 * P2PState::kSlots, m, ok, s));
+  for (int i = 0; i < P2PState::kSlots; ++i) {
+    P.peer_slot_c[i].assign(c->nranks, nullptr);
+    P.peer_slot_d[i].assign(c->nranks, nullptr);
+    for (int q = 0; q < c->nranks; ++q) {
+      P.peer_slot_c[i][q] = (uint32_t *)m[2 * i][q];
+      P.peer_slot_d[i][q] = (uint32_t *)m[2 * i + 1][q];
+    }
+  }
+  if (!ok) {
+    P.close_slots(c->rank);
+    return EQC_E_UNSUPPORTED;
+  }
+  P.slot_px = px;
   return EQC_OK;
 }
 
@@ -1418,7 +1491,8 @@ int direct_send_p2p_pipelined(eqc_comm *c, const Geometry &g, const uint32_t *co
   EQC_CUDA_TRY(cudaStreamWaitEvent(s, P.ev_pulled, 0));
   // every band is complete on the destination (and nobody reads partials)
   EQC_TRY(p2p_barrier(c, s));
-  if (me == g.dest) {
+  // (the destination's frame may be the comm's gather buffer itself)
+  if (me == g.dest && !(g.out == P.fin_c.as<uint32_t>() && g.out_pitch == g.w)) {
     for (int q = 0; q < n; ++q) {
       const int qy0 = row0[q], qrows = row0[q + 1] - row0[q];
       if (q == me || qrows == 0) continue;
@@ -1454,6 +1528,12 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   // ROI (depth compositing only): computed (EQC_FLAG_ROI) or application-provided
   const bool roi = ((g.flags & EQC_FLAG_ROI) != 0 || g.src_roi) && g.op == EQC_OP_DEPTH;
   int32_t *my_roi = P.flags.as<int32_t>() + kRoiSlot;
+  // one depth partial that is a frame slot (eqc_comm_frame_buffers): the
+  // peers pull it in place; every rank passes its slot-i buffers or none does
+  const int slot = (!roi && !g.src_roi && g.op == EQC_OP_DEPTH && g.n_local == 1 && g.pitch == g.w && depth &&
+                    (int64_t)g.w * g.h <= P.slot_px)
+                       ? P.slot_of(color[0], depth[0])
+                       : -1;
   // (1) local pre-composite into the IPC-exposed partial frame.  With
   // EQC_FLAG_ROI the same kernel reduces the bounding box of
   // the partial's rendered pixels (the ROI "computed by analysing the
@@ -1473,9 +1553,11 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
     EQC_TRY(P.roi_local.ensure(eqc_depth_bbox_scratch_bytes()));
     EQC_TRY(eqc_depth_composite_bbox(g.n_local, color, depth, g.w, g.h, g.pitch, P.part_c.as<uint32_t>(),
                                      P.part_d.as<uint32_t>(), g.w, P.roi_local.p, my_roi, s));
-  } else {
+  } else if (slot < 0) {
     EQC_TRY(op_local(g, color, depth, P.part_c.as<uint32_t>(), P.part_d.as<uint32_t>(), s));
-  }
+  }  // else: the caller's partial frame already is slot `slot` (peer-mapped)
+  const std::vector<uint32_t *> &src_c = slot < 0 ? P.peer_part_c : P.peer_slot_c[slot];
+  const std::vector<uint32_t *> &src_d = slot < 0 ? P.peer_part_d : P.peer_slot_d[slot];
   EQC_TRY(p2p_barrier(c, s));
   // (2)+(3)+(4) band composite pulling every peer's band over NVLink, output
   // pushed into the destination's frame
@@ -1483,8 +1565,8 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   if (rows > 0) {
     std::vector<const uint32_t *> cs(n), ds(n);
     for (int q = 0; q < n; ++q) {
-      cs[q] = P.peer_part_c[q] + (size_t)y0 * g.w;
-      ds[q] = P.peer_part_d[q] + (size_t)y0 * g.w;
+      cs[q] = src_c[q] + (size_t)y0 * g.w;
+      ds[q] = src_d[q] + (size_t)y0 * g.w;
       if (q != me) {
         stats[0] += 1;
         stats[3] += (int64_t)rows * g.w * 8;
@@ -1507,7 +1589,8 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   }
   EQC_TRY(p2p_barrier(c, s));
   // (5) destination: move the pushed bands into the caller's frame
-  if (me == g.dest) {
+  // (the destination's frame may be the comm's gather buffer itself)
+  if (me == g.dest && !(g.out == P.fin_c.as<uint32_t>() && g.out_pitch == g.w)) {
     for (int q = 0; q < n; ++q) {
       const int qy0 = row0[q], qrows = row0[q + 1] - row0[q];
       if (q == me || qrows == 0) continue;
@@ -1550,6 +1633,11 @@ extern "C" int eqc_comm_destroy(eqc_comm *comm) {
   if (!comm) return EQC_E_INVALID;
   cudaDeviceSynchronize();
   comm->p2p.close_peers(comm->rank);
+  comm->p2p.close_slots(comm->rank);
+  for (int i = 0; i < P2PState::kSlots; ++i) {
+    comm->p2p.slot_c[i].release();
+    comm->p2p.slot_d[i].release();
+  }
   if (comm->p2p.aux) cudaStreamDestroy(comm->p2p.aux);
   if (comm->p2p.ev_start) cudaEventDestroy(comm->p2p.ev_start);
   if (comm->p2p.ev_pulled) cudaEventDestroy(comm->p2p.ev_pulled);
@@ -1563,6 +1651,22 @@ extern "C" int eqc_comm_destroy(eqc_comm *comm) {
   if (comm->nccl && ncclCommDestroy(comm->nccl) != ncclSuccess) rc = EQC_E_NCCL;
   delete comm;
   return rc;
+}
+
+extern "C" int eqc_comm_frame_buffers(eqc_comm *comm, int w, int h, int slot, uint32_t **color, uint32_t **depth,
+                                      uint32_t **final_color, void *stream) {
+  if (!comm || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || !color || !depth || !final_color)
+    return EQC_E_INVALID;
+  if (comm->nranks < 2) return EQC_E_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t px = (int64_t)w * h;
+  EQC_TRY(p2p_setup(comm, px, s));
+  if (comm->p2p.capable != 1) return EQC_E_UNSUPPORTED;
+  EQC_TRY(p2p_slots(comm, px, s));
+  *color = comm->p2p.slot_c[slot].as<uint32_t>();
+  *depth = comm->p2p.slot_d[slot].as<uint32_t>();
+  *final_color = comm->p2p.fin_c.as<uint32_t>();
+  return EQC_OK;
 }
 
 extern "C" int eqc_comm_stats(const eqc_comm *comm, int64_t out[4]) {

@@ -66,6 +66,7 @@ def _load():
         "eqc_comm_init": ([P, i32, i32, P], i32),
         "eqc_comm_destroy": ([P], i32),
         "eqc_comm_stats": ([P, P], i32),
+        "eqc_comm_frame_buffers": ([P, i32, i32, i32, P, P, P, P], i32),
         "eqc_plan_bands": ([i32, i32, P], i32),
         "eqc_plan_binary_swap": ([i32, i32, i32, P, i32], i32),
         "compose_direct_send": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
@@ -278,6 +279,15 @@ def eqc_plan_binary_swap(h: int, n: int, rank: int):
     return [tuple(buf[6 * i:6 * i + 6]) for i in range(k)]
 
 
+class _DeviceView:
+    """A [h, w] int32 view of device memory owned by the library
+    (__cuda_array_interface__, so torch.as_tensor wraps it without a copy)."""
+
+    def __init__(self, ptr: int, h: int, w: int):
+        self.__cuda_array_interface__ = {"shape": (h, w), "typestr": "<i4", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
 class Comm:
     """An eqc_comm: NCCL clique of one process per GPU (current device)."""
 
@@ -313,6 +323,21 @@ class Comm:
         out = (ctypes.c_int64 * 4)()
         _check(_lib.eqc_comm_stats(self._h, out), "eqc_comm_stats")
         return list(out)
+
+    def frame_buffers(self, w: int, h: int, slot: int, stream=None):
+        """eqc_comm_frame_buffers: slot `slot`'s peer-mapped (color, depth)
+        partial-frame buffers and the comm's gather buffer, as [h, w] int32
+        tensor views of comm-owned memory (collective); None when the ranks
+        cannot map each other's memory (E_UNSUPPORTED)."""
+        import torch
+        c, d, f = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        rc = _lib.eqc_comm_frame_buffers(self._h, w, h, slot, ctypes.byref(c), ctypes.byref(d), ctypes.byref(f),
+                                         _stream(stream))
+        if rc == E_UNSUPPORTED:
+            return None
+        _check(rc, "eqc_comm_frame_buffers")
+        dev = torch.cuda.current_device()
+        return tuple(torch.as_tensor(_DeviceView(x.value, h, w), device=f"cuda:{dev}") for x in (c, d, f))
 
     def destroy(self):
         if self._h:

@@ -135,6 +135,29 @@ def main():
         if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.average(c)).all():
             failures.append(f"average {algo} nl={nl} {w}x{h} flags={fl}: mismatch")
         dist.barrier()
+    # comm-owned peer-mapped frame slots (eqc_comm_frame_buffers): partials
+    # written into slot k % 2 are pulled in place; the destination's frame is
+    # either the comm's gather buffer (no band copy) or a caller tensor
+    for w, h, dest in [(640, 361, 0), (1920, 1080, world - 1), (300, 41, 1 % world)]:
+        fb = [comm.frame_buffers(w, h, i) for i in range(2)]
+        if any(x is None for x in fb):
+            failures.append(f"frame slots {w}x{h}: E_UNSUPPORTED on a peer-capable box")
+            break
+        user_out = torch.zeros((h, w), dtype=torch.int32, device=dev)
+        for k in range(4):
+            c, d = synth.depth_sources(synth.SEED_BASE + 700 + 10 * k + w, world, w, h)
+            sc, sd, fin = fb[k % 2]
+            sc.copy_(torch.from_numpy(c[rank].view(np.int32)))
+            sd.copy_(torch.from_numpy(d[rank].view(np.int32)))
+            out = fin if k < 2 else user_out
+            eqc.compose_direct_send(comm, [sc], [sd], out if rank == dest else None, dest_rank=dest)
+            torch.cuda.synchronize()
+            st = comm.stats()
+            if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.depth_composite(c, d)[0]).all():
+                failures.append(f"frame slot {k % 2} {w}x{h} out={'gather' if k < 2 else 'user'}: mismatch")
+            if st[0] != world - 1:
+                failures.append(f"frame slots: rank {rank} sent {st[0]} band messages, want {world - 1}")
+            dist.barrier()
     comm.destroy()
     t = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(t)
