@@ -185,12 +185,10 @@ def run_eqc(args):
         final = torch.empty((H, W), dtype=torch.int32, device=dev) if rank == 0 else None
     xflags = {"raw": 0, "rle": eqc.FLAG_RLE, "nccl": eqc.FLAG_NCCL}[args.exchange]
     slots = False
-    if comm is not None and args.exchange == "raw" and args.frame_slots:
+    if comm is not None and args.exchange == "raw" and not args.no_frame_slots:
         # decode the partial frames straight into the comm's peer-mapped slots:
         # the direct send reads them in place (no pre-composite copy) and the
-        # peers' bands land in rank 0's final frame directly.  Opt-in: it cuts
-        # the compose latency by ~30 % (scripts/bench_compose.py, 1 partial per
-        # GPU) but measured 2-4 % LOWER pipelined throughput
+        # peers' bands land in rank 0's final frame directly
         fb = [comm.frame_buffers(W, H, i) for i in range(2)]
         if all(x is not None for x in fb):
             slots = True
@@ -200,7 +198,13 @@ def run_eqc(args):
     # asynchronous compositing pipeline: the multi-GPU exchange +
     # composite of frame k runs on its own stream while frame k+1 is encoded
     pipelined = world > 1 and not args.no_pipeline
-    comm_stream = torch.cuda.Stream(device=dev) if pipelined else stream
+    if pipelined and args.exchange == "raw" and not args.no_overlap_flag:
+        xflags |= eqc.FLAG_OVERLAP  # the compose shares the GPU with the next frame's encode
+    # the compose runs on a high-priority stream: its (<= 1 CTA/SM, EQC_FLAG_OVERLAP)
+    # pulls are dispatched as soon as the peers' partials are ready instead of
+    # queueing behind the next frame's encoder CTAs
+    comm_stream = (torch.cuda.Stream(device=dev, priority=0 if args.no_comm_priority else -1)
+                   if pipelined else stream)
     composed = [None, None]  # event: compose of the frame in outs[i] finished
     nstep = [0]
 
@@ -386,7 +390,9 @@ def run_eqc(args):
             "parallelism": (f"screen-partition direct send ({args.exchange}) over {world} GPU(s)" +
                             (", compose of frame k overlapped with frame k+1 (async compositing pipeline, "
                              "P:2302-2310)" if pipelined else "") +
-                            (", partial frames decoded into peer-mapped frame slots (zero-copy)" if slots else "")
+                            (", partial frames decoded into peer-mapped frame slots (zero-copy)" if slots else "") +
+                            (", EQC_FLAG_OVERLAP (peer pulls <= 1 CTA/SM)" if xflags & eqc.FLAG_OVERLAP else "") +
+                            (", compose on a high-priority stream" if pipelined and not args.no_comm_priority else "")
                             ) if world > 1 else "single GPU",
         },
         "output_mpx_per_s": round(world * P / (ms * 1e-3) / 1e6, 1),
@@ -498,8 +504,12 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="rows of the frame in one CPU-oracle sample (0 = calibrate to a time budget)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--frame-slots", action="store_true",
-                    help="N>1: decode into the comm's peer-mapped frame slots (zero-copy direct send)")
+    ap.add_argument("--no-frame-slots", action="store_true",
+                    help="N>1: decode into own buffers, not the comm's peer-mapped frame slots (zero-copy direct send)")
+    ap.add_argument("--no-comm-priority", action="store_true",
+                    help="N>1 pipelined: run the compose on a normal-priority stream")
+    ap.add_argument("--no-overlap-flag", action="store_true",
+                    help="N>1 pipelined: do not pass EQC_FLAG_OVERLAP (peer pulls then take every SM)")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N > 1: run the multi-GPU compose of frame k before encoding frame k+1")
     ap.add_argument("--exchange", default="raw", choices=["raw", "rle", "nccl"],

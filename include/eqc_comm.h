@@ -41,6 +41,10 @@ typedef struct eqc_comm eqc_comm;
 #define EQC_FLAG_NCCL 2     /* direct send: force NCCL grouped send/recv instead of the NVLink peer-memory path */
 #define EQC_FLAG_ROI 4      /* region of interest: peer-memory direct send reads and composites
                                only the ROI of every partial frame (computed on the device) */
+#define EQC_FLAG_OVERLAP 8  /* the compose runs alongside other GPU work (the asynchronous pipeline,
+                               P:2302-2310): the peer-memory pull kernels use at most one CTA per SM,
+                               leaving the SMs to the overlapped kernels (higher pipeline throughput,
+                               ~10 % longer compose latency when run alone) */
 
 /* NCCL unique id of a new clique (rank 0 calls this and broadcasts the bytes). */
 EQC_API int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]);

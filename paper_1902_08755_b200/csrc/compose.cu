@@ -34,6 +34,7 @@ int eqc_depth_roi_launch(int n, const uint32_t *const *color, const uint32_t *co
                          cudaStream_t stream);
 // composite.cu: compositor_depth that also reduces the ROI of its output
 size_t eqc_depth_bbox_scratch_bytes();
+extern thread_local int eqc_grid_cap;
 int eqc_depth_composite_bbox(int n, const uint32_t *const *color, const uint32_t *const *depth, int w, int h,
                              int64_t pitch, uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
                              void *scratch, int32_t *out_roi, cudaStream_t s);
@@ -294,6 +295,15 @@ int op_final(const Geometry &g, int n, const uint32_t *const *c, const uint32_t 
   if (g.op == EQC_OP_AVERAGE)
     return eqc_average(false, n, c, d, g.w, rows, g.w, g.n * g.n_local, out, nullptr, nullptr, opitch, s);
   return compositor_depth(n, c, d, g.w, rows, g.w, out, nullptr, opitch, s);
+}
+// op_final of a peer-memory pull: with EQC_FLAG_OVERLAP at most one CTA per
+// SM (the pull is NVLink-latency-bound; the SMs stay with the overlapped work)
+int op_final_pull(const Geometry &g, int n, const uint32_t *const *c, const uint32_t *const *d, int rows,
+                  uint32_t *out, int64_t opitch, cudaStream_t s) {
+  eqc_grid_cap = (g.flags & EQC_FLAG_OVERLAP) ? eqc_num_sms() : 0;
+  const int rc = op_final(g, n, c, d, rows, out, opitch, s);
+  eqc_grid_cap = 0;
+  return rc;
 }
 // k partials (back / lower ranks first) -> 1 partial (swap rounds, folds)
 int op_merge(const Geometry &g, int k, const uint32_t *const *c, const uint32_t *const *d, int rows,
@@ -1065,7 +1075,7 @@ int validate(int nranks, int n_local, const void *color, const void *depth, int 
   if (op != EQC_OP_DEPTH && op != EQC_OP_BLEND && op != EQC_OP_AVERAGE) return EQC_E_UNSUPPORTED;
   if (op == EQC_OP_AVERAGE && (int64_t)nranks * n_local > 256) return EQC_E_UNSUPPORTED;  // 16-bit sums
   if (!color || (op == EQC_OP_DEPTH && !depth) || w <= 0 || h <= 0 || pitch < w) return EQC_E_INVALID;
-  if (flags & ~(EQC_FLAG_RLE | EQC_FLAG_NCCL | EQC_FLAG_ROI)) return EQC_E_INVALID;
+  if (flags & ~(EQC_FLAG_RLE | EQC_FLAG_NCCL | EQC_FLAG_ROI | EQC_FLAG_OVERLAP)) return EQC_E_INVALID;
   if (dest < 0 || dest >= nranks) return EQC_E_INVALID;
   if (is_dest && (!out || out_pitch < w)) return EQC_E_INVALID;
   return EQC_OK;
@@ -1469,7 +1479,7 @@ int direct_send_p2p_pipelined(eqc_comm *c, const Geometry &g, const uint32_t *co
       EQC_TRY(eqc_depth_roi_launch(n, pc.data(), pd.data(), rp.data(), y0, nullptr, g.w, y1 - y0, g.w, out,
                                    nullptr, opitch, P.aux));
     } else {
-      EQC_TRY(op_final(g, n, pc.data(), pd.data(), y1 - y0, out, opitch, P.aux));
+      EQC_TRY(op_final_pull(g, n, pc.data(), pd.data(), y1 - y0, out, opitch, P.aux));
     }
   }
   mark(P.aux);
@@ -1580,7 +1590,7 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
       EQC_TRY(eqc_depth_roi_launch(n, cs.data(), ds.data(), rp.data(), y0, nullptr, g.w, rows, g.w, out, nullptr,
                                    opitch, s));
     } else {
-      EQC_TRY(op_final(g, n, cs.data(), ds.data(), rows, out, opitch, s));
+      EQC_TRY(op_final_pull(g, n, cs.data(), ds.data(), rows, out, opitch, s));
     }
     if (me != g.dest) {
       stats[1] += 1;

@@ -756,7 +756,13 @@ inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 // Grid of a grid-stride kernel over `items` 4-pixel groups: one group per
 // thread, at most `cap` CTAs (16 per SM measured best for the streaming
 // kernels: several waves even out the per-thread iteration counts).
+}  // namespace
+// Internal (compose.cu): CTA cap of the streaming kernels launched by the
+// calling host thread (0 = default); set around a pipelined peer pull.
+thread_local int eqc_grid_cap = 0;
+namespace {
 inline int grid_for(int64_t items, int cap = 16 * eqc_num_sms()) {
+  if (eqc_grid_cap > 0 && cap > eqc_grid_cap) cap = eqc_grid_cap;
   int64_t blocks = (items + 255) / 256;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;

@@ -29,6 +29,7 @@ OP_AVERAGE = 2
 FLAG_RLE = 1
 FLAG_NCCL = 2
 FLAG_ROI = 4
+FLAG_OVERLAP = 8  # the compose overlaps other GPU work: peer pulls use <= 1 CTA per SM
 
 
 class EqcError(RuntimeError):

@@ -78,6 +78,16 @@ def main():
             return eqc.compose_direct_send_roi(comm_, dc_, dd_, app_roi, final_, dest_rank=dest_rank, flags=flags,
                                                stream=stream)
         variants.insert(2, ("direct_send_p2p_app_roi", ds_app_roi, 0))
+        fb = comm.frame_buffers(W, H, 0) if nl == 1 else None
+        if fb is not None:  # one partial per GPU already in a peer-mapped frame slot: no pre-composite copy
+            fb[0].copy_(dc[0])
+            fb[1].copy_(dd[0])
+            torch.cuda.synchronize()
+
+            def ds_slots(comm_, dc_, dd_, final_, dest_rank=0, flags=0, op=0, stream=None):
+                return eqc.compose_direct_send(comm_, [fb[0]], [fb[1]], fb[2] if rank == dest_rank else None,
+                                               dest_rank=dest_rank, flags=flags, stream=stream)
+            variants.insert(1, ("direct_send_p2p_slots", ds_slots, 0))
     if blend:
         variants = [v for v in variants if "roi" not in v[0]]
     for name, fn, flags in variants:

@@ -29,7 +29,7 @@ def main():
     # send, FLAG_NCCL = NCCL grouped send/recv, FLAG_RLE = RLE streams over NCCL,
     # FLAG_ROI = peer-memory direct send restricted to each partial's ROI
     R, X, O = eqc.FLAG_RLE, eqc.FLAG_NCCL, eqc.FLAG_ROI
-    cases = [("ds", 2, 640, 361, 0, 0), ("ds", 1, 300, 41, world - 1, 0), ("ds", 2, 1920, 1080, 1 % world, 0),
+    cases = [("ds", 2, 640, 361, 0, 0), ("ds", 1, 300, 41, world - 1, eqc.FLAG_OVERLAP), ("ds", 2, 1920, 1080, 1 % world, 0),
              ("ds", 2, 640, 361, 0, X), ("ds", 1, 300, 41, world - 1, R), ("ds", 2, 1920, 1080, 0, R),
              ("ds", 2, 640, 361, 0, O, "compact"), ("ds", 1, 301, 43, world - 1, O, "compact"),
              ("ds", 3, 1920, 1080, 1 % world, O, "compact"), ("ds", 2, 640, 361, 0, O, "scattered"),
@@ -42,7 +42,8 @@ def main():
     cases += [("st", 2, 640, 361, 0, 0), ("st", 1, 300, 41, world - 1, R)]
     # config c4 (8 sources of 7680x4320 over the ranks), checked on sampled rows
     if 8 % world == 0:
-        cases += [("ds", 8 // world, 7680, 4320, 0, 0), ("ds", 8 // world, 7680, 4320, 0, R)]
+        cases += [("ds", 8 // world, 7680, 4320, 0, 0), ("ds", 8 // world, 7680, 4320, 0, R),
+                  ("ds", 8 // world, 7680, 4320, 0, eqc.FLAG_OVERLAP)]
         if world & (world - 1) == 0:
             cases += [("bs", 8 // world, 7680, 4320, 0, 0)]
     for algo, nl, w, h, dest, rle, *scene in cases:
@@ -150,7 +151,8 @@ def main():
             sc.copy_(torch.from_numpy(c[rank].view(np.int32)))
             sd.copy_(torch.from_numpy(d[rank].view(np.int32)))
             out = fin if k < 2 else user_out
-            eqc.compose_direct_send(comm, [sc], [sd], out if rank == dest else None, dest_rank=dest)
+            eqc.compose_direct_send(comm, [sc], [sd], out if rank == dest else None, dest_rank=dest,
+                                    flags=eqc.FLAG_OVERLAP if k % 2 else 0)
             torch.cuda.synchronize()
             st = comm.stats()
             if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.depth_composite(c, d)[0]).all():
