@@ -94,3 +94,24 @@ def test_host_validation_rejects_before_launch(libeqc):
     assert L.image_compress_rle(0x1000, 4, 4, 4, 1, 1, 0x2000, 1 << 20, 0x3000, 0x4000, 1 << 20, None) == -4
     assert L.image_compress_rle(0x1000, 4, 4, 4, 0, 0, 0x2000, 10, 0x3000, 0x4000, 1 << 20, None) == -2
     assert L.image_compress_rle(0x1000, 4, 4, 4, 2, 0, 0x2000, 1 << 20, 0x3000, 0x4000, 1 << 20, None) == -1
+
+
+def test_comm_frame_buffers_and_flags_validation(libeqc):
+    """eqc_comm_frame_buffers rejects a null comm / bad slot / null outputs on
+    the host; compose rejects unknown flag bits (EQC_FLAG_OVERLAP = 8 is known)."""
+    L = libeqc
+    P = ctypes.c_void_p
+    L.eqc_comm_frame_buffers.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
+    c, d, f = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    refs = [ctypes.byref(c), ctypes.byref(d), ctypes.byref(f)]
+    assert L.eqc_comm_frame_buffers(None, 64, 64, 0, *refs, None) == -1
+    assert L.eqc_comm_frame_buffers(0x1000, 64, 64, 2, *refs, None) == -1
+    assert L.eqc_comm_frame_buffers(0x1000, 0, 64, 0, *refs, None) == -1
+    assert L.eqc_comm_frame_buffers(0x1000, 64, 64, 0, None, refs[1], refs[2], None) == -1
+    L.compose_direct_send_local.argtypes = [ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
+                                            ctypes.c_int64, P, P]
+    fake = (ctypes.c_void_p * 2)(0x1000, 0x2000)
+    assert L.compose_direct_send_local(2, 1, fake, fake, 4, 4, 4, 0, 16, 0, 0x3000, 4, None, None) == -1
+    from paper_1902_08755_b200 import eqc
+    assert eqc.FLAG_OVERLAP == 8
