@@ -300,7 +300,9 @@ int op_final(const Geometry &g, int n, const uint32_t *const *c, const uint32_t 
 // SM (the pull is NVLink-latency-bound; the SMs stay with the overlapped work)
 int op_final_pull(const Geometry &g, int n, const uint32_t *const *c, const uint32_t *const *d, int rows,
                   uint32_t *out, int64_t opitch, cudaStream_t s) {
-  eqc_grid_cap = (g.flags & EQC_FLAG_OVERLAP) ? eqc_num_sms() : 0;
+  // EQC_OVERLAP_CTAS: tuning override of the cap (default one CTA per SM)
+  static const int cap_env = getenv("EQC_OVERLAP_CTAS") ? atoi(getenv("EQC_OVERLAP_CTAS")) : 0;
+  eqc_grid_cap = (g.flags & EQC_FLAG_OVERLAP) ? (cap_env > 0 ? cap_env : eqc_num_sms()) : 0;
   const int rc = op_final(g, n, c, d, rows, out, opitch, s);
   eqc_grid_cap = 0;
   return rc;
