@@ -33,6 +33,9 @@
 #ifndef EQC_FUSED_MINB
 #define EQC_FUSED_MINB (32 / EQC_FWARPS)  // 32 warps per SM (64 registers)
 #endif
+#ifndef EQC_DEPTH_SKIP
+#define EQC_DEPTH_SKIP 1  // fused decode: significance-first depth records (skip losing sources' low planes)
+#endif
 #ifndef EQC_CLS_BATCH
 #define EQC_CLS_BATCH 8
 #endif
@@ -491,6 +494,37 @@ __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int
     const int sz = (int)((ps >> (8 * q)) & 0xFFu);
     if (!decode_plane(r, sz, L, lane, q, px, info)) return false;
     r += sz;
+  }
+  return true;
+}
+
+// Significance-first decode of a staged DEPTH record: the most significant
+// byte plane (plane 3, the record's last) first.  With `check`, when that
+// byte alone makes the source deeper than best[] at every pixel of the chunk
+// (it then cannot win: ties keep the lower index), planes 0-2 are not
+// decoded and `skip` is set.  One decode_plane call site (the kernel must
+// stay inside the instruction cache).  Warp-uniform result.
+__device__ __forceinline__ bool decode_depth_sigfirst(const uint8_t *r, uint32_t ps, int L, int lane, uint16_t *info,
+                                                      uint32_t px[4], bool check, const uint32_t best[4],
+                                                      bool &skip) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) px[j] = 0;
+  const int s0 = (int)(ps & 0xFFu), s1 = (int)((ps >> 8) & 0xFFu), s2 = (int)((ps >> 16) & 0xFFu);
+  skip = false;
+#pragma unroll 1
+  for (int t = 0; t < 4; ++t) {
+    const int q = (t + 3) & 3;  // planes 3, 0, 1, 2
+    const int off = q == 3 ? s0 + s1 + s2 : q == 0 ? 0 : q == 1 ? s0 : s0 + s1;
+    if (!decode_plane(r + off, (int)((ps >> (8 * q)) & 0xFFu), L, lane, q, px, info)) return false;
+    if (t == 0 && check) {
+      bool lose = true;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lose = lose && (4 * lane + j >= L || (px[j] >> 24) > (best[j] >> 24));
+      if (__all_sync(EQC_FULL, lose)) {
+        skip = true;
+        return true;
+      }
+    }
   }
   return true;
 }
@@ -1021,9 +1055,14 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
 #pragma unroll
       for (int j = 0; j < 4; ++j) d[j] = dz;
     } else if (npass == 1 && od >= 0) {
-      okd = decode_staged(reinterpret_cast<const uint8_t *>(pre + od) +
-                              ((uintptr_t)(p.src[n + i] + payload0 + dx) & 15u),
-                          dy, L, lane, info[warp], d);
+      const uint8_t *r = reinterpret_cast<const uint8_t *>(pre + od) + ((uintptr_t)(p.src[n + i] + payload0 + dx) & 15u);
+#if EQC_DEPTH_SKIP
+      bool skip = false;
+      okd = decode_depth_sigfirst(r, dy, L, lane, info[warp], d, i > 0, bd, skip);
+      if (okd && skip) continue;  // deeper than the current best everywhere: cannot win
+#else
+      okd = decode_staged(r, dy, L, lane, info[warp], d);
+#endif
     } else {
       okd = decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane, stage[warp],
                           info[warp], d);

@@ -303,6 +303,26 @@ def test_fused_decode_depth_composite(eqc, n, w, h):
     np.testing.assert_array_equal(to_host(out_d), od)
 
 
+@pytest.mark.parametrize("n,w,h,ties,mode", [(8, 1920, 1080, True, "scattered"), (5, 333, 77, True, "scattered"),
+                                              (8, 1024, 512, False, "compact"), (2, 128, 9, True, "compact")])
+def test_fused_decode_significance_first(eqc, n, w, h, ties, mode):
+    """The fused decode skips a depth record's low byte planes when its most
+    significant plane already loses at every pixel; quantised depths (many
+    equal high bytes and exact ties) and compact sources exercise both the
+    skip and the full decode: still bit-exact against O1."""
+    c, d = synth.depth_sources(SEED + 40 + n + w, n, w, h, ties=ties, mode=mode)
+    oc, od = oracle.depth_composite(c, d)
+    cs = [stream_dev(oracle.rle_encode(x, kind=0, flags=1)) for x in c]
+    ds = [stream_dev(oracle.rle_encode(x, kind=1, flags=0)) for x in d]
+    out_c, out_d = out_frame(h, w), out_frame(h, w)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    eqc.compositor_depth_rle(cs, ds, out_c, out_d, status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    np.testing.assert_array_equal(to_host(out_c), oc)
+    np.testing.assert_array_equal(to_host(out_d), od)
+
+
 def test_target_pipeline_4k_one_image_exact(eqc):
     """One full 3840x2160 colour (swizzled) and depth image, in bench.py's
     launch configuration, byte-exact against the oracle stream."""
