@@ -20,6 +20,7 @@ exchange of its partial frame (compose_direct_send, when available).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -114,7 +115,12 @@ class ClockSampler:
         self._stop.set()
         self._th.join(timeout=10)
 
+    def mark(self):
+        """Start of the timed region: summary() uses the samples taken after it."""
+        self._mark = len(self.samples)
+
     def summary(self):
+        samples = self.samples[getattr(self, "_mark", 0):] or self.samples
         names = []
         r = self.reasons
         if r & self.HW_SLOW:
@@ -127,8 +133,8 @@ class ClockSampler:
             names.append("sw_power_cap")
         if r & 0x1:
             names.append("gpu_idle")
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(samples) if samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(samples)}
 
 
 # ---------------------------------------------------------- eqc arm ----
@@ -259,27 +265,43 @@ def run_eqc(args):
     r = stream_bytes / (len(imgs) * 4 * P)
     log(f"rank {rank}: compressed {stream_bytes/1e6:.1f} MB, ratio r={r:.3f}")
 
-    # ---- timed region: K steps, barrier + synchronize on both sides
+    # ---- timed region: K steps, barrier + synchronize on both sides.  The
+    # clock sampler is already running (its start-up is outside the region;
+    # only samples taken inside it count) and the garbage collector is off,
+    # so no host pause can starve a rank's queue -- with peer barriers in the
+    # compose one rank's stall would stall every rank.
+    sampler = ClockSampler(local)
+    sampler.__enter__()
+    t_wait = time.time()
+    while not sampler.samples and time.time() - t_wait < 1.0:
+        time.sleep(0.005)
+    gc.collect()
+    gc.disable()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     evs = []
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
-    with sampler:
-        t0.record(stream)
-        for _ in range(args.steps):
-            step(evs)
-        drain()
-        t1.record(stream)
-        torch.cuda.synchronize()
+    sampler.mark()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(evs)
+    drain()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    sampler.__exit__(None, None, None)
+    gc.enable()
     if world > 1:
         dist.barrier()
     ms_total = t0.elapsed_time(t1)
     enc_ms = statistics.mean(a.elapsed_time(b) for a, b, _, _ in evs)
     dec_ms = statistics.mean(b.elapsed_time(c) for _, b, c, _ in evs)
     comp_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in evs) if world > 1 else 0.0
+    if os.environ.get("EQC_BENCH_RANKS"):  # diagnostics: every rank's own event times on stderr
+        starts = [t0.elapsed_time(a) for a, _, _, _ in evs]
+        log(f"rank {rank}: step {ms_total / args.steps:.4f} ms, encode {enc_ms:.4f}, decode {dec_ms:.4f}, "
+            f"compose latency {comp_ms:.4f}, step starts (ms) {[round(x, 3) for x in starts[:6]]}")
     ms = ms_total / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
