@@ -98,6 +98,42 @@ EQC_API int eqc_comm_frame_buffers(eqc_comm *comm, int w, int h, int slot, uint3
                                    uint32_t **final_color, void *stream);
 
 /*
+ * eqc_comm_stream_buffers -- peer-mapped RLE stream slots for
+ * compose_direct_send_rle_pull (collective, same arguments on every rank;
+ * the first call for a (n_streams, cap) allocates and maps both slots).
+ *   n_streams   2 * n_local: streams 0..n_local-1 = the rank's colour
+ *               streams, n_local..2*n_local-1 = its depth streams (the order
+ *               image_compress_rle_batch fills them in).
+ *   cap_bytes   capacity of one stream (>= image_rle_max_size(w, h)).
+ *   ptrs[0..n_streams-1]  receive slot `slot`'s stream buffers (device).
+ * Ownership and reuse as for eqc_comm_frame_buffers.  Errors: EQC_E_INVALID,
+ * EQC_E_UNSUPPORTED (one rank, or no peer mapping), EQC_E_CUDA, EQC_E_NCCL.
+ */
+EQC_API int eqc_comm_stream_buffers(eqc_comm *comm, int n_streams, int64_t cap_bytes, int slot, uint8_t **ptrs,
+                                    void *stream);
+
+/*
+ * compose_direct_send_rle_pull -- direct send of COMPRESSED sources: the
+ * thesis pipeline "compress, transmit, decompress, assemble"
+ * with the transmit step done by the decoder itself.  Every rank has encoded
+ * its n_local sources into stream slot `slot` (eqc_comm_stream_buffers);
+ * after a peer-memory barrier rank j runs the fused decode + depth composite
+ * (compositor_depth_rle) over rows of band j (R-C13) of ALL n * n_local
+ * sources -- the peers' streams read in place over NVLink, so only the
+ * compressed records of band j cross the links (≈ r of the raw bytes) and no
+ * partial frame is ever written -- and stores its band straight into the
+ * destination's frame; colour gathered as in compose_direct_send.
+ * Global source order is rank-major (R-C5): bit-identical to compositor_depth
+ * over all sources.  out_color: [h][out_pitch] on dest_rank (the comm's gather
+ * buffer from eqc_comm_frame_buffers avoids the final band copy).  d_status:
+ * device int32, set non-zero if a stream is corrupt (as compositor_depth_rle).
+ * Errors: EQC_E_INVALID (arguments, no stream slots of 2 * n_local streams,
+ * n * n_local > 64), EQC_E_UNSUPPORTED (no peer mapping), EQC_E_CUDA.
+ */
+EQC_API int compose_direct_send_rle_pull(eqc_comm *comm, int n_local, int w, int h, int slot, int dest_rank,
+                                         uint32_t *out_color, int64_t out_pitch, int32_t *d_status, void *stream);
+
+/*
  * Host-side schedule plans (no GPU needed; used by the executors below and
  * by the tests).
  * eqc_plan_bands: row0[j] = floor(j*h/n), j = 0..n (band j = rows

@@ -35,6 +35,10 @@ int eqc_depth_roi_launch(int n, const uint32_t *const *color, const uint32_t *co
 // composite.cu: compositor_depth that also reduces the ROI of its output
 size_t eqc_depth_bbox_scratch_bytes();
 extern thread_local int eqc_grid_cap;
+int eqc_depth_rle_band(int n, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
+                       const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h, int y0, int y1,
+                       uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch, int32_t *d_status,
+                       void *stream);
 int eqc_depth_composite_bbox(int n, const uint32_t *const *color, const uint32_t *const *depth, int w, int h,
                              int64_t pitch, uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
                              void *scratch, int32_t *out_roi, cudaStream_t s);
@@ -1203,6 +1207,13 @@ struct P2PState {
   DevBuf slot_c[kSlots], slot_d[kSlots];
   std::vector<uint32_t *> peer_slot_c[kSlots], peer_slot_d[kSlots];
 
+  // caller-visible, peer-mapped RLE stream slots (eqc_comm_stream_buffers):
+  // slot i holds sn streams of scap bytes each, contiguous
+  int sn = 0;
+  int64_t scap = 0;
+  DevBuf sslot[kSlots];
+  std::vector<uint8_t *> peer_sslot[kSlots];
+
   // slot of (color, depth) when they are exactly slot i's buffers, else -1
   int slot_of(const uint32_t *color, const uint32_t *depth) const {
     for (int i = 0; i < kSlots; ++i)
@@ -1218,6 +1229,13 @@ struct P2PState {
       }
       peer_slot_c[i].clear();
       peer_slot_d[i].clear();
+    }
+  }
+  void close_sslots(int rank) {
+    for (int i = 0; i < kSlots; ++i) {
+      for (size_t q = 0; q < peer_sslot[i].size(); ++q)
+        if ((int)q != rank && peer_sslot[i][q]) cudaIpcCloseMemHandle(peer_sslot[i][q]);
+      peer_sslot[i].clear();
     }
   }
 
@@ -1646,9 +1664,11 @@ extern "C" int eqc_comm_destroy(eqc_comm *comm) {
   cudaDeviceSynchronize();
   comm->p2p.close_peers(comm->rank);
   comm->p2p.close_slots(comm->rank);
+  comm->p2p.close_sslots(comm->rank);
   for (int i = 0; i < P2PState::kSlots; ++i) {
     comm->p2p.slot_c[i].release();
     comm->p2p.slot_d[i].release();
+    comm->p2p.sslot[i].release();
   }
   if (comm->p2p.aux) cudaStreamDestroy(comm->p2p.aux);
   if (comm->p2p.ev_start) cudaEventDestroy(comm->p2p.ev_start);
@@ -1678,6 +1698,100 @@ extern "C" int eqc_comm_frame_buffers(eqc_comm *comm, int w, int h, int slot, ui
   *color = comm->p2p.slot_c[slot].as<uint32_t>();
   *depth = comm->p2p.slot_d[slot].as<uint32_t>();
   *final_color = comm->p2p.fin_c.as<uint32_t>();
+  return EQC_OK;
+}
+
+extern "C" int eqc_comm_stream_buffers(eqc_comm *comm, int n_streams, int64_t cap_bytes, int slot, uint8_t **ptrs,
+                                       void *stream) {
+  if (!comm || n_streams < 2 || n_streams > 2 * EQC_MAX_SOURCES || cap_bytes < 32 || slot < 0 ||
+      slot >= P2PState::kSlots || !ptrs)
+    return EQC_E_INVALID;
+  if (comm->nranks < 2) return EQC_E_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  P2PState &P = comm->p2p;
+  EQC_TRY(p2p_setup(comm, 1, s));
+  if (P.capable != 1) return EQC_E_UNSUPPORTED;
+  const int64_t cap = (cap_bytes + 255) & ~(int64_t)255;
+  if (n_streams != P.sn || cap > P.scap) {  // (re)allocate and map both slots
+    cudaStreamSynchronize(s);
+    P.close_sslots(comm->rank);
+    P.sn = 0;
+    P.scap = 0;
+    void *ptr2[P2PState::kSlots];
+    for (int i = 0; i < P2PState::kSlots; ++i) {
+      P.sslot[i].release();
+      EQC_TRY(P.sslot[i].ensure((size_t)n_streams * (size_t)cap));
+      ptr2[i] = P.sslot[i].p;
+    }
+    std::vector<std::vector<void *>> m;
+    int ok = 0;
+    EQC_TRY(ipc_exchange(comm, ptr2, P2PState::kSlots, m, ok, s));
+    for (int i = 0; i < P2PState::kSlots; ++i) {
+      P.peer_sslot[i].assign(comm->nranks, nullptr);
+      for (int q = 0; q < comm->nranks; ++q) P.peer_sslot[i][q] = (uint8_t *)m[i][q];
+    }
+    if (!ok) {
+      P.close_sslots(comm->rank);
+      return EQC_E_UNSUPPORTED;
+    }
+    P.sn = n_streams;
+    P.scap = cap;
+  }
+  for (int i = 0; i < n_streams; ++i) ptrs[i] = P.sslot[slot].as<uint8_t>() + (size_t)i * (size_t)P.scap;
+  return EQC_OK;
+}
+
+extern "C" int compose_direct_send_rle_pull(eqc_comm *comm, int n_local, int w, int h, int slot, int dest_rank,
+                                            uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
+                                            void *stream) {
+  if (!comm || n_local < 1 || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || dest_rank < 0 ||
+      dest_rank >= comm->nranks || !d_status)
+    return EQC_E_INVALID;
+  const int n = comm->nranks, me = comm->rank;
+  if ((int64_t)n * n_local > EQC_MAX_SOURCES) return EQC_E_INVALID;
+  if (me == dest_rank && (!out_color || out_pitch < w)) return EQC_E_INVALID;
+  P2PState &P = comm->p2p;
+  if (P.sn != 2 * n_local || P.peer_sslot[slot].size() != (size_t)n) return EQC_E_INVALID;  // no stream slots
+  cudaStream_t s = (cudaStream_t)stream;
+  EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
+  if (P.capable != 1) return EQC_E_UNSUPPORTED;
+  int64_t *stats = comm->st.stats;
+  for (int i = 0; i < 4; ++i) stats[i] = 0;
+  std::vector<int> row0(n + 1);
+  plan_bands(h, n, row0.data());
+  // every rank's streams are complete (encoded into its slot)
+  EQC_TRY(p2p_barrier(comm, s));
+  const int y0 = row0[me], y1 = row0[me + 1];
+  if (y1 > y0) {
+    const int nt = n * n_local;  // global source order: rank-major (R-C5)
+    std::vector<const uint8_t *> cs(nt), ds(nt);
+    std::vector<int64_t> cb(nt, P.scap), db(nt, P.scap);
+    for (int q = 0; q < n; ++q)
+      for (int i = 0; i < n_local; ++i) {
+        cs[q * n_local + i] = P.peer_sslot[slot][q] + (size_t)i * (size_t)P.scap;
+        ds[q * n_local + i] = P.peer_sslot[slot][q] + (size_t)(n_local + i) * (size_t)P.scap;
+      }
+    uint32_t *out = me == dest_rank ? out_color + (size_t)y0 * out_pitch : P.peer_fin_c[dest_rank] + (size_t)y0 * w;
+    const int64_t opitch = me == dest_rank ? out_pitch : w;
+    EQC_TRY(eqc_depth_rle_band(nt, cs.data(), ds.data(), cb.data(), db.data(), w, h, y0, y1, out, nullptr, opitch,
+                               d_status, s));
+    stats[0] = n - 1;
+    if (me != dest_rank) {
+      stats[1] = 1;
+      stats[2] = (int64_t)(y1 - y0) * w * 4;
+    }
+  }
+  // every band is on the destination; nobody reads the stream slots any more
+  EQC_TRY(p2p_barrier(comm, s));
+  if (me == dest_rank && !(out_color == P.fin_c.as<uint32_t>() && out_pitch == w)) {
+    for (int q = 0; q < n; ++q) {
+      const int qy0 = row0[q], qrows = row0[q + 1] - row0[q];
+      if (q == me || qrows == 0) continue;
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(out_color + (size_t)qy0 * out_pitch, out_pitch * 4,
+                                     P.fin_c.as<uint32_t>() + (size_t)qy0 * w, (size_t)w * 4, (size_t)w * 4, qrows,
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+  }
   return EQC_OK;
 }
 

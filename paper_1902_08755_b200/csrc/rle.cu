@@ -899,6 +899,7 @@ struct FusedParams {
   int32_t *status;
   int64_t out_pitch;
   int n, w, h, S;
+  int y0, y1;  // rows composited (a band of the full-frame streams); out_* point at row y0
   int vec;
 };
 
@@ -945,8 +946,8 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   }
   const int nch = p.S * p.h;
   const int64_t payload0 = 32 + 8 * (int64_t)nch;
-  const int c = blockIdx.x * kFWarps + warp;  // chunk position of this warp
-  if (c >= nch) return;
+  const int c = p.y0 * p.S + blockIdx.x * kFWarps + warp;  // chunk position of this warp
+  if (c >= p.y1 * p.S) return;
   const int y = c / p.S, k = c - y * p.S;
   const int L = min(kC, p.w - k * kC);
   // ---- phase A: lane i < n validates and probes source i's depth and colour
@@ -978,7 +979,7 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
     if (lane == 0) set_corrupt(p.status);
     return;
   }
-  const int64_t row = (int64_t)y * p.out_pitch + (int64_t)k * kC;
+  const int64_t row = (int64_t)(y - p.y0) * p.out_pitch + (int64_t)k * kC;
   if (__all_sync(EQC_FULL, allc)) {
     // every chunk of this position is one value: composite the scalars --
     // minimum depth, ties to the lowest source index
@@ -1264,10 +1265,27 @@ extern "C" int image_decompress_rle(const uint8_t *src, int64_t src_bytes, uint3
   return image_decompress_rle_batch(1, s, &src_bytes, d, pitch, w, h, d_status, stream);
 }
 
+// Internal (compose.cu): compositor_depth_rle over rows [y0, y1) of the
+// full-frame streams (any device / peer-mapped pointers); out_* point at row y0.
+int eqc_depth_rle_band(int n, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
+                       const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h, int y0, int y1,
+                       uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch, int32_t *d_status,
+                       void *stream);
+
 extern "C" int compositor_depth_rle(int n, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
                                     const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h,
                                     uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch,
                                     int32_t *d_status, void *stream) {
+  return eqc_depth_rle_band(n, color_rle, depth_rle, color_bytes, depth_bytes, w, h, 0, h, out_color, out_depth,
+                            out_pitch, d_status, stream);
+}
+
+int eqc_depth_rle_band(int n, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
+                       const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h, int y0, int y1,
+                       uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch, int32_t *d_status,
+                       void *stream) {
+  if (y0 < 0 || y1 > h || y0 > y1) return EQC_E_INVALID;
+  if (y0 == y1) return EQC_OK;
   if (n < 1 || n > EQC_MAX_SOURCES || !color_rle || !depth_rle || !color_bytes || !depth_bytes || !out_color ||
       !d_status)
     return EQC_E_INVALID;
@@ -1290,8 +1308,10 @@ extern "C" int compositor_depth_rle(int n, const uint8_t *const *color_rle, cons
   p.w = w;
   p.h = h;
   p.S = (w + kC - 1) / kC;
+  p.y0 = y0;
+  p.y1 = y1;
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
-  const int64_t grid = ((int64_t)p.S * h + kFWarps - 1) / kFWarps;
+  const int64_t grid = ((int64_t)p.S * (y1 - y0) + kFWarps - 1) / kFWarps;
   if (grid > 0x7FFFFFFFll || (int64_t)p.S * h > 0x7FFFFFFFll) return EQC_E_INVALID;
   depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();

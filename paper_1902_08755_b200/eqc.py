@@ -68,6 +68,8 @@ def _load():
         "eqc_comm_destroy": ([P], i32),
         "eqc_comm_stats": ([P, P], i32),
         "eqc_comm_frame_buffers": ([P, i32, i32, i32, P, P, P, P], i32),
+        "eqc_comm_stream_buffers": ([P, i32, i64, i32, P, P], i32),
+        "compose_direct_send_rle_pull": ([P, i32, i32, i32, i32, i32, P, i64, P, P], i32),
         "eqc_plan_bands": ([i32, i32, P], i32),
         "eqc_plan_binary_swap": ([i32, i32, i32, P, i32], i32),
         "compose_direct_send": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
@@ -284,8 +286,8 @@ class _DeviceView:
     """A [h, w] int32 view of device memory owned by the library
     (__cuda_array_interface__, so torch.as_tensor wraps it without a copy)."""
 
-    def __init__(self, ptr: int, h: int, w: int):
-        self.__cuda_array_interface__ = {"shape": (h, w), "typestr": "<i4", "data": (ptr, False),
+    def __init__(self, ptr: int, h: int, w: int, typestr: str = "<i4"):
+        self.__cuda_array_interface__ = {"shape": (h, w), "typestr": typestr, "data": (ptr, False),
                                          "version": 3, "strides": None, "stream": None}
 
 
@@ -340,6 +342,19 @@ class Comm:
         dev = torch.cuda.current_device()
         return tuple(torch.as_tensor(_DeviceView(x.value, h, w), device=f"cuda:{dev}") for x in (c, d, f))
 
+    def stream_buffers(self, n_streams: int, cap_bytes: int, slot: int, stream=None):
+        """eqc_comm_stream_buffers: slot `slot`'s peer-mapped RLE stream
+        buffers as uint8 tensor views of comm-owned memory (collective);
+        None when the ranks cannot map each other's memory."""
+        import torch
+        ptrs = (ctypes.c_void_p * n_streams)()
+        rc = _lib.eqc_comm_stream_buffers(self._h, n_streams, cap_bytes, slot, ptrs, _stream(stream))
+        if rc == E_UNSUPPORTED:
+            return None
+        _check(rc, "eqc_comm_stream_buffers")
+        dev = torch.cuda.current_device()
+        return [torch.as_tensor(_DeviceView(p, cap_bytes, 1, "|u1"), device=f"cuda:{dev}").view(-1) for p in ptrs]
+
     def destroy(self):
         if self._h:
             _check(_lib.eqc_comm_destroy(self._h), "eqc_comm_destroy")
@@ -354,6 +369,16 @@ def _compose(fn, name, comm, colors, depths, out_color, dest_rank, flags, op, st
             dest_rank, _addr(out_color),
             opitch, _stream(stream))
     return _check(rc, name)
+
+
+def compose_direct_send_rle_pull(comm, n_local: int, w: int, h: int, slot: int, out_color=None, status=None,
+                                 dest_rank: int = 0, stream=None):
+    """compose_direct_send_rle_pull: direct send of the RLE streams in stream
+    slot `slot` (decoder pulls the peers' records over NVLink)."""
+    opitch = _frame_geom(out_color)[2] if out_color is not None else w
+    return _check(_lib.compose_direct_send_rle_pull(comm.handle, n_local, w, h, slot, dest_rank, _addr(out_color),
+                                                    opitch, _addr(status), _stream(stream)),
+                  "compose_direct_send_rle_pull")
 
 
 def compose_direct_send(comm, colors, depths, out_color=None, dest_rank: int = 0, flags: int = 0,

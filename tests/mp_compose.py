@@ -160,6 +160,34 @@ def main():
             if st[0] != world - 1:
                 failures.append(f"frame slots: rank {rank} sent {st[0]} band messages, want {world - 1}")
             dist.barrier()
+    # direct send of the compressed sources: each rank encodes its sources into
+    # a peer-mapped stream slot; the fused decoder of band j pulls every rank's
+    # records over NVLink (compose_direct_send_rle_pull)
+    for k, (nl, w, h, dest) in enumerate([(2, 640, 361, 0), (3, 1920, 1080, world - 1), (1, 300, 41, 1 % world),
+                                          (2, 640, 361, 0)]):
+        N = world * nl
+        c, d = synth.depth_sources(synth.SEED_BASE + 800 + N + w + k, N, w, h)
+        mine = range(rank * nl, (rank + 1) * nl)
+        imgs = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine] + \
+               [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
+        cap = eqc.image_rle_max_size(w, h)
+        sb = comm.stream_buffers(2 * nl, cap, k % 2)
+        if sb is None:
+            failures.append("stream slots: E_UNSUPPORTED on a peer-capable box")
+            break
+        sizes = torch.zeros(2 * nl, dtype=torch.int64, device=dev)
+        ws = torch.zeros(eqc.image_rle_workspace_size_batch(2 * nl, w, h), dtype=torch.uint8, device=dev)
+        eqc.image_compress_rle_batch(imgs, [0] * nl + [1] * nl, [1] * nl + [0] * nl, sb, sizes, ws)
+        fb = comm.frame_buffers(w, h, 0)
+        out = fb[2] if k == 3 else torch.zeros((h, w), dtype=torch.int32, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        eqc.compose_direct_send_rle_pull(comm, nl, w, h, k % 2, out if rank == dest else None, status, dest_rank=dest)
+        torch.cuda.synchronize()
+        if int(status.item()) != 0:
+            failures.append(f"rle-pull {w}x{h} nl={nl}: status {int(status.item())}")
+        if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.depth_composite(c, d)[0]).all():
+            failures.append(f"rle-pull {w}x{h} nl={nl} out={'gather' if k == 3 else 'user'}: mismatch")
+        dist.barrier()
     comm.destroy()
     t = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(t)
