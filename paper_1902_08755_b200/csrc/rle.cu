@@ -1146,7 +1146,9 @@ extern "C" int64_t image_rle_max_size(int w, int h) {
 extern "C" size_t image_rle_workspace_size_batch(int count, int w, int h) {
   if (count <= 0 || w <= 0 || h <= 0) return 0;
   const int64_t runs = (int64_t)count * enc_runs_per_image(w, h);
-  return enc_scratch_offset(runs, count) + (size_t)runs * kScratchPerWarp;
+  // + 256: the record scratch is aligned to 256 bytes in absolute address
+  // (its L2 lines are discarded whole), whatever the workspace's alignment
+  return enc_scratch_offset(runs, count) + 256 + (size_t)runs * kScratchPerWarp;
 }
 
 extern "C" size_t image_rle_workspace_size(int w, int h) { return image_rle_workspace_size_batch(1, w, h); }
@@ -1189,7 +1191,8 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   const int64_t tiles = (int64_t)count * p.tiles_per_image;
   if (runs > 0x7FFFFFFFll || p.nchunks > 0x7FFFFFFFll) return EQC_E_INVALID;
   p.run_size = reinterpret_cast<int32_t *>(workspace);
-  p.scratch = reinterpret_cast<uint8_t *>(workspace) + enc_scratch_offset(runs, count);
+  p.scratch = reinterpret_cast<uint8_t *>(
+      ((uintptr_t)workspace + enc_scratch_offset(runs, count) + 255) & ~(uintptr_t)255);
   uint32_t *run_off = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(workspace) + enc_runoff_offset(runs));
   static bool configured = false;
   const size_t smem = sizeof(EncSmem);

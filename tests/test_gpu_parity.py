@@ -371,3 +371,89 @@ def test_display_wall_tile_64_sources_rle_transport(eqc):
         eqc.image_decompress_rle(cs[i], o, status)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(to_host(o), c[i])
+
+
+def test_bench_step_8x4k_exact(eqc):
+    """bench.py's exact step on its exact inputs: image_compress_rle_batch of
+    the 16 images of synth.depth_sources(SEED + 10, 8, 3840, 2160) (colour
+    swizzled, depth plain) in one launch, then compositor_depth_rle.  Every
+    stream byte-for-byte against oracle.rle_encode; every output colour and
+    depth pixel against oracle.depth_composite."""
+    n, w, h = 8, 3840, 2160
+    c, d = synth.depth_sources(SEED + 10, n, w, h)
+    imgs = c + d
+    kinds = [eqc.KIND_RGBA8] * n + [eqc.KIND_DEPTH32] * n
+    flags = [eqc.FLAG_SWIZZLE] * n + [0] * n
+    srcs = [to_dev(x) for x in imgs]
+    cap = eqc.image_rle_max_size(w, h)
+    streams = [torch.empty(cap, dtype=torch.uint8, device="cuda") for _ in imgs]
+    sizes = torch.zeros(len(imgs), dtype=torch.int64, device="cuda")
+    ws = torch.zeros(eqc.image_rle_workspace_size_batch(len(imgs), w, h), dtype=torch.uint8, device="cuda")
+    out_c, out_d = out_frame(h, w), out_frame(h, w)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for _ in range(2):  # as in the bench: the workspace is reused without a reset
+        eqc.image_compress_rle_batch(srcs, kinds, flags, streams, sizes, ws)
+        eqc.compositor_depth_rle(streams[:n], streams[n:], out_c, out_d, status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    got_sizes = sizes.tolist()
+    for i, img in enumerate(imgs):
+        want = oracle.rle_encode(img, kind=kinds[i], flags=flags[i])
+        assert got_sizes[i] == len(want), i
+        assert bytes_of(streams[i], len(want)) == want, i
+    oc, od = oracle.depth_composite(c, d)
+    np.testing.assert_array_equal(to_host(out_c), oc)
+    np.testing.assert_array_equal(to_host(out_d), od)
+
+
+def _fused_status(eqc, cs, ds, w, h):
+    out_c, out_d = out_frame(h, w), out_frame(h, w)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    eqc.compositor_depth_rle([stream_dev(s) for s in cs], [stream_dev(s) for s in ds], out_c, out_d, status)
+    torch.cuda.synchronize()
+    return int(status.item())
+
+
+def test_fused_decode_corruption(eqc):
+    """compositor_depth_rle flags a corrupt header field, a broken table offset
+    and a malformed record it decodes (one noise source: every chunk of both
+    streams is non-constant and decoded)."""
+    w, h = 300, 3
+    c, d = synth.random_frames(SEED + 77, 1, w, h)
+    cs = bytearray(oracle.rle_encode(c[0], kind=0, flags=1))
+    ds = bytearray(oracle.rle_encode(d[0], kind=1, flags=0))
+    assert _fused_status(eqc, [bytes(cs)], [bytes(ds)], w, h) == 0
+    S = (w + 127) // 128
+    pay0 = 32 + 8 * S * h
+    cases = []
+    t = bytearray(ds); t[8] ^= 0x01; cases.append(("depth header W", bytes(cs), bytes(t)))
+    t = bytearray(cs); t[12] ^= 0x02; cases.append(("colour header H", bytes(t), bytes(ds)))
+    t = bytearray(cs); t[32 + 8 * 2] ^= 0x04; cases.append(("colour table offset", bytes(t), bytes(ds)))
+    t = bytearray(ds); t[32 + 8 * 4] ^= 0x01; cases.append(("depth table offset", bytes(cs), bytes(t)))
+    t = bytearray(ds); t[pay0] = 0; cases.append(("depth record ntok = 0", bytes(cs), bytes(t)))
+    t = bytearray(cs); t[pay0] = 0; cases.append(("colour record ntok = 0", bytes(t), bytes(ds)))
+    t = bytearray(ds); t[pay0 + 1] = 0x80 | 3; cases.append(("depth token lengths", bytes(cs), bytes(t)))
+    for name, a, b in cases:
+        assert _fused_status(eqc, [a], [b], w, h) == eqc.E_CORRUPT, name
+
+
+def test_encoder_workspace_any_8_byte_alignment(eqc):
+    """The encoder workspace need only be 8-byte aligned (eqc.h): a workspace
+    starting 8 bytes into an allocation gives the same, exact streams."""
+    n, w, h = 4, 900, 40
+    c, d = synth.depth_sources(SEED + 78, n, w, h)
+    imgs = c[:2] + d[:2]
+    kinds, flags = [0, 0, 1, 1], [1, 1, 0, 0]
+    srcs = [to_dev(x) for x in imgs]
+    cap = eqc.image_rle_max_size(w, h)
+    streams = [torch.empty(cap, dtype=torch.uint8, device="cuda") for _ in imgs]
+    sizes = torch.zeros(len(imgs), dtype=torch.int64, device="cuda")
+    need = eqc.image_rle_workspace_size_batch(len(imgs), w, h)
+    for off in (8, 24, 136):
+        base = torch.full((need + off,), 0x5A, dtype=torch.uint8, device="cuda")
+        eqc.image_compress_rle_batch(srcs, kinds, flags, streams, sizes, base[off:])
+        torch.cuda.synchronize()
+        for i, img in enumerate(imgs):
+            want = oracle.rle_encode(img, kind=kinds[i], flags=flags[i])
+            assert int(sizes[i].item()) == len(want), (off, i)
+            assert bytes_of(streams[i], len(want)) == want, (off, i)

@@ -121,3 +121,25 @@ def test_fused_decode_rejects_rle64(eqc):
     eqc.compositor_depth_rle([cs], [ds], oc, None, status)
     torch.cuda.synchronize()
     assert int(status.item()) == eqc.E_CORRUPT  # the fused path takes per-component streams only
+
+
+def test_rle64_golden_streams_on_gpu(eqc):
+    """The hand-derived RLE-64 streams (tests/golden/rle64_streams.txt): the
+    GPU encoder emits them byte for byte and the GPU decoder inverts them."""
+    from test_oracle_rle64 import golden_rle64_streams
+    for name, kind, img, want in golden_rle64_streams():
+        h, w = img.shape
+        cap = eqc.image_rle_max_size(w, h)
+        st = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+        sz = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ws = torch.zeros(eqc.image_rle_workspace_size_batch(1, w, h), dtype=torch.uint8, device="cuda")
+        eqc.image_compress_rle_batch([to_dev(img)], [kind], [eqc.FLAG_RLE64], [st], sz, ws)
+        torch.cuda.synchronize()
+        assert int(sz.item()) == len(want), name
+        assert bytes_of(st, len(want)) == want, name
+        out = out_frame(h, w)
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        eqc.image_decompress_rle_batch([stream_dev(want)], [out], status)
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0, name
+        np.testing.assert_array_equal(to_host(out), img)
