@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "rle.cuh"
+#include "rle_enc.cuh"
 
 #ifndef EQC_ENC_WARPS
 #define EQC_ENC_WARPS 1
@@ -101,15 +102,15 @@ __device__ __forceinline__ void copy_run(uint8_t *g, const uint8_t *src, int64_t
   const uintptr_t end = ga + (uintptr_t)size;
   const uintptr_t last_w = end & ~(uintptr_t)3;
   if (first_w >= last_w) {
-    for (int64_t k = lane; k < size; k += 32) g[k] = src[k];
+    for (int64_t k = lane; k < size; k += 32) g[k] = __ldcg(src + k);
     return;
   }
   const int head = (int)(first_w - ga);
   const int tail = (int)(end - last_w);
-  if (lane < head) g[lane] = src[lane];
+  if (lane < head) g[lane] = __ldcg(src + lane);
   if (lane >= 8 && lane < 8 + tail) {
     const int64_t q = (int64_t)(last_w - ga) + lane - 8;
-    g[q] = src[q];
+    g[q] = __ldcg(src + q);
   }
   const int64_t nw = (int64_t)((last_w - first_w) >> 2);
   const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src) + (head >> 2);
@@ -122,8 +123,8 @@ __device__ __forceinline__ void copy_run(uint8_t *g, const uint8_t *src, int64_t
     uint32_t lo[8], hi[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      lo[u] = __ldg(s32 + k + 32 * u);
-      hi[u] = sh ? __ldg(s32 + k + 32 * u + 1) : 0u;
+      lo[u] = __ldcg(s32 + k + 32 * u);
+      hi[u] = sh ? __ldcg(s32 + k + 32 * u + 1) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) gw[k + 32 * u] = sh ? __funnelshift_r(lo[u], hi[u], 8 * sh) : lo[u];
@@ -132,8 +133,8 @@ __device__ __forceinline__ void copy_run(uint8_t *g, const uint8_t *src, int64_t
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int64_t kk = k + 32 * u;
-    lo[u] = kk < nw ? __ldg(s32 + kk) : 0u;
-    hi[u] = (kk < nw && sh) ? __ldg(s32 + kk + 1) : 0u;
+    lo[u] = kk < nw ? __ldcg(s32 + kk) : 0u;
+    hi[u] = (kk < nw && sh) ? __ldcg(s32 + kk + 1) : 0u;
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
@@ -415,6 +416,328 @@ __global__ void __launch_bounds__(kCompactWarps * 32) rle_compact_kernel(const _
     copy_run(im.dst + 32 + 8 * p.nchunks + base, scr, run, lane);
     __syncwarp();
     for (int l = lane; (int64_t)l * 128 < run; l += 32) discard_l2(scr + 128 * l);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// v1 encoder, fused (image_compress_rle_batch without RLE-64): one persistent
+// launch, warps pulling two kinds of work:
+//   ENCODE (m, r)   code run r (kRun3 consecutive chunks) of image m into a
+//                   per-warp shared span (records at run-relative offsets),
+//                   copy it to the run's record-scratch slot, write the run
+//                   size (also added to its block of 64 runs) and the
+//                   run-relative table entries; tickets in image order;
+//   COMPACT (m, g)  once every run of image m is coded: move runs
+//                   [g*kCmpRuns, ...) to their payload offsets (the sum of the
+//                   preceding blocks and runs), rebase their table entries and
+//                   drop their scratch lines from L2; the last group writes the
+//                   header and the stream size.
+// A warp takes compaction work first, but only of an image whose runs are all
+// coded (so no warp ever waits while holding work another warp needs); it
+// waits only when every encode ticket is gone.  Images finish roughly in
+// ticket order, so an image is moved while its scratch is still L2-resident,
+// overlapped with the encoding of later images.
+// ---------------------------------------------------------------------------
+#ifndef EQC_E3_WARPS
+#define EQC_E3_WARPS 4
+#endif
+#ifndef EQC_E3_MINB
+#define EQC_E3_MINB 6
+#endif
+#ifndef EQC_E3_CWARPS
+#define EQC_E3_CWARPS 0  // compaction warps per CTA (0: run-scan + compaction kernels after the encoder)
+#endif
+constexpr int kRun3 = kSTChunksPerWarp;  // chunks per encode item (same scratch layout as the RLE-64 path)
+constexpr int kE3Warps = EQC_E3_WARPS;   // warps per CTA, the last kE3CWarps of them compaction warps
+constexpr int kE3CWarps = EQC_E3_CWARPS;
+constexpr int kCmpRuns = 4;              // runs per compaction item
+
+struct E3Warp {
+  uint8_t span[kRun3 * kRecMax + 16];    // the run's records (+ garbage slack)
+  uint8_t tp[(eqc_enc::kTpBytes + 15) & ~15];
+  uint32_t cps[kRun3];
+  uint16_t csz[kRun3];
+  uint8_t q[kRun3];
+};
+
+struct Enc3Params {
+  EncImage img[kMaxBatch];
+  int32_t *run_size;   // [count][R]
+  uint8_t *scratch;    // [count][R] slots of kScratchPerWarp bytes
+  uint32_t *ctr;       // one 128-byte line each: [0] encode ticket, [32] first image with unclaimed
+                       // compaction, [64 + 32 m] done runs of image m, [64 + 32 (count + m)] compaction
+                       // groups claimed; then blk[count][NB] at [64 + 64 count] (see e3_ctr_*)
+  int64_t pitch, nchunks;
+  int count, w, h, S, R, G, NB;  // NB = blocks of 64 runs per image
+  int total_enc;
+  int vec;             // 128-bit loads allowed
+};
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *a) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t *a, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// CONTIG: pitch == w, w % 128 == 0, 16-byte aligned: a run is one contiguous
+// span of full chunks (straight-line loads with immediate offsets).
+// FULL: w % 128 == 0 (every chunk has 128 pixels).
+template <bool FULL, bool CONTIG>
+__device__ void e3_encode_run(const Enc3Params &p, int m, int r, int lane, E3Warp &W, const eqc_enc::LaneK &K,
+                              const uint32_t *lut_sel, const uint32_t *lut_st) {
+  const EncImage im = p.img[m];
+  const int nch = (int)p.nchunks;
+  const bool swz = (im.flags & EQC_FLAG_SWIZZLE) != 0;
+  const int c0 = r * kRun3;
+  const int cnt = min(kRun3, nch - c0);
+  const int Llast = p.w - (p.S - 1) * kC;
+  const int y0 = c0 / p.S, k0 = c0 - y0 * p.S;
+  const uint32_t *row0 = im.src + (int64_t)y0 * p.pitch;
+  auto chunk_ptr = [&](int j, int &L) -> const uint32_t * {
+    if (CONTIG) {
+      L = kC;
+      return row0 + (int64_t)(k0 + j) * kC;
+    }
+    const int kk = k0 + j;
+    const int dy = kk / p.S, k = kk - dy * p.S;
+    L = (!FULL && k == p.S - 1) ? Llast : kC;
+    return row0 + (int64_t)dy * p.pitch + k * kC;
+  };
+  // ---- A: classify (8 chunks in flight per lane)
+  uint32_t cmask = 0, myc = 0;  // myc: lane j keeps the value of constant chunk j
+  int ng = 0;
+  for (int j0 = 0; j0 < cnt; j0 += 8) {
+    uint32_t px[8][4];
+    int Ls[8];
+    if (CONTIG) {
+      const uint4 *base = reinterpret_cast<const uint4 *>(row0 + (int64_t)(k0 + j0) * kC) + lane;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint4 v = ld_stream_u4_if(base + 32 * u, j0 + u < cnt);
+        px[u][0] = v.x, px[u][1] = v.y, px[u][2] = v.z, px[u][3] = v.w;
+        Ls[u] = kC;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        Ls[u] = 0;
+        px[u][0] = px[u][1] = px[u][2] = px[u][3] = 0u;
+        if (j0 + u < cnt) {
+          const uint32_t *cp = chunk_ptr(j0 + u, Ls[u]);
+          if (p.vec && (FULL || 4 * lane + 4 <= Ls[u])) {
+            const uint4 v = ld_stream_u4(cp + 4 * lane);
+            px[u][0] = v.x, px[u][1] = v.y, px[u][2] = v.z, px[u][3] = v.w;
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) px[u][q] = 4 * lane + q < Ls[u] ? ld_stream_u32(cp + 4 * lane + q) : 0u;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (j0 + u >= cnt) break;
+      const int L = Ls[u];
+      const uint32_t v0 = __shfl_sync(EQC_FULL, px[u][0], 0);
+      bool same;
+      if (FULL) {
+        same = ((px[u][0] ^ v0) | (px[u][1] ^ v0) | (px[u][2] ^ v0) | (px[u][3] ^ v0)) == 0u;
+      } else {
+        same = true;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) same = same && (px[u][q] == v0 || 4 * lane + q >= L);
+      }
+      if (__all_sync(EQC_FULL, same) && (FULL || L >= 3)) {
+        cmask |= 1u << (j0 + u);
+        myc = lane == j0 + u ? v0 : myc;
+      } else {
+        if (lane == 0) W.q[ng] = (uint8_t)(j0 + u);
+        ++ng;
+      }
+    }
+  }
+  __syncwarp();
+  // ---- B: code the other chunks (re-read from L2, the next one in flight)
+  int coded = 0;
+  uint32_t nx[4] = {0u, 0u, 0u, 0u};
+  int Ln = kC;
+  auto load = [&](int j) {
+    const uint32_t *cp = chunk_ptr(j, Ln);
+    if (CONTIG || (p.vec && (FULL || 4 * lane + 4 <= Ln))) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(cp + 4 * lane));
+      nx[0] = v.x, nx[1] = v.y, nx[2] = v.z, nx[3] = v.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nx[q] = 4 * lane + q < Ln ? __ldcg(cp + 4 * lane + q) : 0u;
+    }
+  };
+  if (ng > 0) load(W.q[0]);
+#pragma unroll 1
+  for (int g = 0; g < ng; ++g) {
+    uint32_t x[4] = {nx[0], nx[1], nx[2], nx[3]};
+    const int L = Ln;
+    const int j = W.q[g];
+    if (g + 1 < ng) load(W.q[g + 1]);
+    if (swz) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = swizzle(x[q]);
+    }
+    const int off = 12 * __popc(cmask & ((1u << j) - 1u)) + coded;
+    uint32_t ps;
+    const int sz = eqc_enc::code_chunk<FULL>(x, L, lane, K, W.span + off, W.tp, lut_sel, lut_st, &ps);
+    if (lane == 0) {
+      W.csz[j] = (uint16_t)sz;
+      W.cps[j] = ps;
+    }
+    coded += sz;
+  }
+  __syncwarp();
+  // ---- C: offsets, constant records, table entries, run -> scratch
+  const int j = lane;
+  const bool isc = j < cnt && ((cmask >> j) & 1u);
+  const int s = j < cnt ? (isc ? 12 : (int)W.csz[j]) : 0;
+  const int inc = (int)warp_incl_scan_add((uint32_t)s, lane);
+  const int run = __shfl_sync(EQC_FULL, inc, 31);
+  const int off = inc - s;
+  if (isc) {
+    int L = kC;
+    if (!FULL) chunk_ptr(j, L);
+    const uint32_t v = swz ? swizzle(myc) : myc;
+    const uint32_t c = 0x80u | (uint32_t)(L - 1);
+    // [01][c][v0] [01][c][v1] [01][c][v2] [01][c][v3] as three words, stored bytewise
+    const uint32_t w0 = 1u | (c << 8) | ((v & 0xFFu) << 16) | (1u << 24);
+    const uint32_t w1 = c | (((v >> 8) & 0xFFu) << 8) | (1u << 16) | (c << 24);
+    const uint32_t w2 = ((v >> 16) & 0xFFu) | (1u << 8) | (c << 16) | ((v >> 24) << 24);
+    uint8_t *g = W.span + off;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      g[q] = (uint8_t)(w0 >> (8 * q));
+      g[4 + q] = (uint8_t)(w1 >> (8 * q));
+      g[8 + q] = (uint8_t)(w2 >> (8 * q));
+    }
+  }
+  if (j < cnt) {
+    uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
+    table[j] = make_uint2((uint32_t)off, isc ? 0x03030303u : W.cps[j]);
+  }
+  __syncwarp();
+  const int64_t gr = (int64_t)m * p.R + r;
+  uint4 *slot = reinterpret_cast<uint4 *>(p.scratch + (size_t)gr * kScratchPerWarp);
+  const uint4 *sp = reinterpret_cast<const uint4 *>(W.span);
+  for (int i = lane; 16 * i < run; i += 32) slot[i] = sp[i];
+  if (lane == 0) p.run_size[gr] = run;
+  if (kE3CWarps > 0) {
+    __syncwarp();  // the warp's scratch, table and size stores before lane 0's release
+    if (lane == 0) {
+      red_release_add(p.ctr + 64 + 64 * p.count + m * p.NB + (r >> 6), (uint32_t)run);  // the run's block total
+      red_release_add(p.ctr + 64 + 32 * m, 1u);                                             // one more run done
+    }
+  }
+}
+
+// Compaction item (image m fully coded): the payload offset of run r0 is the
+// sum of the block totals before r0's block plus the sizes of the runs of its
+// block before it (<= 2 x 64 values, one load round); the item of the image's
+// last runs also writes the header and the stream size.
+__device__ void e3_compact(const Enc3Params &p, int m, int g, int lane) {
+  const EncImage im = p.img[m];
+  const int nch = (int)p.nchunks;
+  const int r0 = g * kCmpRuns, r1 = min(p.R, r0 + kCmpRuns);
+  const int32_t *rs = p.run_size + (int64_t)m * p.R;
+  const uint32_t *blk = p.ctr + 64 + 64 * p.count + (int64_t)m * p.NB;
+  const int b0 = r0 >> 6, q0 = b0 << 6;
+  uint32_t part = 0;
+  for (int i = lane; i < b0; i += 32) part += __ldcg(blk + i);
+  for (int i = q0 + lane; i < r0; i += 32) part += (uint32_t)__ldcg(rs + i);
+  uint32_t base = __reduce_add_sync(EQC_FULL, part);
+  const bool last = r1 == p.R;
+  uint8_t *payload = im.dst + 32 + 8 * p.nchunks;
+  for (int r = r0; r < r1; ++r) {
+    const int64_t gr = (int64_t)m * p.R + r;
+    const int run = __ldcg(rs + r);
+    const int c0 = r * kRun3, cnt = min(kRun3, nch - c0);
+    uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
+    if (lane < cnt) {
+      uint2 e = __ldcg(table + lane);
+      e.x += base;
+      table[lane] = e;
+    }
+    const uint8_t *scr = p.scratch + (size_t)gr * kScratchPerWarp;
+    if (run > 0) {
+      copy_run(payload + base, scr, run, lane);
+      __syncwarp();
+      for (int l = lane; l * 128 < run; l += 32) discard_l2(scr + 128 * l);
+    }
+    base += (uint32_t)run;
+  }
+  if (last && lane == 0) {
+    const uint32_t total = base;
+    uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
+    h32[0] = kMagic;
+    h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) | ((uint32_t)kLog2C << 24);
+    h32[2] = (uint32_t)p.w;
+    h32[3] = (uint32_t)p.h;
+    h32[4] = (uint32_t)p.nchunks;
+    h32[5] = 0u;
+    h32[6] = total;
+    h32[7] = 0u;
+    *im.d_size = 32 + 8 * p.nchunks + (int64_t)total;
+  }
+}
+
+template <bool FULL, bool CONTIG>
+__global__ void __launch_bounds__(kE3Warps * 32, EQC_E3_MINB) rle_encode3_kernel(const __grid_constant__ Enc3Params p) {
+  __shared__ uint32_t s_lut[16 + 256];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 16 + 256; i += blockDim.x) s_lut[i] = reinterpret_cast<const uint32_t *>(&eqc_enc::g_enc_luts)[i];
+  __syncthreads();  // the only CTA-wide barrier: warps are independent below
+  uint32_t *const ectr = p.ctr, *const cimg = p.ctr + 32, *const done = p.ctr + 64, *const ccnt = p.ctr + 64 + 32 * p.count;
+  if (kE3CWarps > 0 && warp >= kE3Warps - kE3CWarps) {
+    // ---- compaction warp: move the runs of images whose runs are all coded
+    for (;;) {
+      int job = -1, jm = 0, fin = 0;
+      if (lane == 0) {
+        int m = (int)ld_relaxed_u32(cimg);
+        while (m < p.count && ld_relaxed_u32(done + 32 * m) == (uint32_t)p.R) {
+          const int g = (int)atomicAdd(ccnt + 32 * m, 1u);
+          if (g < p.G) {
+            job = g, jm = m;
+            if (g == p.G - 1) atomicMax(cimg, (uint32_t)(m + 1));
+            break;
+          }
+          atomicMax(cimg, (uint32_t)(m + 1));
+          ++m;
+        }
+        fin = m >= p.count;
+        if (job >= 0) fence_acq_rel_gpu();  // acquire: the image's runs (observed complete)
+      }
+      job = __shfl_sync(EQC_FULL, job, 0);
+      if (job >= 0) {
+        e3_compact(p, __shfl_sync(EQC_FULL, jm, 0), job, lane);
+      } else {
+        if (__shfl_sync(EQC_FULL, fin, 0)) break;
+        __nanosleep(1000);
+      }
+    }
+    return;
+  }
+  // ---- encode warp
+  E3Warp &W = reinterpret_cast<E3Warp *>(smem_raw)[warp];
+  const eqc_enc::LaneK K = eqc_enc::lane_consts(lane);
+  int e = 0;  // encode ticket
+  if (lane == 0) e = (int)atomicAdd(ectr, 1u);
+  e = __shfl_sync(EQC_FULL, e, 0);
+  while (e < p.total_enc) {
+    int en = 0;
+    if (lane == 0) en = (int)atomicAdd(ectr, 1u);  // the next ticket, in flight meanwhile
+    const int m = e / p.R;
+    e3_encode_run<FULL, CONTIG>(p, m, e - m * p.R, lane, W, K, s_lut, s_lut + 16);
+    e = __shfl_sync(EQC_FULL, en, 0);
   }
 }
 
@@ -1132,8 +1455,16 @@ inline int64_t enc_runs_per_image(int w, int h) {
 // workspace: run_size[runs] int32, run_off[runs + count] uint32, then (256-byte
 // aligned) the record scratch
 inline size_t enc_runoff_offset(int64_t runs) { return (size_t)runs * sizeof(int32_t); }
+inline size_t enc_ctr_offset(int64_t runs, int count) {
+  return enc_runoff_offset(runs) + ((size_t)runs + count) * sizeof(uint32_t);
+}
+// fused v1 encoder counters: ticket, done runs per image, size of every block
+// of 64 runs per image
+inline size_t enc_ctr_words(int count, int64_t runs_per_image) {
+  return 64 + 64 * (size_t)count + (size_t)count * (size_t)((runs_per_image + 63) / 64);
+}
 inline size_t enc_scratch_offset(int64_t runs, int count) {
-  return (enc_runoff_offset(runs) + ((size_t)runs + count) * sizeof(uint32_t) + 255) & ~(size_t)255;
+  return (enc_ctr_offset(runs, count) + 4 * enc_ctr_words(count, runs / count) + 255) & ~(size_t)255;
 }
 
 }  // namespace
@@ -1205,10 +1536,51 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
     configured = true;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (r64)
+  if (!r64) {
+    // v1: one fused launch (encode + compaction), after zeroing its counters
+    Enc3Params e;
+    for (int i = 0; i < count; ++i) e.img[i] = p.img[i];
+    e.run_size = p.run_size;
+    e.scratch = p.scratch;
+    e.ctr = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(workspace) + enc_ctr_offset(runs, count));
+    e.pitch = pitch;
+    e.nchunks = p.nchunks;
+    e.count = count;
+    e.w = w;
+    e.h = h;
+    e.S = p.S;
+    e.R = p.runs_per_image;
+    e.G = (e.R + kCmpRuns - 1) / kCmpRuns;
+    e.NB = (e.R + 63) / 64;
+    e.total_enc = count * e.R;
+    e.vec = vec ? 1 : 0;
+    const bool full = (w % kC) == 0;
+    const bool contig = full && vec && pitch == w;
+    static bool configured3 = false;
+    const size_t smem3 = sizeof(E3Warp) * (kE3Warps - kE3CWarps);
+    if (!configured3) {
+      if (cudaFuncSetAttribute(rle_encode3_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem3) != cudaSuccess ||
+          cudaFuncSetAttribute(rle_encode3_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem3) != cudaSuccess ||
+          cudaFuncSetAttribute(rle_encode3_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem3) != cudaSuccess)
+        return EQC_E_CUDA;
+      configured3 = true;
+    }
+    EQC_CUDA_TRY(cudaMemsetAsync(e.ctr, 0, 4 * enc_ctr_words(count, e.R), st));
+    const int64_t item_ctas = ((int64_t)e.total_enc + kE3Warps - kE3CWarps - 1) / (kE3Warps - kE3CWarps);
+    auto launch = [&](auto kern) {
+      const int res = eqc_resident_ctas(kern, kE3Warps * 32, smem3);
+      kern<<<(unsigned)std::min<int64_t>(res, item_ctas), kE3Warps * 32, smem3, st>>>(e);
+    };
+    if (contig) launch(rle_encode3_kernel<true, true>);
+    else if (full) launch(rle_encode3_kernel<true, false>);
+    else launch(rle_encode3_kernel<false, false>);
+    if (kE3CWarps > 0) return eqc_launch_status();
+  } else {
     rle_encode_kernel<true><<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
-  else
-    rle_encode_kernel<false><<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
+  }
   CompactParams c;
   for (int i = 0; i < count; ++i) c.img[i] = p.img[i];
   rle_runscan_kernel<<<count, 1024, 0, st>>>(p.run_size, run_off, p.runs_per_image);
