@@ -420,37 +420,31 @@ __global__ void __launch_bounds__(kCompactWarps * 32) rle_compact_kernel(const _
 }
 
 // ---------------------------------------------------------------------------
-// v1 encoder, fused (image_compress_rle_batch without RLE-64): one persistent
-// launch, warps pulling two kinds of work:
-//   ENCODE (m, r)   code run r (kRun3 consecutive chunks) of image m into a
-//                   per-warp shared span (records at run-relative offsets),
-//                   copy it to the run's record-scratch slot, write the run
-//                   size (also added to its block of 64 runs) and the
-//                   run-relative table entries; tickets in image order;
-//   COMPACT (m, g)  once every run of image m is coded: move runs
-//                   [g*kCmpRuns, ...) to their payload offsets (the sum of the
-//                   preceding blocks and runs), rebase their table entries and
-//                   drop their scratch lines from L2; the last group writes the
-//                   header and the stream size.
-// A warp takes compaction work first, but only of an image whose runs are all
-// coded (so no warp ever waits while holding work another warp needs); it
-// waits only when every encode ticket is gone.  Images finish roughly in
-// ticket order, so an image is moved while its scratch is still L2-resident,
-// overlapped with the encoding of later images.
+// v1 encoder (image_compress_rle_batch without RLE-64): two launches.
+//   rle_encode3_kernel   persistent warps take runs (kRun3 consecutive chunks
+//                        of one image) by ticket, in image order: classify the
+//                        run's chunks, code the non-constant ones
+//                        (eqc_enc::code_chunk) into a per-warp shared span at
+//                        run-relative offsets, write the constant chunks'
+//                        12-byte records and the run-relative table entries,
+//                        copy the span to the run's record-scratch slot (L2
+//                        evict-last), store the run size and add it to its
+//                        block of 64 runs;
+//   rle_compact3_kernel  moves every run to its payload offset (below).
+// (A single launch with the compaction overlapped was measured slower: the
+// completion signalling costs every run a release fence.)
 // ---------------------------------------------------------------------------
+#ifndef EQC_E3_GROUP_MB
+#define EQC_E3_GROUP_MB 4096  // raw megabytes of images per encoder/compaction launch pair
+#endif
 #ifndef EQC_E3_WARPS
 #define EQC_E3_WARPS 4
 #endif
 #ifndef EQC_E3_MINB
 #define EQC_E3_MINB 6
 #endif
-#ifndef EQC_E3_CWARPS
-#define EQC_E3_CWARPS 0  // compaction warps per CTA (0: run-scan + compaction kernels after the encoder)
-#endif
 constexpr int kRun3 = kSTChunksPerWarp;  // chunks per encode item (same scratch layout as the RLE-64 path)
-constexpr int kE3Warps = EQC_E3_WARPS;   // warps per CTA, the last kE3CWarps of them compaction warps
-constexpr int kE3CWarps = EQC_E3_CWARPS;
-constexpr int kCmpRuns = 4;              // runs per compaction item
+constexpr int kE3Warps = EQC_E3_WARPS;
 
 struct E3Warp {
   uint8_t span[kRun3 * kRecMax + 16];    // the run's records (+ garbage slack)
@@ -464,24 +458,41 @@ struct Enc3Params {
   EncImage img[kMaxBatch];
   int32_t *run_size;   // [count][R]
   uint8_t *scratch;    // [count][R] slots of kScratchPerWarp bytes
-  uint32_t *ctr;       // one 128-byte line each: [0] encode ticket, [32] first image with unclaimed
-                       // compaction, [64 + 32 m] done runs of image m, [64 + 32 (count + m)] compaction
-                       // groups claimed; then blk[count][NB] at [64 + 64 count] (see e3_ctr_*)
+  uint32_t *ctr;       // [0] encode ticket
+  uint32_t *blk;       // [count][NB] block totals (sum of the sizes of 64 consecutive runs)
   int64_t pitch, nchunks;
-  int count, w, h, S, R, G, NB;  // NB = blocks of 64 runs per image
+  int count, w, h, S, R, NB;  // NB = blocks of 64 runs per image
   int total_enc;
   int vec;             // 128-bit loads allowed
 };
 
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *a) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
+
+#ifndef EQC_E3_L2HINT
+#define EQC_E3_L2HINT 2  // 1: record scratch stored L2 evict_last; 2: + classify loads L2 evict_first
+#endif
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
-__device__ __forceinline__ void red_release_add(uint32_t *a, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_u4_hint(void *a, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_stream_u4_if_hint(const void *p, bool pred, uint64_t pol) {
+  uint4 r = make_uint4(0, 0, 0, 0);
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+      : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+      : "l"(p), "r"((uint32_t)pred), "l"(pol));
+  return r;
+}
 
 // CONTIG: pitch == w, w % 128 == 0, 16-byte aligned: a run is one contiguous
 // span of full chunks (straight-line loads with immediate offsets).
@@ -517,7 +528,8 @@ __device__ void e3_encode_run(const Enc3Params &p, int m, int r, int lane, E3War
       const uint4 *base = reinterpret_cast<const uint4 *>(row0 + (int64_t)(k0 + j0) * kC) + lane;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint4 v = ld_stream_u4_if(base + 32 * u, j0 + u < cnt);
+        const uint4 v = EQC_E3_L2HINT >= 2 ? ld_stream_u4_if_hint(base + 32 * u, j0 + u < cnt, l2_policy_evict_first())
+                                           : ld_stream_u4_if(base + 32 * u, j0 + u < cnt);
         px[u][0] = v.x, px[u][1] = v.y, px[u][2] = v.z, px[u][3] = v.w;
         Ls[u] = kC;
       }
@@ -628,54 +640,67 @@ __device__ void e3_encode_run(const Enc3Params &p, int m, int r, int lane, E3War
   const int64_t gr = (int64_t)m * p.R + r;
   uint4 *slot = reinterpret_cast<uint4 *>(p.scratch + (size_t)gr * kScratchPerWarp);
   const uint4 *sp = reinterpret_cast<const uint4 *>(W.span);
-  for (int i = lane; 16 * i < run; i += 32) slot[i] = sp[i];
-  if (lane == 0) p.run_size[gr] = run;
-  if (kE3CWarps > 0) {
-    __syncwarp();  // the warp's scratch, table and size stores before lane 0's release
-    if (lane == 0) {
-      red_release_add(p.ctr + 64 + 64 * p.count + m * p.NB + (r >> 6), (uint32_t)run);  // the run's block total
-      red_release_add(p.ctr + 64 + 32 * m, 1u);                                             // one more run done
-    }
+  if (EQC_E3_L2HINT >= 1) {
+    const uint64_t pol = l2_policy_evict_last();
+    for (int i = lane; 16 * i < run; i += 32) st_u4_hint(slot + i, sp[i], pol);
+  } else {
+    for (int i = lane; 16 * i < run; i += 32) slot[i] = sp[i];
   }
+  if (lane == 0) p.run_size[gr] = run;
+  if (lane == 0) atomicAdd(p.blk + (int64_t)m * p.NB + (r >> 6), (uint32_t)run);  // the run's block of 64 runs
 }
 
-// Compaction item (image m fully coded): the payload offset of run r0 is the
-// sum of the block totals before r0's block plus the sizes of the runs of its
-// block before it (<= 2 x 64 values, one load round); the item of the image's
-// last runs also writes the header and the stream size.
-__device__ void e3_compact(const Enc3Params &p, int m, int g, int lane) {
+// Compaction (v1): one warp per run.  The run's payload offset is the sum of
+// the block totals before its block of 64 runs plus the sizes of the runs of
+// its block before it; every load of the run -- those partial sums, its size,
+// its table entries and the first 512 B of its records -- is issued at once
+// (one memory round trip for a background run), then the records are stored at
+// their offset (whole destination words funnel-shifted, the <= 3 head and tail
+// bytes by byte stores), the table entries rebased, and the scratch lines
+// dropped from L2.  The warp of an image's last run writes the header.
+struct Cmp3Params {
+  EncImage img[kMaxBatch];
+  const int32_t *run_size;  // [count][R]
+  const uint32_t *blk;      // [count][NB]
+  const uint8_t *scratch;
+  int64_t nchunks;
+  int count, w, h, R, NB;
+};
+
+constexpr int kCmp3Warps = 8;
+
+__global__ void __launch_bounds__(kCmp3Warps * 32) rle_compact3_kernel(const __grid_constant__ Cmp3Params p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gr = (int64_t)blockIdx.x * kCmp3Warps + (threadIdx.x >> 5);
+  if (gr >= (int64_t)p.count * p.R) return;
+  const int m = (int)(gr / p.R), r = (int)(gr - (int64_t)m * p.R);
   const EncImage im = p.img[m];
   const int nch = (int)p.nchunks;
-  const int r0 = g * kCmpRuns, r1 = min(p.R, r0 + kCmpRuns);
+  const int c0 = r * kRun3, cnt = min(kRun3, nch - c0);
   const int32_t *rs = p.run_size + (int64_t)m * p.R;
-  const uint32_t *blk = p.ctr + 64 + 64 * p.count + (int64_t)m * p.NB;
-  const int b0 = r0 >> 6, q0 = b0 << 6;
+  const uint32_t *blk = p.blk + (int64_t)m * p.NB;
+  const uint32_t *src = reinterpret_cast<const uint32_t *>(p.scratch + (size_t)gr * kScratchPerWarp);
+  uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
+  // ---- every load at once
+  const int b = r >> 6, q0 = b << 6;
   uint32_t part = 0;
-  for (int i = lane; i < b0; i += 32) part += __ldcg(blk + i);
-  for (int i = q0 + lane; i < r0; i += 32) part += (uint32_t)__ldcg(rs + i);
-  uint32_t base = __reduce_add_sync(EQC_FULL, part);
-  const bool last = r1 == p.R;
-  uint8_t *payload = im.dst + 32 + 8 * p.nchunks;
-  for (int r = r0; r < r1; ++r) {
-    const int64_t gr = (int64_t)m * p.R + r;
-    const int run = __ldcg(rs + r);
-    const int c0 = r * kRun3, cnt = min(kRun3, nch - c0);
-    uint2 *table = reinterpret_cast<uint2 *>(im.dst + 32) + c0;
-    if (lane < cnt) {
-      uint2 e = __ldcg(table + lane);
-      e.x += base;
-      table[lane] = e;
-    }
-    const uint8_t *scr = p.scratch + (size_t)gr * kScratchPerWarp;
-    if (run > 0) {
-      copy_run(payload + base, scr, run, lane);
-      __syncwarp();
-      for (int l = lane; l * 128 < run; l += 32) discard_l2(scr + 128 * l);
-    }
-    base += (uint32_t)run;
+  for (int i = lane; i < b; i += 32) part += __ldcg(blk + i);
+  for (int i = q0 + lane; i < r; i += 32) part += (uint32_t)__ldcg(rs + i);
+  const int run = __ldcg(rs + r);
+  uint2 e = make_uint2(0u, 0u);
+  if (lane < cnt) e = __ldcg(table + lane);
+  constexpr int U = 4;  // words per lane in the first round (512 B per warp: a background run)
+  uint32_t w[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) w[u] = __ldcg(src + 32 * u + lane);
+  const uint32_t base = __reduce_add_sync(EQC_FULL, part);
+  if (lane < cnt) {
+    e.x += base;
+    table[lane] = e;
   }
-  if (last && lane == 0) {
-    const uint32_t total = base;
+  uint8_t *dst = im.dst + 32 + 8 * p.nchunks + base;
+  if (r == p.R - 1 && lane == 0) {
+    const uint32_t total = base + (uint32_t)run;
     uint32_t *h32 = reinterpret_cast<uint32_t *>(im.dst);
     h32[0] = kMagic;
     h32[1] = (uint32_t)kVersion | ((uint32_t)im.kind << 8) | ((uint32_t)im.flags << 16) | ((uint32_t)kLog2C << 24);
@@ -687,6 +712,51 @@ __device__ void e3_compact(const Enc3Params &p, int m, int g, int lane) {
     h32[7] = 0u;
     *im.d_size = 32 + 8 * p.nchunks + (int64_t)total;
   }
+  if (run <= 0) return;
+  // destination word k (k >= 0) = bytes [4k - a, 4k - a + 4) of the run, a =
+  // dst & 3; for a > 0 it is funnel(src word k-1, src word k); its bytes
+  // outside [0, run) belong to the neighbouring runs (byte stores there)
+  const int a = (int)((uintptr_t)dst & 3u);
+  uint32_t *dw = reinterpret_cast<uint32_t *>(dst - a);
+  const int nk = (run + a + 3) >> 2;  // destination words touched
+  auto put = [&](int k, uint32_t lo, uint32_t hi) {
+    // lo = src word k - 1 (unused when a == 0), hi = src word k
+    const uint32_t v = a ? __funnelshift_r(lo, hi, 8 * (4 - a)) : hi;
+    const int b0 = 4 * k - a;  // run byte at the word's first byte
+    if (b0 >= 0 && b0 + 4 <= run) {
+      dw[k] = v;
+    } else {
+      uint8_t *d8 = reinterpret_cast<uint8_t *>(dw + k);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (b0 + q >= 0 && b0 + q < run) d8[q] = (uint8_t)(v >> (8 * q));
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    // src word k - 1 of k = 32u + lane: the previous lane's word u, or (lane 0)
+    // lane 31's word u - 1
+    const uint32_t up = __shfl_up_sync(EQC_FULL, w[u], 1);
+    const uint32_t wrap = __shfl_sync(EQC_FULL, u ? w[u - 1] : 0u, 31);
+    const int k = 32 * u + lane;
+    if (k < nk) put(k, lane ? up : wrap, w[u]);
+  }
+  for (int k0 = 32 * U; k0 < nk; k0 += 4 * 32) {  // longer runs: the rest, 4 words per lane in flight
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 32 * u + lane;
+      lo[u] = k < nk ? __ldcg(src + k - 1) : 0u;
+      hi[u] = k < nk ? __ldcg(src + k) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 32 * u + lane;
+      if (k < nk) put(k, lo[u], hi[u]);
+    }
+  }
+  __syncwarp();
+  for (int l = lane; l * 128 < run; l += 32) discard_l2(reinterpret_cast<const uint8_t *>(src) + 128 * l);
 }
 
 template <bool FULL, bool CONTIG>
@@ -696,36 +766,7 @@ __global__ void __launch_bounds__(kE3Warps * 32, EQC_E3_MINB) rle_encode3_kernel
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 16 + 256; i += blockDim.x) s_lut[i] = reinterpret_cast<const uint32_t *>(&eqc_enc::g_enc_luts)[i];
   __syncthreads();  // the only CTA-wide barrier: warps are independent below
-  uint32_t *const ectr = p.ctr, *const cimg = p.ctr + 32, *const done = p.ctr + 64, *const ccnt = p.ctr + 64 + 32 * p.count;
-  if (kE3CWarps > 0 && warp >= kE3Warps - kE3CWarps) {
-    // ---- compaction warp: move the runs of images whose runs are all coded
-    for (;;) {
-      int job = -1, jm = 0, fin = 0;
-      if (lane == 0) {
-        int m = (int)ld_relaxed_u32(cimg);
-        while (m < p.count && ld_relaxed_u32(done + 32 * m) == (uint32_t)p.R) {
-          const int g = (int)atomicAdd(ccnt + 32 * m, 1u);
-          if (g < p.G) {
-            job = g, jm = m;
-            if (g == p.G - 1) atomicMax(cimg, (uint32_t)(m + 1));
-            break;
-          }
-          atomicMax(cimg, (uint32_t)(m + 1));
-          ++m;
-        }
-        fin = m >= p.count;
-        if (job >= 0) fence_acq_rel_gpu();  // acquire: the image's runs (observed complete)
-      }
-      job = __shfl_sync(EQC_FULL, job, 0);
-      if (job >= 0) {
-        e3_compact(p, __shfl_sync(EQC_FULL, jm, 0), job, lane);
-      } else {
-        if (__shfl_sync(EQC_FULL, fin, 0)) break;
-        __nanosleep(1000);
-      }
-    }
-    return;
-  }
+  uint32_t *const ectr = p.ctr;
   // ---- encode warp
   E3Warp &W = reinterpret_cast<E3Warp *>(smem_raw)[warp];
   const eqc_enc::LaneK K = eqc_enc::lane_consts(lane);
@@ -1461,7 +1502,7 @@ inline size_t enc_ctr_offset(int64_t runs, int count) {
 // fused v1 encoder counters: ticket, done runs per image, size of every block
 // of 64 runs per image
 inline size_t enc_ctr_words(int count, int64_t runs_per_image) {
-  return 64 + 64 * (size_t)count + (size_t)count * (size_t)((runs_per_image + 63) / 64);
+  return 32 * (size_t)count + (size_t)count * (size_t)((runs_per_image + 63) / 64);  // <= count group tickets
 }
 inline size_t enc_scratch_offset(int64_t runs, int count) {
   return (enc_ctr_offset(runs, count) + 4 * enc_ctr_words(count, runs / count) + 255) & ~(size_t)255;
@@ -1537,27 +1578,14 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (!r64) {
-    // v1: one fused launch (encode + compaction), after zeroing its counters
-    Enc3Params e;
-    for (int i = 0; i < count; ++i) e.img[i] = p.img[i];
-    e.run_size = p.run_size;
-    e.scratch = p.scratch;
-    e.ctr = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(workspace) + enc_ctr_offset(runs, count));
-    e.pitch = pitch;
-    e.nchunks = p.nchunks;
-    e.count = count;
-    e.w = w;
-    e.h = h;
-    e.S = p.S;
-    e.R = p.runs_per_image;
-    e.G = (e.R + kCmpRuns - 1) / kCmpRuns;
-    e.NB = (e.R + 63) / 64;
-    e.total_enc = count * e.R;
-    e.vec = vec ? 1 : 0;
+    // v1: the batch in groups of images whose raw size stays below
+    // EQC_E3_GROUP_MB (so a group's record scratch is still L2-resident when
+    // its compaction runs): per group an encoder launch and a compaction
+    // launch, after one zeroing of all groups' counters
     const bool full = (w % kC) == 0;
     const bool contig = full && vec && pitch == w;
     static bool configured3 = false;
-    const size_t smem3 = sizeof(E3Warp) * (kE3Warps - kE3CWarps);
+    const size_t smem3 = sizeof(E3Warp) * kE3Warps;
     if (!configured3) {
       if (cudaFuncSetAttribute(rle_encode3_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem3) != cudaSuccess ||
@@ -1568,19 +1596,53 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
         return EQC_E_CUDA;
       configured3 = true;
     }
-    EQC_CUDA_TRY(cudaMemsetAsync(e.ctr, 0, 4 * enc_ctr_words(count, e.R), st));
-    const int64_t item_ctas = ((int64_t)e.total_enc + kE3Warps - kE3CWarps - 1) / (kE3Warps - kE3CWarps);
-    auto launch = [&](auto kern) {
-      const int res = eqc_resident_ctas(kern, kE3Warps * 32, smem3);
-      kern<<<(unsigned)std::min<int64_t>(res, item_ctas), kE3Warps * 32, smem3, st>>>(e);
-    };
-    if (contig) launch(rle_encode3_kernel<true, true>);
-    else if (full) launch(rle_encode3_kernel<true, false>);
-    else launch(rle_encode3_kernel<false, false>);
-    if (kE3CWarps > 0) return eqc_launch_status();
-  } else {
-    rle_encode_kernel<true><<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
+    const int R = p.runs_per_image, NB = (R + 63) / 64;
+    uint32_t *ctr = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(workspace) + enc_ctr_offset(runs, count));
+    EQC_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * enc_ctr_words(count, R), st));
+    const int64_t img_bytes = 4 * (int64_t)w * h;
+    const int per = (int)std::max<int64_t>(1, std::min<int64_t>(count, ((int64_t)EQC_E3_GROUP_MB << 20) / img_bytes));
+    for (int g0 = 0; g0 < count; g0 += per) {
+      const int gc = std::min(per, count - g0);
+      Enc3Params e;
+      for (int i = 0; i < gc; ++i) e.img[i] = p.img[g0 + i];
+      e.run_size = p.run_size + (int64_t)g0 * R;
+      e.scratch = p.scratch + (size_t)g0 * R * kScratchPerWarp;
+      e.ctr = ctr + 32 * (g0 / per);  // the group's ticket (its own 128-byte line)
+      e.blk = ctr + 32 * ((count + per - 1) / per) + (int64_t)g0 * NB;
+      e.pitch = pitch;
+      e.nchunks = p.nchunks;
+      e.count = gc;
+      e.w = w;
+      e.h = h;
+      e.S = p.S;
+      e.R = R;
+      e.NB = NB;
+      e.total_enc = gc * R;
+      e.vec = vec ? 1 : 0;
+      const int64_t item_ctas = ((int64_t)e.total_enc + kE3Warps - 1) / kE3Warps;
+      auto launch = [&](auto kern) {
+        const int res = eqc_resident_ctas(kern, kE3Warps * 32, smem3);
+        kern<<<(unsigned)std::min<int64_t>(res, item_ctas), kE3Warps * 32, smem3, st>>>(e);
+      };
+      if (contig) launch(rle_encode3_kernel<true, true>);
+      else if (full) launch(rle_encode3_kernel<true, false>);
+      else launch(rle_encode3_kernel<false, false>);
+      Cmp3Params c;
+      for (int i = 0; i < gc; ++i) c.img[i] = e.img[i];
+      c.run_size = e.run_size;
+      c.blk = e.blk;
+      c.scratch = e.scratch;
+      c.nchunks = e.nchunks;
+      c.count = gc;
+      c.w = w;
+      c.h = h;
+      c.R = R;
+      c.NB = NB;
+      rle_compact3_kernel<<<(unsigned)(((int64_t)gc * R + kCmp3Warps - 1) / kCmp3Warps), kCmp3Warps * 32, 0, st>>>(c);
+    }
+    return eqc_launch_status();
   }
+  rle_encode_kernel<true><<<(unsigned)tiles, kEncWarps * 32, smem, st>>>(p);
   CompactParams c;
   for (int i = 0; i < count; ++i) c.img[i] = p.img[i];
   rle_runscan_kernel<<<count, 1024, 0, st>>>(p.run_size, run_off, p.runs_per_image);
