@@ -44,6 +44,12 @@ _OUT = sys.stdout
 
 
 EVENT_EVERY = 8  # timed steps per step carrying per-kernel events
+KREP = 10        # back-to-back calls per per-call timing
+# compression-ratio anchors of SURVEY 8(d) (r ~ 0.3, ~ 0.5): footprint F, fixed
+# full per-source coverage, noise bits per channel
+ANCHORS = [("r0.3", {"F": 0.9, "cover": 1.0, "noise_bits": 5}),
+           ("r0.5", {"F": 1.0, "cover": 1.0, "noise_bits": 5})]
+NVLINK_SPEC_GBS = 900.0  # NVLink 5 per direction (spec)
 
 
 def log(*a):
@@ -145,6 +151,66 @@ def make_inputs(seed, n, w, h):
     import synth
     c, d = synth.depth_sources(seed, n, w, h)
     return c, d
+
+
+def synth_sources(seed, n, w, h, **kw):
+    import synth
+    return synth.depth_sources(seed, n, w, h, **kw)
+
+
+def compose_block(eqc, comm, rank, world, dev, stream, reps=10):
+    """SURVEY 8(e) scaling rows on config c4: 8 sources of 7680x4320 (seed
+    20190213 + 3), rank g holding sources [g*8/n, (g+1)*8/n); every schedule
+    timed over `reps` back-to-back calls (max over ranks) against the roof
+    T_pre + T_x: T_pre = the rank's local pre-composite at HBM peak,
+    (8 * n_local + 8) * P bytes; T_x = the destination's inbound bytes
+    (n-1)/n * 12 * P (colour+depth bands + colour gather) at the NVLink line."""
+    import torch
+    import torch.distributed as dist
+    import synth
+    W8, H8, N8 = 7680, 4320, 8
+    if N8 % world:
+        return None
+    nl = N8 // world
+    c, d = synth.depth_sources(synth.SEED_BASE + 3, N8, W8, H8)
+    mine = range(rank * nl, (rank + 1) * nl)
+    dc = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine]
+    dd = [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
+    del c, d
+    final = torch.empty((H8, W8), dtype=torch.int32, device=dev) if rank == 0 else None
+    P8 = W8 * H8
+    variants = [("direct_send_p2p", eqc.compose_direct_send, 0), ("direct_send_nccl", eqc.compose_direct_send,
+                                                                   eqc.FLAG_NCCL)]
+    if world & (world - 1) == 0:
+        variants.append(("binary_swap", eqc.compose_binary_swap, 0))
+    else:
+        variants.append(("swap23", eqc.compose_swap23, 0))
+    peak = measured_peaks()[0]
+    t_pre = (8 * nl + 8) * P8 / (peak * 1e9) * 1e6
+    inbound = (world - 1) / world * 12 * P8
+    t_x = inbound / (NVLINK_SPEC_GBS * 1e9) * 1e6
+    out = {"config": f"c4: {N8} sources {W8}x{H8}, {nl} per GPU, {world} GPUs (strong scaling: fixed frame)",
+           "roof_us": round(t_pre + t_x, 1), "roof_terms_us": {"T_pre_hbm": round(t_pre, 1), "T_x_nvlink": round(t_x, 1)},
+           "nvlink_gbs_per_dir": NVLINK_SPEC_GBS, "dest_inbound_bytes": int(inbound), "schedules": {}}
+    for name, fn, fl in variants:
+        for _ in range(3):
+            fn(comm, dc, dd, final, dest_rank=0, flags=fl, stream=stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn(comm, dc, dd, final, dest_rank=0, flags=fl, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / reps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        out["schedules"][name] = {"ms": round(ms, 4), "source_mpx_per_s": round(N8 * P8 / (ms * 1e-3) / 1e6, 1),
+                                  "frac_of_roof": round((t_pre + t_x) / (ms * 1e3), 3)}
+    del dc, dd, final
+    torch.cuda.synchronize()
+    return out
 
 
 def launches_per_compose(n, exchange, slots=False):
@@ -365,6 +431,72 @@ def run_eqc(args):
     h2d = sum(x.numel() * 4 for x in host_in)
     d2h = host_out.numel() * 4 if (world == 1 or rank == 0) else 0
 
+    # ---- per-call GPU time of each C-ABI entry: KREP back-to-back calls on the
+    # launching stream between one event pair (an event between two calls
+    # costs a few microseconds of drain, which per-call events would charge
+    # to every call)
+    def per_call_ms(fn, reps=KREP):
+        for _ in range(2):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    oc0, od0 = outs[0]
+    enc_call_ms = per_call_ms(lambda: eqc.image_compress_rle_batch(imgs, kinds, flags, streams, sizes, ws,
+                                                                   stream=stream))
+    dec_call_ms = per_call_ms(lambda: eqc.compositor_depth_rle(streams[:NSRC], streams[NSRC:], oc0, od0, status,
+                                                               stream=stream))
+    assert int(status.item()) == 0, "decode reported a corrupt stream"
+    if world > 1:
+        t = torch.tensor([enc_call_ms, dec_call_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        enc_call_ms, dec_call_ms = (float(x) for x in t.tolist())
+
+    # ---- the step at the survey's compression anchors (r = 0.3,
+    # 0.5): denser, noisier synthetic frames, same
+    # shapes; N = 1 only
+    anchors = None
+    if world == 1 and not args.no_anchors:
+        anchors = {}
+        for name, kw in ANCHORS:
+            ca, da = synth_sources(SEED, NSRC, W, H, **kw)
+            aimgs = [torch.from_numpy(x.view(np.int32)).to(dev) for x in list(ca) + list(da)]
+            del ca, da
+            fe = lambda: eqc.image_compress_rle_batch(aimgs, kinds, flags, streams, sizes, ws, stream=stream)
+            fd = lambda: eqc.compositor_depth_rle(streams[:NSRC], streams[NSRC:], oc0, od0, status, stream=stream)
+
+            def fstep():
+                fe()
+                fd()
+            e_ms, d_ms, s_ms = per_call_ms(fe), per_call_ms(fd), per_call_ms(fstep)
+            assert int(status.item()) == 0, "decode reported a corrupt stream"
+            sb = int(sizes.sum().item())
+            ra = sb / (len(aimgs) * 4 * P)
+            eb, db = len(aimgs) * 4 * P + sb, sb + 8 * P
+            ns = NSRC * P * (24 + 16 * ra) + 8 * P
+            anchors[name] = {
+                "synth": kw, "compression_ratio_r": round(ra, 4), "ms_per_step": round(s_ms, 4),
+                "source_mpx_per_s": round(NSRC * P / (s_ms * 1e-3) / 1e6, 1),
+                "image_compress_rle_batch": {"ms": round(e_ms, 4), "alg_bytes": eb,
+                                             "frac": round(eb / (e_ms * 1e-3) / 1e9 / measured_peaks()[0], 3)},
+                "compositor_depth_rle": {"ms": round(d_ms, 4), "alg_bytes": db,
+                                         "frac": round(db / (d_ms * 1e-3) / 1e9 / measured_peaks()[0], 3)},
+                "north_star_frac_of_peak": round(ns / (s_ms * 1e-3) / 1e9 / measured_peaks()[0], 3)}
+            del aimgs
+        torch.cuda.synchronize()
+
+    # ---- N > 1: the survey's scaling rows: config c4, 8 sources
+    # of 7680x4320 split over the N ranks, direct send (peer-memory pull) and
+    # binary swap, each against an NVLink-plus-HBM roof
+    compose = None
+    if world > 1 and not args.no_compose_block:
+        compose = compose_block(eqc, comm, rank, world, dev, stream)
+
     if rank != 0:
         if comm is not None:
             comm.destroy()
@@ -377,8 +509,8 @@ def run_eqc(args):
     enc_bytes = len(imgs) * 4 * P + stream_bytes          # read raw, write streams
     dec_bytes = stream_bytes + 8 * P                      # read streams, write colour + depth
     kern = {
-        "image_compress_rle_batch": {"ms": enc_ms, "bytes": enc_bytes},
-        "compositor_depth_rle": {"ms": dec_ms, "bytes": dec_bytes},
+        "image_compress_rle_batch": {"ms": enc_call_ms, "bytes": enc_bytes, "inloop_ms": enc_ms},
+        "compositor_depth_rle": {"ms": dec_call_ms, "bytes": dec_bytes, "inloop_ms": dec_ms},
     }
     for k in kern.values():
         k["gbs"] = k["bytes"] / (k["ms"] * 1e-3) / 1e9
@@ -413,7 +545,9 @@ def run_eqc(args):
                         "colour swizzled) -> fused RLE decode + depth composite",
             "sources_per_gpu": NSRC, "width": W, "height": H,
             "compression_ratio_r": round(r, 4),
-            "kernel_timing": f"CUDA events around the calls of every {EVENT_EVERY}th timed step (launching streams)",
+            "kernel_timing": f"per C-ABI call: {KREP} back-to-back calls between one CUDA event pair on the "
+                             f"launching stream, right after the timed region (inloop_ms: events around the "
+                             f"calls of every {EVENT_EVERY}th timed step, each charged a few us of event drain)",
             "l2": f"inputs larger than L2 ({len(imgs) * 4 * P / 1e6:.0f} MB of source frames per step > 126 MB L2)",
             "parallelism": (f"screen-partition direct send ({args.exchange}) over {world} GPU(s)" +
                             (", compose of frame k overlapped with frame k+1 (async compositing pipeline, "
@@ -436,16 +570,19 @@ def run_eqc(args):
             "frac_of_peak": round((NSRC * P * (24 + 16 * r) + 8 * P) / (ms * 1e-3) / 1e9 / peak, 3),
             "target_frac": 0.60,
             "definition": "SURVEY.md 8(d): B = N*P*(24 + 16r) + 8P, r = compressed/raw"},
-        "kernels": {k: {"ms": round(v["ms"], 4), "alg_bytes": v["bytes"], "gbs": round(v["gbs"], 1),
-                        "frac": round(v["frac"], 3)} for k, v in kern.items()},
+        "kernels": {k: {"ms": round(v["ms"], 4), "inloop_ms": round(v["inloop_ms"], 4), "alg_bytes": v["bytes"],
+                        "gbs": round(v["gbs"], 1), "frac": round(v["frac"], 3)} for k, v in kern.items()},
+        "compression_anchors": anchors,
+        "compose_scaling": compose,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(kern[dom]["gbs"], 1), "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": round(kern[dom]["frac"], 3),
                      "traffic": traffic},
         "cpu_baseline": cpu,
         "e2e": {"value": round(world * NSRC * P / (e2e_ms * 1e-3) / 1e6, 1), "unit": UNIT,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        # per step: encode batch (encode, run scan, compaction kernels) + fused decode/composite
-        "gpu_launches": (4 + (launches_per_compose(world, args.exchange, slots) if world > 1 else 0)) * args.steps,
+        # per step: encode batch (encoder + compaction kernels; its counter reset is a runtime memset)
+        # + fused decode/composite
+        "gpu_launches": (3 + (launches_per_compose(world, args.exchange, slots) if world > 1 else 0)) * args.steps,
         "clocks": clocks,
     }
     emit(line)
@@ -477,15 +614,34 @@ def calibrate_rows(c_np, d_np, seconds):
     return int(max(1, min(H, seconds / max(per_row, 1e-6))))
 
 
+def host_cpu():
+    """nproc and the CPU model of this host (lscpu)."""
+    model = None
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
 def cpu_baseline(args, rows=None):
     c_np, d_np = make_inputs(SEED, NSRC, W, H)
-    rows = rows or args.cpu_rows or calibrate_rows(c_np, d_np, 15.0)
-    t = time.perf_counter()
-    oracle_sample_step(c_np, d_np, rows)
-    dt = time.perf_counter() - t
+    rows = rows or args.cpu_rows or calibrate_rows(c_np, d_np, 5.0)
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        oracle_sample_step(c_np, d_np, rows)
+        ts.append(time.perf_counter() - t)
+    dt = statistics.median(ts)
     return {"value": round(NSRC * W * rows / dt / 1e6, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "host": host_cpu(), "median_s": round(dt, 3), "min_s": round(min(ts), 3),
+            "value_at_min": round(NSRC * W * rows / min(ts) / 1e6, 3),
             "sample": f"{rows} of {H} rows of the target step (8 sources x 3840 wide: encode 16 streams, "
-                      f"decode, composite), single-threaded C oracle, {dt:.1f} s"}
+                      f"decode, composite), single-threaded C oracle, median of 3 runs"}
 
 
 def run_reference(args):
@@ -512,7 +668,7 @@ def run_reference(args):
             "config": {"workload": "target: 8 sources x 3840x2160 RGBA8+depth32 (row sample), RLE encode -> "
                                    "decode -> depth composite", "rows_per_step": rows},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "host": host_cpu(), "sample": sample},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -532,6 +688,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="rows of the frame in one CPU-oracle sample (0 = calibrate to a time budget)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-anchors", action="store_true", help="N=1: skip the r = 0.3 / 0.5 anchor steps")
+    ap.add_argument("--no-compose-block", action="store_true", help="N>1: skip the c4 schedule rows")
     ap.add_argument("--no-frame-slots", action="store_true",
                     help="N>1: decode into own buffers, not the comm's peer-mapped frame slots (zero-copy direct send)")
     ap.add_argument("--no-comm-priority", action="store_true",

@@ -52,7 +52,10 @@ def _ellipse_mask(h, w, cx, cy, rx, ry):
 
 
 def footprint(seed: int, w: int, h: int, F: float = 0.5) -> np.ndarray:
-    """Union of 6 random ellipses covering roughly F of the screen."""
+    """Union of 6 random ellipses covering roughly F of the screen (F >= 1:
+    the whole screen)."""
+    if F >= 1.0:
+        return np.ones((h, w), bool)
     rng = np.random.default_rng([seed, 0xF00])
     fp = np.zeros((h, w), bool)
     area = F * w * h / 6.0 * 1.35  # overlap compensation
@@ -85,7 +88,7 @@ def kd_cells(n: int, x0: int, y0: int, x1: int, y1: int):
 
 def depth_sources(seed: int, n: int, w: int, h: int, F: float = 0.5,
                   noise_bits: int = 1, ties: bool = False, pitch: int | None = None,
-                  mode: str = "scattered"):
+                  mode: str = "scattered", cover: float | None = None):
     """N sort-last source frames: (colors, depths), each a list of [H, W] uint32.
 
     ``mode="scattered"`` (default): every source's fragments fall anywhere in
@@ -93,6 +96,11 @@ def depth_sources(seed: int, n: int, w: int, h: int, F: float = 0.5,
     source i's fragment centres fall in the i-th kD cell of the footprint's
     bounding box (spatially compact allocation),
     so each source covers a small screen region -- the case the ROI targets.
+
+    ``cover`` (default: drawn per source from U[1/sqrt(N), 1]) fixes every
+    source's fragment area as a fraction of the footprint; with ``F`` >= 1,
+    ``cover`` = 1 and more ``noise_bits`` the frames compress less (the
+    compression-ratio anchors of DESIGN.md section 6).
 
     If ``pitch`` > W the arrays are [H, pitch] buffers and the returned frames
     are [H, W] views into them (row pitch = ``pitch`` words); the padding holds
@@ -125,8 +133,10 @@ def depth_sources(seed: int, n: int, w: int, h: int, F: float = 0.5,
         dep = dbuf[:, :w]
         col[:] = 0
         dep[:] = BG_DEPTH
-        cover = float(rng.uniform(1.0 / math.sqrt(max(n, 1)), 1.0))
-        frag_area = cover * src_area / 32.0 * 1.2
+        cov = float(rng.uniform(1.0 / math.sqrt(max(n, 1)), 1.0))
+        if cover is not None:
+            cov = float(cover)
+        frag_area = cov * src_area / 32.0 * 1.2
         for _f in range(32):
             c = int(src_idx[int(rng.integers(0, src_idx.size))])
             cy, cx = c // w + 0.5, c % w + 0.5
