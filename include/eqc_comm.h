@@ -79,7 +79,8 @@ EQC_API int eqc_comm_stats(const eqc_comm *comm, int64_t out[4]);
  *               (pitch w).  Pass them (n_local = 1, pitch = w, EQC_OP_DEPTH,
  *               no ROI) to compose_direct_send and it skips the local copy;
  *               EVERY rank must then pass its own slot-`slot` buffers (like
- *               the matching calls of a collective).
+ *               the matching calls of a collective; a mismatch is detected
+ *               and reported by eqc_comm_check).
  *   *final_color  receives the comm's gather buffer [h][w]: passed as
  *               out_color (out_pitch = w) on dest_rank, the peers' bands land
  *               in it directly and the final band copy is skipped.
@@ -175,7 +176,10 @@ EQC_API int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_ro
  * directly into the destination's frame (two peer-memory flag barriers order
  * the steps; no staging, no NCCL on the data path).  Otherwise, or with
  * EQC_FLAG_NCCL, the bands move with NCCL grouped send/recv.  With
- * EQC_FLAG_RLE the call synchronises `stream` once (message sizes).
+ * EQC_FLAG_RLE the call synchronises `stream` once (the message sizes are
+ * read back to the host), so it returns only after the encodes finished and
+ * cannot be captured in a CUDA graph; the same holds for the EQC_FLAG_RLE
+ * variants of compose_binary_swap, compose_swap23 and compose_stream.
  * EQC_FLAG_ROI (peer-memory path; other transports ignore it): the local
  * pre-composite also reduces the bounding box of its rendered pixels (the
  * ROI computed "by analysing the framebuffer", fused: no extra
@@ -283,6 +287,64 @@ EQC_API int compose_direct_send_roi_local(int nranks, int n_local, const uint32_
                                           const uint32_t *const *depth, const int32_t *d_src_roi, int w, int h,
                                           int64_t pitch, int flags, int dest_rank, uint32_t *out_color,
                                           int64_t out_pitch, int64_t *out_stats, void *stream);
+
+/*
+ * Peer-memory transport on ONE GPU: compose_direct_send's NVLink peer-memory
+ * path (P:2302-2310 stages (2)-(5) with no staging copy) run
+ * for nranks virtual ranks of this process.  Every virtual rank gets its own
+ * partial frame, gather buffer and flags page; the "peer mappings" are the
+ * other virtual ranks' plain device pointers, and each virtual rank's part of
+ * the call runs on its own stream (its flag barriers must run concurrently
+ * with the others'), forked from and joined back to `stream`.  The host code
+ * and kernels are those of the multi-process path.  The call synchronises
+ * `stream` (its scratch is freed before it returns).
+ *   mode  EQC_P2P_PLAIN      one pre-composite, barrier, pull + band
+ *                            composite, barrier, band copy-out;
+ *         EQC_P2P_PIPELINED  bands cut into pieces, pre-composite of piece
+ *                            k+1 overlapped with the pull of piece k (progress
+ *                            counters in peer memory; no EQC_FLAG_ROI);
+ *         EQC_P2P_SLOTS      the partial frames are frame slots read in place
+ *                            (n_local = 1, EQC_OP_DEPTH, no ROI; the caller's
+ *                            frames are copied into the slots first).
+ *   color/depth: nranks * n_local device pointers (rank-major), as
+ *   compose_direct_send_local.  Result bit-identical to compositor_depth (or
+ *   the op's single-GPU result) over all sources.
+ * Errors: as compose_direct_send; EQC_E_NCCL if a flag wait timed out
+ * (EQC_P2P_TIMEOUT_MS); EQC_E_INVALID if the ranks disagreed on frame slots.
+ */
+#define EQC_P2P_PLAIN 0
+#define EQC_P2P_PIPELINED 1
+#define EQC_P2P_SLOTS 2
+EQC_API int compose_direct_send_p2p_local(int nranks, int n_local, const uint32_t *const *color,
+                                          const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
+                                          int flags, int mode, int dest_rank, uint32_t *out_color,
+                                          int64_t out_pitch, int64_t *out_stats, void *stream);
+
+/*
+ * compose_direct_send_rle_pull on ONE GPU (virtual ranks as above): rank q's
+ * 2 * n_local streams (colour 0..n_local-1, then depth) lie contiguously at
+ * rank_streams[q], cap_bytes apart; the fused decode + composite of band j
+ * (rows [floor(jh/n), floor((j+1)h/n)), R-C13) reads every rank's records in
+ * place.  d_status as compositor_depth_rle.  Synchronises `stream`.
+ */
+EQC_API int compose_direct_send_rle_pull_local(int nranks, int n_local, const uint8_t *const *rank_streams,
+                                               int64_t cap_bytes, int w, int h, int dest_rank,
+                                               uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
+                                               int64_t *out_stats, void *stream);
+
+/*
+ * eqc_comm_check -- synchronise `stream`, then report the comm's health:
+ * EQC_E_NCCL if NCCL reports an asynchronous error (ncclCommGetAsyncError)
+ * or a peer-memory flag wait gave up (a dead or stalled peer: every wait
+ * spins at most EQC_P2P_TIMEOUT_MS, default 60000, read at comm creation, so
+ * the GPU never hangs on it); EQC_E_INVALID if the ranks passed different
+ * frame slots to a compose call (see eqc_comm_frame_buffers); else EQC_OK.
+ * After an error the results of the compose calls since the last check are
+ * undefined.  eqc_comm_abort -- ncclCommAbort (unblocks NCCL operations of a
+ * failed job); the comm may then only be destroyed.
+ */
+EQC_API int eqc_comm_check(eqc_comm *comm, void *stream);
+EQC_API int eqc_comm_abort(eqc_comm *comm);
 
 #ifdef __cplusplus
 }

@@ -35,6 +35,9 @@ int eqc_depth_roi_launch(int n, const uint32_t *const *color, const uint32_t *co
 // composite.cu: compositor_depth that also reduces the ROI of its output
 size_t eqc_depth_bbox_scratch_bytes();
 extern thread_local int eqc_grid_cap;
+int eqc_preload_composite();
+int eqc_preload_rle();
+int eqc_preload_roi();
 int eqc_depth_rle_band(int n, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
                        const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h, int y0, int y1,
                        uint32_t *out_color, uint32_t *out_depth, int64_t out_pitch, int32_t *d_status,
@@ -61,10 +64,14 @@ namespace {
     if (_r != ncclSuccess) return EQC_E_NCCL; \
   } while (0)
 
-#define EQC_TRY(expr)           \
-  do {                          \
-    int _rc = (expr);           \
-    if (_rc != EQC_OK) return _rc; \
+// EQC_TRACE_ERRORS=1: print where an error code first surfaced (debug aid)
+#define EQC_TRY(expr)                                                                   \
+  do {                                                                                  \
+    int _rc = (expr);                                                                   \
+    if (_rc != EQC_OK) {                                                                \
+      if (getenv("EQC_TRACE_ERRORS")) fprintf(stderr, "eqc: %d at %s:%d\n", _rc, __FILE__, __LINE__); \
+      return _rc;                                                                       \
+    }                                                                                   \
   } while (0)
 
 struct DevBuf {
@@ -1100,36 +1107,69 @@ int validate(int nranks, int n_local, const void *color, const void *depth, int 
 // bands complete before the destination copies them out.
 namespace {
 
+// The IPC-exposed `flags` allocation holds the barrier flags (EQC_MAX_SOURCES
+// ints), the rank's partial-frame ROI {x, y, w, h} (kRoiSlot), the progress
+// counter of its pipelined pre-composite (kProgSlot), a local error word
+// (kErrSlot: bit 0 a flag wait timed out, bit 1 the ranks passed different
+// frame slots) and the frame slot this rank's call passed (kSlotSlot).
+constexpr int kRoiSlot = EQC_MAX_SOURCES;  // int offset, 16-byte aligned
+constexpr int kProgSlot = kRoiSlot + 4;
+constexpr int kErrSlot = kProgSlot + 4;
+constexpr int kSlotSlot = kErrSlot + 1;
+constexpr int kFlagInts = kErrSlot + 4;
+constexpr int kErrTimeout = 1, kErrSlotMismatch = 2;
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *f - target >= 0 (acquire, system scope) or the deadline passes
+// (then the timeout bit goes into *err): a dead or stalled peer cannot hang
+// the GPU; eqc_comm_check reports it.
+__device__ __forceinline__ void wait_flag(const int *f, int target, int64_t timeout_ns, int *err, int sleep_ns) {
+  const uint64_t t0 = global_ns();
+  int v;
+  while (true) {
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v - target >= 0) break;
+    if ((int64_t)(global_ns() - t0) > timeout_ns) {
+      atomicOr(err, kErrTimeout);
+      break;
+    }
+    __nanosleep(sleep_ns);
+  }
+}
+
 struct BarrierArgs {
   int *peer_flags[EQC_MAX_SOURCES];  // flags array of every rank (own = local)
   int *my_flags;
   int n, rank, epoch;
+  int check_slot, slot;  // publish this call's frame slot and check every rank passed the same one
+  int64_t timeout_ns;
 };
 
 __global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
   const int i = threadIdx.x;
+  if (a.check_slot && i == 0) a.my_flags[kSlotSlot] = a.slot;
+  __syncthreads();
   __threadfence_system();
   if (i < a.n) {
     int *f = a.peer_flags[i] + a.rank;
     asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(a.epoch) : "memory");
   }
   if (i < a.n) {
-    const int *f = a.my_flags + i;
-    int v;
-    while (true) {
-      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      if (v - a.epoch >= 0) break;
-      __nanosleep(64);
+    wait_flag(a.my_flags + i, a.epoch, a.timeout_ns, a.my_flags + kErrSlot, 64);
+    if (a.check_slot && !(*(volatile int *)(a.my_flags + kErrSlot) & kErrTimeout)) {
+      int v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(a.peer_flags[i] + kSlotSlot) : "memory");
+      if (v != a.slot) atomicOr(a.my_flags + kErrSlot, kErrSlotMismatch);
     }
   }
   __syncthreads();
 }
 
-// The IPC-exposed `flags` allocation holds the barrier flags (EQC_MAX_SOURCES
-// ints) followed by the rank's partial-frame ROI {x, y, w, h} (kRoiSlot).
-constexpr int kRoiSlot = EQC_MAX_SOURCES;  // int offset, 16-byte aligned
-constexpr int kProgSlot = kRoiSlot + 4;    // progress counter of the rank's pipelined pre-composite
-constexpr int kFlagInts = kProgSlot + 4;
 #ifndef EQC_P2P_PIECES
 #define EQC_P2P_PIECES 2  // pieces per band of the pipelined peer-memory direct send
 #endif
@@ -1149,22 +1189,16 @@ __global__ void p2p_signal_kernel(int *my_flags, int value) {
 
 struct WaitArgs {
   const int *peer_flags[EQC_MAX_SOURCES];
+  int *err;
   int n, target;
+  int64_t timeout_ns;
 };
 
 // ... and a puller waits until every rank's counter reached the piece
 // (acquire, system scope, polling peer memory over NVLink).
 __global__ void p2p_wait_kernel(const __grid_constant__ WaitArgs a) {
   const int i = threadIdx.x;
-  if (i < a.n) {
-    const int *f = a.peer_flags[i] + kProgSlot;
-    int v;
-    while (true) {
-      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      if (v - a.target >= 0) break;
-      __nanosleep(32);
-    }
-  }
+  if (i < a.n) wait_flag(a.peer_flags[i] + kProgSlot, a.target, a.timeout_ns, a.err, 32);
   __syncthreads();
 }
 
@@ -1189,8 +1223,16 @@ __global__ void roi_union_kernel(const int32_t *in, int n, int32_t *out) {
                                                               (int)min(y1 - y0, (int64_t)INT32_MAX));
 }
 
+inline int64_t p2p_timeout_ns() {
+  const char *e = getenv("EQC_P2P_TIMEOUT_MS");
+  const long long ms = e ? atoll(e) : 60000;
+  return (int64_t)(ms > 0 ? ms : 60000) * 1000000;
+}
+
 struct P2PState {
   int capable = -1;  // -1 unknown, 0 no (NCCL transport), 1 yes
+  int64_t timeout_ns = p2p_timeout_ns();  // flag waits give up after this (EQC_P2P_TIMEOUT_MS, default 60 s)
+  bool skip_barriers = false;  // test hook of the virtual-rank executor: this rank never arrives
   int64_t cap_px = 0;
   int prog = 0;                    // this rank's published progress counter
   cudaStream_t aux = nullptr;      // pulling stream of the pipelined direct send
@@ -1312,11 +1354,14 @@ int ipc_exchange(eqc_comm *c, void *const *ptrs, int k, std::vector<std::vector<
   return EQC_OK;
 }
 
+int eqc_preload_kernels();
+
 // (Re)build the IPC mappings for frames of `px` pixels.  Collective.
 int p2p_setup(eqc_comm *c, int64_t px, cudaStream_t s) {
   P2PState &P = c->p2p;
   if (P.capable == 0) return EQC_OK;
   if (P.capable == 1 && px <= P.cap_px) return EQC_OK;
+  EQC_TRY(eqc_preload_kernels());  // no lazy kernel load while a flag barrier spins
   cudaStreamSynchronize(s);
   P.close_peers(c->rank);
   const size_t bytes = (size_t)px * 4;
@@ -1381,7 +1426,7 @@ int p2p_slots(eqc_comm *c, int64_t px, cudaStream_t s) {
   return EQC_OK;
 }
 
-int p2p_barrier(eqc_comm *c, cudaStream_t s) {
+int p2p_barrier(eqc_comm *c, cudaStream_t s, int check_slot = 0, int slot = -1) {
   P2PState &P = c->p2p;
   BarrierArgs a;
   for (int q = 0; q < c->nranks; ++q) a.peer_flags[q] = P.peer_flags[q];
@@ -1389,6 +1434,10 @@ int p2p_barrier(eqc_comm *c, cudaStream_t s) {
   a.n = c->nranks;
   a.rank = c->rank;
   a.epoch = ++P.epoch;
+  a.check_slot = check_slot;
+  a.slot = slot;
+  a.timeout_ns = P.timeout_ns;
+  if (P.skip_barriers) return EQC_OK;
   p2p_barrier_kernel<<<1, 64, 0, s>>>(a);
   return eqc_launch_status();
 }
@@ -1478,8 +1527,10 @@ int direct_send_p2p_pipelined(eqc_comm *c, const Geometry &g, const uint32_t *co
     // (2)-(4) on the pulling stream: wait for piece k everywhere, pull + composite it
     WaitArgs wa;
     for (int q = 0; q < n; ++q) wa.peer_flags[q] = P.peer_flags[q];
+    wa.err = P.flags.as<int>() + kErrSlot;
     wa.n = n;
     wa.target = base + k + 1;
+    wa.timeout_ns = P.timeout_ns;
     p2p_wait_kernel<<<1, 64, 0, P.aux>>>(wa);
     EQC_TRY(eqc_launch_status());
     mark(P.aux);
@@ -1588,7 +1639,11 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   }  // else: the caller's partial frame already is slot `slot` (peer-mapped)
   const std::vector<uint32_t *> &src_c = slot < 0 ? P.peer_part_c : P.peer_slot_c[slot];
   const std::vector<uint32_t *> &src_d = slot < 0 ? P.peer_part_d : P.peer_slot_d[slot];
-  EQC_TRY(p2p_barrier(c, s));
+  // every rank publishes the slot it passed (-1: none) and checks the peers
+  // agree (a rank passing its own buffers while another passes a slot would
+  // read a partial that was never written): a mismatch sets the comm's error
+  // word (eqc_comm_check)
+  EQC_TRY(p2p_barrier(c, s, 1, slot));
   // (2)+(3)+(4) band composite pulling every peer's band over NVLink, output
   // pushed into the destination's frame
   const int y0 = row0[me], rows = row0[me + 1] - row0[me];
@@ -1741,20 +1796,12 @@ extern "C" int eqc_comm_stream_buffers(eqc_comm *comm, int n_streams, int64_t ca
   return EQC_OK;
 }
 
-extern "C" int compose_direct_send_rle_pull(eqc_comm *comm, int n_local, int w, int h, int slot, int dest_rank,
-                                            uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
-                                            void *stream) {
-  if (!comm || n_local < 1 || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || dest_rank < 0 ||
-      dest_rank >= comm->nranks || !d_status)
-    return EQC_E_INVALID;
+namespace {
+// The body of compose_direct_send_rle_pull (peer mappings in place).
+int rle_pull_body(eqc_comm *comm, int n_local, int w, int h, int slot, int dest_rank, uint32_t *out_color,
+                  int64_t out_pitch, int32_t *d_status, cudaStream_t s) {
   const int n = comm->nranks, me = comm->rank;
-  if ((int64_t)n * n_local > EQC_MAX_SOURCES) return EQC_E_INVALID;
-  if (me == dest_rank && (!out_color || out_pitch < w)) return EQC_E_INVALID;
   P2PState &P = comm->p2p;
-  if (P.sn != 2 * n_local || P.peer_sslot[slot].size() != (size_t)n) return EQC_E_INVALID;  // no stream slots
-  cudaStream_t s = (cudaStream_t)stream;
-  EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
-  if (P.capable != 1) return EQC_E_UNSUPPORTED;
   int64_t *stats = comm->st.stats;
   for (int i = 0; i < 4; ++i) stats[i] = 0;
   std::vector<int> row0(n + 1);
@@ -1793,6 +1840,282 @@ extern "C" int compose_direct_send_rle_pull(eqc_comm *comm, int n_local, int w, 
     }
   }
   return EQC_OK;
+}
+}  // namespace
+
+extern "C" int compose_direct_send_rle_pull(eqc_comm *comm, int n_local, int w, int h, int slot, int dest_rank,
+                                            uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
+                                            void *stream) {
+  if (!comm || n_local < 1 || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || dest_rank < 0 ||
+      dest_rank >= comm->nranks || !d_status)
+    return EQC_E_INVALID;
+  const int n = comm->nranks, me = comm->rank;
+  if ((int64_t)n * n_local > EQC_MAX_SOURCES) return EQC_E_INVALID;
+  if (me == dest_rank && (!out_color || out_pitch < w)) return EQC_E_INVALID;
+  P2PState &P = comm->p2p;
+  if (P.sn != 2 * n_local || P.peer_sslot[slot].size() != (size_t)n) return EQC_E_INVALID;  // no stream slots
+  cudaStream_t s = (cudaStream_t)stream;
+  EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
+  if (P.capable != 1) return EQC_E_UNSUPPORTED;
+  return rle_pull_body(comm, n_local, w, h, slot, dest_rank, out_color, out_pitch, d_status, s);
+}
+
+extern "C" int eqc_comm_check(eqc_comm *comm, void *stream) {
+  if (!comm) return EQC_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  if (comm->nccl) {
+    ncclResult_t ae = ncclSuccess;
+    if (ncclCommGetAsyncError(comm->nccl, &ae) != ncclSuccess || ae != ncclSuccess) return EQC_E_NCCL;
+  }
+  P2PState &P = comm->p2p;
+  if (P.flags.p) {
+    int err = 0;
+    EQC_CUDA_TRY(cudaMemcpy(&err, P.flags.as<int>() + kErrSlot, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err & kErrTimeout) return EQC_E_NCCL;
+    if (err & kErrSlotMismatch) return EQC_E_INVALID;
+  }
+  return EQC_OK;
+}
+
+extern "C" int eqc_comm_abort(eqc_comm *comm) {
+  if (!comm) return EQC_E_INVALID;
+  if (comm->nccl) {
+    ncclCommAbort(comm->nccl);
+    comm->nccl = nullptr;
+  }
+  return EQC_OK;
+}
+
+// ---- virtual ranks of the peer-memory transport on one GPU ------------------
+// nranks comms without NCCL whose P2P state points at each other's buffers
+// (plain device pointers where the real transport has IPC mappings); every
+// virtual rank's part of the call runs on its own stream (the flag barriers
+// of different ranks must run concurrently), forked from and joined back to
+// the caller's stream.  The same host code and kernels as the multi-process
+// transport run; only the mapping step differs.
+namespace {
+
+// Every kernel of the library loaded (CUDA lazy loading otherwise loads a
+// kernel at its first launch and waits for the device to do so: with one
+// virtual rank's flag barrier spinning and the rank it waits for enqueued
+// after it on the host, that wait never ends).
+int eqc_preload_kernels() {
+  static int rc = 1;
+  if (rc == 1) {
+    cudaFuncAttributes a;
+    bool ok = cudaFuncGetAttributes(&a, p2p_barrier_kernel) == cudaSuccess &&
+              cudaFuncGetAttributes(&a, p2p_signal_kernel) == cudaSuccess &&
+              cudaFuncGetAttributes(&a, p2p_wait_kernel) == cudaSuccess &&
+              cudaFuncGetAttributes(&a, roi_union_kernel) == cudaSuccess;
+    rc = ok ? EQC_OK : EQC_E_CUDA;
+    if (rc == EQC_OK) rc = eqc_preload_composite();
+    if (rc == EQC_OK) rc = eqc_preload_rle();
+    if (rc == EQC_OK) rc = eqc_preload_roi();
+  }
+  return rc;
+}
+
+struct VirtualP2P {
+  std::vector<eqc_comm> c;
+  std::vector<cudaStream_t> st;
+  std::vector<cudaEvent_t> ev;
+  int n = 0;
+  int init(int nranks, int64_t px, cudaStream_t s) {
+    n = nranks;
+    c.resize(n);
+    st.assign(n, nullptr);
+    ev.assign(n + 1, nullptr);
+    const char *drop = getenv("EQC_P2P_DROP_RANK");  // test hook: this virtual rank never arrives
+    const int dropped = drop ? atoi(drop) : -1;
+    for (int q = 0; q < n; ++q) {
+      c[q].nranks = n;
+      c[q].rank = q;
+      c[q].st.rank = q;
+      P2PState &P = c[q].p2p;
+      EQC_TRY(P.part_c.ensure((size_t)px * 4));
+      EQC_TRY(P.part_d.ensure((size_t)px * 4));
+      EQC_TRY(P.fin_c.ensure((size_t)px * 4));
+      EQC_TRY(P.flags.ensure_zeroed(kFlagInts * sizeof(int)));
+      // every allocation up front: a cudaMalloc while another virtual rank's
+      // flag barrier spins would wait for the device (implicit sync) and so
+      // for a rank whose launches come after it -- a deadlock
+      EQC_TRY(P.roi_local.ensure(eqc_depth_bbox_scratch_bytes()));
+      P.capable = 1;
+      P.cap_px = px;
+      P.skip_barriers = q == dropped;
+      EQC_CUDA_TRY(cudaStreamCreateWithFlags(&st[q], cudaStreamNonBlocking));
+      EQC_CUDA_TRY(cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming));
+    }
+    EQC_CUDA_TRY(cudaEventCreateWithFlags(&ev[n], cudaEventDisableTiming));
+    EQC_TRY(eqc_preload_kernels());
+    for (int q = 0; q < n; ++q) {
+      P2PState &P = c[q].p2p;
+      P.peer_part_c.assign(n, nullptr);
+      P.peer_part_d.assign(n, nullptr);
+      P.peer_fin_c.assign(n, nullptr);
+      P.peer_flags.assign(n, nullptr);
+      for (int r = 0; r < n; ++r) {
+        P.peer_part_c[r] = c[r].p2p.part_c.as<uint32_t>();
+        P.peer_part_d[r] = c[r].p2p.part_d.as<uint32_t>();
+        P.peer_fin_c[r] = c[r].p2p.fin_c.as<uint32_t>();
+        P.peer_flags[r] = c[r].p2p.flags.as<int>();
+      }
+    }
+    EQC_CUDA_TRY(cudaEventRecord(ev[n], s));
+    for (int q = 0; q < n; ++q) EQC_CUDA_TRY(cudaStreamWaitEvent(st[q], ev[n], 0));
+    return EQC_OK;
+  }
+  // join every virtual rank's stream into s, wait, and report the ranks'
+  // error words (a timed-out wait -> EQC_E_NCCL, a slot mismatch -> EQC_E_INVALID)
+  int join(cudaStream_t s, int64_t *out_stats) {
+    for (int q = 0; q < n; ++q) {
+      EQC_CUDA_TRY(cudaEventRecord(ev[q], st[q]));
+      EQC_CUDA_TRY(cudaStreamWaitEvent(s, ev[q], 0));
+    }
+    EQC_CUDA_TRY(cudaStreamSynchronize(s));
+    int err = 0;
+    for (int q = 0; q < n; ++q) {
+      int e = 0;
+      EQC_CUDA_TRY(cudaMemcpy(&e, c[q].p2p.flags.as<int>() + kErrSlot, sizeof(int), cudaMemcpyDeviceToHost));
+      err |= e;
+    }
+    if (out_stats) {
+      for (int i = 0; i < 4; ++i) out_stats[i] = 0;
+      for (auto &x : c)
+        for (int i = 0; i < 4; ++i) out_stats[i] += x.st.stats[i];
+    }
+    if (err & kErrTimeout) return EQC_E_NCCL;
+    if (err & kErrSlotMismatch) return EQC_E_INVALID;
+    return EQC_OK;
+  }
+  ~VirtualP2P() {
+    cudaDeviceSynchronize();
+    for (auto &x : c) {
+      P2PState &P = x.p2p;
+      P.peer_part_c.clear();  // plain pointers: nothing to unmap
+      P.peer_part_d.clear();
+      P.peer_fin_c.clear();
+      P.peer_flags.clear();
+      for (int i = 0; i < P2PState::kSlots; ++i) {
+        P.peer_slot_c[i].clear();
+        P.peer_slot_d[i].clear();
+        P.peer_sslot[i].clear();
+        P.slot_c[i].release();
+        P.slot_d[i].release();
+      }
+      P.part_c.release();
+      P.part_d.release();
+      P.fin_c.release();
+      P.flags.release();
+      P.roi_local.release();
+      P.xfer.release();
+      if (P.aux) cudaStreamDestroy(P.aux);
+      if (P.ev_start) cudaEventDestroy(P.ev_start);
+      if (P.ev_pulled) cudaEventDestroy(P.ev_pulled);
+      P.aux = nullptr;
+      x.st.release();
+    }
+    for (auto s : st)
+      if (s) cudaStreamDestroy(s);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+}  // namespace
+
+extern "C" int compose_direct_send_p2p_local(int nranks, int n_local, const uint32_t *const *color,
+                                             const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
+                                             int flags, int mode, int dest_rank, uint32_t *out_color,
+                                             int64_t out_pitch, int64_t *out_stats, void *stream) {
+  EQC_TRY(validate(nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch, true));
+  if (nranks < 2 || (flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) return EQC_E_INVALID;
+  if (mode < EQC_P2P_PLAIN || mode > EQC_P2P_SLOTS) return EQC_E_INVALID;
+  if (mode == EQC_P2P_PIPELINED && (flags & EQC_FLAG_ROI)) return EQC_E_INVALID;
+  if (mode == EQC_P2P_SLOTS && (n_local != 1 || op != EQC_OP_DEPTH || !depth || (flags & EQC_FLAG_ROI)))
+    return EQC_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t px = (int64_t)w * h;
+  VirtualP2P V;
+  EQC_TRY(V.init(nranks, px, s));
+  std::vector<const uint32_t *> cs((size_t)nranks * n_local), dsv((size_t)nranks * n_local);
+  for (size_t i = 0; i < cs.size(); ++i) {
+    cs[i] = color[i];
+    dsv[i] = depth ? depth[i] : nullptr;
+  }
+  if (mode == EQC_P2P_SLOTS) {
+    // each virtual rank's partial frame lives in its slot 0 (the caller's
+    // data copied in: the path under test reads the slots in place)
+    for (int q = 0; q < nranks; ++q) {
+      P2PState &P = V.c[q].p2p;
+      EQC_TRY(P.slot_c[0].ensure((size_t)px * 4));
+      EQC_TRY(P.slot_d[0].ensure((size_t)px * 4));
+      EQC_TRY(P.slot_c[1].ensure(4));
+      EQC_TRY(P.slot_d[1].ensure(4));
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(P.slot_c[0].p, (size_t)w * 4, color[q], (size_t)pitch * 4, (size_t)w * 4, h,
+                                     cudaMemcpyDeviceToDevice, V.st[q]));
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(P.slot_d[0].p, (size_t)w * 4, depth[q], (size_t)pitch * 4, (size_t)w * 4, h,
+                                     cudaMemcpyDeviceToDevice, V.st[q]));
+      P.slot_px = px;
+      cs[q] = P.slot_c[0].as<uint32_t>();
+      dsv[q] = P.slot_d[0].as<uint32_t>();
+    }
+    for (int q = 0; q < nranks; ++q)
+      for (int i = 0; i < P2PState::kSlots; ++i) {
+        V.c[q].p2p.peer_slot_c[i].assign(nranks, nullptr);
+        V.c[q].p2p.peer_slot_d[i].assign(nranks, nullptr);
+        for (int r = 0; r < nranks; ++r) {
+          V.c[q].p2p.peer_slot_c[i][r] = V.c[r].p2p.slot_c[i].as<uint32_t>();
+          V.c[q].p2p.peer_slot_d[i][r] = V.c[r].p2p.slot_d[i].as<uint32_t>();
+        }
+      }
+  }
+  const int64_t use_pitch = mode == EQC_P2P_SLOTS ? w : pitch;
+  for (int q = 0; q < nranks; ++q) {
+    Geometry g;
+    g.n = nranks;
+    g.n_local = n_local;
+    g.w = w;
+    g.h = h;
+    g.pitch = use_pitch;
+    g.op = op;
+    g.flags = flags;
+    g.dest = dest_rank;
+    g.out = q == dest_rank ? out_color : nullptr;
+    g.out_pitch = q == dest_rank ? out_pitch : w;
+    const uint32_t *const *cq = cs.data() + (size_t)q * n_local;
+    const uint32_t *const *dq = depth ? dsv.data() + (size_t)q * n_local : nullptr;
+    EQC_TRY(mode == EQC_P2P_PIPELINED ? direct_send_p2p_pipelined(&V.c[q], g, cq, dq, V.st[q])
+                                      : direct_send_p2p(&V.c[q], g, cq, dq, V.st[q]));
+  }
+  return V.join(s, out_stats);
+}
+
+extern "C" int compose_direct_send_rle_pull_local(int nranks, int n_local, const uint8_t *const *rank_streams,
+                                                  int64_t cap_bytes, int w, int h, int dest_rank,
+                                                  uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
+                                                  int64_t *out_stats, void *stream) {
+  if (nranks < 2 || n_local < 1 || !rank_streams || cap_bytes <= 0 || w <= 0 || h <= 0 || dest_rank < 0 ||
+      dest_rank >= nranks || !out_color || out_pitch < w || !d_status)
+    return EQC_E_INVALID;
+  if ((int64_t)nranks * n_local > EQC_MAX_SOURCES) return EQC_E_INVALID;
+  for (int q = 0; q < nranks; ++q)
+    if (!rank_streams[q]) return EQC_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  VirtualP2P V;
+  EQC_TRY(V.init(nranks, (int64_t)w * h, s));
+  for (int q = 0; q < nranks; ++q) {
+    P2PState &P = V.c[q].p2p;
+    P.sn = 2 * n_local;
+    P.scap = cap_bytes;
+    P.peer_sslot[0].assign(nranks, nullptr);
+    for (int r = 0; r < nranks; ++r) P.peer_sslot[0][r] = const_cast<uint8_t *>(rank_streams[r]);
+  }
+  for (int q = 0; q < nranks; ++q)
+    EQC_TRY(rle_pull_body(&V.c[q], n_local, w, h, 0, dest_rank, q == dest_rank ? out_color : nullptr,
+                          q == dest_rank ? out_pitch : w, d_status, V.st[q]));
+  return V.join(s, out_stats);
 }
 
 extern "C" int eqc_comm_stats(const eqc_comm *comm, int64_t out[4]) {

@@ -1077,3 +1077,31 @@ extern "C" int compositor_blend_ordered_roi(int n, const uint32_t *const *color,
   blend_ordered_roi_kernel<<<grid_for(groups, EQC_ROI_GRID(blend_ordered_roi_kernel)), 256, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
+
+// Load every kernel of this file now (CUDA lazy loading would otherwise load
+// one at its first launch, which waits for the device: fatal while another
+// virtual rank's flag barrier spins, see compose.cu VirtualP2P).
+int eqc_preload_composite() {
+  cudaFuncAttributes a;
+  bool ok = true;
+  ok = ok && cudaFuncGetAttributes(&a, depth_composite_kernel<true, false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, depth_composite_kernel<false, false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, depth_composite_kernel<true, true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, depth_composite_kernel<false, true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, bbox_finalize_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_ordered_kernel<true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_ordered_kernel<false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, depth_composite_roi_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_ordered_roi_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_partial_kernel<true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_partial_kernel<false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_partials_kernel<true, true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_partials_kernel<true, false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_partials_kernel<false, true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, blend_partials_kernel<false, false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, average_kernel<true, true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, average_kernel<true, false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, average_kernel<false, true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, average_kernel<false, false>) == cudaSuccess;
+  return ok ? EQC_OK : EQC_E_CUDA;
+}

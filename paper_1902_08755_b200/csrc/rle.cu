@@ -1753,3 +1753,20 @@ int eqc_depth_rle_band(int n, const uint8_t *const *color_rle, const uint8_t *co
   depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
+
+// Load every kernel of this file now (see eqc_preload_composite).
+int eqc_preload_rle() {
+  cudaFuncAttributes a;
+  bool ok = true;
+  ok = ok && cudaFuncGetAttributes(&a, rle_encode_kernel<true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle_runscan_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle_compact_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle_compact3_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle_encode3_kernel<true, true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle_encode3_kernel<true, false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle_encode3_kernel<false, false>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle64_decode_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, rle_decode_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, depth_rle_kernel) == cudaSuccess;
+  return ok ? EQC_OK : EQC_E_CUDA;
+}

@@ -153,3 +153,12 @@ extern "C" int image_roi(int n, const uint32_t *const *frames, int w, int h, int
   roi_finalize_kernel<<<1, 64, 0, s>>>(d_roi, n);
   return eqc_launch_status();
 }
+
+// Load every kernel of this file now (see eqc_preload_composite).
+int eqc_preload_roi() {
+  cudaFuncAttributes a;
+  bool ok = cudaFuncGetAttributes(&a, roi_init_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, roi_scan_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, roi_finalize_kernel) == cudaSuccess;
+  return ok ? EQC_OK : EQC_E_CUDA;
+}

@@ -30,6 +30,7 @@ FLAG_RLE = 1
 FLAG_NCCL = 2
 FLAG_ROI = 4
 FLAG_OVERLAP = 8  # the compose overlaps other GPU work: peer pulls use <= 1 CTA per SM
+P2P_PLAIN, P2P_PIPELINED, P2P_SLOTS = 0, 1, 2  # compose_direct_send_p2p_local modes
 
 
 class EqcError(RuntimeError):
@@ -70,6 +71,10 @@ def _load():
         "eqc_comm_frame_buffers": ([P, i32, i32, i32, P, P, P, P], i32),
         "eqc_comm_stream_buffers": ([P, i32, i64, i32, P, P], i32),
         "compose_direct_send_rle_pull": ([P, i32, i32, i32, i32, i32, P, i64, P, P], i32),
+        "compose_direct_send_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, i32, P, i64, P, P], i32),
+        "compose_direct_send_rle_pull_local": ([i32, i32, P, i64, i32, i32, i32, P, i64, P, P, P], i32),
+        "eqc_comm_check": ([P, P], i32),
+        "eqc_comm_abort": ([P], i32),
         "eqc_plan_bands": ([i32, i32, P], i32),
         "eqc_plan_binary_swap": ([i32, i32, i32, P, i32], i32),
         "compose_direct_send": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
@@ -322,6 +327,14 @@ class Comm:
     def handle(self):
         return self._h
 
+    def check(self, stream=None):
+        """eqc_comm_check: synchronise, then raise on an NCCL async error, a
+        peer-memory wait that timed out, or mismatched frame slots."""
+        return _check(_lib.eqc_comm_check(self._h, _stream(stream)), "eqc_comm_check")
+
+    def abort(self):
+        return _check(_lib.eqc_comm_abort(self._h), "eqc_comm_abort")
+
     def stats(self):
         out = (ctypes.c_int64 * 4)()
         _check(_lib.eqc_comm_stats(self._h, out), "eqc_comm_stats")
@@ -411,6 +424,34 @@ def compose_direct_send_local(nranks, colors, depths, out_color, dest_rank: int 
     """Virtual-rank direct send on one GPU; returns summed traffic counters."""
     return _compose_local(_lib.compose_direct_send_local, "compose_direct_send_local", nranks, colors, depths,
                           out_color, dest_rank, flags, op, stream)
+
+
+def compose_direct_send_p2p_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
+                                  op: int = OP_DEPTH, mode: int = P2P_PLAIN, stream=None):
+    """The peer-memory direct send for virtual ranks on one GPU (same host code
+    and kernels as the multi-process path); returns summed traffic counters."""
+    total = len(colors)
+    assert total % nranks == 0
+    w, h, pitch = _frame_geom(colors[0])
+    opitch = _frame_geom(out_color)[2]
+    stats = (ctypes.c_int64 * 4)()
+    rc = _lib.compose_direct_send_p2p_local(nranks, total // nranks, _ptrs(colors),
+                                            _ptrs(depths) if depths is not None else None, w, h, pitch, op, flags,
+                                            mode, dest_rank, _addr(out_color), opitch, stats, _stream(stream))
+    _check(rc, "compose_direct_send_p2p_local")
+    return list(stats)
+
+
+def compose_direct_send_rle_pull_local(nranks, n_local, rank_streams, cap_bytes, w, h, out_color, status,
+                                       dest_rank: int = 0, stream=None):
+    """compose_direct_send_rle_pull for virtual ranks on one GPU: rank q's
+    2*n_local streams lie contiguously (cap_bytes apart) at rank_streams[q]."""
+    opitch = _frame_geom(out_color)[2]
+    stats = (ctypes.c_int64 * 4)()
+    rc = _lib.compose_direct_send_rle_pull_local(nranks, n_local, _ptrs(rank_streams), cap_bytes, w, h, dest_rank,
+                                                 _addr(out_color), opitch, _addr(status), stats, _stream(stream))
+    _check(rc, "compose_direct_send_rle_pull_local")
+    return list(stats)
 
 
 def compose_binary_swap_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
