@@ -200,6 +200,11 @@ EQC_API int compose_direct_send(eqc_comm *comm, int n_local, const uint32_t *con
  * half is composited with ties going to the bit-0 group (R-C5).  Finally
  * every rank's region (colour) is gathered on dest_rank.
  * EQC_E_UNSUPPORTED unless nranks is a power of two.
+ * Transport: as compose_direct_send -- without EQC_FLAG_RLE / EQC_FLAG_NCCL
+ * and when every rank maps every peer, each round's merge reads the
+ * partner's half in place over NVLink (flag barriers between rounds) and the
+ * last round writes straight into the destination's frame; otherwise NCCL
+ * grouped send/recv per round.
  */
 EQC_API int compose_binary_swap(eqc_comm *comm, int n_local, const uint32_t *const *color,
                                 const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
@@ -319,6 +324,19 @@ EQC_API int compose_direct_send_p2p_local(int nranks, int n_local, const uint32_
                                           const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
                                           int flags, int mode, int dest_rank, uint32_t *out_color,
                                           int64_t out_pitch, int64_t *out_stats, void *stream);
+
+/*
+ * compose_binary_swap_p2p_local -- the peer-memory binary swap (the default
+ * transport of compose_binary_swap when every rank maps every peer, no
+ * EQC_FLAG_RLE / EQC_FLAG_NCCL) for virtual ranks on one GPU, as above:
+ * round r merges the kept half in place, reading the partner's rows of it
+ * over NVLink; the last round writes the final colour into the destination's
+ * frame.  nranks must be a power of two (else EQC_E_UNSUPPORTED).
+ */
+EQC_API int compose_binary_swap_p2p_local(int nranks, int n_local, const uint32_t *const *color,
+                                          const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
+                                          int flags, int dest_rank, uint32_t *out_color, int64_t out_pitch,
+                                          int64_t *out_stats, void *stream);
 
 /*
  * compose_direct_send_rle_pull on ONE GPU (virtual ranks as above): rank q's

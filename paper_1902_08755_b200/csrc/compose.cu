@@ -1687,6 +1687,65 @@ int direct_send_p2p(eqc_comm *c, const Geometry &g0, const uint32_t *const *colo
   return EQC_OK;
 }
 
+// Peer-memory binary swap: log2 n rounds; in round r rank g
+// and its partner g ^ 2^r each merge their KEPT half of the current region
+// in place in their own (IPC-exposed) partial frame, reading the partner's
+// rows of that half straight out of the partner's partial over NVLink (the
+// partner reads only the other half, which this rank does not write this
+// round).  A flag barrier orders the rounds; the last round's merge writes
+// the final colour of the rank's region straight into the destination's
+// frame (the gather fused into it).  Ties go to the bit-r = 0 group (R-C5).
+int binary_swap_p2p(eqc_comm *c, const Geometry &g, const uint32_t *const *color, const uint32_t *const *depth,
+                    cudaStream_t s) {
+  P2PState &P = c->p2p;
+  const int n = c->nranks, me = c->rank;
+  int64_t *stats = c->st.stats;
+  for (int i = 0; i < 4; ++i) stats[i] = 0;
+  std::vector<BsRound> plan;
+  const int k = plan_bs(g.h, n, me, plan);
+  if (k < 0) return k;
+  uint32_t *pc = P.part_c.as<uint32_t>(), *pd = P.part_d.as<uint32_t>();
+  EQC_TRY(op_local(g, color, depth, pc, pd, s));
+  for (int rd = 0; rd < k; ++rd) {
+    EQC_TRY(p2p_barrier(c, s));  // the partner's current data is complete (and no longer read by anyone else)
+    const BsRound &b = plan[rd];
+    const int krows = b.keep_y1 - b.keep_y0;
+    if (b.send_y1 > b.send_y0) stats[0] += 1;
+    if (krows <= 0) continue;
+    stats[3] += (int64_t)krows * g.w * 8;
+    const size_t off = (size_t)b.keep_y0 * g.w;
+    const uint32_t *mine_c = pc + off, *mine_d = pd + off;
+    const uint32_t *their_c = P.peer_part_c[b.partner] + off, *their_d = P.peer_part_d[b.partner] + off;
+    const uint32_t *cc[2] = {b.low ? mine_c : their_c, b.low ? their_c : mine_c};
+    const uint32_t *dd[2] = {b.low ? mine_d : their_d, b.low ? their_d : mine_d};
+    if (rd + 1 < k) {
+      EQC_TRY(op_merge(g, 2, cc, dd, krows, pc + off, pd + off, s));
+    } else {
+      // last round: the region's final colour, into the destination's frame
+      uint32_t *out = me == g.dest ? g.out + (size_t)b.keep_y0 * g.out_pitch : P.peer_fin_c[g.dest] + off;
+      const int64_t opitch = me == g.dest ? g.out_pitch : g.w;
+      EQC_TRY(op_final(g, 2, cc, dd, krows, out, opitch, s));
+      if (me != g.dest) {
+        stats[1] += 1;
+        stats[2] += (int64_t)krows * g.w * 4;
+      }
+    }
+  }
+  if (k == 0) return EQC_OK;
+  EQC_TRY(p2p_barrier(c, s));  // every final region is on the destination
+  if (me == g.dest && !(g.out == P.fin_c.as<uint32_t>() && g.out_pitch == g.w)) {
+    for (int q = 0; q < n; ++q) {
+      int y0, y1;
+      final_region_bs(g.h, n, q, y0, y1);
+      if (q == me || y1 <= y0) continue;
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)y0 * g.out_pitch, g.out_pitch * 4,
+                                     P.fin_c.as<uint32_t>() + (size_t)y0 * g.w, (size_t)g.w * 4, (size_t)g.w * 4,
+                                     y1 - y0, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return EQC_OK;
+}
+
 }  // namespace
 
 extern "C" int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]) {
@@ -2092,6 +2151,34 @@ extern "C" int compose_direct_send_p2p_local(int nranks, int n_local, const uint
   return V.join(s, out_stats);
 }
 
+extern "C" int compose_binary_swap_p2p_local(int nranks, int n_local, const uint32_t *const *color,
+                                             const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
+                                             int flags, int dest_rank, uint32_t *out_color, int64_t out_pitch,
+                                             int64_t *out_stats, void *stream) {
+  EQC_TRY(validate(nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch, true));
+  if (nranks < 2 || (flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) return EQC_E_INVALID;
+  if (nranks & (nranks - 1)) return EQC_E_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  VirtualP2P V;
+  EQC_TRY(V.init(nranks, (int64_t)w * h, s));
+  for (int q = 0; q < nranks; ++q) {
+    Geometry g;
+    g.n = nranks;
+    g.n_local = n_local;
+    g.w = w;
+    g.h = h;
+    g.pitch = pitch;
+    g.op = op;
+    g.flags = flags;
+    g.dest = dest_rank;
+    g.out = q == dest_rank ? out_color : nullptr;
+    g.out_pitch = q == dest_rank ? out_pitch : w;
+    EQC_TRY(binary_swap_p2p(&V.c[q], g, color + (size_t)q * n_local, depth ? depth + (size_t)q * n_local : nullptr,
+                            V.st[q]));
+  }
+  return V.join(s, out_stats);
+}
+
 extern "C" int compose_direct_send_rle_pull_local(int nranks, int n_local, const uint8_t *const *rank_streams,
                                                   int64_t cap_bytes, int w, int h, int dest_rank,
                                                   uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
@@ -2179,6 +2266,10 @@ static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *
       return (!(flags & EQC_FLAG_ROI) && big) ? direct_send_p2p_pipelined(comm, g, color, depth, s)
                                               : direct_send_p2p(comm, g, color, depth, s);
     }
+  }
+  if (algo == kBinarySwap && comm->nranks > 1 && !(flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) {
+    EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
+    if (comm->p2p.capable == 1) return binary_swap_p2p(comm, g, color, depth, s);
   }
   NcclTransport T(comm->nccl, s);
   std::vector<RankState *> ranks{&comm->st};

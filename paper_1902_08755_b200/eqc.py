@@ -73,6 +73,7 @@ def _load():
         "compose_direct_send_rle_pull": ([P, i32, i32, i32, i32, i32, P, i64, P, P], i32),
         "compose_direct_send_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, i32, P, i64, P, P], i32),
         "compose_direct_send_rle_pull_local": ([i32, i32, P, i64, i32, i32, i32, P, i64, P, P, P], i32),
+        "compose_binary_swap_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
         "eqc_comm_check": ([P, P], i32),
         "eqc_comm_abort": ([P], i32),
         "eqc_plan_bands": ([i32, i32, P], i32),
@@ -440,6 +441,13 @@ def compose_direct_send_p2p_local(nranks, colors, depths, out_color, dest_rank: 
                                             mode, dest_rank, _addr(out_color), opitch, stats, _stream(stream))
     _check(rc, "compose_direct_send_p2p_local")
     return list(stats)
+
+
+def compose_binary_swap_p2p_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
+                                  op: int = OP_DEPTH, stream=None):
+    """The peer-memory binary swap for virtual ranks on one GPU."""
+    return _compose_local(_lib.compose_binary_swap_p2p_local, "compose_binary_swap_p2p_local", nranks, colors,
+                          depths, out_color, dest_rank, flags, op, stream)
 
 
 def compose_direct_send_rle_pull_local(nranks, n_local, rank_streams, cap_bytes, w, h, out_color, status,

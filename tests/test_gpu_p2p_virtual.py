@@ -1,6 +1,7 @@
 """GPU parity of the peer-memory (NVLink P2P) transport on ONE GPU.
 
-compose_direct_send_p2p_local / compose_direct_send_rle_pull_local run the
+compose_direct_send_p2p_local / compose_binary_swap_p2p_local /
+compose_direct_send_rle_pull_local run the
 multi-process peer-memory host code and kernels for virtual ranks of one
 process (their "peer mappings" are plain device pointers, every virtual rank
 on its own stream): the plain peer-memory direct send, the pipelined variant
@@ -169,3 +170,42 @@ except eqc.EqcError as e:
     line = [x for x in r.stdout.splitlines() if x.startswith(("CODE", "NOERROR"))][-1]
     assert line.startswith("CODE -6"), line  # EQC_E_NCCL
     assert float(line.split()[2]) < 60.0
+
+
+BS_CASES = [
+    # (nranks, n_local, w, h, pitch, out_pitch, dest, op, gen)
+    (2, 2, 300, 41, None, None, 0, "depth", "scene"),
+    (4, 1, 130, 37, 136, 140, 2, "depth", "ties"),
+    (8, 1, 128, 19, None, None, 7, "depth", "scene"),
+    (4, 2, 640, 360, None, None, 1, "depth", "scene"),
+    (2, 8, 320, 180, None, None, 1, "blend", "bricks"),
+    (4, 2, 257, 77, None, 264, 3, "blend", "bricks"),
+]
+
+
+@pytest.mark.parametrize("case", BS_CASES, ids=[f"n{c[0]}x{c[1]}_{c[2]}x{c[3]}_{c[7]}_d{c[6]}" for c in BS_CASES])
+def test_p2p_binary_swap_virtual_ranks(eqc, case):
+    # depth: bit-exact vs O1 over all sources (R-C5 tie rule: bit-0 group);
+    # blend: within 1/255 of O2 over all layers (R-C4, R-C6)
+    nr, nl, w, h, pitch, opitch, dest, op, gen = case
+    N = nr * nl
+    out = out_frame(h, w, opitch)
+    if op == "depth":
+        c, d = _scene(N, w, h, synth.SEED_BASE + 97 + N + w, ties=gen == "ties")
+        want, _ = oracle.depth_composite(c, d)
+        stats = eqc.compose_binary_swap_p2p_local(nr, [to_dev(x, pitch) for x in c], [to_dev(x, pitch) for x in d],
+                                                  out, dest_rank=dest)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(to_host(out), want)
+        if h >= 2 * nr:
+            assert stats[0] == nr * (nr.bit_length() - 1)  # one half sent per rank per round
+            assert stats[1] == nr - 1
+    else:
+        layers = synth.volume_bricks(synth.SEED_BASE + 98 + N, N, w, h)
+        want = oracle.blend_ordered(layers)
+        eqc.compose_binary_swap_p2p_local(nr, [to_dev(x, pitch) for x in layers], None, out, dest_rank=dest,
+                                          op=eqc.OP_BLEND)
+        torch.cuda.synchronize()
+        got = to_host(out)
+        diff = np.abs(got.view(np.uint8).astype(int) - want.view(np.uint8).astype(int))
+        assert diff.max() <= 1
