@@ -294,6 +294,34 @@ EQC_API int compose_direct_send_roi_local(int nranks, int n_local, const uint32_
                                           int64_t out_pitch, int64_t *out_stats, void *stream);
 
 /*
+ * compose_tiles -- the display wall: direct send over the
+ * wall's tiles, no gather.  The w x h frame is a tiles_x x tiles_y grid of
+ * display tiles (segments/channels of a tiled wall):
+ * tile t = (t % tiles_x, t / tiles_x) covers x in [floor(c w / tiles_x),
+ * floor((c+1) w / tiles_x)), y likewise, and is owned by rank
+ * floor(t * nranks / (tiles_x * tiles_y)) -- the channel driving it.
+ * Every rank pre-composites its n_local sources (global indices as
+ * compose_direct_send), ships each tile of its partial wall to the tile's
+ * owner -- with EQC_FLAG_RLE as RLE-BP streams (colour swizzled + depth; the
+ * owner runs the fused decode + depth composite over the n streams), else as
+ * raw rectangles -- and the owner writes its composited tiles into out_color
+ * [h][out_pitch] (its display frame; other tiles untouched).  Result: on
+ * every tile, bit-identical to compositor_depth over all sources.  NCCL
+ * transport; EQC_FLAG_RLE synchronises `stream` once (stream sizes).
+ * EQC_OP_DEPTH only.  flags: 0 or EQC_FLAG_RLE.
+ * compose_tiles_local: virtual ranks on one GPU, every rank writing its tiles
+ *   into the one out_color; EQC_E_CORRUPT if a stream failed to decode.
+ * eqc_plan_tiles: rect = {x0, y0, w, h, owner} of tile `tile`.
+ */
+EQC_API int compose_tiles(eqc_comm *comm, int n_local, const uint32_t *const *color, const uint32_t *const *depth,
+                          int w, int h, int64_t pitch, int tiles_x, int tiles_y, int flags, uint32_t *out_color,
+                          int64_t out_pitch, void *stream);
+EQC_API int compose_tiles_local(int nranks, int n_local, const uint32_t *const *color, const uint32_t *const *depth,
+                                int w, int h, int64_t pitch, int tiles_x, int tiles_y, int flags,
+                                uint32_t *out_color, int64_t out_pitch, int64_t *out_stats, void *stream);
+EQC_API int eqc_plan_tiles(int w, int h, int tiles_x, int tiles_y, int nranks, int tile, int *rect);
+
+/*
  * Peer-memory transport on ONE GPU: compose_direct_send's NVLink peer-memory
  * path (P:2302-2310 stages (2)-(5) with no staging copy) run
  * for nranks virtual ranks of this process.  Every virtual rank gets its own

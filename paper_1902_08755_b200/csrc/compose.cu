@@ -609,6 +609,194 @@ int bs_alloc(RankState &r, const Geometry &g) {
   return EQC_OK;
 }
 
+// ---- c5: display-wall tiles (display segments and the
+// wall's channels) -------------------------------------
+// Direct send over the wall's tiles instead of row bands: tile t (row-major,
+// tiles_x x tiles_y, edges at floor(k w / tiles_x), floor(k h / tiles_y)) is
+// owned by rank floor(t n / T) (the channel driving that display);
+// every rank pre-composites its sources, ships each tile of its partial wall
+// (RLE streams with EQC_FLAG_RLE, else raw rectangles) to the tile's owner,
+// and the owner composites the n partial tiles into its frame -- no gather.
+struct TileRect {
+  int x0, y0, w, h, owner;
+};
+
+TileRect plan_tile(int w, int h, int tx, int ty, int n, int t) {
+  const int col = t % tx, row = t / tx;
+  TileRect r;
+  r.x0 = (int)((int64_t)col * w / tx);
+  r.w = (int)((int64_t)(col + 1) * w / tx) - r.x0;
+  r.y0 = (int)((int64_t)row * h / ty);
+  r.h = (int)((int64_t)(row + 1) * h / ty) - r.y0;
+  r.owner = (int)((int64_t)t * n / ((int64_t)tx * ty));
+  return r;
+}
+
+int run_tiles(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaStream_t s, int tx, int ty) {
+  const int nt = tx * ty, n = g.n;
+  const bool rle = (g.flags & EQC_FLAG_RLE) != 0;
+  std::vector<TileRect> tr(nt);
+  int twm = 0, thm = 0;
+  for (int t = 0; t < nt; ++t) {
+    tr[t] = plan_tile(g.w, g.h, tx, ty, n, t);
+    twm = std::max(twm, tr[t].w);
+    thm = std::max(thm, tr[t].h);
+  }
+  // stream / rectangle slot bytes (8-byte aligned streams: 256-byte slots)
+  const int64_t cap = rle ? ((image_rle_max_size(twm, thm) + 255) & ~(int64_t)255) : (int64_t)twm * thm * 4;
+  auto owned = [&](int r, int &t0, int &t1) {
+    t0 = nt;
+    t1 = nt;
+    for (int t = 0; t < nt; ++t)
+      if (tr[t].owner == r) {
+        if (t0 == nt) t0 = t;
+        t1 = t + 1;
+      }
+    if (t0 == nt) t0 = t1 = 0;
+  };
+  // (1) pre-composite; (2) every tile of the partial wall into its slot
+  for (RankState *r : ranks) {
+    for (int i = 0; i < 4; ++i) r->stats[i] = 0;
+    EQC_TRY(r->part_c[0].ensure(frame_bytes(g, g.h)));
+    EQC_TRY(r->part_d[0].ensure(frame_bytes(g, g.h)));
+    EQC_TRY(local_precomposite(*r, g, s));
+    EQC_TRY(r->enc.ensure((size_t)(2 * nt) * cap));
+    EQC_TRY(r->sizes.ensure(((size_t)n * 2 * nt + 64) * sizeof(int64_t)));  // + batch-order sizes
+    EQC_TRY(r->status.ensure_zeroed(sizeof(int32_t)));
+    const uint32_t *pc = r->part_c[0].as<uint32_t>(), *pd = r->part_d[0].as<uint32_t>();
+    if (rle) {
+      // batches of <= 32 tiles of one size (64 streams: colour swizzled + depth)
+      std::vector<int> done(nt, 0);
+      for (int t0 = 0; t0 < nt; ++t0) {
+        if (done[t0]) continue;
+        std::vector<int> batch;
+        for (int t = t0; t < nt && (int)batch.size() < 32; ++t)
+          if (!done[t] && tr[t].w == tr[t0].w && tr[t].h == tr[t0].h) {
+            batch.push_back(t);
+            done[t] = 1;
+          }
+        const int bw = tr[t0].w, bh = tr[t0].h, cnt = (int)batch.size();
+        std::vector<const uint32_t *> src(2 * cnt);
+        std::vector<uint8_t *> dst(2 * cnt);
+        std::vector<int> kinds(2 * cnt), fl(2 * cnt);
+        for (int i = 0; i < cnt; ++i) {
+          const TileRect &q = tr[batch[i]];
+          const size_t off = (size_t)q.y0 * g.w + q.x0;
+          src[i] = pc + off;
+          src[cnt + i] = pd + off;
+          dst[i] = r->enc.as<uint8_t>() + (size_t)(2 * batch[i]) * cap;
+          dst[cnt + i] = r->enc.as<uint8_t>() + (size_t)(2 * batch[i] + 1) * cap;
+          kinds[i] = EQC_KIND_RGBA8, fl[i] = EQC_FLAG_SWIZZLE;
+          kinds[cnt + i] = EQC_KIND_DEPTH32, fl[cnt + i] = 0;
+        }
+        const size_t wsb = image_rle_workspace_size_batch(2 * cnt, bw, bh);
+        EQC_TRY(r->ws.ensure(wsb));
+        // sizes land in batch order after the size rows, then move to the
+        // rank's own row ([2t] colour, [2t+1] depth)
+        int64_t *dsz = r->sizes.as<int64_t>() + (size_t)r->rank * 2 * nt;
+        int64_t *bsz = r->sizes.as<int64_t>() + (size_t)n * 2 * nt;
+        EQC_TRY(image_compress_rle_batch(2 * cnt, src.data(), bw, bh, g.w, kinds.data(), fl.data(), dst.data(), cap,
+                                         bsz, r->ws.p, wsb, s));
+        for (int i = 0; i < cnt; ++i) {
+          EQC_CUDA_TRY(cudaMemcpyAsync(dsz + 2 * batch[i], bsz + i, 8, cudaMemcpyDeviceToDevice, s));
+          EQC_CUDA_TRY(cudaMemcpyAsync(dsz + 2 * batch[i] + 1, bsz + cnt + i, 8, cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    } else {
+      for (int t = 0; t < nt; ++t) {  // pack each tile rectangle (pitch tile width)
+        const TileRect &q = tr[t];
+        const size_t off = (size_t)q.y0 * g.w + q.x0;
+        EQC_CUDA_TRY(cudaMemcpy2DAsync(r->enc.as<uint8_t>() + (size_t)(2 * t) * cap, (size_t)q.w * 4, pc + off,
+                                       (size_t)g.w * 4, (size_t)q.w * 4, q.h, cudaMemcpyDeviceToDevice, s));
+        EQC_CUDA_TRY(cudaMemcpy2DAsync(r->enc.as<uint8_t>() + (size_t)(2 * t + 1) * cap, (size_t)q.w * 4, pd + off,
+                                       (size_t)g.w * 4, (size_t)q.w * 4, q.h, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  }
+  // (3) RLE: every rank's stream sizes to every rank, read back (one sync)
+  std::vector<std::vector<int64_t>> hs(ranks.size());
+  if (rle) {
+    if (n > 1) {
+      EQC_TRY(T.start());
+      for (RankState *r : ranks) {
+        int64_t *row = r->sizes.as<int64_t>();
+        for (int q = 0; q < n; ++q) {
+          if (q == r->rank) continue;
+          EQC_TRY(T.send(*r, q, row + (size_t)r->rank * 2 * nt, 2 * nt * sizeof(int64_t)));
+          EQC_TRY(T.recv(*r, q, row + (size_t)q * 2 * nt, 2 * nt * sizeof(int64_t)));
+        }
+      }
+      EQC_TRY(T.end());
+    }
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      hs[i].resize((size_t)n * 2 * nt);
+      EQC_CUDA_TRY(cudaMemcpyAsync(hs[i].data(), ranks[i]->sizes.p, hs[i].size() * 8, cudaMemcpyDeviceToHost, s));
+    }
+    EQC_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  auto bytes_of = [&](size_t ri, int q, int t, int k) -> size_t {
+    return rle ? (size_t)hs[ri][(size_t)q * 2 * nt + 2 * t + k] : (size_t)tr[t].w * tr[t].h * 4;
+  };
+  // (4) tile payloads to their owners
+  for (RankState *r : ranks) {
+    int t0, t1;
+    owned(r->rank, t0, t1);
+    EQC_TRY(r->dec.ensure((size_t)std::max(1, (t1 - t0) * n * 2) * cap));
+  }
+  if (n > 1) {
+    EQC_TRY(T.start());
+    for (size_t ri = 0; ri < ranks.size(); ++ri) {
+      RankState &r = *ranks[ri];
+      for (int t = 0; t < nt; ++t) {
+        const int o = tr[t].owner;
+        if (o == r.rank) continue;
+        EQC_TRY(T.send(r, o, r.enc.as<uint8_t>() + (size_t)(2 * t) * cap, bytes_of(ri, r.rank, t, 0)));
+        EQC_TRY(T.send(r, o, r.enc.as<uint8_t>() + (size_t)(2 * t + 1) * cap, bytes_of(ri, r.rank, t, 1)));
+        r.stats[0] += 1;
+      }
+      int t0, t1;
+      owned(r.rank, t0, t1);
+      for (int t = t0; t < t1; ++t)
+        for (int q = 0; q < n; ++q) {
+          if (q == r.rank) continue;
+          uint8_t *slot = r.dec.as<uint8_t>() + (size_t)(((t - t0) * n + q) * 2) * cap;
+          EQC_TRY(T.recv(r, q, slot, bytes_of(ri, q, t, 0)));
+          EQC_TRY(T.recv(r, q, slot + cap, bytes_of(ri, q, t, 1)));
+        }
+    }
+    EQC_TRY(T.end());
+  }
+  // (5) the owner composites its tiles, n partials in rank order (R-C5)
+  for (RankState *r : ranks) {
+    int t0, t1;
+    owned(r->rank, t0, t1);
+    for (int t = t0; t < t1; ++t) {
+      const TileRect &q = tr[t];
+      uint32_t *out = g.out + (size_t)q.y0 * g.out_pitch + q.x0;
+      std::vector<const uint8_t *> cs(n), ds(n);
+      for (int k = 0; k < n; ++k) {
+        const uint8_t *base = k == r->rank ? r->enc.as<uint8_t>() + (size_t)(2 * t) * cap
+                                           : r->dec.as<uint8_t>() + (size_t)(((t - t0) * n + k) * 2) * cap;
+        cs[k] = base;
+        ds[k] = base + cap;
+      }
+      if (rle) {
+        const std::vector<int64_t> cb(n, cap), db(n, cap);
+        EQC_TRY(compositor_depth_rle(n, cs.data(), ds.data(), cb.data(), db.data(), q.w, q.h, out, nullptr,
+                                     g.out_pitch, r->status.as<int32_t>(), s));
+      } else {
+        std::vector<const uint32_t *> c(n), d(n);
+        for (int k = 0; k < n; ++k) {
+          c[k] = reinterpret_cast<const uint32_t *>(cs[k]);
+          d[k] = reinterpret_cast<const uint32_t *>(ds[k]);
+        }
+        EQC_TRY(compositor_depth(n, c.data(), d.data(), q.w, q.h, q.w, out, nullptr, g.out_pitch, s));
+      }
+    }
+  }
+  return EQC_OK;
+}
+
 int run_binary_swap(std::vector<RankState *> &ranks, Geometry &g, Transport &T, cudaStream_t s) {
   std::vector<std::vector<BsRound>> plans(ranks.size());
   int k = 0;
@@ -2327,6 +2515,89 @@ static int compose_local(Algo algo, int nranks, int n_local, const uint32_t *con
            : algo == kSwap23     ? run_swap23(ranks, g, T, s)
                                  : run_stream(ranks, g, T, s);
   cudaStreamSynchronize(s);  // scratch is freed below
+  if (out_stats) {
+    for (int i = 0; i < 4; ++i) out_stats[i] = 0;
+    for (auto &st : states)
+      for (int i = 0; i < 4; ++i) out_stats[i] += st.stats[i];
+  }
+  for (auto &st : states) st.release();
+  return rc;
+}
+
+static int tiles_validate(int nranks, int n_local, const void *color, const void *depth, int w, int h, int64_t pitch,
+                          int tiles_x, int tiles_y, int flags, const void *out, int64_t out_pitch) {
+  if (nranks < 1 || n_local < 1 || n_local > EQC_MAX_SOURCES || nranks > EQC_MAX_SOURCES) return EQC_E_INVALID;
+  if (!color || !depth || w <= 0 || h <= 0 || pitch < w || !out || out_pitch < w) return EQC_E_INVALID;
+  if (tiles_x < 1 || tiles_y < 1 || tiles_x > w || tiles_y > h || (int64_t)tiles_x * tiles_y > 4096)
+    return EQC_E_INVALID;
+  if (flags & ~EQC_FLAG_RLE) return EQC_E_INVALID;
+  return EQC_OK;
+}
+
+static Geometry tiles_geometry(int nranks, int n_local, int w, int h, int64_t pitch, int flags, uint32_t *out,
+                               int64_t out_pitch) {
+  Geometry g;
+  g.n = nranks;
+  g.n_local = n_local;
+  g.w = w;
+  g.h = h;
+  g.pitch = pitch;
+  g.op = EQC_OP_DEPTH;
+  g.flags = flags;
+  g.out = out;
+  g.out_pitch = out_pitch;
+  return g;
+}
+
+extern "C" int eqc_plan_tiles(int w, int h, int tiles_x, int tiles_y, int nranks, int tile, int *rect) {
+  if (w <= 0 || h <= 0 || tiles_x < 1 || tiles_y < 1 || tiles_x > w || tiles_y > h || nranks < 1 || !rect ||
+      tile < 0 || tile >= tiles_x * tiles_y)
+    return EQC_E_INVALID;
+  const TileRect r = plan_tile(w, h, tiles_x, tiles_y, nranks, tile);
+  rect[0] = r.x0, rect[1] = r.y0, rect[2] = r.w, rect[3] = r.h, rect[4] = r.owner;
+  return EQC_OK;
+}
+
+extern "C" int compose_tiles(eqc_comm *comm, int n_local, const uint32_t *const *color, const uint32_t *const *depth,
+                             int w, int h, int64_t pitch, int tiles_x, int tiles_y, int flags, uint32_t *out_color,
+                             int64_t out_pitch, void *stream) {
+  if (!comm) return EQC_E_INVALID;
+  EQC_TRY(tiles_validate(comm->nranks, n_local, color, depth, w, h, pitch, tiles_x, tiles_y, flags, out_color,
+                         out_pitch));
+  Geometry g = tiles_geometry(comm->nranks, n_local, w, h, pitch, flags, out_color, out_pitch);
+  comm->st.color = color;
+  comm->st.depth = depth;
+  cudaStream_t s = (cudaStream_t)stream;
+  NcclTransport T(comm->nccl, s);
+  std::vector<RankState *> ranks{&comm->st};
+  return run_tiles(ranks, g, T, s, tiles_x, tiles_y);
+}
+
+extern "C" int compose_tiles_local(int nranks, int n_local, const uint32_t *const *color,
+                                   const uint32_t *const *depth, int w, int h, int64_t pitch, int tiles_x,
+                                   int tiles_y, int flags, uint32_t *out_color, int64_t out_pitch,
+                                   int64_t *out_stats, void *stream) {
+  EQC_TRY(tiles_validate(nranks, n_local, color, depth, w, h, pitch, tiles_x, tiles_y, flags, out_color, out_pitch));
+  Geometry g = tiles_geometry(nranks, n_local, w, h, pitch, flags, out_color, out_pitch);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<RankState> states(nranks);
+  std::vector<RankState *> ranks;
+  for (int q = 0; q < nranks; ++q) {
+    states[q].rank = q;
+    states[q].color = color + (size_t)q * n_local;
+    states[q].depth = depth + (size_t)q * n_local;
+    ranks.push_back(&states[q]);
+  }
+  LocalTransport T(s);
+  int rc = run_tiles(ranks, g, T, s, tiles_x, tiles_y);
+  cudaStreamSynchronize(s);
+  if (rc == EQC_OK) {
+    for (auto &st : states) {
+      int32_t bad = 0;
+      if (st.status.p) cudaMemcpy(&bad, st.status.p, sizeof(bad), cudaMemcpyDeviceToHost);
+      if (bad) rc = EQC_E_CORRUPT;
+    }
+  }
   if (out_stats) {
     for (int i = 0; i < 4; ++i) out_stats[i] = 0;
     for (auto &st : states)

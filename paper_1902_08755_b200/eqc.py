@@ -74,6 +74,9 @@ def _load():
         "compose_direct_send_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, i32, P, i64, P, P], i32),
         "compose_direct_send_rle_pull_local": ([i32, i32, P, i64, i32, i32, i32, P, i64, P, P, P], i32),
         "compose_binary_swap_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
+        "compose_tiles": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
+        "compose_tiles_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
+        "eqc_plan_tiles": ([i32, i32, i32, i32, i32, i32, P], i32),
         "eqc_comm_check": ([P, P], i32),
         "eqc_comm_abort": ([P], i32),
         "eqc_plan_bands": ([i32, i32, P], i32),
@@ -440,6 +443,36 @@ def compose_direct_send_p2p_local(nranks, colors, depths, out_color, dest_rank: 
                                             _ptrs(depths) if depths is not None else None, w, h, pitch, op, flags,
                                             mode, dest_rank, _addr(out_color), opitch, stats, _stream(stream))
     _check(rc, "compose_direct_send_p2p_local")
+    return list(stats)
+
+
+def plan_tiles(w: int, h: int, tiles_x: int, tiles_y: int, nranks: int, tile: int):
+    """(x0, y0, w, h, owner) of a display-wall tile (eqc_plan_tiles)."""
+    r = (ctypes.c_int * 5)()
+    _check(_lib.eqc_plan_tiles(w, h, tiles_x, tiles_y, nranks, tile, r), "eqc_plan_tiles")
+    return tuple(r)
+
+
+def compose_tiles(comm, colors, depths, out_color, tiles_x: int = 6, tiles_y: int = 4, flags: int = FLAG_RLE,
+                  stream=None):
+    """Display-wall direct send (c5): every rank writes the tiles it owns into out_color."""
+    w, h, pitch = _frame_geom(colors[0])
+    opitch = _frame_geom(out_color)[2]
+    return _check(_lib.compose_tiles(comm.handle, len(colors), _ptrs(colors), _ptrs(depths), w, h, pitch, tiles_x,
+                                     tiles_y, flags, _addr(out_color), opitch, _stream(stream)), "compose_tiles")
+
+
+def compose_tiles_local(nranks, colors, depths, out_color, tiles_x: int = 6, tiles_y: int = 4,
+                        flags: int = FLAG_RLE, stream=None):
+    """compose_tiles for virtual ranks on one GPU; returns summed traffic counters."""
+    total = len(colors)
+    assert total % nranks == 0
+    w, h, pitch = _frame_geom(colors[0])
+    opitch = _frame_geom(out_color)[2]
+    stats = (ctypes.c_int64 * 4)()
+    rc = _lib.compose_tiles_local(nranks, total // nranks, _ptrs(colors), _ptrs(depths), w, h, pitch, tiles_x,
+                                  tiles_y, flags, _addr(out_color), opitch, stats, _stream(stream))
+    _check(rc, "compose_tiles_local")
     return list(stats)
 
 

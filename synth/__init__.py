@@ -262,3 +262,72 @@ def structured_planes(seed: int, count: int, max_len: int = 128):
             b = rng.integers(0, 2, size=L)
         out.append(bytes(np.asarray(b, dtype=np.uint8).tolist()))
     return out
+
+
+def depth_sources_torch(seed: int, n: int, w: int, h: int, F: float = 0.3, noise_bits: int = 1,
+                        device="cuda", indices=None):
+    """The depth_sources recipe ("scattered" mode) generated ON THE GPU with
+    torch, for the display-wall workload (config c5: 64 sources of
+    15360x5760, 45 GB -- too large to draw on the host).  Same structure and
+    parameter draws (footprint of 6 ellipses covering ~F, 32 fragment ellipses
+    per source with planar depth and shaded colour, source-local z-buffer);
+    the per-pixel noise comes from a torch generator seeded per fragment, so
+    the frames differ from depth_sources' bit for bit but are a deterministic
+    function of (seed, n, w, h, F, noise_bits).  Returns (colors, depths):
+    lists of [H, W] int32 CUDA tensors (uint32 bit patterns) for the sources in
+    `indices` (default all n).
+    """
+    import torch
+    fp_np = footprint(seed, w, h, F)
+    fp_idx = np.flatnonzero(fp_np)
+    fp_area = float(fp_idx.size)
+    fp = torch.from_numpy(fp_np).to(device)
+    colors, depths = [], []
+    for i in (range(n) if indices is None else indices):
+        rng = np.random.default_rng([seed, 1, i])
+        dep = torch.full((h, w), 0xFFFFFFFF, dtype=torch.int64, device=device)
+        col = torch.zeros((h, w), dtype=torch.int64, device=device)
+        cov = float(rng.uniform(1.0 / math.sqrt(max(n, 1)), 1.0))
+        frag_area = cov * fp_area / 32.0 * 1.2
+        for f in range(32):
+            c = int(fp_idx[int(rng.integers(0, fp_idx.size))])
+            cy, cx = c // w + 0.5, c % w + 0.5
+            aspect = float(rng.uniform(0.4, 2.5))
+            rx = max(math.sqrt(frag_area * aspect / math.pi), 1.0)
+            ry = max(math.sqrt(frag_area / aspect / math.pi), 1.0)
+            x0 = max(0, int(math.floor(cx - rx)))
+            x1 = min(w, int(math.ceil(cx + rx)) + 1)
+            y0 = max(0, int(math.floor(cy - ry)))
+            y1 = min(h, int(math.ceil(cy + ry)) + 1)
+            z0 = int(rng.integers(1 << 28, 0xE0000000))
+            gx = int(rng.integers(-(1 << 16), (1 << 16) + 1))
+            gy = int(rng.integers(-(1 << 16), (1 << 16) + 1))
+            base = rng.integers(32, 256, size=3)
+            nseed = int(rng.integers(0, 1 << 62))
+            if x0 >= x1 or y0 >= y1:
+                continue
+            ys = (torch.arange(y0, y1, device=device, dtype=torch.float64)[:, None] + 0.5 - cy) / ry
+            xs = (torch.arange(x0, x1, device=device, dtype=torch.float64)[None, :] + 0.5 - cx) / rx
+            r2 = xs * xs + ys * ys
+            m = (r2 <= 1.0) & fp[y0:y1, x0:x1]
+            dx = torch.arange(x0, x1, device=device, dtype=torch.int64)[None, :] - int(cx)
+            dy = torch.arange(y0, y1, device=device, dtype=torch.int64)[:, None] - int(cy)
+            z = torch.clamp(z0 + gx * dx + gy * dy, 0, 0xFFFFFFFE)
+            shade = 1.0 - 0.5 * torch.clamp(r2, 0.0, 1.0)
+            rgb = [torch.clamp(torch.floor(float(b) * shade), 0, 255).to(torch.int64) for b in base]
+            if noise_bits:
+                nmask = (1 << noise_bits) - 1
+                g = torch.Generator(device=device)
+                g.manual_seed(nseed)
+                nz = torch.randint(0, 1 << 30, (y1 - y0, x1 - x0), generator=g, device=device, dtype=torch.int64)
+                rgb = [(ch & ~nmask) | ((nz >> (8 * k)) & nmask) for k, ch in enumerate(rgb)]
+            pix = rgb[0] | (rgb[1] << 8) | (rgb[2] << 16) | 0xFF000000
+            sub_d = dep[y0:y1, x0:x1]
+            win = m & (z < sub_d)
+            sub_d.copy_(torch.where(win, z, sub_d))
+            sub_c = col[y0:y1, x0:x1]
+            sub_c.copy_(torch.where(win, pix, sub_c))
+        colors.append((col - ((col >> 31) << 32)).to(torch.int32))  # uint32 bit patterns as int32
+        depths.append((dep - ((dep >> 31) << 32)).to(torch.int32))
+        del dep, col
+    return colors, depths
