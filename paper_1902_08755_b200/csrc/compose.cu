@@ -2580,12 +2580,22 @@ extern "C" int compose_tiles_local(int nranks, int n_local, const uint32_t *cons
   EQC_TRY(tiles_validate(nranks, n_local, color, depth, w, h, pitch, tiles_x, tiles_y, flags, out_color, out_pitch));
   Geometry g = tiles_geometry(nranks, n_local, w, h, pitch, flags, out_color, out_pitch);
   cudaStream_t s = (cudaStream_t)stream;
-  std::vector<RankState> states(nranks);
+  // the virtual ranks' scratch (GBs at wall size) is kept for the next call
+  // with the same number of ranks (EQC_TILES_LOCAL_KEEP=0: freed every call)
+  static std::vector<RankState> states;
+  static const bool keep = !getenv("EQC_TILES_LOCAL_KEEP") || atoi(getenv("EQC_TILES_LOCAL_KEEP")) != 0;
+  if ((int)states.size() != nranks) {
+    cudaStreamSynchronize(s);
+    for (auto &st : states) st.release();
+    states.clear();
+    states.resize(nranks);
+  }
   std::vector<RankState *> ranks;
   for (int q = 0; q < nranks; ++q) {
     states[q].rank = q;
     states[q].color = color + (size_t)q * n_local;
     states[q].depth = depth + (size_t)q * n_local;
+    if (states[q].status.p) cudaMemsetAsync(states[q].status.p, 0, sizeof(int32_t), s);
     ranks.push_back(&states[q]);
   }
   LocalTransport T(s);
@@ -2603,7 +2613,10 @@ extern "C" int compose_tiles_local(int nranks, int n_local, const uint32_t *cons
     for (auto &st : states)
       for (int i = 0; i < 4; ++i) out_stats[i] += st.stats[i];
   }
-  for (auto &st : states) st.release();
+  if (!keep || rc != EQC_OK) {
+    for (auto &st : states) st.release();
+    states.clear();
+  }
   return rc;
 }
 
