@@ -25,11 +25,10 @@
 // four byte stores at the lane's prefix offset; the token starts likewise
 // (256-entry table indexed by the T and R nibbles) into a start list, from
 // which one lane per token derives the ctrl byte (length = next start -
-// start).  Byte stores run from the highest byte down: a lane writes all four
-// bytes even when it owns fewer, and every byte it does not own lies at a
-// higher offset that its owner writes later (lanes that own none store
-// nothing).  The few bytes past a region's end are rewritten by the next
-// region in program order (see code_chunk).
+// start).  A lane writes all four bytes of its compacted word even when it
+// owns fewer; the stores go in four byte-index phases, highest first, with
+// __syncwarp between them, so every byte's owner writes it after any garbage
+// aimed at it (see code_chunk).
 #pragma once
 
 #include "eqc_common.cuh"
@@ -102,26 +101,6 @@ __device__ __forceinline__ uint32_t eq_bytes01(uint32_t a, uint32_t b, uint32_t 
 }
 
 __device__ __forceinline__ int bytei(uint32_t v, int p) { return (int)__byte_perm(v, 0u, 0x4440u + (uint32_t)p); }
-
-// Ordered shared-memory byte stores (volatile: ptxas keeps their order; asm
-// volatile + memory clobber: so does the compiler, also relative to the
-// surrounding plain accesses).
-__device__ __forceinline__ void sts_u8(uint8_t *a, uint32_t v) {
-  asm volatile("st.volatile.shared.u8 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(a)), "r"(v) : "memory");
-}
-// If `pred`: the four bytes of v at a[0..3], highest address first
-// (predicated, no branch).
-__device__ __forceinline__ void sts_u8x4_desc_if(uint8_t *a, uint32_t v, uint32_t pred) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(a);
-  asm volatile(
-      "{\n\t.reg .b32 t;\n\t.reg .pred q;\n\t"
-      "setp.ne.u32 q, %2, 0;\n\t"
-      "shr.b32 t, %1, 24;\n\t@q st.volatile.shared.u8 [%0+3], t;\n\t"
-      "shr.b32 t, %1, 16;\n\t@q st.volatile.shared.u8 [%0+2], t;\n\t"
-      "shr.b32 t, %1, 8;\n\t@q st.volatile.shared.u8 [%0+1], t;\n\t"
-      "@q st.volatile.shared.u8 [%0], %1;\n\t}" ::"r"(s), "r"(v), "r"(pred)
-      : "memory");
-}
 
 // Inclusive warp prefix sum (shuffle with the in-range predicate: no select).
 __device__ __forceinline__ uint32_t scan_add(uint32_t v) {
@@ -216,23 +195,32 @@ __device__ __forceinline__ int code_chunk(const uint32_t x[4], int L, int lane, 
     pw[2] = __byte_perm(c, d, 0x5410);
     pw[3] = __byte_perm(c, d, 0x7632);
   }
-  // ---- payload bytes and token starts, plane by plane (ascending: a plane's
-  // trailing garbage lands in the next plane's header / start list, which is
-  // written afterwards).  The table reads go first; the byte stores are
-  // ordered asm (the compiler must not reorder them: the cross-lane overwrite
-  // order is the point).
-  uint32_t sel[4], sv[4];
+  // ---- payload bytes and token starts.  A lane owning c >= 1 bytes of a
+  // region writes all four bytes of its compacted word at its prefix offset;
+  // the 4 - c it does not own belong to lanes (or, past the region's end, to
+  // the next plane's header / start list / payload) that write them at a
+  // LOWER byte index j.  So the stores go in four phases, j = 3, 2, 1, 0,
+  // every plane's bytes j in phase j, __syncwarp between phases: each byte's
+  // owner writes it after any garbage aimed at it.  (Lanes owning nothing
+  // store nothing: two lanes never write one byte in the same phase.)
+  uint32_t cw[4], sv[4];
+  uint8_t *pa[4], *pb[4];
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    sel[p] = *reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(lut_sel) + bytei(iE, p));
-    sv[p] = lut_st[bytei(iTR, p)] + k.p4;
+    const uint32_t sel = *reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(lut_sel) + bytei(iE, p));
+    cw[p] = __byte_perm(pw[p], 0u, sel);                     // payload bytes, compacted by E
+    sv[p] = lut_st[bytei(iTR, p)] + k.p4;                    // token starts (+ REPEAT flag), compacted by T
+    pa[p] = rec + off[p] + 1 + nt[p] + bytei(exE, p);        // record byte off + 1 + ntok + (E prefix)
+    pb[p] = tp + P[p] + p + bytei(exT, p);                   // start-list entry P + p + (T prefix)
   }
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    // payload: record byte off[p] + 1 + nt[p] + (E prefix)
-    sts_u8x4_desc_if(rec + off[p] + 1 + nt[p] + bytei(exE, p), __byte_perm(pw[p], 0u, sel[p]), cE & (0xFFu << (8 * p)));
-    // token starts: start list entry P[p] + p + (T prefix)
-    sts_u8x4_desc_if(tp + P[p] + p + bytei(exT, p), sv[p], cT & (0xFFu << (8 * p)));
+  for (int j = 3; j >= 0; --j) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      if (cE & (0xFFu << (8 * p))) pa[p][j] = (uint8_t)(cw[p] >> (8 * j));
+      if (cT & (0xFFu << (8 * p))) pb[p][j] = (uint8_t)(sv[p] >> (8 * j));
+    }
+    __syncwarp();
   }
   // sentinel after each plane's starts (the end of its last token) and the
   // ntok bytes
@@ -241,8 +229,8 @@ __device__ __forceinline__ int code_chunk(const uint32_t x[4], int L, int lane, 
     if (lane == 1) sp = P[2] + 1, ro = off[1], n = nt[1];
     if (lane == 2) sp = P[3] + 2, ro = off[2], n = nt[2];
     if (lane == 3) sp = ntot + 3, ro = off[3], n = nt[3];
-    sts_u8(tp + sp, (uint32_t)L);
-    sts_u8(rec + ro, (uint32_t)n);
+    tp[sp] = (uint8_t)L;
+    rec[ro] = (uint8_t)n;
   }
   __syncwarp();
   // ---- ctrl bytes: token q of the concatenated start lists (plane p's start
