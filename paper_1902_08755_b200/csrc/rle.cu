@@ -668,11 +668,17 @@ struct Cmp3Params {
 };
 
 constexpr int kCmp3Warps = 8;
+#ifndef EQC_CMP_REVERSE
+#define EQC_CMP_REVERSE 1
+#endif
 
 __global__ void __launch_bounds__(kCmp3Warps * 32) rle_compact3_kernel(const __grid_constant__ Cmp3Params p) {
   const int lane = threadIdx.x & 31;
-  const int64_t gr = (int64_t)blockIdx.x * kCmp3Warps + (threadIdx.x >> 5);
-  if (gr >= (int64_t)p.count * p.R) return;
+  const int64_t gq = (int64_t)blockIdx.x * kCmp3Warps + (threadIdx.x >> 5);
+  if (gq >= (int64_t)p.count * p.R) return;
+  // EQC_CMP_REVERSE: the images coded last (whose scratch is the most likely
+  // to be still in L2) first
+  const int64_t gr = EQC_CMP_REVERSE ? (int64_t)p.count * p.R - 1 - gq : gq;
   const int m = (int)(gr / p.R), r = (int)(gr - (int64_t)m * p.R);
   const EncImage im = p.img[m];
   const int nch = (int)p.nchunks;
