@@ -41,13 +41,15 @@ def main():
     ap.add_argument("tag")
     ap.add_argument("--rep")
     ap.add_argument("--launches")
+    ap.add_argument("--max-id", type=int, default=None,
+                    help="launch list: only IDs <= this (e.g. the bench's headline workload, before its anchors)")
     a = ap.parse_args()
     rep = a.rep or os.path.join(ROOT, "gpurun_out", f"prof_{a.tag}.ncu-rep")
     launches = a.launches or os.path.join(ROOT, "gpurun_out", f"launches_{a.tag}.csv")
     lines = [f"# ncu summary `{a.tag}`", "",
-             "Captured under gpurun on one B200 with `--clock-control none` (scripts/gpu_prof.sh running "
-             "scripts/prof_step.py: 8 x 3840x2160 sources, encode batch -> fused decode+composite, plain "
-             "decode batch, plain depth composite, 16-brick blend). Per-launch times under ncu are cold-cache "
+             "Captured under gpurun on one B200 with `--clock-control none`. Launch list: "
+             f"`{os.path.relpath(launches, ROOT)}`" + (f" (IDs <= {a.max_id})" if a.max_id is not None else "") +
+             "; full capture: " f"`{os.path.relpath(rep, ROOT)}`" ". Per-launch times under ncu are cold-cache "
              "and serialised: compare SHARES, not absolutes.", ""]
     traffic = {}
     if os.path.exists(launches):
@@ -57,6 +59,8 @@ def main():
         ki, mi, vi, idi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("ID")
         per = collections.OrderedDict()
         for r in rows[hi + 1:]:
+            if a.max_id is not None and int(r[idi]) > a.max_id:
+                continue
             per.setdefault((int(r[idi]), short(r[ki])), {})[r[mi]] = float(r[vi].replace(",", ""))
         lines += ["## Launch list (gpu__time_duration, dram bytes)", "",
                   "| ID | kernel | time us | DRAM read MB | DRAM write MB |", "|---|---|---|---|---|"]
@@ -122,7 +126,9 @@ def main():
             if k.startswith("at::"):
                 continue  # torch setup kernels (workspace zero-fill), not timed
             old[k] = v
-        if "rle_encode_kernel" in base:
+        if "rle_encode3_kernel" in base:  # round 2: encoder + compaction
+            old["image_compress_rle_batch"] = sum(base.get(k, 0) for k in ("rle_encode3_kernel", "rle_compact3_kernel"))
+        elif "rle_encode_kernel" in base:
             old["image_compress_rle_batch"] = sum(base.get(k, 0) for k in
                                                   ("rle_encode_kernel", "rle_runscan_kernel", "rle_compact_kernel"))
         if "depth_rle_kernel" in base:
