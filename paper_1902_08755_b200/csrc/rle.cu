@@ -674,12 +674,12 @@ constexpr int kCmp3Warps = 8;
 
 __global__ void __launch_bounds__(kCmp3Warps * 32) rle_compact3_kernel(const __grid_constant__ Cmp3Params p) {
   const int lane = threadIdx.x & 31;
-  const int64_t gq = (int64_t)blockIdx.x * kCmp3Warps + (threadIdx.x >> 5);
-  if (gq >= (int64_t)p.count * p.R) return;
-  // EQC_CMP_REVERSE: the images coded last (whose scratch is the most likely
-  // to be still in L2) first
-  const int64_t gr = EQC_CMP_REVERSE ? (int64_t)p.count * p.R - 1 - gq : gq;
-  const int m = (int)(gr / p.R), r = (int)(gr - (int64_t)m * p.R);
+  // grid (runs / kCmp3Warps, images); EQC_CMP_REVERSE: the images coded last
+  // (whose scratch is the most likely to be still in L2) first
+  const int r = blockIdx.x * kCmp3Warps + (threadIdx.x >> 5);
+  if (r >= p.R) return;
+  const int m = EQC_CMP_REVERSE ? p.count - 1 - (int)blockIdx.y : (int)blockIdx.y;
+  const int64_t gr = (int64_t)m * p.R + r;
   const EncImage im = p.img[m];
   const int nch = (int)p.nchunks;
   const int c0 = r * kRun3, cnt = min(kRun3, nch - c0);
@@ -1644,7 +1644,8 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
       c.h = h;
       c.R = R;
       c.NB = NB;
-      rle_compact3_kernel<<<(unsigned)(((int64_t)gc * R + kCmp3Warps - 1) / kCmp3Warps), kCmp3Warps * 32, 0, st>>>(c);
+      rle_compact3_kernel<<<dim3((unsigned)((R + kCmp3Warps - 1) / kCmp3Warps), (unsigned)gc), kCmp3Warps * 32, 0,
+                            st>>>(c);
     }
     return eqc_launch_status();
   }
