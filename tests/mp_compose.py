@@ -80,7 +80,10 @@ def main():
             failures.append(f"{algo}: rank {rank} sent {st[0]} band messages, want {world - 1}")
         dist.barrier()
     # application-provided source ROIs, P2P and NCCL transports
-    for nl, w, h, dest, fl in [(2, 640, 361, 0, 0), (1, 300, 41, world - 1, X), (2, 1920, 1080, 1 % world, 0)]:
+    # (the 7680x4320, 2-per-rank case takes the pipelined peer-memory branch:
+    # >= 2 sources and >= 6 Mpx per band)
+    for nl, w, h, dest, fl in [(2, 640, 361, 0, 0), (1, 300, 41, world - 1, X), (2, 1920, 1080, 1 % world, 0),
+                               (2, 7680, 4320, 0, 0)]:
         N = world * nl
         c, d = synth.depth_sources(synth.SEED_BASE + 90 + N + w, N, w, h, mode="compact")
         mine = range(rank * nl, (rank + 1) * nl)
