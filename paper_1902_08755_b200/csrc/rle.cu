@@ -448,7 +448,7 @@ constexpr int kE3Warps = EQC_E3_WARPS;
 
 struct E3Warp {
   uint8_t span[kRun3 * kRecMax + 16];    // the run's records (+ garbage slack)
-  uint8_t tp[(eqc_enc::kTpBytes + 15) & ~15];
+  uint8_t tp[(eqc_enc::kTpBytes + 4 + 15) & ~15];  // start list + trash bytes
   uint32_t cps[kRun3];
   uint16_t csz[kRun3];
   uint8_t q[kRun3];

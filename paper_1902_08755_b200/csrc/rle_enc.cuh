@@ -121,6 +121,7 @@ __device__ __forceinline__ uint32_t scan_add(uint32_t v) {
 // per-warp shared scratch of >= kTpBytes.  Returns the record size; *psizes =
 // the four plane record sizes (byte p = plane p).
 constexpr int kTpBytes = 4 * kC + 4 + 4;
+constexpr int kTrashOff = kTpBytes;       // 4 trash bytes after the start list (tp must hold kTpBytes + 4)
 
 template <bool FULL>
 __device__ __forceinline__ int code_chunk(const uint32_t x[4], int L, int lane, const LaneK &k, uint8_t *rec,
@@ -202,23 +203,27 @@ __device__ __forceinline__ int code_chunk(const uint32_t x[4], int L, int lane, 
   // LOWER byte index j.  So the stores go in four phases, j = 3, 2, 1, 0,
   // every plane's bytes j in phase j, __syncwarp between phases: each byte's
   // owner writes it after any garbage aimed at it.  (Lanes owning nothing
-  // store nothing: two lanes never write one byte in the same phase.)
+  // store into a trash word: two lanes never write one real byte in the same
+  // phase.)
   uint32_t cw[4], sv[4];
   uint8_t *pa[4], *pb[4];
+  uint8_t *const trash = tp + kTrashOff;
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const uint32_t sel = *reinterpret_cast<const uint32_t *>(reinterpret_cast<const uint8_t *>(lut_sel) + bytei(iE, p));
     cw[p] = __byte_perm(pw[p], 0u, sel);                     // payload bytes, compacted by E
     sv[p] = lut_st[bytei(iTR, p)] + k.p4;                    // token starts (+ REPEAT flag), compacted by T
-    pa[p] = rec + off[p] + 1 + nt[p] + bytei(exE, p);        // record byte off + 1 + ntok + (E prefix)
-    pb[p] = tp + P[p] + p + bytei(exT, p);                   // start-list entry P + p + (T prefix)
+    // a lane owning no byte of a region writes into the trash bytes instead
+    // (no predicate per store)
+    pa[p] = (cE & (0xFFu << (8 * p))) ? rec + off[p] + 1 + nt[p] + bytei(exE, p) : trash;  // off + 1 + ntok + E prefix
+    pb[p] = (cT & (0xFFu << (8 * p))) ? tp + P[p] + p + bytei(exT, p) : trash;              // P + p + T prefix
   }
 #pragma unroll
   for (int j = 3; j >= 0; --j) {
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      if (cE & (0xFFu << (8 * p))) pa[p][j] = (uint8_t)(cw[p] >> (8 * j));
-      if (cT & (0xFFu << (8 * p))) pb[p][j] = (uint8_t)(sv[p] >> (8 * j));
+      pa[p][j] = (uint8_t)(cw[p] >> (8 * j));
+      pb[p][j] = (uint8_t)(sv[p] >> (8 * j));
     }
     __syncwarp();
   }
