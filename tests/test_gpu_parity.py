@@ -457,3 +457,48 @@ def test_encoder_workspace_any_8_byte_alignment(eqc):
             want = oracle.rle_encode(img, kind=kinds[i], flags=flags[i])
             assert int(sizes[i].item()) == len(want), (off, i)
             assert bytes_of(streams[i], len(want)) == want, (off, i)
+
+
+def test_rle_large_image_offsets_beyond_2_30(eqc):
+    """A 16384 x 16384 noise image (1 GiB raw, incompressible: payload offsets
+    pass 2^30 and the table holds 2 M chunks) on the v1 path: the stream
+    decodes back to the image exactly, its size equals the oracle's size
+    formula for all-literal chunks, and sampled row bands re-encoded by the
+    oracle give the same table entries (rebased) and records."""
+    w = h = 16384
+    free = torch.cuda.mem_get_info()[0]
+    if free < 8 << 30:
+        pytest.skip("needs ~8 GB of free device memory")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(SEED + 80)
+    img = torch.randint(-(1 << 31), (1 << 31) - 1, (h, w), generator=g, device="cuda", dtype=torch.int64)
+    img = img.to(torch.int32)
+    cap = eqc.image_rle_max_size(w, h)
+    dst = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    d_size = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(eqc.image_rle_workspace_size(w, h), dtype=torch.uint8, device="cuda")
+    eqc.image_compress_rle(img, eqc.KIND_DEPTH32, 0, dst, d_size, ws)
+    torch.cuda.synchronize()
+    n = int(d_size.item())
+    S = (w + 127) // 128
+    nch = S * h
+    assert n > (1 << 30) + 32 + 8 * nch
+    out = torch.empty_like(img)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    eqc.image_decompress_rle(dst, out, status, src_bytes=n)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    assert torch.equal(out, img)
+    del out
+    table = dst[32:32 + 8 * nch].view(torch.int32).view(nch, 2)
+    for y in (0, 1, h // 2, h - 1):
+        band = img[y:y + 1].cpu().numpy().view(np.uint32)
+        want = oracle.rle_encode(np.ascontiguousarray(band), kind=1, flags=0)
+        wtab = np.frombuffer(want[32:32 + 8 * S], dtype=np.uint32).reshape(S, 2)
+        gtab = table[y * S:(y + 1) * S].cpu().numpy().view(np.uint32)
+        base = int(gtab[0, 0])
+        np.testing.assert_array_equal(gtab[:, 1], wtab[:, 1])
+        np.testing.assert_array_equal(gtab[:, 0] - base, wtab[:, 0])
+        payload = 32 + 8 * nch + base
+        rec = bytes_of(dst[payload:], len(want) - 32 - 8 * S)
+        assert rec == want[32 + 8 * S:], y
