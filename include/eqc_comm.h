@@ -238,8 +238,10 @@ EQC_API int compose_binary_swap_local(int nranks, int n_local, const uint32_t *c
  * k parts at y0 + floor(u (y1 - y0) / k); digit t keeps part t, receives it
  * from the k - 1 other members and composites the k partials in rank order.
  * For a power of two this is binary swap.  Final regions are gathered on
- * dest_rank.  All ops and flags of compose_direct_send except the
- * peer-memory path (NCCL transport).
+ * dest_rank.  All ops and flags of compose_direct_send; transport: peer
+ * memory (in-place merges reading the members over NVLink, as
+ * compose_binary_swap) when every rank maps every peer and neither
+ * EQC_FLAG_RLE nor EQC_FLAG_NCCL is set, else NCCL.
  * eqc_plan_swap23 -- the plan of `rank` as ints: {fold_role (0 none, 1
  *   receiver, 2 sender), fold_partner, k rounds, final_y0, final_y1}, then per
  *   round {radix, digit, member[3] (-1 padded), bound[4]}; returns k.
@@ -365,6 +367,18 @@ EQC_API int compose_binary_swap_p2p_local(int nranks, int n_local, const uint32_
                                           const uint32_t *const *depth, int w, int h, int64_t pitch, int op,
                                           int flags, int dest_rank, uint32_t *out_color, int64_t out_pitch,
                                           int64_t *out_stats, void *stream);
+
+/*
+ * compose_swap23_p2p_local -- the peer-memory 2-3 swap (the default transport
+ * of compose_swap23 when every rank maps every peer, no EQC_FLAG_RLE /
+ * EQC_FLAG_NCCL): the fold and each mixed-radix round merge in place, reading
+ * the other members' rows over NVLink; the last round writes into the
+ * destination's frame.  Virtual ranks on one GPU, any nranks >= 2.
+ */
+EQC_API int compose_swap23_p2p_local(int nranks, int n_local, const uint32_t *const *color,
+                                     const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                     int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                     void *stream);
 
 /*
  * compose_direct_send_rle_pull on ONE GPU (virtual ranks as above): rank q's

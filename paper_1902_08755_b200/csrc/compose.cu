@@ -1934,6 +1934,83 @@ int binary_swap_p2p(eqc_comm *c, const Geometry &g, const uint32_t *const *color
   return EQC_OK;
 }
 
+// Peer-memory 2-3 swap (R-C21): the fold and every mixed-radix
+// round merge in place, reading the other members' rows of this rank's part
+// straight out of their partial frames over NVLink (each member reads only
+// its own part's rows of the others, which nobody writes in that round); a
+// flag barrier before the fold, before every round and at the end; the last
+// round writes the final colour into the destination's frame.
+int swap23_p2p(eqc_comm *c, const Geometry &g, const uint32_t *const *color, const uint32_t *const *depth,
+               cudaStream_t s) {
+  P2PState &P = c->p2p;
+  const int n = c->nranks, me = c->rank;
+  int64_t *stats = c->st.stats;
+  for (int i = 0; i < 4; ++i) stats[i] = 0;
+  S23Plan plan;
+  if (plan_swap23(g.h, n, me, plan) < 0) return EQC_E_INVALID;
+  // rounds of the active ranks (the same for all of them; folded senders have none)
+  size_t nrounds = plan.rounds.size();
+  for (int q = 0; q < n; ++q) {
+    S23Plan o;
+    plan_swap23(g.h, n, q, o);
+    nrounds = std::max(nrounds, o.rounds.size());
+  }
+  uint32_t *pc = P.part_c.as<uint32_t>(), *pd = P.part_d.as<uint32_t>();
+  EQC_TRY(op_local(g, color, depth, pc, pd, s));
+  EQC_TRY(p2p_barrier(c, s));
+  if (plan.fold_role == 1) {  // lower rank of the pair: whole frames, own first (ties to it)
+    const uint32_t *cc[2] = {pc, P.peer_part_c[plan.fold_partner]};
+    const uint32_t *dd[2] = {pd, P.peer_part_d[plan.fold_partner]};
+    if (nrounds == 0) {
+      uint32_t *out = me == g.dest ? g.out : P.peer_fin_c[g.dest];
+      EQC_TRY(op_final(g, 2, cc, dd, g.h, out, me == g.dest ? g.out_pitch : g.w, s));
+    } else {
+      EQC_TRY(op_merge(g, 2, cc, dd, g.h, pc, pd, s));
+    }
+    stats[3] += (int64_t)g.h * g.w * 8;
+  } else if (plan.fold_role == 2) {
+    stats[0] += 1;
+  }
+  for (size_t rd = 0; rd < nrounds; ++rd) {
+    EQC_TRY(p2p_barrier(c, s));
+    if (rd >= plan.rounds.size()) continue;
+    const S23Round &R = plan.rounds[rd];
+    const int ky0 = R.bnd[R.t], rows = R.bnd[R.t + 1] - ky0;
+    stats[0] += R.k - 1;
+    if (rows <= 0) continue;
+    const size_t off = (size_t)ky0 * g.w;
+    const uint32_t *cc[3], *dd[3];
+    for (int u = 0; u < R.k; ++u) {  // members in rank order
+      const int q = R.members[u];
+      cc[u] = (u == R.t ? pc : P.peer_part_c[q]) + off;
+      dd[u] = (u == R.t ? pd : P.peer_part_d[q]) + off;
+    }
+    stats[3] += (int64_t)rows * g.w * 8 * (R.k - 1);
+    if (rd + 1 < nrounds) {
+      EQC_TRY(op_merge(g, R.k, cc, dd, rows, pc + off, pd + off, s));
+    } else {
+      uint32_t *out = me == g.dest ? g.out + (size_t)ky0 * g.out_pitch : P.peer_fin_c[g.dest] + off;
+      EQC_TRY(op_final(g, R.k, cc, dd, rows, out, me == g.dest ? g.out_pitch : g.w, s));
+      if (me != g.dest) {
+        stats[1] += 1;
+        stats[2] += (int64_t)rows * g.w * 4;
+      }
+    }
+  }
+  EQC_TRY(p2p_barrier(c, s));  // every final region is on the destination
+  if (me == g.dest && !(g.out == P.fin_c.as<uint32_t>() && g.out_pitch == g.w)) {
+    for (int q = 0; q < n; ++q) {
+      S23Plan o;
+      plan_swap23(g.h, n, q, o);
+      if (q == me || o.fy1 <= o.fy0) continue;
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(g.out + (size_t)o.fy0 * g.out_pitch, g.out_pitch * 4,
+                                     P.fin_c.as<uint32_t>() + (size_t)o.fy0 * g.w, (size_t)g.w * 4, (size_t)g.w * 4,
+                                     o.fy1 - o.fy0, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return EQC_OK;
+}
+
 }  // namespace
 
 extern "C" int eqc_comm_get_unique_id(uint8_t id[EQC_UNIQUE_ID_BYTES]) {
@@ -2367,6 +2444,33 @@ extern "C" int compose_binary_swap_p2p_local(int nranks, int n_local, const uint
   return V.join(s, out_stats);
 }
 
+extern "C" int compose_swap23_p2p_local(int nranks, int n_local, const uint32_t *const *color,
+                                        const uint32_t *const *depth, int w, int h, int64_t pitch, int op, int flags,
+                                        int dest_rank, uint32_t *out_color, int64_t out_pitch, int64_t *out_stats,
+                                        void *stream) {
+  EQC_TRY(validate(nranks, n_local, color, depth, w, h, pitch, op, flags, dest_rank, out_color, out_pitch, true));
+  if (nranks < 2 || (flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) return EQC_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  VirtualP2P V;
+  EQC_TRY(V.init(nranks, (int64_t)w * h, s));
+  for (int q = 0; q < nranks; ++q) {
+    Geometry g;
+    g.n = nranks;
+    g.n_local = n_local;
+    g.w = w;
+    g.h = h;
+    g.pitch = pitch;
+    g.op = op;
+    g.flags = flags;
+    g.dest = dest_rank;
+    g.out = q == dest_rank ? out_color : nullptr;
+    g.out_pitch = q == dest_rank ? out_pitch : w;
+    EQC_TRY(swap23_p2p(&V.c[q], g, color + (size_t)q * n_local, depth ? depth + (size_t)q * n_local : nullptr,
+                       V.st[q]));
+  }
+  return V.join(s, out_stats);
+}
+
 extern "C" int compose_direct_send_rle_pull_local(int nranks, int n_local, const uint8_t *const *rank_streams,
                                                   int64_t cap_bytes, int w, int h, int dest_rank,
                                                   uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
@@ -2455,9 +2559,10 @@ static int compose_nccl(Algo algo, eqc_comm *comm, int n_local, const uint32_t *
                                               : direct_send_p2p(comm, g, color, depth, s);
     }
   }
-  if (algo == kBinarySwap && comm->nranks > 1 && !(flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) {
+  if ((algo == kBinarySwap || algo == kSwap23) && comm->nranks > 1 && !(flags & (EQC_FLAG_RLE | EQC_FLAG_NCCL))) {
     EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
-    if (comm->p2p.capable == 1) return binary_swap_p2p(comm, g, color, depth, s);
+    if (comm->p2p.capable == 1)
+      return algo == kBinarySwap ? binary_swap_p2p(comm, g, color, depth, s) : swap23_p2p(comm, g, color, depth, s);
   }
   NcclTransport T(comm->nccl, s);
   std::vector<RankState *> ranks{&comm->st};

@@ -74,6 +74,7 @@ def _load():
         "compose_direct_send_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, i32, P, i64, P, P], i32),
         "compose_direct_send_rle_pull_local": ([i32, i32, P, i64, i32, i32, i32, P, i64, P, P, P], i32),
         "compose_binary_swap_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
+        "compose_swap23_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
         "compose_tiles": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
         "compose_tiles_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
         "eqc_plan_tiles": ([i32, i32, i32, i32, i32, i32, P], i32),
@@ -481,6 +482,13 @@ def compose_binary_swap_p2p_local(nranks, colors, depths, out_color, dest_rank: 
     """The peer-memory binary swap for virtual ranks on one GPU."""
     return _compose_local(_lib.compose_binary_swap_p2p_local, "compose_binary_swap_p2p_local", nranks, colors,
                           depths, out_color, dest_rank, flags, op, stream)
+
+
+def compose_swap23_p2p_local(nranks, colors, depths, out_color, dest_rank: int = 0, flags: int = 0,
+                             op: int = OP_DEPTH, stream=None):
+    """The peer-memory 2-3 swap for virtual ranks on one GPU."""
+    return _compose_local(_lib.compose_swap23_p2p_local, "compose_swap23_p2p_local", nranks, colors, depths,
+                          out_color, dest_rank, flags, op, stream)
 
 
 def compose_direct_send_rle_pull_local(nranks, n_local, rank_streams, cap_bytes, w, h, out_color, status,

@@ -209,3 +209,35 @@ def test_p2p_binary_swap_virtual_ranks(eqc, case):
         got = to_host(out)
         diff = np.abs(got.view(np.uint8).astype(int) - want.view(np.uint8).astype(int))
         assert diff.max() <= 1
+
+
+S23_CASES = [
+    # (nranks, n_local, w, h, dest, op, gen) -- 2-3 swap over peer memory (R-C21)
+    (3, 2, 300, 41, 0, "depth", "scene"),
+    (5, 1, 130, 37, 4, "depth", "ties"),
+    (6, 1, 257, 77, 2, "depth", "scene"),
+    (7, 2, 128, 45, 5, "depth", "ties"),
+    (2, 3, 200, 30, 1, "depth", "scene"),
+    (3, 4, 320, 180, 1, "blend", "bricks"),
+    (5, 2, 130, 37, 0, "blend", "bricks"),
+]
+
+
+@pytest.mark.parametrize("case", S23_CASES, ids=[f"n{c[0]}x{c[1]}_{c[2]}x{c[3]}_{c[5]}_d{c[4]}" for c in S23_CASES])
+def test_p2p_swap23_virtual_ranks(eqc, case):
+    nr, nl, w, h, dest, op, gen = case
+    N = nr * nl
+    out = out_frame(h, w)
+    if op == "depth":
+        c, d = _scene(N, w, h, synth.SEED_BASE + 99 + N + w, ties=gen == "ties")
+        want, _ = oracle.depth_composite(c, d)
+        eqc.compose_swap23_p2p_local(nr, [to_dev(x) for x in c], [to_dev(x) for x in d], out, dest_rank=dest)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(to_host(out), want)
+    else:
+        layers = synth.volume_bricks(synth.SEED_BASE + 100 + N, N, w, h)
+        want = oracle.blend_ordered(layers)
+        eqc.compose_swap23_p2p_local(nr, [to_dev(x) for x in layers], None, out, dest_rank=dest, op=eqc.OP_BLEND)
+        torch.cuda.synchronize()
+        diff = np.abs(to_host(out).view(np.uint8).astype(int) - want.view(np.uint8).astype(int))
+        assert diff.max() <= 1
