@@ -64,10 +64,11 @@ def main():
                 ("direct_send_nccl", eqc.compose_direct_send, eqc.FLAG_NCCL),
                 ("direct_send_rle", eqc.compose_direct_send, eqc.FLAG_RLE)]
     if n & (n - 1) == 0:
-        variants += [("binary_swap_nccl", eqc.compose_binary_swap, 0),
+        variants += [("binary_swap_p2p", eqc.compose_binary_swap, 0),
+                     ("binary_swap_nccl", eqc.compose_binary_swap, eqc.FLAG_NCCL),
                      ("binary_swap_rle", eqc.compose_binary_swap, eqc.FLAG_RLE)]
-    variants += [("swap23_nccl", eqc.compose_swap23, 0), ("swap23_rle", eqc.compose_swap23, eqc.FLAG_RLE),
-                 ("stream_nccl", eqc.compose_stream, 0)]
+    variants += [("swap23_p2p", eqc.compose_swap23, 0), ("swap23_nccl", eqc.compose_swap23, eqc.FLAG_NCCL),
+                 ("swap23_rle", eqc.compose_swap23, eqc.FLAG_RLE), ("stream_nccl", eqc.compose_stream, 0)]
     op = eqc.OP_BLEND if blend else eqc.OP_DEPTH
     if not blend:  # application-provided ROIs: here the sources' exact boxes, from image_roi
         app_roi = torch.zeros((len(dd), 4), dtype=torch.int32, device=dev)
