@@ -173,8 +173,15 @@ EQC_API size_t image_rle_workspace_size(int w, int h);
  *              image_rle_max_size(w, h) bytes (else EQC_E_CAPACITY), so the
  *              encoder never needs a host round trip.
  *   d_size     device int64: receives the stream size in bytes.
- *   workspace  device scratch of >= image_rle_workspace_size(w, h) bytes.
+ *   workspace  device scratch of >= image_rle_workspace_size(w, h) bytes,
+ *              8-byte aligned.
  *   The stream is byte-identical to the CPU oracle's (deterministic).
+ *   Enqueues (all asynchronous on `stream`, CUDA-graph capturable): a
+ *   cudaMemsetAsync of the workspace's counters, the persistent encoder
+ *   kernel (records into the workspace's record scratch) and the compaction
+ *   kernel (records to their payload offsets, table, header, size); RLE-64
+ *   batches use the encoder, run-scan and compaction kernels of the round-1
+ *   design.
  */
 EQC_API int image_compress_rle(const uint32_t *src, int w, int h, int64_t pitch, int kind, int flags,
                        uint8_t *dst, int64_t dst_capacity, int64_t *d_size, void *workspace,
