@@ -851,56 +851,51 @@ __device__ __forceinline__ bool probe_const(const uint8_t *rec, uint32_t ps, int
   return ok;
 }
 
-// Stage a record (aligned 4-byte words; byte loads at the stream end) and
-// decode its four planes into px[0..3].  Warp-cooperative; returns false
-// (warp-uniform) on a malformed record.
+// Decode a staged record into px[0..3], planes in the order 3, 0, 1, 2 (the
+// most significant byte first).  With `check`, when that byte alone makes the
+// source deeper than best[] at every pixel of the chunk (it then cannot win:
+// ties keep the lower index), planes 0-2 are not decoded and `skip` is set.
+// One decode_plane_w call site (the kernels must stay inside the instruction
+// cache).  Warp-uniform result; false on a malformed record.
 __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int L, int lane, uint16_t *info,
-                                              uint32_t px[4]) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) px[j] = 0;
-  // one (not unrolled) loop over the planes keeps the decoder body small
-#pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
-    const int sz = (int)((ps >> (8 * q)) & 0xFFu);
-    if (!decode_plane(r, sz, L, lane, q, px, info)) return false;
-    r += sz;
-  }
-  return true;
-}
-
-// Significance-first decode of a staged DEPTH record: the most significant
-// byte plane (plane 3, the record's last) first.  With `check`, when that
-// byte alone makes the source deeper than best[] at every pixel of the chunk
-// (it then cannot win: ties keep the lower index), planes 0-2 are not
-// decoded and `skip` is set.  One decode_plane call site (the kernel must
-// stay inside the instruction cache).  Warp-uniform result.
-__device__ __forceinline__ bool decode_depth_sigfirst(const uint8_t *r, uint32_t ps, int L, int lane, uint16_t *info,
-                                                      uint32_t px[4], bool check, const uint32_t best[4],
-                                                      bool &skip) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) px[j] = 0;
-  const int s0 = (int)(ps & 0xFFu), s1 = (int)((ps >> 8) & 0xFFu), s2 = (int)((ps >> 16) & 0xFFu);
+                                              uint32_t px[4], bool check, const uint32_t best[4], bool &skip) {
+  // plane sizes and record offsets in decode order: rotate plane 3 first
+  uint32_t sz = __funnelshift_l(ps, ps, 8);  // bytes: s3, s0, s1, s2
+  int off = (int)(ps & 0xFFu) + (int)((ps >> 8) & 0xFFu) + (int)((ps >> 16) & 0xFFu);
+  uint32_t X0 = 0, X1 = 0, X2 = 0, X3 = 0;  // shift register of plane words
   skip = false;
 #pragma unroll 1
   for (int t = 0; t < 4; ++t) {
-    const int q = (t + 3) & 3;  // planes 3, 0, 1, 2
-    const int off = q == 3 ? s0 + s1 + s2 : q == 0 ? 0 : q == 1 ? s0 : s0 + s1;
-    if (!decode_plane(r + off, (int)((ps >> (8 * q)) & 0xFFu), L, lane, q, px, info)) return false;
+    const int size = (int)(sz & 0xFFu);
+    uint32_t w;
+    if (!decode_plane_w(r + off, size, L, lane, w, info)) return false;
+    X3 = X2;
+    X2 = X1;
+    X1 = X0;
+    X0 = w;
     if (t == 0 && check) {
       bool lose = true;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) lose = lose && (4 * lane + j >= L || (px[j] >> 24) > (best[j] >> 24));
+      for (int j = 0; j < 4; ++j) lose = lose && (4 * lane + j >= L || ((w >> (8 * j)) & 0xFFu) > (best[j] >> 24));
       if (__all_sync(EQC_FULL, lose)) {
         skip = true;
         return true;
       }
     }
+    off = t == 0 ? 0 : off + size;
+    sz >>= 8;
   }
+  // decode order 3, 0, 1, 2: X3 = plane 3, X2 = plane 0, X1 = plane 1, X0 = plane 2
+  const uint32_t W[4] = {X2, X1, X0, X3};
+  planes_to_px(W, px);
   return true;
 }
 
+// Stage a record from global memory (aligned 4-byte words; byte loads at the
+// stream end) into `stage` (>= 3 + 520 + 8 bytes), then decode_staged.
 __device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8_t *rec, uint32_t ps, int L,
-                              int lane, uint8_t *stage, uint16_t *info, uint32_t px[4]) {
+                              int lane, uint8_t *stage, uint16_t *info, uint32_t px[4], bool check,
+                              const uint32_t best[4], bool &skip) {
   const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
   const int total = s0 + s1 + s2 + s3;
   const uintptr_t a0 = (uintptr_t)rec & ~(uintptr_t)3;
@@ -922,7 +917,7 @@ __device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8
     st32[q] = v;
   }
   __syncwarp();
-  return decode_staged(stage + sh, ps, L, lane, info, px);
+  return decode_staged(stage + sh, ps, L, lane, info, px, check, best, skip);
 }
 
 // 16-byte units of the aligned window covering a record.
@@ -1241,7 +1236,9 @@ __global__ void __launch_bounds__(kWarps * 32, EQC_DEC_MINB) rle_decode_kernel(c
         }
         __syncwarp();
         const uint8_t *rec = im.src + hd.payload0 + offi;
-        const bool okr = decode_staged(stage[warp][buf] + ((uintptr_t)rec & 15u), psi, Li, lane, info[warp], px);
+        bool skip;
+        const bool okr =
+            decode_staged(stage[warp][buf] + ((uintptr_t)rec & 15u), psi, Li, lane, info[warp], px, false, px, skip);
         __syncwarp();  // the buffer is refilled two records later
         buf ^= 1;
         if (!okr) {
@@ -1280,54 +1277,38 @@ constexpr int kMaxStreams = 2 * EQC_MAX_SOURCES;
 constexpr int kFWarps = EQC_FWARPS;  // fused kernel: one chunk position per warp, EQC_FWARPS warps per CTA
 constexpr int kPreWords = 1024; // per-warp record prefetch buffer (4 KB)
 
-// Warp per 8 consecutive chunk positions.
-//  Phase A (4 lanes per position, lane sub = lane & 3 takes sources
-//   i = sub, sub + 4, ...): the depth and colour table entries of every
-//   stream are validated and probed for constant chunks; while all streams of
-//   a position are constant the depth composite is evaluated on the scalar
-//   values, then the four partial minima are merged by (depth, index).
-//  Phase B: all-constant positions are written with one 128-bit store per
-//   lane per output; every other position is decoded warp-cooperatively,
-//   depth first: all depth records give the winning source of every pixel,
-//   then a source's colour chunk is decoded only if it wins at least one
-//   pixel of the chunk in the final result.
-__global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel(const __grid_constant__ FusedParams p) {
-  __shared__ __align__(16) uint8_t stage[kFWarps][kStageBytes];
-  __shared__ __align__(16) uint16_t info[kFWarps][kC];
-  __shared__ int64_t s_pb[kMaxStreams];
-  __shared__ uint8_t s_flags[kMaxStreams];
-  __shared__ int s_bad;
-  __shared__ __align__(16) uint32_t s_pre[kFWarps * kPreWords];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n = p.n, ns = 2 * n;
-  if (tid == 0) s_bad = 0;
-  __syncthreads();
-  for (int q = tid; q < ns; q += blockDim.x) {
-    const bool is_depth = q >= n;
-    StreamHdr hd = read_header(p.src[q], p.src_bytes[q], p.w, p.h);
-    if (!hd.ok || hd.kind != (is_depth ? 1 : 0) || hd.log2c != kLog2C) s_bad = 1;
-    s_pb[q] = hd.payload_bytes;
-    s_flags[q] = (uint8_t)hd.flags;
-  }
-  __syncthreads();
-  if (s_bad) {
-    if (tid == 0) set_corrupt(p.status);
-    return;
-  }
+#ifndef EQC_FPOS
+#define EQC_FPOS 16
+#endif
+constexpr int kFPos = EQC_FPOS;  // chunk positions per CTA (claimed by its warps from a shared counter)
+
+// One chunk position (128 pixels of one row) of the fused decode, by one warp.
+//  Phase A (lane i takes source i; sources 32.. in a second pass unless ONE):
+//   the depth and colour table entries of every stream are validated and
+//   probed for constant chunks; if every chunk of the position is constant
+//   the depth composite is evaluated on the scalar values (minimum depth, ties
+//   to the lowest index) and written with one 128-bit store per lane.
+//  Phase B: every non-constant record of the position is prefetched into the
+//   warp's buffer (asynchronous copies, one round trip), then decoded depth
+//   first: all depth records give the winning source of every pixel, then a
+//   source's colour chunk is decoded only if it wins at least one pixel.
+// Returns false (warp-uniform) on a corrupt stream (status already set).
+template <bool ONE>
+__device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int lane, const int64_t *s_pb,
+                                               const uint8_t *s_flags, uint8_t *stage, uint16_t *info,
+                                               uint4 *pre) {
+  const int n = p.n;
   const int nch = p.S * p.h;
   const int64_t payload0 = 32 + 8 * (int64_t)nch;
-  const int c = p.y0 * p.S + blockIdx.x * kFWarps + warp;  // chunk position of this warp
-  if (c >= p.y1 * p.S) return;
   const int y = c / p.S, k = c - y * p.S;
   const int L = min(kC, p.w - k * kC);
-  // ---- phase A: lane i < n validates and probes source i's depth and colour
-  // chunks (sources 32.. in further passes); results stay in registers
-  const int npass = (n + 31) >> 5;
-  uint4 ed[2], ec[2];  // {offset, plane sizes, value, constant} per pass
+  constexpr int NP = ONE ? 1 : 2;
+  const int npass = ONE ? 1 : (n + 31) >> 5;
+  uint4 ed[NP], ec[NP];  // {offset, plane sizes, value, constant} per pass
   bool ok = true;
   bool allc = true;
 #pragma unroll
-  for (int ps = 0; ps < 2; ++ps) {
+  for (int ps = 0; ps < NP; ++ps) {
     ed[ps] = ec[ps] = make_uint4(0, 0, 0, 1);
     if (ps >= npass) continue;
     const int i = ps * 32 + lane;
@@ -1347,7 +1328,7 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   }
   if (!__all_sync(EQC_FULL, ok)) {
     if (lane == 0) set_corrupt(p.status);
-    return;
+    return false;
   }
   const int64_t row = (int64_t)(y - p.y0) * p.out_pitch + (int64_t)k * kC;
   if (__all_sync(EQC_FULL, allc)) {
@@ -1355,7 +1336,9 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
     // minimum depth, ties to the lowest source index
     uint32_t bdv = 0xFFFFFFFFu, bcv = 0;
     int bi = 0x7FFFFFFF;
-    for (int ps = 0; ps < npass; ++ps) {
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) {
+      if (ps >= npass) break;
       const int i = ps * 32 + lane;
       const uint32_t dv = i < n ? ed[ps].z : 0xFFFFFFFFu;
       const uint32_t m = __reduce_min_sync(EQC_FULL, dv);
@@ -1372,15 +1355,12 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
     const uint32_t pc[4] = {bcv, bcv, bcv, bcv}, pd[4] = {bdv, bdv, bdv, bdv};
     store_px(p.out_color + row, L, lane, p.vec != 0, pc);
     if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, pd);
-    return;
+    return true;
   }
-  // ---- phase B: prefetch every non-constant record of this position into a
-  // per-warp buffer (asynchronous copies, one round trip for all of them),
-  // then decode depth first; a source's colour only where it wins.
-  // Lane i plans source i: word offsets of its depth and colour records.
-  uint4 *pre = reinterpret_cast<uint4 *>(s_pre + (size_t)warp * kPreWords);
+  // ---- phase B.  Lane i plans source i: 16-byte slot offsets of its depth
+  // and colour records in the prefetch buffer (-1: not prefetched)
   constexpr int kPreQuads = kPreWords / 4;
-  int wd0 = 0, wc0 = 0;  // 16-byte slot offsets (-1: not prefetched)
+  int wd0 = 0, wc0 = 0;
   {
     int nwd = 0, nwc = 0;
     if (npass == 1 && lane < n) {
@@ -1393,6 +1373,7 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
     wd0 = (nwd && ex + nwd <= kPreQuads) ? ex : -1;
     wc0 = (nwc && ex + tot <= kPreQuads) ? ex + nwd : -1;
   }
+  __syncwarp();  // the previous position's readers are done with the buffer
   if (npass == 1) {
     for (int i = 0; i < n; ++i) {
       const int od = __shfl_sync(EQC_FULL, wd0, i), oc = __shfl_sync(EQC_FULL, wc0, i);
@@ -1415,8 +1396,8 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   uint32_t bd[4] = {0, 0, 0, 0};
   int bi[4] = {0, 0, 0, 0};
   for (int i = 0; i < n; ++i) {
-    const int ps = i >> 5, li = i & 31;
-    const uint4 e1 = ps ? ed[1] : ed[0];
+    const int li = i & 31;
+    const uint4 e1 = (ONE || i < 32) ? ed[0] : ed[NP - 1];
     const uint32_t dx = __shfl_sync(EQC_FULL, e1.x, li), dy = __shfl_sync(EQC_FULL, e1.y, li),
                    dz = __shfl_sync(EQC_FULL, e1.z, li), dw = __shfl_sync(EQC_FULL, e1.w, li);
     const int od = __shfl_sync(EQC_FULL, wd0, li);
@@ -1425,22 +1406,20 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
     if (dw) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) d[j] = dz;
-    } else if (npass == 1 && od >= 0) {
-      const uint8_t *r = reinterpret_cast<const uint8_t *>(pre + od) + ((uintptr_t)(p.src[n + i] + payload0 + dx) & 15u);
-#if EQC_DEPTH_SKIP
-      bool skip = false;
-      okd = decode_depth_sigfirst(r, dy, L, lane, info[warp], d, i > 0, bd, skip);
-      if (okd && skip) continue;  // deeper than the current best everywhere: cannot win
-#else
-      okd = decode_staged(r, dy, L, lane, info[warp], d);
-#endif
     } else {
-      okd = decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane, stage[warp],
-                          info[warp], d);
+      bool skip = false;
+      const bool check = EQC_DEPTH_SKIP && i > 0;
+      if (npass == 1 && od >= 0)
+        okd = decode_staged(reinterpret_cast<const uint8_t *>(pre + od) + ((uintptr_t)(p.src[n + i] + payload0 + dx) & 15u),
+                            dy, L, lane, info, d, check, bd, skip);
+      else
+        okd = decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane, stage, info,
+                            d, check, bd, skip);
+      if (okd && skip) continue;  // deeper than the current best everywhere: cannot win
     }
     if (!okd) {
       if (lane == 0) set_corrupt(p.status);
-      return;
+      return false;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -1453,8 +1432,8 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   uint32_t bc[4] = {0, 0, 0, 0};
   for (int i = 0; i < n; ++i) {
     if (!__any_sync(EQC_FULL, bi[0] == i || bi[1] == i || bi[2] == i || bi[3] == i)) continue;
-    const int ps = i >> 5, li = i & 31;
-    const uint4 e2 = ps ? ec[1] : ec[0];
+    const int li = i & 31;
+    const uint4 e2 = (ONE || i < 32) ? ec[0] : ec[NP - 1];
     const uint32_t cx = __shfl_sync(EQC_FULL, e2.x, li), cy = __shfl_sync(EQC_FULL, e2.y, li),
                    cz = __shfl_sync(EQC_FULL, e2.z, li), cw = __shfl_sync(EQC_FULL, e2.w, li);
     const int oc = __shfl_sync(EQC_FULL, wc0, li);
@@ -1463,17 +1442,16 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
 #pragma unroll
       for (int j = 0; j < 4; ++j) col[j] = cz;  // already unswizzled
     } else {
-      bool okc;
+      bool okc, skip;
       if (npass == 1 && oc >= 0)
-        okc = decode_staged(reinterpret_cast<const uint8_t *>(pre + oc) +
-                                ((uintptr_t)(p.src[i] + payload0 + cx) & 15u),
-                            cy, L, lane, info[warp], col);
+        okc = decode_staged(reinterpret_cast<const uint8_t *>(pre + oc) + ((uintptr_t)(p.src[i] + payload0 + cx) & 15u),
+                            cy, L, lane, info, col, false, col, skip);
       else
-        okc = decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, L, lane, stage[warp], info[warp],
-                            col);
+        okc = decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, L, lane, stage, info, col, false,
+                            col, skip);
       if (!okc) {
         if (lane == 0) set_corrupt(p.status);
-        return;
+        return false;
       }
       if (s_flags[i] & EQC_FLAG_SWIZZLE) {
 #pragma unroll
@@ -1485,6 +1463,48 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   }
   store_px(p.out_color + row, L, lane, p.vec != 0, bc);
   if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, bd);
+  return true;
+}
+
+// A CTA takes kFPos consecutive chunk positions; its warps claim them one at
+// a time from a shared counter (the stream headers are validated once per
+// CTA).  ONE: n <= 32 (one phase-A pass; the entries stay in registers).
+template <bool ONE>
+__global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel(const __grid_constant__ FusedParams p) {
+  __shared__ __align__(16) uint8_t stage[kFWarps][kStageBytes];
+  __shared__ __align__(16) uint16_t info[kFWarps][kC];
+  __shared__ int64_t s_pb[kMaxStreams];
+  __shared__ uint8_t s_flags[kMaxStreams];
+  __shared__ int s_bad, s_next;
+  __shared__ __align__(16) uint32_t s_pre[kFWarps * kPreWords + 4];  // + 16 B: decode_plane_w reads past a record
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = p.n, ns = 2 * n;
+  if (tid == 0) {
+    s_bad = 0;
+    s_next = kFWarps;
+  }
+  __syncthreads();
+  for (int q = tid; q < ns; q += blockDim.x) {
+    const bool is_depth = q >= n;
+    StreamHdr hd = read_header(p.src[q], p.src_bytes[q], p.w, p.h);
+    if (!hd.ok || hd.kind != (is_depth ? 1 : 0) || hd.log2c != kLog2C) s_bad = 1;
+    s_pb[q] = hd.payload_bytes;
+    s_flags[q] = (uint8_t)hd.flags;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) set_corrupt(p.status);
+    return;
+  }
+  const int c0 = p.y0 * p.S + blockIdx.x * kFPos;
+  const int cnt = min(kFPos, p.y1 * p.S - c0);
+  uint4 *pre = reinterpret_cast<uint4 *>(s_pre + (size_t)warp * kPreWords);
+  for (int j = warp; j < cnt;) {
+    int nj = 0;
+    if (lane == 0) nj = atomicAdd(&s_next, 1);  // claimed ahead: the atomic overlaps the work
+    if (!fused_position<ONE>(p, c0 + j, lane, s_pb, s_flags, stage[warp], info[warp], pre)) return;
+    j = __shfl_sync(EQC_FULL, nj, 0);
+  }
 }
 
 inline bool aligned(const void *q, uintptr_t a) { return ((uintptr_t)q & (a - 1)) == 0; }
@@ -1755,9 +1775,12 @@ int eqc_depth_rle_band(int n, const uint8_t *const *color_rle, const uint8_t *co
   p.y0 = y0;
   p.y1 = y1;
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
-  const int64_t grid = ((int64_t)p.S * (y1 - y0) + kFWarps - 1) / kFWarps;
+  const int64_t grid = ((int64_t)p.S * (y1 - y0) + kFPos - 1) / kFPos;
   if (grid > 0x7FFFFFFFll || (int64_t)p.S * h > 0x7FFFFFFFll) return EQC_E_INVALID;
-  depth_rle_kernel<<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
+  if (n <= 32)
+    depth_rle_kernel<true><<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
+  else
+    depth_rle_kernel<false><<<(unsigned)grid, kFWarps * 32, 0, (cudaStream_t)stream>>>(p);
   return eqc_launch_status();
 }
 
@@ -1774,6 +1797,7 @@ int eqc_preload_rle() {
   ok = ok && cudaFuncGetAttributes(&a, rle_encode3_kernel<false, false>) == cudaSuccess;
   ok = ok && cudaFuncGetAttributes(&a, rle64_decode_kernel) == cudaSuccess;
   ok = ok && cudaFuncGetAttributes(&a, rle_decode_kernel) == cudaSuccess;
-  ok = ok && cudaFuncGetAttributes(&a, depth_rle_kernel) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, depth_rle_kernel<true>) == cudaSuccess;
+  ok = ok && cudaFuncGetAttributes(&a, depth_rle_kernel<false>) == cudaSuccess;
   return ok ? EQC_OK : EQC_E_CUDA;
 }

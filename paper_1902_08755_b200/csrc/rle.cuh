@@ -326,193 +326,193 @@ __device__ __forceinline__ void store_record(uint8_t *g, const uint8_t *st, int 
 
 // ---- decoder ---------------------------------------------------------------
 
-// Decode plane record r[0..size) (staging bytes) of a chunk of length L into
-// byte p of out[0..3] (positions 4*lane + j).  `info` is per-warp scratch of
-// 128 uint16.  Returns false if the record is malformed (warp-uniform).
-template <bool FULL>
-__device__ __forceinline__ bool decode_plane_t(const uint8_t *r, int size, int L_, int lane, int p,
-                                               uint32_t out[4], uint16_t *info) {
-  // FULL: a 128-pixel chunk (every lane's 4 positions are valid)
-  const int L = FULL ? kC : L_;
-  const int i0 = 4 * lane;
+// ---- word-per-lane decoder --------------------------------------------------
+// A plane record r[0..size) = [ntok][ctrl x ntok][payload] (R-C8).  Position i
+// takes payload byte r[ntok + A(i)], where A(i) counts the positions k <= i
+// that advance the payload: token starts and positions inside a LITERAL token.
+// The advancing positions are disjoint ranges [s, e) (literal: e = s + len,
+// repeat: e = s + 1); with S = {s} and E = {e} as 128-bit masks their mask is
+// the integer E - S (an end at 128 wraps to 0).  Lane l forms the word of
+// positions 4l..4l+3 with one byte permute of the 8 payload bytes at its first
+// position's index: byte j is offset by the advancing positions among
+// 4l+1..4l+j (bits 1..j of the lane's nibble of the mask).
+
+// PRMT selector offsets (byte j: o_j << 4j) for the advance nibble `nib`.
+__device__ __forceinline__ uint32_t adv_sel(uint32_t nib) {
+  // byte t of the table = o2 | o3 << 4 for t = nib >> 1 = (b1, b2, b3):
+  // o2 = b1 + b2, o3 = o2 + b3
+  const uint32_t hi = __byte_perm(0x22111100u, 0x32212110u, nib >> 1);
+  return ((nib & 2u) << 3) | (hi << 8);
+}
+
+// Bytes r[pi + o_j], j = 0..3 (o_j from the selector offsets): two aligned
+// word loads and a permute.
+__device__ __forceinline__ uint32_t ld_window(const uint8_t *r, int pi, uint32_t sel) {
+  const uint8_t *b = r + pi;
+  const uint32_t mis = (uint32_t)(uintptr_t)b & 3u;
+  // pointer arithmetic (not an integer round trip) keeps the shared-memory
+  // address space visible to the compiler: LDS, not generic loads
+  const uint32_t *w = reinterpret_cast<const uint32_t *>(b - mis);
+  return __byte_perm(w[0], w[1], mis * 0x1111u + sel);
+}
+
+// Word of positions 4*lane .. 4*lane+3 (byte j = position 4*lane + j; bytes of
+// positions >= L unspecified) of the plane record r[0..size).  Reads up to 8
+// bytes past the record (callers' buffers keep that slack).  `info`: per-warp
+// scratch of 128 uint16 (records of more than 32 tokens).  Returns false if the
+// record is malformed (warp-uniform).
+__device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L, int lane, uint32_t &W,
+                                               uint16_t *info) {
   if (size < 2) return false;
   const int ntok = r[0];
-  if (ntok < 1 || 1 + ntok > size) return false;
-  if (ntok == 1) {  // single-token fast paths (uniform)
+  if (ntok < 1 || 1 + ntok > size || ntok > L) return false;
+  const int i0 = 4 * lane;
+  if (ntok == 1) {  // single-token fast paths
     const int c = r[1];
-    const int len = (c & 0x7F) + 1;
-    if (len != L) return false;
+    if ((c & 0x7F) + 1 != L) return false;
     if (c & 0x80) {
       if (size != 3) return false;
-      const uint32_t v = (uint32_t)r[2] << (8 * p);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) out[j] |= v;
+      W = (uint32_t)r[2] * 0x01010101u;
     } else {
       if (size != 2 + L) return false;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (FULL || i0 + j < L) out[j] |= (uint32_t)r[2 + i0 + j] << (8 * p);
+      W = ld_window(r, 2 + i0, 0x3210u);
     }
     return true;
   }
+  uint32_t nib;  // advancing positions among 4*lane .. 4*lane+3
+  int cntb;      // advancing positions before 4*lane
   if (ntok <= 4) {
-    // few tokens (typical of mixed background/foreground chunks): the token
-    // boundaries are computed once (uniform), each position selects its token
-    // by comparison -- no scans, no shuffles, no scratch
-    // token t covers [st[t], st[t+1]); its byte for position i is
-    // r[bs[t] + lt[t] * i] (literal: bs = payload index - start, lt = 1;
-    // repeat: bs = payload index, lt = 0)
-    int st[4], bs[4], lt[4];
-    int pos = 0, pay = 1 + ntok;
+    // token boundaries computed by every lane (uniform); the lane's nibble and
+    // count are sums over the <= 4 ranges
+    int pos = 0, pay = 0;
+    nib = 0;
+    cntb = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      st[t] = 0x7FFF;  // never selected
-      bs[t] = 0;
-      lt[t] = 0;
       if (t < ntok) {
         const int c = r[1 + t];
         const int len = (c & 0x7F) + 1;
         const bool lit = !(c & 0x80);
-        st[t] = pos;
-        bs[t] = lit ? pay - pos : pay;
-        lt[t] = lit;
+        const int e = lit ? pos + len : pos + 1;
+        const int lo = min(max(pos - i0, 0), 4), hi = min(max(e - i0, 0), 4);
+        nib |= (1u << hi) - (1u << lo);
+        cntb += max(min(e, i0) - pos, 0);
         pos += len;
         pay += lit ? len : 1;
       }
     }
-    if (pos != L || pay != size) return false;
+    if (pos != L || pay != size - 1 - ntok) return false;
+  } else {
+    uint32_t A[4];
+    if (ntok <= 32) {
+      // lane t holds token t: starts and payload sums by one packed warp
+      // scan, then the S and E masks by OR-reductions
+      const bool act = lane < ntok;
+      const int c = act ? r[1 + lane] : 0;
+      const int len = act ? (c & 0x7F) + 1 : 0;
+      const bool lit = !(c & 0x80);
+      const int pay = lit ? len : 1;
+      const uint32_t packed = (uint32_t)len | ((uint32_t)pay << 16);
+      const uint32_t inc = warp_incl_scan_add(packed, lane);
+      const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
+      if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
+      const int s = (int)((inc - packed) & 0xFFFFu);
+      const int e = lit ? s + len : s + 1;
+      const uint32_t sb = act ? 1u << (s & 31) : 0u, eb = act ? 1u << (e & 31) : 0u;
+      uint32_t S[4], E[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = i0 + j;
-      if (FULL || i < L) {
-        // the covering token is the last one starting at or before i
-        int b = bs[0], l = lt[0];
+      for (int w = 0; w < 4; ++w) {
+        S[w] = __reduce_or_sync(EQC_FULL, (s >> 5) == w ? sb : 0u);
+        E[w] = __reduce_or_sync(EQC_FULL, (e >> 5) == w ? eb : 0u);  // e == 128: dropped
+      }
+      const uint64_t lo = ((uint64_t)E[1] << 32 | E[0]) - ((uint64_t)S[1] << 32 | S[0]);
+      const uint64_t hi = ((uint64_t)E[3] << 32 | E[2]) - ((uint64_t)S[3] << 32 | S[2]) -
+                          (((uint64_t)E[1] << 32 | E[0]) < ((uint64_t)S[1] << 32 | S[0]) ? 1u : 0u);
+      A[0] = (uint32_t)lo;
+      A[1] = (uint32_t)(lo >> 32);
+      A[2] = (uint32_t)hi;
+      A[3] = (uint32_t)(hi >> 32);
+    } else {
+      // lane l holds tokens 4l .. 4l+3 (ntok <= L <= 128); S and E as byte
+      // markers in the scratch, then gathered by ballots
+      int sl = 0, sp = 0;
 #pragma unroll
-        for (int t = 1; t < 4; ++t) {
-          const bool in = i >= st[t];
-          b = in ? bs[t] : b;
-          l = in ? lt[t] : l;
+      for (int k = 0; k < 4; ++k) {
+        const int t = i0 + k;
+        if (t < ntok) {
+          const int c = r[1 + t];
+          const int len = (c & 0x7F) + 1;
+          sl += len;
+          sp += (c & 0x80) ? 1 : len;
         }
-        out[j] |= (uint32_t)r[b + l * i] << (8 * p);
       }
-    }
-    return true;
-  }
-  if (ntok <= 32) {
-    // lane t holds token t: start positions and payload indices by one packed
-    // warp scan; each position finds its token as the last start at or before
-    // it (token-index markers + a running max over positions) and reads the
-    // token's {start, payload index, type} with one shuffle.
-    const int c = lane < ntok ? r[1 + lane] : 0;
-    const int len = lane < ntok ? (c & 0x7F) + 1 : 0;
-    const int pay = (c & 0x80) ? 1 : len;
-    const uint32_t packed = (uint32_t)len | ((uint32_t)pay << 16);
-    const uint32_t inc = warp_incl_scan_add(packed, lane);
-    const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
-    if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
-    const uint32_t ex = inc - packed;
-    const int tstart = (int)(ex & 0xFFFFu);
-    const int tpay = 1 + ntok + (int)(ex >> 16);
-    const uint32_t tinfo = (uint32_t)tstart | ((uint32_t)tpay << 8) | ((uint32_t)(c & 0x80) << 24);
-    uint8_t *mk = reinterpret_cast<uint8_t *>(info);
-    __syncwarp();
-    reinterpret_cast<uint32_t *>(mk)[lane] = 0u;
-    __syncwarp();
-    if (lane < ntok) mk[tstart] = (uint8_t)(lane + 1);
-    __syncwarp();
-    const uint32_t w4 = reinterpret_cast<const uint32_t *>(mk)[lane];
-    // markers grow with position, so the running max is the last marker
-    const int lmax = (int)max(max(w4 & 0xFFu, (w4 >> 8) & 0xFFu), max((w4 >> 16) & 0xFFu, w4 >> 24));
-    int pre = lmax;
+      const uint32_t packed = (uint32_t)sl | ((uint32_t)sp << 16);
+      const uint32_t inc = warp_incl_scan_add(packed, lane);
+      const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
+      if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
+      uint8_t *mS = reinterpret_cast<uint8_t *>(info), *mE = mS + 128;
+      __syncwarp();  // the scratch may still be read by a previous plane
+      reinterpret_cast<uint2 *>(info)[lane] = make_uint2(0u, 0u);
+      __syncwarp();
+      int spos = (int)((inc - packed) & 0xFFFFu);
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int o = __shfl_up_sync(EQC_FULL, pre, d);
-      if (lane >= d) pre = max(pre, o);
-    }
-    int run = __shfl_up_sync(EQC_FULL, pre, 1);
-    if (lane == 0) run = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      run = max(run, (int)((w4 >> (8 * j)) & 0xFFu));
-      const uint32_t ti = __shfl_sync(EQC_FULL, tinfo, max(run - 1, 0));
-      const int i = i0 + j;
-      if (FULL || i < L) {
-        const int pi = (int)((ti >> 8) & 0xFFFFu) + ((ti >> 31) ? 0 : i - (int)(ti & 0xFFu));
-        out[j] |= (uint32_t)r[pi] << (8 * p);
+      for (int k = 0; k < 4; ++k) {
+        const int t = i0 + k;
+        if (t < ntok) {
+          const int c = r[1 + t];
+          const int len = (c & 0x7F) + 1;
+          const int e = (c & 0x80) ? spos + 1 : spos + len;
+          mS[spos] = 1;
+          if (e < 128) mE[e] = 1;
+          spos += len;
+        }
       }
+      __syncwarp();
+      // lane l reads its 4 marker bytes (positions 4l..4l+3) of each mask
+      const uint32_t ms = reinterpret_cast<const uint32_t *>(mS)[lane];
+      const uint32_t me = reinterpret_cast<const uint32_t *>(mE)[lane];
+      // bytes 0/1 -> nibble (byte j -> bit j)
+      const uint32_t ns = (ms | (ms >> 7) | (ms >> 14) | (ms >> 21)) & 0xFu;
+      const uint32_t ne = (me | (me >> 7) | (me >> 14) | (me >> 21)) & 0xFu;
+      // word w of a mask = nibbles of lanes 8w .. 8w+7
+      uint32_t vs = ns << (4 * (lane & 7)), ve = ne << (4 * (lane & 7));
+#pragma unroll
+      for (int d = 1; d < 8; d <<= 1) {
+        vs |= __shfl_xor_sync(EQC_FULL, vs, d);
+        ve |= __shfl_xor_sync(EQC_FULL, ve, d);
+      }
+      uint32_t S[4], E[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        S[w] = __shfl_sync(EQC_FULL, vs, 8 * w);
+        E[w] = __shfl_sync(EQC_FULL, ve, 8 * w);
+      }
+      const uint64_t lo = ((uint64_t)E[1] << 32 | E[0]) - ((uint64_t)S[1] << 32 | S[0]);
+      const uint64_t hi = ((uint64_t)E[3] << 32 | E[2]) - ((uint64_t)S[3] << 32 | S[2]) -
+                          (((uint64_t)E[1] << 32 | E[0]) < ((uint64_t)S[1] << 32 | S[0]) ? 1u : 0u);
+      A[0] = (uint32_t)lo;
+      A[1] = (uint32_t)(lo >> 32);
+      A[2] = (uint32_t)hi;
+      A[3] = (uint32_t)(hi >> 32);
     }
-    return true;
+    const int w = lane >> 3, sh = 4 * (lane & 7);
+    const uint32_t Aw = w == 0 ? A[0] : w == 1 ? A[1] : w == 2 ? A[2] : A[3];
+    const int pre = (w > 0 ? __popc(A[0]) : 0) + (w > 1 ? __popc(A[1]) : 0) + (w > 2 ? __popc(A[2]) : 0);
+    cntb = pre + __popc(Aw & ((1u << sh) - 1u));
+    nib = (Aw >> sh) & 0xFu;
   }
-  // many tokens: tokens 4*lane .. 4*lane+3 per lane, positions by prefix sums
-  __syncwarp();  // the info scratch may still be read by the previous plane
-  int sl = 0, sp = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int t = i0 + k;
-    if (t < ntok) {
-      const int c = r[1 + t];
-      const int len = (c & 0x7F) + 1;
-      const int pay = (c & 0x80) ? 1 : len;
-      sl += len;
-      sp += pay;
-    }
-  }
-  const uint32_t packed = (uint32_t)sl | ((uint32_t)sp << 16);
-  const uint32_t inc = warp_incl_scan_add(packed, lane);
-  const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
-  if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
-  uint32_t ex = inc - packed;
-  int spos = (int)(ex & 0xFFFFu);
-  int ppos = 1 + ntok + (int)(ex >> 16);
-  // clear the per-position info table, then mark each token start with
-  // (payload index | literal flag << 15)
-  reinterpret_cast<uint2 *>(info)[lane] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int t = i0 + k;
-    if (t < ntok) {
-      const int c = r[1 + t];
-      const int len = (c & 0x7F) + 1;
-      info[spos] = (uint16_t)(ppos | ((c & 0x80) ? 0 : 0x8000));
-      spos += len;
-      ppos += (c & 0x80) ? 1 : len;
-    }
-  }
-  __syncwarp();
-  // covering token start of each position: running max of start positions
-  const uint2 iw = reinterpret_cast<const uint2 *>(info)[lane];
-  const uint16_t inf[4] = {(uint16_t)(iw.x & 0xFFFF), (uint16_t)(iw.x >> 16), (uint16_t)(iw.y & 0xFFFF),
-                           (uint16_t)(iw.y >> 16)};
-  int lmax = -1;
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (inf[j] != 0xFFFF && i0 + j < L) lmax = i0 + j;
-  int pre = lmax;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int o = __shfl_up_sync(EQC_FULL, pre, d);
-    if (lane >= d) pre = max(pre, o);
-  }
-  int run = __shfl_up_sync(EQC_FULL, pre, 1);
-  if (lane == 0) run = -1;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int i = i0 + j;
-    if (i < L) {
-      if (inf[j] != 0xFFFF) run = i;
-      const uint32_t ti = info[run];
-      const int pi = (int)(ti & 0x7FFFu) + ((ti & 0x8000u) ? (i - run) : 0);
-      out[j] |= (uint32_t)r[pi] << (8 * p);
-    }
-  }
+  W = ld_window(r, ntok + cntb + (int)(nib & 1u), adv_sel(nib));
   return true;
 }
 
-__device__ __forceinline__ bool decode_plane(const uint8_t *r, int size, int L, int lane, int p, uint32_t out[4],
-                                             uint16_t *info) {
-  return L == kC ? decode_plane_t<true>(r, size, L, lane, p, out, info)
-                 : decode_plane_t<false>(r, size, L, lane, p, out, info);
+// 4x4 byte transpose: pixel j = byte j of the plane words W[0..3].
+__device__ __forceinline__ void planes_to_px(const uint32_t W[4], uint32_t px[4]) {
+  const uint32_t t0 = __byte_perm(W[0], W[1], 0x5140), t1 = __byte_perm(W[0], W[1], 0x7362);
+  const uint32_t t2 = __byte_perm(W[2], W[3], 0x5140), t3 = __byte_perm(W[2], W[3], 0x7362);
+  px[0] = __byte_perm(t0, t2, 0x5410);
+  px[1] = __byte_perm(t0, t2, 0x7632);
+  px[2] = __byte_perm(t1, t3, 0x5410);
+  px[3] = __byte_perm(t1, t3, 0x7632);
 }
 
 }  // namespace eqc_rle
