@@ -863,17 +863,17 @@ __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int
   uint32_t sz = __funnelshift_l(ps, ps, 8);  // bytes: s3, s0, s1, s2
   int off = (int)(ps & 0xFFu) + (int)((ps >> 8) & 0xFFu) + (int)((ps >> 16) & 0xFFu);
   uint32_t X0 = 0, X1 = 0, X2 = 0, X3 = 0;  // shift register of plane words
+  bool ok = true;
   skip = false;
 #pragma unroll 1
   for (int t = 0; t < 4; ++t) {
     const int size = (int)(sz & 0xFFu);
-    uint32_t w;
-    if (!decode_plane_w(r + off, size, L, lane, w, info)) return false;
+    const uint32_t w = decode_plane_w(r + off, size, L, lane, ok, info);
     X3 = X2;
     X2 = X1;
     X1 = X0;
     X0 = w;
-    if (t == 0 && check) {
+    if (t == 0 && check && ok) {
       bool lose = true;
 #pragma unroll
       for (int j = 0; j < 4; ++j) lose = lose && (4 * lane + j >= L || ((w >> (8 * j)) & 0xFFu) > (best[j] >> 24));
@@ -888,14 +888,15 @@ __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int
   // decode order 3, 0, 1, 2: X3 = plane 3, X2 = plane 0, X1 = plane 1, X0 = plane 2
   const uint32_t W[4] = {X2, X1, X0, X3};
   planes_to_px(W, px);
-  return true;
+  return ok;
 }
 
 // Stage a record from global memory (aligned 4-byte words; byte loads at the
-// stream end) into `stage` (>= 3 + 520 + 8 bytes), then decode_staged.
-__device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8_t *rec, uint32_t ps, int L,
-                              int lane, uint8_t *stage, uint16_t *info, uint32_t px[4], bool check,
-                              const uint32_t best[4], bool &skip) {
+// stream end) into `stage` (>= 3 + 520 + 8 bytes); returns the staged
+// record's first byte.  Not inlined: the fallback for records that do not fit
+// the prefetch buffer.
+__device__ __noinline__ const uint8_t *stage_record(const uint8_t *src, int64_t src_bytes, const uint8_t *rec,
+                                                    uint32_t ps, int lane, uint8_t *stage) {
   const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
   const int total = s0 + s1 + s2 + s3;
   const uintptr_t a0 = (uintptr_t)rec & ~(uintptr_t)3;
@@ -917,7 +918,7 @@ __device__ bool decode_record(const uint8_t *src, int64_t src_bytes, const uint8
     st32[q] = v;
   }
   __syncwarp();
-  return decode_staged(stage + sh, ps, L, lane, info, px, check, best, skip);
+  return stage + sh;
 }
 
 // 16-byte units of the aligned window covering a record.
@@ -1409,12 +1410,11 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
     } else {
       bool skip = false;
       const bool check = EQC_DEPTH_SKIP && i > 0;
-      if (npass == 1 && od >= 0)
-        okd = decode_staged(reinterpret_cast<const uint8_t *>(pre + od) + ((uintptr_t)(p.src[n + i] + payload0 + dx) & 15u),
-                            dy, L, lane, info, d, check, bd, skip);
-      else
-        okd = decode_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, L, lane, stage, info,
-                            d, check, bd, skip);
+      const uint8_t *rec = p.src[n + i] + payload0 + dx;
+      const uint8_t *r = (npass == 1 && od >= 0)
+                             ? reinterpret_cast<const uint8_t *>(pre + od) + ((uintptr_t)rec & 15u)
+                             : stage_record(p.src[n + i], p.src_bytes[n + i], rec, dy, lane, stage);
+      okd = decode_staged(r, dy, L, lane, info, d, check, bd, skip);
       if (okd && skip) continue;  // deeper than the current best everywhere: cannot win
     }
     if (!okd) {
@@ -1442,13 +1442,11 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
 #pragma unroll
       for (int j = 0; j < 4; ++j) col[j] = cz;  // already unswizzled
     } else {
-      bool okc, skip;
-      if (npass == 1 && oc >= 0)
-        okc = decode_staged(reinterpret_cast<const uint8_t *>(pre + oc) + ((uintptr_t)(p.src[i] + payload0 + cx) & 15u),
-                            cy, L, lane, info, col, false, col, skip);
-      else
-        okc = decode_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, L, lane, stage, info, col, false,
-                            col, skip);
+      bool skip;
+      const uint8_t *rec = p.src[i] + payload0 + cx;
+      const uint8_t *r = (npass == 1 && oc >= 0) ? reinterpret_cast<const uint8_t *>(pre + oc) + ((uintptr_t)rec & 15u)
+                                                 : stage_record(p.src[i], p.src_bytes[i], rec, cy, lane, stage);
+      const bool okc = decode_staged(r, cy, L, lane, info, col, false, col, skip);
       if (!okc) {
         if (lane == 0) set_corrupt(p.status);
         return false;

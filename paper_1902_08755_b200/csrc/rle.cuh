@@ -357,30 +357,26 @@ __device__ __forceinline__ uint32_t ld_window(const uint8_t *r, int pi, uint32_t
 }
 
 // Word of positions 4*lane .. 4*lane+3 (byte j = position 4*lane + j; bytes of
-// positions >= L unspecified) of the plane record r[0..size).  Reads up to 8
-// bytes past the record (callers' buffers keep that slack).  `info`: per-warp
-// scratch of 128 uint16 (records of more than 32 tokens).  Returns false if the
-// record is malformed (warp-uniform).
-__device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L, int lane, uint32_t &W,
-                                               uint16_t *info) {
-  if (size < 2) return false;
-  const int ntok = r[0];
-  if (ntok < 1 || 1 + ntok > size || ntok > L) return false;
+// positions >= L unspecified) of the plane record r[0..size), size <= L + 2.
+// `ok` is cleared if the record is malformed (warp-uniform); a malformed
+// record is still read only inside r[0 .. size + 8) (callers' buffers keep 8
+// bytes of slack past every record), so validation is deferred to one test
+// per record.  `info`: per-warp scratch of 128 uint16 (records of more than
+// 32 tokens).
+__device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, int L, int lane, bool &ok,
+                                                   uint16_t *info) {
+  const int ntok = r[0];  // (size 0: a byte of the next plane or the slack)
+  ok = ok && size >= 2 && ntok >= 1 && 1 + ntok <= size && ntok <= L;
   const int i0 = 4 * lane;
-  if (ntok == 1) {  // single-token fast paths
-    const int c = r[1];
-    if ((c & 0x7F) + 1 != L) return false;
-    if (c & 0x80) {
-      if (size != 3) return false;
-      W = (uint32_t)r[2] * 0x01010101u;
-    } else {
-      if (size != 2 + L) return false;
-      W = ld_window(r, 2 + i0, 0x3210u);
-    }
-    return true;
-  }
   uint32_t nib;  // advancing positions among 4*lane .. 4*lane+3
   int cntb;      // advancing positions before 4*lane
+  if (ntok <= 1) {  // single-token fast paths
+    const int c = r[1];
+    const bool rep = (c & 0x80) != 0;
+    ok = ok && (c & 0x7F) + 1 == L && size == (rep ? 3 : 2 + L);
+    if (rep) return (uint32_t)r[2] * 0x01010101u;
+    return ld_window(r, 2 + min(i0, L), 0x3210u);  // (lanes past L: inside the slack)
+  }
   if (ntok <= 4) {
     // token boundaries computed by every lane (uniform); the lane's nibble and
     // count are sums over the <= 4 ranges
@@ -401,7 +397,7 @@ __device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L
         pay += lit ? len : 1;
       }
     }
-    if (pos != L || pay != size - 1 - ntok) return false;
+    ok = ok && pos == L && pay == size - 1 - ntok;
   } else {
     uint32_t A[4];
     if (ntok <= 32) {
@@ -415,7 +411,7 @@ __device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L
       const uint32_t packed = (uint32_t)len | ((uint32_t)pay << 16);
       const uint32_t inc = warp_incl_scan_add(packed, lane);
       const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
-      if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
+      ok = ok && (int)(tot & 0xFFFFu) == L && (int)(tot >> 16) == size - 1 - ntok;
       const int s = (int)((inc - packed) & 0xFFFFu);
       const int e = lit ? s + len : s + 1;
       const uint32_t sb = act ? 1u << (s & 31) : 0u, eb = act ? 1u << (e & 31) : 0u;
@@ -433,13 +429,14 @@ __device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L
       A[2] = (uint32_t)hi;
       A[3] = (uint32_t)(hi >> 32);
     } else {
-      // lane l holds tokens 4l .. 4l+3 (ntok <= L <= 128); S and E as byte
-      // markers in the scratch, then gathered by ballots
+      // lane l holds tokens 4l .. 4l+3 (of at most 128: ntok <= L); S and E
+      // as byte markers in the scratch, gathered into words by shuffles
+      const int nt = min(ntok, L);
       int sl = 0, sp = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int t = i0 + k;
-        if (t < ntok) {
+        if (t < nt) {
           const int c = r[1 + t];
           const int len = (c & 0x7F) + 1;
           sl += len;
@@ -449,7 +446,7 @@ __device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L
       const uint32_t packed = (uint32_t)sl | ((uint32_t)sp << 16);
       const uint32_t inc = warp_incl_scan_add(packed, lane);
       const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
-      if ((int)(tot & 0xFFFFu) != L || (int)(tot >> 16) != size - 1 - ntok) return false;
+      ok = ok && (int)(tot & 0xFFFFu) == L && (int)(tot >> 16) == size - 1 - ntok;
       uint8_t *mS = reinterpret_cast<uint8_t *>(info), *mE = mS + 128;
       __syncwarp();  // the scratch may still be read by a previous plane
       reinterpret_cast<uint2 *>(info)[lane] = make_uint2(0u, 0u);
@@ -458,11 +455,11 @@ __device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int t = i0 + k;
-        if (t < ntok) {
+        if (t < nt) {
           const int c = r[1 + t];
           const int len = (c & 0x7F) + 1;
           const int e = (c & 0x80) ? spos + 1 : spos + len;
-          mS[spos] = 1;
+          if (spos < 128) mS[spos] = 1;
           if (e < 128) mE[e] = 1;
           spos += len;
         }
@@ -501,8 +498,8 @@ __device__ __forceinline__ bool decode_plane_w(const uint8_t *r, int size, int L
     cntb = pre + __popc(Aw & ((1u << sh) - 1u));
     nib = (Aw >> sh) & 0xFu;
   }
-  W = ld_window(r, ntok + cntb + (int)(nib & 1u), adv_sel(nib));
-  return true;
+  // (a malformed record: the index is clamped into the record)
+  return ld_window(r, min(ntok + cntb + (int)(nib & 1u), size), adv_sel(nib));
 }
 
 // 4x4 byte transpose: pixel j = byte j of the plane words W[0..3].
