@@ -34,9 +34,6 @@
 #ifndef EQC_FUSED_MINB
 #define EQC_FUSED_MINB (32 / EQC_FWARPS)  // 32 warps per SM (64 registers)
 #endif
-#ifndef EQC_DEPTH_SKIP
-#define EQC_DEPTH_SKIP 1  // fused decode: significance-first depth records (skip losing sources' low planes)
-#endif
 #ifndef EQC_CLS_BATCH
 #define EQC_CLS_BATCH 8
 #endif
@@ -1297,7 +1294,7 @@ constexpr int kFPos = EQC_FPOS;  // chunk positions per CTA (claimed by its warp
 template <bool ONE>
 __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int lane, const int64_t *s_pb,
                                                const uint8_t *s_flags, uint8_t *stage, uint16_t *info,
-                                               uint4 *pre) {
+                                               uint4 *pre, uint4 *desc) {
   const int n = p.n;
   const int nch = p.S * p.h;
   const int64_t payload0 = 32 + 8 * (int64_t)nch;
@@ -1358,106 +1355,162 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
     if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, pd);
     return true;
   }
-  // ---- phase B.  Lane i plans source i: 16-byte slot offsets of its depth
-  // and colour records in the prefetch buffer (-1: not prefetched)
+  // ---- phase B
+  uint32_t bd[4] = {0, 0, 0, 0};
+  int bi[4] = {0, 0, 0, 0};
+  uint32_t bc[4] = {0, 0, 0, 0};
   constexpr int kPreQuads = kPreWords / 4;
-  int wd0 = 0, wc0 = 0;
-  {
-    int nwd = 0, nwc = 0;
-    if (npass == 1 && lane < n) {
-      if (!ed[0].w) nwd = record_quads(p.src[n + lane] + payload0 + ed[0].x, ed[0].y);
-      if (!ec[0].w) nwc = record_quads(p.src[lane] + payload0 + ec[0].x, ec[0].y);
-    }
+  if constexpr (ONE) {
+    // Lane i plans source i: 16-byte slots of its depth and colour records in
+    // the prefetch buffer, and a descriptor per record in shared memory
+    // {offset, plane sizes, value, w}: w bit 0 = constant, bits 1-4 = the
+    // record's address mod 16, bits 5.. = slot + 1 (0: not prefetched).
+    const bool act = lane < n;
+    const int qd = act ? n + lane : 0, qc = act ? lane : 0;
+    const uint8_t *recd = p.src[qd] + payload0 + ed[0].x, *recc = p.src[qc] + payload0 + ec[0].x;
+    const int nwd = (act && !ed[0].w) ? record_quads(recd, ed[0].y) : 0;
+    const int nwc = (act && !ec[0].w) ? record_quads(recc, ec[0].y) : 0;
     const int tot = nwd + nwc;
-    const int inc = (int)warp_incl_scan_add((uint32_t)tot, lane);
-    const int ex = inc - tot;
-    wd0 = (nwd && ex + nwd <= kPreQuads) ? ex : -1;
-    wc0 = (nwc && ex + tot <= kPreQuads) ? ex + nwd : -1;
-  }
-  __syncwarp();  // the previous position's readers are done with the buffer
-  if (npass == 1) {
-    for (int i = 0; i < n; ++i) {
-      const int od = __shfl_sync(EQC_FULL, wd0, i), oc = __shfl_sync(EQC_FULL, wc0, i);
-      if (od >= 0) {
-        const uint32_t x = __shfl_sync(EQC_FULL, ed[0].x, i), y2 = __shfl_sync(EQC_FULL, ed[0].y, i);
-        const uint8_t *rec = p.src[n + i] + payload0 + x;
-        stage_async16(p.src[n + i], p.src_bytes[n + i], rec, record_quads(rec, y2), pre + od, lane);
-      }
-      if (oc >= 0) {
-        const uint32_t x = __shfl_sync(EQC_FULL, ec[0].x, i), y2 = __shfl_sync(EQC_FULL, ec[0].y, i);
-        const uint8_t *rec = p.src[i] + payload0 + x;
-        stage_async16(p.src[i], p.src_bytes[i], rec, record_quads(rec, y2), pre + oc, lane);
+    const int ex = (int)warp_incl_scan_add((uint32_t)tot, lane) - tot;
+    // a record is prefetched if it fits the buffer and its aligned window
+    // ends inside the stream (else it is staged when decoded)
+    const uintptr_t ad = (uintptr_t)recd & ~(uintptr_t)15, ac = (uintptr_t)recc & ~(uintptr_t)15;
+    const bool fd = nwd && ex + nwd <= kPreQuads && ad + 16 * (uintptr_t)nwd <= (uintptr_t)p.src[qd] + p.src_bytes[qd];
+    const bool fc = nwc && ex + tot <= kPreQuads && ac + 16 * (uintptr_t)nwc <= (uintptr_t)p.src[qc] + p.src_bytes[qc];
+    const int sd0 = fd ? ex : -1, sc0 = fc ? ex + nwd : -1;
+    __syncwarp();  // the previous position's readers are done with the buffer and descriptors
+    if (act) {
+      desc[lane] = make_uint4(ed[0].x, ed[0].y, ed[0].z,
+                              ed[0].w ? 1u : ((((uint32_t)(uintptr_t)recd & 15u) << 1) | ((uint32_t)(sd0 + 1) << 5)));
+      desc[32 + lane] = make_uint4(ec[0].x, ec[0].y, ec[0].z,
+                                   ec[0].w ? 1u : ((((uint32_t)(uintptr_t)recc & 15u) << 1) | ((uint32_t)(sc0 + 1) << 5)));
+    }
+    // prefetch: one round trip for every prefetched record of the position
+#pragma unroll 1
+    for (int kind = 0; kind < 2; ++kind) {
+      unsigned m = __ballot_sync(EQC_FULL, kind ? fc : fd);
+      const uintptr_t a = kind ? ac : ad;
+      const uint32_t sn = kind ? ((uint32_t)sc0 | ((uint32_t)nwc << 16)) : ((uint32_t)sd0 | ((uint32_t)nwd << 16));
+      while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        const uintptr_t ai = ((uintptr_t)__shfl_sync(EQC_FULL, (uint32_t)((uint64_t)a >> 32), i) << 32) |
+                             __shfl_sync(EQC_FULL, (uint32_t)a, i);
+        const uint32_t si = __shfl_sync(EQC_FULL, sn, i);
+        const int slot = (int)(si & 0xFFFFu), nq = (int)(si >> 16);
+        for (int q = lane; q < nq; q += 32) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(pre + slot + q);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(ai + 16 * (uintptr_t)q) : "memory");
+        }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-  }
-  __syncwarp();
-  // depth pass: running minimum and the index of the winning source per pixel
-  uint32_t bd[4] = {0, 0, 0, 0};
-  int bi[4] = {0, 0, 0, 0};
-  for (int i = 0; i < n; ++i) {
-    const int li = i & 31;
-    const uint4 e1 = (ONE || i < 32) ? ed[0] : ed[NP - 1];
-    const uint32_t dx = __shfl_sync(EQC_FULL, e1.x, li), dy = __shfl_sync(EQC_FULL, e1.y, li),
-                   dz = __shfl_sync(EQC_FULL, e1.z, li), dw = __shfl_sync(EQC_FULL, e1.w, li);
-    const int od = __shfl_sync(EQC_FULL, wd0, li);
-    uint32_t d[4];
-    bool okd = true;
-    if (dw) {
+    __syncwarp();
+    // depth pass: running minimum and the index of the winning source per pixel
+    for (int i = 0; i < n; ++i) {
+      const uint4 e = desc[i];
+      uint32_t d[4];
+      if (e.w & 1u) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) d[j] = dz;
-    } else {
-      bool skip = false;
-      const bool check = EQC_DEPTH_SKIP && i > 0;
-      const uint8_t *rec = p.src[n + i] + payload0 + dx;
-      const uint8_t *r = (npass == 1 && od >= 0)
-                             ? reinterpret_cast<const uint8_t *>(pre + od) + ((uintptr_t)rec & 15u)
-                             : stage_record(p.src[n + i], p.src_bytes[n + i], rec, dy, lane, stage);
-      okd = decode_staged(r, dy, L, lane, info, d, check, bd, skip);
-      if (okd && skip) continue;  // deeper than the current best everywhere: cannot win
-    }
-    if (!okd) {
-      if (lane == 0) set_corrupt(p.status);
-      return false;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool t = (i == 0) || d[j] < bd[j];  // ties keep the lower index
-      bd[j] = t ? d[j] : bd[j];
-      bi[j] = t ? i : bi[j];
-    }
-  }
-  // colour pass: only the sources that win at least one pixel of the chunk
-  uint32_t bc[4] = {0, 0, 0, 0};
-  for (int i = 0; i < n; ++i) {
-    if (!__any_sync(EQC_FULL, bi[0] == i || bi[1] == i || bi[2] == i || bi[3] == i)) continue;
-    const int li = i & 31;
-    const uint4 e2 = (ONE || i < 32) ? ec[0] : ec[NP - 1];
-    const uint32_t cx = __shfl_sync(EQC_FULL, e2.x, li), cy = __shfl_sync(EQC_FULL, e2.y, li),
-                   cz = __shfl_sync(EQC_FULL, e2.z, li), cw = __shfl_sync(EQC_FULL, e2.w, li);
-    const int oc = __shfl_sync(EQC_FULL, wc0, li);
-    uint32_t col[4];
-    if (cw) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) col[j] = cz;  // already unswizzled
-    } else {
-      bool skip;
-      const uint8_t *rec = p.src[i] + payload0 + cx;
-      const uint8_t *r = (npass == 1 && oc >= 0) ? reinterpret_cast<const uint8_t *>(pre + oc) + ((uintptr_t)rec & 15u)
-                                                 : stage_record(p.src[i], p.src_bytes[i], rec, cy, lane, stage);
-      const bool okc = decode_staged(r, cy, L, lane, info, col, false, col, skip);
-      if (!okc) {
-        if (lane == 0) set_corrupt(p.status);
-        return false;
+        for (int j = 0; j < 4; ++j) d[j] = e.z;
+      } else {
+        const int slot = (int)(e.w >> 5) - 1;
+        const uint8_t *r = slot >= 0 ? reinterpret_cast<const uint8_t *>(pre + slot) + ((e.w >> 1) & 15u)
+                                     : stage_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + e.x,
+                                                    e.y, lane, stage);
+        bool skip = false;
+        if (!decode_staged(r, e.y, L, lane, info, d, i > 0, bd, skip)) {
+          if (lane == 0) set_corrupt(p.status);
+          return false;
+        }
+        if (skip) continue;  // deeper than the current best everywhere: cannot win
       }
-      if (s_flags[i] & EQC_FLAG_SWIZZLE) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
+      for (int j = 0; j < 4; ++j) {
+        const bool t = (i == 0) || d[j] < bd[j];  // ties keep the lower index
+        bd[j] = t ? d[j] : bd[j];
+        bi[j] = t ? i : bi[j];
       }
     }
+    // colour pass: only the sources that win at least one pixel of the chunk
+    for (int i = 0; i < n; ++i) {
+      if (!__any_sync(EQC_FULL, bi[0] == i || bi[1] == i || bi[2] == i || bi[3] == i)) continue;
+      const uint4 e = desc[32 + i];
+      uint32_t col[4];
+      if (e.w & 1u) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) bc[j] = bi[j] == i ? col[j] : bc[j];
+        for (int j = 0; j < 4; ++j) col[j] = e.z;  // already unswizzled
+      } else {
+        const int slot = (int)(e.w >> 5) - 1;
+        const uint8_t *r = slot >= 0 ? reinterpret_cast<const uint8_t *>(pre + slot) + ((e.w >> 1) & 15u)
+                                     : stage_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + e.x, e.y, lane,
+                                                    stage);
+        bool skip;
+        if (!decode_staged(r, e.y, L, lane, info, col, false, col, skip)) {
+          if (lane == 0) set_corrupt(p.status);
+          return false;
+        }
+        if (s_flags[i] & EQC_FLAG_SWIZZLE) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bc[j] = bi[j] == i ? col[j] : bc[j];
+    }
+  } else {
+    // n > 32 (two phase-A passes): each record is staged when it is decoded
+    for (int i = 0; i < n; ++i) {
+      const int li = i & 31;
+      const uint4 e1 = i < 32 ? ed[0] : ed[NP - 1];
+      const uint32_t dx = __shfl_sync(EQC_FULL, e1.x, li), dy = __shfl_sync(EQC_FULL, e1.y, li),
+                     dz = __shfl_sync(EQC_FULL, e1.z, li), dw = __shfl_sync(EQC_FULL, e1.w, li);
+      uint32_t d[4];
+      if (dw) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[j] = dz;
+      } else {
+        bool skip = false;
+        const uint8_t *r = stage_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, lane, stage);
+        if (!decode_staged(r, dy, L, lane, info, d, i > 0, bd, skip)) {
+          if (lane == 0) set_corrupt(p.status);
+          return false;
+        }
+        if (skip) continue;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool t = (i == 0) || d[j] < bd[j];
+        bd[j] = t ? d[j] : bd[j];
+        bi[j] = t ? i : bi[j];
+      }
+    }
+    for (int i = 0; i < n; ++i) {
+      if (!__any_sync(EQC_FULL, bi[0] == i || bi[1] == i || bi[2] == i || bi[3] == i)) continue;
+      const int li = i & 31;
+      const uint4 e2 = i < 32 ? ec[0] : ec[NP - 1];
+      const uint32_t cx = __shfl_sync(EQC_FULL, e2.x, li), cy = __shfl_sync(EQC_FULL, e2.y, li),
+                     cz = __shfl_sync(EQC_FULL, e2.z, li), cw = __shfl_sync(EQC_FULL, e2.w, li);
+      uint32_t col[4];
+      if (cw) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) col[j] = cz;
+      } else {
+        bool skip;
+        const uint8_t *r = stage_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, lane, stage);
+        if (!decode_staged(r, cy, L, lane, info, col, false, col, skip)) {
+          if (lane == 0) set_corrupt(p.status);
+          return false;
+        }
+        if (s_flags[i] & EQC_FLAG_SWIZZLE) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bc[j] = bi[j] == i ? col[j] : bc[j];
+    }
   }
   store_px(p.out_color + row, L, lane, p.vec != 0, bc);
   if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, bd);
@@ -1475,6 +1528,7 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   __shared__ uint8_t s_flags[kMaxStreams];
   __shared__ int s_bad, s_next;
   __shared__ __align__(16) uint32_t s_pre[kFWarps * kPreWords + 4];  // + 16 B: decode_plane_w reads past a record
+  __shared__ uint4 s_desc[kFWarps][64];  // per-record descriptors of the warp's position (n <= 32)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = p.n, ns = 2 * n;
   if (tid == 0) {
@@ -1500,7 +1554,7 @@ __global__ void __launch_bounds__(kFWarps * 32, EQC_FUSED_MINB) depth_rle_kernel
   for (int j = warp; j < cnt;) {
     int nj = 0;
     if (lane == 0) nj = atomicAdd(&s_next, 1);  // claimed ahead: the atomic overlaps the work
-    if (!fused_position<ONE>(p, c0 + j, lane, s_pb, s_flags, stage[warp], info[warp], pre)) return;
+    if (!fused_position<ONE>(p, c0 + j, lane, s_pb, s_flags, stage[warp], info[warp], pre, s_desc[warp])) return;
     j = __shfl_sync(EQC_FULL, nj, 0);
   }
 }

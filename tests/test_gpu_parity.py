@@ -288,8 +288,12 @@ def test_rle_batch_16_streams(eqc):
         np.testing.assert_array_equal(to_host(o), img)
 
 
-@pytest.mark.parametrize("n,w,h", [(2, 64, 64), (8, 1920, 1080), (3, 300, 5), (16, 130, 3)])
+@pytest.mark.parametrize("n,w,h", [(2, 64, 64), (8, 1920, 1080), (3, 300, 5), (16, 130, 3),
+                                   (32, 384, 6), (33, 200, 5), (64, 130, 4)])
 def test_fused_decode_depth_composite(eqc, n, w, h):
+    """n <= 32: descriptors + one prefetch round trip per position (n = 32 at
+    384 px overflows the per-warp prefetch buffer: the staging fallback);
+    n > 32: every record staged when decoded."""
     c, d = synth.depth_sources(SEED + n + w, n, w, h)
     oc, od = oracle.depth_composite(c, d)
     cs = [stream_dev(oracle.rle_encode(x, kind=0, flags=1)) for x in c]
