@@ -855,7 +855,8 @@ __device__ __forceinline__ bool probe_const(const uint8_t *rec, uint32_t ps, int
 // One decode_plane_w call site (the kernels must stay inside the instruction
 // cache).  Warp-uniform result; false on a malformed record.
 __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int L, int lane, uint16_t *info,
-                                              uint32_t px[4], bool check, const uint32_t best[4], bool &skip) {
+                                              uint32_t px[4], bool check, const uint32_t best[4], bool &skip,
+                                              bool swz = false) {
   // plane sizes and record offsets in decode order: rotate plane 3 first
   uint32_t sz = __funnelshift_l(ps, ps, 8);  // bytes: s3, s0, s1, s2
   int off = (int)(ps & 0xFFu) + (int)((ps >> 8) & 0xFFu) + (int)((ps >> 16) & 0xFFu);
@@ -883,7 +884,8 @@ __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int
     sz >>= 8;
   }
   // decode order 3, 0, 1, 2: X3 = plane 3, X2 = plane 0, X1 = plane 1, X0 = plane 2
-  const uint32_t W[4] = {X2, X1, X0, X3};
+  uint32_t W[4] = {X2, X1, X0, X3};
+  if (swz) unswizzle_planes(W);
   planes_to_px(W, px);
   return ok;
 }
@@ -1235,17 +1237,13 @@ __global__ void __launch_bounds__(kWarps * 32, EQC_DEC_MINB) rle_decode_kernel(c
         __syncwarp();
         const uint8_t *rec = im.src + hd.payload0 + offi;
         bool skip;
-        const bool okr =
-            decode_staged(stage[warp][buf] + ((uintptr_t)rec & 15u), psi, Li, lane, info[warp], px, false, px, skip);
+        const bool okr = decode_staged(stage[warp][buf] + ((uintptr_t)rec & 15u), psi, Li, lane, info[warp], px,
+                                       false, px, skip, swz);
         __syncwarp();  // the buffer is refilled two records later
         buf ^= 1;
         if (!okr) {
           if (lane == 0) set_corrupt(p.status);
           continue;
-        }
-        if (swz) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) px[j] = unswizzle(px[j]);
         }
       }
       store_px(im.dst + (int64_t)yi * p.pitch + (int64_t)ki * C, Li, lane, p.vec != 0 && C == kC, px);
@@ -1305,6 +1303,27 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
   uint4 ed[NP], ec[NP];  // {offset, plane sizes, value, constant} per pass
   bool ok = true;
   bool allc = true;
+  if (ONE && n <= 16) {
+    // lane q validates and probes stream q (colour 0..n-1, depth n..2n-1);
+    // lane i < n then takes its depth entry from lane n + i
+    const int q = lane;
+    uint4 e = make_uint4(0, 0, 0, 1);
+    if (q < 2 * n) {
+      int64_t o;
+      uint32_t ps;
+      ok = entry_local(p.src[q], s_pb[q], nch, c, L, o, ps);
+      uint32_t v = 0;
+      const bool cst = ok && probe_const(p.src[q] + payload0 + o, ps, L, v);
+      if (cst && q < n && (s_flags[q] & EQC_FLAG_SWIZZLE)) v = unswizzle(v);
+      e = make_uint4((uint32_t)o, ps, v, cst ? 1u : 0u);
+      allc = cst;
+    }
+    const int sl = (n + lane) & 31;
+    ed[0] = make_uint4(__shfl_sync(EQC_FULL, e.x, sl), __shfl_sync(EQC_FULL, e.y, sl), __shfl_sync(EQC_FULL, e.z, sl),
+                       __shfl_sync(EQC_FULL, e.w, sl));
+    ec[0] = e;
+    if (lane >= n) ed[0] = ec[0] = make_uint4(0, 0, 0, 1);
+  } else {
 #pragma unroll
   for (int ps = 0; ps < NP; ++ps) {
     ed[ps] = ec[ps] = make_uint4(0, 0, 0, 1);
@@ -1323,6 +1342,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
       ec[ps] = make_uint4((uint32_t)oc, pc, cv, cc ? 1u : 0u);
       allc = allc && dc && cc;
     }
+  }
   }
   if (!__all_sync(EQC_FULL, ok)) {
     if (lane == 0) set_corrupt(p.status);
@@ -1447,13 +1467,9 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
                                      : stage_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + e.x, e.y, lane,
                                                     stage);
         bool skip;
-        if (!decode_staged(r, e.y, L, lane, info, col, false, col, skip)) {
+        if (!decode_staged(r, e.y, L, lane, info, col, false, col, skip, (s_flags[i] & EQC_FLAG_SWIZZLE) != 0)) {
           if (lane == 0) set_corrupt(p.status);
           return false;
-        }
-        if (s_flags[i] & EQC_FLAG_SWIZZLE) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) col[j] = unswizzle(col[j]);
         }
       }
 #pragma unroll

@@ -502,6 +502,35 @@ __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, i
   return ld_window(r, min(ntok + cntb + (int)(nib & 1u), size), adv_sel(nib));
 }
 
+// unswizzle() of the four pixels held as plane words W[q] (byte j = byte q
+// of pixel j): the same delta swaps, as swaps within each word (steps inside a
+// byte) or between two words (steps across bytes); the byte reversal renames
+// the words.  48 operations for four pixels instead of 4 x 17.
+__device__ __forceinline__ void unswizzle_planes(uint32_t W[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) W[q] = delta_swap(delta_swap(W[q], 1, 0x22222222u), 3, 0x0A0A0A0Au);
+  // bits 2,3,6,7 of byte 0 (2) <-> bits 0,1,4,5 of byte 1 (3)
+  uint32_t t = ((W[0] >> 2) ^ W[1]) & 0x33333333u;
+  W[1] ^= t;
+  W[0] ^= t << 2;
+  t = ((W[2] >> 2) ^ W[3]) & 0x33333333u;
+  W[3] ^= t;
+  W[2] ^= t << 2;
+  // high nibble of byte 0 (1) <-> low nibble of byte 2 (3)
+  t = ((W[0] >> 4) ^ W[2]) & 0x0F0F0F0Fu;
+  W[2] ^= t;
+  W[0] ^= t << 4;
+  t = ((W[1] >> 4) ^ W[3]) & 0x0F0F0F0Fu;
+  W[3] ^= t;
+  W[1] ^= t << 4;
+  t = W[0];
+  W[0] = W[3];
+  W[3] = t;
+  t = W[1];
+  W[1] = W[2];
+  W[2] = t;
+}
+
 // 4x4 byte transpose: pixel j = byte j of the plane words W[0..3].
 __device__ __forceinline__ void planes_to_px(const uint32_t W[4], uint32_t px[4]) {
   const uint32_t t0 = __byte_perm(W[0], W[1], 0x5140), t1 = __byte_perm(W[0], W[1], 0x7362);
