@@ -1262,6 +1262,7 @@ struct FusedParams {
   int32_t *status;
   int64_t out_pitch;
   int n, w, h, S;
+  float invS;  // 1 / S
   int y0, y1;  // rows composited (a band of the full-frame streams); out_* point at row y0
   int vec;
 };
@@ -1296,7 +1297,17 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
   const int n = p.n;
   const int nch = p.S * p.h;
   const int64_t payload0 = 32 + 8 * (int64_t)nch;
-  const int y = c / p.S, k = c - y * p.S;
+  // y = c / S by a float reciprocal corrected by one (its error is below
+  // one row while h < 2^20; invS = 0 selects the integer division)
+  int y = p.invS != 0.f ? (int)((float)c * p.invS) : c / p.S;
+  int k = c - y * p.S;
+  if (k < 0) {
+    --y;
+    k += p.S;
+  } else if (k >= p.S) {
+    ++y;
+    k -= p.S;
+  }
   const int L = min(kC, p.w - k * kC);
   constexpr int NP = ONE ? 1 : 2;
   const int npass = ONE ? 1 : (n + 31) >> 5;
@@ -1417,11 +1428,12 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
         const uintptr_t ai = ((uintptr_t)__shfl_sync(EQC_FULL, (uint32_t)((uint64_t)a >> 32), i) << 32) |
                              __shfl_sync(EQC_FULL, (uint32_t)a, i);
         const uint32_t si = __shfl_sync(EQC_FULL, sn, i);
-        const int slot = (int)(si & 0xFFFFu), nq = (int)(si >> 16);
-        for (int q = lane; q < nq; q += 32) {
-          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(pre + slot + q);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(ai + 16 * (uintptr_t)q) : "memory");
-        }
+        const int slot = (int)(si & 0xFFFFu), nq = (int)(si >> 16);  // nq <= 34
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(pre + slot + lane);
+        const uintptr_t ga = ai + 16 * (uintptr_t)lane;
+        if (lane < nq) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(ga) : "memory");
+        if (lane + 32 < nq)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 512u), "l"(ga + 512) : "memory");
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1840,6 +1852,7 @@ int eqc_depth_rle_band(int n, const uint8_t *const *color_rle, const uint8_t *co
   p.w = w;
   p.h = h;
   p.S = (w + kC - 1) / kC;
+  p.invS = h < (1 << 20) ? 1.0f / (float)p.S : 0.f;
   p.y0 = y0;
   p.y1 = y1;
   p.vec = ((out_pitch % 4) == 0 && aligned(out_color, 16) && (!out_depth || aligned(out_depth, 16))) ? 1 : 0;
