@@ -850,13 +850,15 @@ __device__ __forceinline__ bool probe_const(const uint8_t *rec, uint32_t ps, int
 
 // Decode a staged record into px[0..3], planes in the order 3, 0, 1, 2 (the
 // most significant byte first).  With `check`, when that byte alone makes the
-// source deeper than best[] at every pixel of the chunk (it then cannot win:
-// ties keep the lower index), planes 0-2 are not decoded and `skip` is set.
+// source deeper than the current best at every pixel of the chunk (bm: byte j
+// = the best depth's most significant byte at pixel j; vinv: 0xFF bytes for
+// pixels past the chunk) it cannot win (ties keep the lower index): planes
+// 0-2 are not decoded and `skip` is set.
 // One decode_plane_w call site (the kernels must stay inside the instruction
 // cache).  Warp-uniform result; false on a malformed record.
 __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int L, int lane, uint16_t *info,
-                                              uint32_t px[4], bool check, const uint32_t best[4], bool &skip,
-                                              bool swz = false) {
+                                              uint32_t px[4], bool check, uint32_t bm, uint32_t vinv,
+                                              bool &skip, bool swz = false) {
   // plane sizes and record offsets in decode order: rotate plane 3 first
   uint32_t sz = __funnelshift_l(ps, ps, 8);  // bytes: s3, s0, s1, s2
   int off = (int)(ps & 0xFFu) + (int)((ps >> 8) & 0xFFu) + (int)((ps >> 16) & 0xFFu);
@@ -872,10 +874,7 @@ __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int
     X1 = X0;
     X0 = w;
     if (t == 0 && check && ok) {
-      bool lose = true;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) lose = lose && (4 * lane + j >= L || ((w >> (8 * j)) & 0xFFu) > (best[j] >> 24));
-      if (__all_sync(EQC_FULL, lose)) {
+      if (__all_sync(EQC_FULL, (__vcmpgtu4(w, bm) | vinv) == 0xFFFFFFFFu)) {
         skip = true;
         return true;
       }
@@ -1238,7 +1237,7 @@ __global__ void __launch_bounds__(kWarps * 32, EQC_DEC_MINB) rle_decode_kernel(c
         const uint8_t *rec = im.src + hd.payload0 + offi;
         bool skip;
         const bool okr = decode_staged(stage[warp][buf] + ((uintptr_t)rec & 15u), psi, Li, lane, info[warp], px,
-                                       false, px, skip, swz);
+                                       false, 0u, 0u, skip, swz);
         __syncwarp();  // the buffer is refilled two records later
         buf ^= 1;
         if (!okr) {
@@ -1390,6 +1389,9 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
   uint32_t bd[4] = {0, 0, 0, 0};
   int bi[4] = {0, 0, 0, 0};
   uint32_t bc[4] = {0, 0, 0, 0};
+  uint32_t bm = 0;  // byte j: most significant byte of bd[j]
+  const int nv = min(max(L - 4 * lane, 0), 4);
+  const uint32_t vinv = nv >= 4 ? 0u : ~((1u << (8 * nv)) - 1u);  // 0xFF bytes: pixels past the chunk
   constexpr int kPreQuads = kPreWords / 4;
   if constexpr (ONE) {
     // Lane i plans source i: 16-byte slots of its depth and colour records in
@@ -1452,7 +1454,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
                                      : stage_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + e.x,
                                                     e.y, lane, stage);
         bool skip = false;
-        if (!decode_staged(r, e.y, L, lane, info, d, i > 0, bd, skip)) {
+        if (!decode_staged(r, e.y, L, lane, info, d, i > 0, bm, vinv, skip)) {
           if (lane == 0) set_corrupt(p.status);
           return false;
         }
@@ -1464,6 +1466,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
         bd[j] = t ? d[j] : bd[j];
         bi[j] = t ? i : bi[j];
       }
+      bm = __byte_perm(__byte_perm(bd[0], bd[1], 0x0073), __byte_perm(bd[2], bd[3], 0x0073), 0x5410);
     }
     // colour pass: only the sources that win at least one pixel of the chunk
     for (int i = 0; i < n; ++i) {
@@ -1479,7 +1482,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
                                      : stage_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + e.x, e.y, lane,
                                                     stage);
         bool skip;
-        if (!decode_staged(r, e.y, L, lane, info, col, false, col, skip, (s_flags[i] & EQC_FLAG_SWIZZLE) != 0)) {
+        if (!decode_staged(r, e.y, L, lane, info, col, false, 0u, 0u, skip, (s_flags[i] & EQC_FLAG_SWIZZLE) != 0)) {
           if (lane == 0) set_corrupt(p.status);
           return false;
         }
@@ -1501,7 +1504,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
       } else {
         bool skip = false;
         const uint8_t *r = stage_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + dx, dy, lane, stage);
-        if (!decode_staged(r, dy, L, lane, info, d, i > 0, bd, skip)) {
+        if (!decode_staged(r, dy, L, lane, info, d, i > 0, bm, vinv, skip)) {
           if (lane == 0) set_corrupt(p.status);
           return false;
         }
@@ -1513,6 +1516,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
         bd[j] = t ? d[j] : bd[j];
         bi[j] = t ? i : bi[j];
       }
+      bm = __byte_perm(__byte_perm(bd[0], bd[1], 0x0073), __byte_perm(bd[2], bd[3], 0x0073), 0x5410);
     }
     for (int i = 0; i < n; ++i) {
       if (!__any_sync(EQC_FULL, bi[0] == i || bi[1] == i || bi[2] == i || bi[3] == i)) continue;
@@ -1527,7 +1531,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
       } else {
         bool skip;
         const uint8_t *r = stage_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, lane, stage);
-        if (!decode_staged(r, cy, L, lane, info, col, false, col, skip)) {
+        if (!decode_staged(r, cy, L, lane, info, col, false, 0u, 0u, skip)) {
           if (lane == 0) set_corrupt(p.status);
           return false;
         }
