@@ -665,6 +665,9 @@ struct Cmp3Params {
 };
 
 constexpr int kCmp3Warps = 8;
+#ifndef EQC_CMP_U
+#define EQC_CMP_U 4
+#endif
 #ifndef EQC_CMP_REVERSE
 #define EQC_CMP_REVERSE 1
 #endif
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(kCmp3Warps * 32) rle_compact3_kernel(const __g
   const int run = __ldcg(rs + r);
   uint2 e = make_uint2(0u, 0u);
   if (lane < cnt) e = __ldcg(table + lane);
-  constexpr int U = 4;  // words per lane in the first round (512 B per warp: a background run)
+  constexpr int U = EQC_CMP_U;  // words per lane in the first round (128 B per warp each)
   uint32_t w[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) w[u] = __ldcg(src + 32 * u + lane);
