@@ -1421,6 +1421,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
       desc[32 + lane] = make_uint4(ec[0].x, ec[0].y, ec[0].z,
                                    ec[0].w ? 1u : ((((uint32_t)(uintptr_t)recc & 15u) << 1) | ((uint32_t)(sc0 + 1) << 5)));
     }
+    const unsigned ncd = __ballot_sync(EQC_FULL, act && !ed[0].w);  // non-constant depth chunks
     // prefetch: one round trip for every prefetched record of the position
 #pragma unroll 1
     for (int kind = 0; kind < 2; ++kind) {
@@ -1444,36 +1445,47 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-    // depth pass: running minimum and the index of the winning source per pixel
-    for (int i = 0; i < n; ++i) {
-      const uint4 e = desc[i];
-      uint32_t d[4];
-      if (e.w & 1u) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) d[j] = e.z;
-      } else {
-        const int slot = (int)(e.w >> 5) - 1;
-        const uint8_t *r = slot >= 0 ? reinterpret_cast<const uint8_t *>(pre + slot) + ((e.w >> 1) & 15u)
-                                     : stage_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + e.x,
-                                                    e.y, lane, stage);
-        bool skip = false;
-        if (!decode_staged(r, e.y, L, lane, info, d, i > 0, bm, vinv, skip)) {
-          if (lane == 0) set_corrupt(p.status);
-          return false;
-        }
-        if (skip) continue;  // deeper than the current best everywhere: cannot win
-      }
+    // depth pass.  The constant depth chunks are reduced first (minimum, ties
+    // to the lowest index: one warp reduction); the non-constant records are
+    // then merged in index order, a tie going to the lower index.
+    {
+      const uint32_t cd = (lane < n && ed[0].w) ? ed[0].z : 0xFFFFFFFFu;
+      const uint32_t m = __reduce_min_sync(EQC_FULL, cd);
+      const unsigned who = __ballot_sync(EQC_FULL, lane < n && ed[0].w && cd == m);
+      const int ci = who ? __ffs(who) - 1 : n;  // n: no constant chunk (any source ties it)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const bool t = (i == 0) || d[j] < bd[j];  // ties keep the lower index
+        bd[j] = m;
+        bi[j] = ci;
+      }
+      bm = m >> 24 | (m >> 24) << 8 | (m >> 24) << 16 | (m >> 24) << 24;
+    }
+    for (unsigned todo = ncd; todo; todo &= todo - 1) {
+      const int i = __ffs(todo) - 1;
+      const uint4 e = desc[i];
+      uint32_t d[4];
+      const int slot = (int)(e.w >> 5) - 1;
+      const uint8_t *r = slot >= 0 ? reinterpret_cast<const uint8_t *>(pre + slot) + ((e.w >> 1) & 15u)
+                                   : stage_record(p.src[n + i], p.src_bytes[n + i], p.src[n + i] + payload0 + e.x,
+                                                  e.y, lane, stage);
+      bool skip = false;
+      if (!decode_staged(r, e.y, L, lane, info, d, true, bm, vinv, skip)) {
+        if (lane == 0) set_corrupt(p.status);
+        return false;
+      }
+      if (skip) continue;  // deeper than the current best everywhere: cannot win
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool t = d[j] < bd[j] || (d[j] == bd[j] && i < bi[j]);
         bd[j] = t ? d[j] : bd[j];
         bi[j] = t ? i : bi[j];
       }
       bm = __byte_perm(__byte_perm(bd[0], bd[1], 0x0073), __byte_perm(bd[2], bd[3], 0x0073), 0x5410);
     }
     // colour pass: only the sources that win at least one pixel of the chunk
-    for (int i = 0; i < n; ++i) {
-      if (!__any_sync(EQC_FULL, bi[0] == i || bi[1] == i || bi[2] == i || bi[3] == i)) continue;
+    const unsigned wins = __reduce_or_sync(EQC_FULL, (1u << bi[0]) | (1u << bi[1]) | (1u << bi[2]) | (1u << bi[3]));
+    for (unsigned todo = wins; todo; todo &= todo - 1) {
+      const int i = __ffs(todo) - 1;
       const uint4 e = desc[32 + i];
       uint32_t col[4];
       if (e.w & 1u) {
