@@ -402,7 +402,7 @@ __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, i
     uint32_t A[4];
     if (ntok <= 32) {
       // lane t holds token t: starts and payload sums by one packed warp
-      // scan, then the S and E masks by OR-reductions
+      // scan, then the mask words by OR-reductions of the token ranges
       const bool act = lane < ntok;
       const int c = act ? r[1 + lane] : 0;
       const int len = act ? (c & 0x7F) + 1 : 0;
@@ -413,21 +413,13 @@ __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, i
       const uint32_t tot = __shfl_sync(EQC_FULL, inc, 31);
       ok = ok && (int)(tot & 0xFFFFu) == L && (int)(tot >> 16) == size - 1 - ntok;
       const int s = (int)((inc - packed) & 0xFFFFu);
-      const int e = lit ? s + len : s + 1;
-      const uint32_t sb = act ? 1u << (s & 31) : 0u, eb = act ? 1u << (e & 31) : 0u;
-      uint32_t S[4], E[4];
+      const int e = lit ? s + len : s + 1;  // (an absent token: e = s, an empty range)
+      // word w of the mask: OR over the tokens of [s, e) within the word
+      // (mask_ge(n) = ~0 << n, 0 for n >= 32: a clamped funnel shift)
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        S[w] = __reduce_or_sync(EQC_FULL, (s >> 5) == w ? sb : 0u);
-        E[w] = __reduce_or_sync(EQC_FULL, (e >> 5) == w ? eb : 0u);  // e == 128: dropped
-      }
-      const uint64_t lo = ((uint64_t)E[1] << 32 | E[0]) - ((uint64_t)S[1] << 32 | S[0]);
-      const uint64_t hi = ((uint64_t)E[3] << 32 | E[2]) - ((uint64_t)S[3] << 32 | S[2]) -
-                          (((uint64_t)E[1] << 32 | E[0]) < ((uint64_t)S[1] << 32 | S[0]) ? 1u : 0u);
-      A[0] = (uint32_t)lo;
-      A[1] = (uint32_t)(lo >> 32);
-      A[2] = (uint32_t)hi;
-      A[3] = (uint32_t)(hi >> 32);
+      for (int w = 0; w < 4; ++w)
+        A[w] = __reduce_or_sync(EQC_FULL, __funnelshift_lc(0u, ~0u, max(s - 32 * w, 0)) &
+                                              ~__funnelshift_lc(0u, ~0u, max(e - 32 * w, 0)));
     } else {
       // lane l holds tokens 4l .. 4l+3 (of at most 128: ntok <= L); S and E
       // as byte markers in the scratch, gathered into words by shuffles
