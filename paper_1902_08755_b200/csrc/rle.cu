@@ -1010,16 +1010,12 @@ __device__ __forceinline__ bool entry_lane(const uint8_t *src, int64_t payload_b
 __device__ __forceinline__ bool entry_local(const uint8_t *src, int64_t payload_bytes, int64_t nchunks, int64_t c,
                                             int L, int64_t &off, uint32_t &ps) {
   const uint2 te = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * c));
+  const uint2 tp = c > 0 ? __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * (c - 1))) : make_uint2(0u, 0u);
   off = te.x;
   ps = te.y;
-  const int s0 = ps & 0xFF, s1 = (ps >> 8) & 0xFF, s2 = (ps >> 16) & 0xFF, s3 = ps >> 24;
-  const int64_t end = off + s0 + s1 + s2 + s3;
-  int64_t prev = 0;
-  if (c > 0) {
-    const uint2 tp = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * (c - 1)));
-    prev = (int64_t)tp.x + (tp.y & 0xFF) + ((tp.y >> 8) & 0xFF) + ((tp.y >> 16) & 0xFF) + (tp.y >> 24);
-  }
-  bool ok = off == prev && end <= payload_bytes && s0 <= L + 2 && s1 <= L + 2 && s2 <= L + 2 && s3 <= L + 2;
+  const int64_t end = off + (int64_t)__dp4a(ps, 0x01010101u, 0u);           // + the four plane sizes
+  const int64_t prev = (int64_t)tp.x + (int64_t)__dp4a(tp.y, 0x01010101u, 0u);  // chunk c-1's end
+  bool ok = off == prev && end <= payload_bytes && __vcmpgtu4(ps, (uint32_t)(L + 2) * 0x01010101u) == 0u;
   if (c == nchunks - 1) ok = ok && end == payload_bytes;
   return ok;
 }
@@ -1327,7 +1323,6 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
       ok = entry_local(p.src[q], s_pb[q], nch, c, L, o, ps);
       uint32_t v = 0;
       const bool cst = ok && probe_const(p.src[q] + payload0 + o, ps, L, v);
-      if (cst && q < n && (s_flags[q] & EQC_FLAG_SWIZZLE)) v = unswizzle(v);
       e = make_uint4((uint32_t)o, ps, v, cst ? 1u : 0u);
       allc = cst;
     }
@@ -1350,7 +1345,6 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
       uint32_t dv = 0, cv = 0;
       const bool dc = ok && probe_const(p.src[n + i] + payload0 + od, pd, L, dv);
       const bool cc = ok && probe_const(p.src[i] + payload0 + oc, pc, L, cv);
-      if (cc && (s_flags[i] & EQC_FLAG_SWIZZLE)) cv = unswizzle(cv);
       ed[ps] = make_uint4((uint32_t)od, pd, dv, dc ? 1u : 0u);
       ec[ps] = make_uint4((uint32_t)oc, pc, cv, cc ? 1u : 0u);
       allc = allc && dc && cc;
@@ -1383,6 +1377,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
         bi = ii;
       }
     }
+    if (s_flags[bi] & EQC_FLAG_SWIZZLE) bcv = unswizzle(bcv);  // (constant colour values are kept as coded)
     const uint32_t pc[4] = {bcv, bcv, bcv, bcv}, pd[4] = {bdv, bdv, bdv, bdv};
     store_px(p.out_color + row, L, lane, p.vec != 0, pc);
     if (p.out_depth) store_px(p.out_depth + row, L, lane, p.vec != 0, pd);
@@ -1489,8 +1484,9 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
       const uint4 e = desc[32 + i];
       uint32_t col[4];
       if (e.w & 1u) {
+        const uint32_t v = (s_flags[i] & EQC_FLAG_SWIZZLE) ? unswizzle(e.z) : e.z;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) col[j] = e.z;  // already unswizzled
+        for (int j = 0; j < 4; ++j) col[j] = v;
       } else {
         const int slot = (int)(e.w >> 5) - 1;
         const uint8_t *r = slot >= 0 ? reinterpret_cast<const uint8_t *>(pre + slot) + ((e.w >> 1) & 15u)
@@ -1541,8 +1537,9 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
                      cz = __shfl_sync(EQC_FULL, e2.z, li), cw = __shfl_sync(EQC_FULL, e2.w, li);
       uint32_t col[4];
       if (cw) {
+        const uint32_t v = (s_flags[i] & EQC_FLAG_SWIZZLE) ? unswizzle(cz) : cz;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) col[j] = cz;
+        for (int j = 0; j < 4; ++j) col[j] = v;
       } else {
         bool skip;
         const uint8_t *r = stage_record(p.src[i], p.src_bytes[i], p.src[i] + payload0 + cx, cy, lane, stage);
