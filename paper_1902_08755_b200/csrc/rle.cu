@@ -1417,12 +1417,9 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
                                    ec[0].w ? 1u : ((((uint32_t)(uintptr_t)recc & 15u) << 1) | ((uint32_t)(sc0 + 1) << 5)));
     }
     const unsigned ncd = __ballot_sync(EQC_FULL, act && !ed[0].w);  // non-constant depth chunks
-    // prefetch: one round trip for every prefetched record of the position
-#pragma unroll 1
-    for (int kind = 0; kind < 2; ++kind) {
-      unsigned m = __ballot_sync(EQC_FULL, kind ? fc : fd);
-      const uintptr_t a = kind ? ac : ad;
-      const uint32_t sn = kind ? ((uint32_t)sc0 | ((uint32_t)nwc << 16)) : ((uint32_t)sd0 | ((uint32_t)nwd << 16));
+    // prefetch: the depth records in one round trip now; the colour records
+    // of the winning sources only, after the depth pass
+    auto prefetch = [&](unsigned m, uintptr_t a, uint32_t sn) {
       while (m) {
         const int i = __ffs(m) - 1;
         m &= m - 1;
@@ -1436,10 +1433,11 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
         if (lane + 32 < nq)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 512u), "l"(ga + 512) : "memory");
       }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+    };
+    prefetch(__ballot_sync(EQC_FULL, fd), ad, (uint32_t)sd0 | ((uint32_t)nwd << 16));
     // depth pass.  The constant depth chunks are reduced first (minimum, ties
     // to the lowest index: one warp reduction); the non-constant records are
     // then merged in index order, a tie going to the lower index.
@@ -1479,6 +1477,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
     }
     // colour pass: only the sources that win at least one pixel of the chunk
     const unsigned wins = __reduce_or_sync(EQC_FULL, (1u << bi[0]) | (1u << bi[1]) | (1u << bi[2]) | (1u << bi[3]));
+    prefetch(__ballot_sync(EQC_FULL, fc) & wins, ac, (uint32_t)sc0 | ((uint32_t)nwc << 16));
     for (unsigned todo = wins; todo; todo &= todo - 1) {
       const int i = __ffs(todo) - 1;
       const uint4 e = desc[32 + i];
