@@ -280,6 +280,10 @@ def run_eqc(args):
     # queueing behind the next frame's encoder CTAs
     comm_stream = (torch.cuda.Stream(device=dev, priority=0 if args.no_comm_priority else -1)
                    if pipelined else stream)
+    # --scatter: the fused decode stores band j straight into rank j's frame
+    # slot (compositor_depth_rle_scatter) and the compose composites local
+    # copies (compose_direct_send_scattered): the exchange rides the decoder
+    scatter = bool(args.scatter and slots and pipelined and args.exchange == "raw")
     composed = [None, None]  # event: compose of the frame in outs[i] finished
     nstep = [0]
 
@@ -296,10 +300,25 @@ def run_eqc(args):
             e1.record(stream)
         if pipelined and composed[k % 2] is not None:
             stream.wait_event(composed[k % 2])  # the compose of frame k-2 has read this buffer
-        eqc.compositor_depth_rle(streams[:NSRC], streams[NSRC:], oc, od, status, stream=stream)
+        if scatter:  # the exchange rides the decoder: band j into rank j's slot k % 2
+            eqc.compositor_depth_rle_scatter(comm, streams[:NSRC], streams[NSRC:], W, H, k % 2, status,
+                                             stream=stream)
+        else:
+            eqc.compositor_depth_rle(streams[:NSRC], streams[NSRC:], oc, od, status, stream=stream)
         if timed_events is not None:
             e2.record(stream)
-        if comm is not None:
+        if comm is not None and scatter:
+            ready = torch.cuda.Event()
+            ready.record(stream)
+            comm_stream.wait_event(ready)
+            eqc.compose_direct_send_scattered(comm, W, H, k % 2, final, dest_rank=0, flags=xflags, stream=comm_stream)
+            if d2h is not None:
+                with torch.cuda.stream(comm_stream):
+                    d2h.copy_(final if final is not None else oc, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(comm_stream)
+            composed[k % 2] = ev
+        elif comm is not None:
             # screen-partition direct send of this GPU's partial frame
             if pipelined:
                 ready = torch.cuda.Event()
@@ -552,7 +571,10 @@ def run_eqc(args):
             "parallelism": (f"screen-partition direct send ({args.exchange}) over {world} GPU(s)" +
                             (", compose of frame k overlapped with frame k+1 (async compositing pipeline, "
                              "P:2302-2310)" if pipelined else "") +
-                            (", partial frames decoded into peer-mapped frame slots (zero-copy)" if slots else "") +
+                            (", partial frames decoded into peer-mapped frame slots (zero-copy)" if slots and not scatter
+                             else "") +
+                            (", fused decode stores band j into rank j's frame slot over NVLink "
+                             "(compositor_depth_rle_scatter; the exchange rides the decode)" if scatter else "") +
                             (", EQC_FLAG_OVERLAP (peer pulls <= 1 CTA/SM)" if xflags & eqc.FLAG_OVERLAP else "") +
                             (", compose on a high-priority stream" if pipelined and not args.no_comm_priority else "")
                             ) if world > 1 else "single GPU",
@@ -698,6 +720,8 @@ def main():
                     help="N>1 pipelined: do not pass EQC_FLAG_OVERLAP (peer pulls then take every SM)")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="N > 1: run the multi-GPU compose of frame k before encoding frame k+1")
+    ap.add_argument("--scatter", action="store_true",
+                    help="N>1: the fused decode writes band j into rank j's frame slot (exchange inside the decode)")
     ap.add_argument("--exchange", default="raw", choices=["raw", "rle", "nccl"],
                     help="direct-send band transport for N > 1: raw = NVLink peer-memory pull fused with the "
                          "band composite, nccl = raw bands over NCCL send/recv, rle = RLE streams over NCCL")

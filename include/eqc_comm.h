@@ -135,6 +135,35 @@ EQC_API int compose_direct_send_rle_pull(eqc_comm *comm, int n_local, int w, int
                                          uint32_t *out_color, int64_t out_pitch, int32_t *d_status, void *stream);
 
 /*
+ * compositor_depth_rle_scatter + compose_direct_send_scattered -- direct send
+ * with the exchange riding the decoder (the thesis's asynchronous pipeline,
+ * P:2302-2310, with "transmit" fused into "decompress").  Rank r runs the
+ * fused decode + depth composite of its n_local sources (as
+ * compositor_depth_rle) band by band (bands R-C13), and stores band j
+ * straight into frame slot `slot` of rank j over NVLink, as copy r of that
+ * band: rows [r * maxband, r * maxband + rows_j) of the slot (pitch w,
+ * maxband = the largest band).  compose_direct_send_scattered then, on every
+ * rank after a peer-memory barrier, composites the n copies of its band from
+ * its own slot (HBM reads only; global source order rank-major, R-C5) and
+ * stores the result into the destination's frame (colour only), as
+ * compose_direct_send.  Both are collective in the sense that every rank
+ * calls them with the same w, h, slot; the scatter of frame k into slot i
+ * must be ordered after every rank's compose of the previous frame that used
+ * slot i (the compose ends with a barrier: order the scatter after it on the
+ * caller's streams).  Slots come from eqc_comm_frame_buffers (they hold the
+ * scattered layout).  d_status as compositor_depth_rle.  flags:
+ * EQC_FLAG_OVERLAP caps the band composite at one CTA per SM.
+ * Errors: EQC_E_INVALID (arguments, slots smaller than the layout),
+ * EQC_E_UNSUPPORTED (one rank, no peer mapping or frame slots), EQC_E_CUDA.
+ */
+EQC_API int compositor_depth_rle_scatter(eqc_comm *comm, int n_local, const uint8_t *const *color_rle,
+                                         const uint8_t *const *depth_rle, const int64_t *color_bytes,
+                                         const int64_t *depth_bytes, int w, int h, int slot, int32_t *d_status,
+                                         void *stream);
+EQC_API int compose_direct_send_scattered(eqc_comm *comm, int w, int h, int slot, int dest_rank,
+                                          uint32_t *out_color, int64_t out_pitch, int flags, void *stream);
+
+/*
  * Host-side schedule plans (no GPU needed; used by the executors below and
  * by the tests).
  * eqc_plan_bands: row0[j] = floor(j*h/n), j = 0..n (band j = rows

@@ -16,6 +16,7 @@
 // stream, NVLink 5 / NVSwitch).
 #include <nccl.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -2073,7 +2074,8 @@ extern "C" int eqc_comm_frame_buffers(eqc_comm *comm, int w, int h, int slot, ui
   const int64_t px = (int64_t)w * h;
   EQC_TRY(p2p_setup(comm, px, s));
   if (comm->p2p.capable != 1) return EQC_E_UNSUPPORTED;
-  EQC_TRY(p2p_slots(comm, px, s));
+  // + n rows: the scattered layout (n copies of the largest band) fits too
+  EQC_TRY(p2p_slots(comm, px + (int64_t)w * comm->nranks, s));
   *color = comm->p2p.slot_c[slot].as<uint32_t>();
   *depth = comm->p2p.slot_d[slot].as<uint32_t>();
   *final_color = comm->p2p.fin_c.as<uint32_t>();
@@ -2182,6 +2184,101 @@ extern "C" int compose_direct_send_rle_pull(eqc_comm *comm, int n_local, int w, 
   EQC_TRY(p2p_setup(comm, (int64_t)w * h, s));
   if (P.capable != 1) return EQC_E_UNSUPPORTED;
   return rle_pull_body(comm, n_local, w, h, slot, dest_rank, out_color, out_pitch, d_status, s);
+}
+
+// ---- fused decode + scatter (the exchange rides the decode) -----------------
+// Band layout in a frame slot for the scattered direct send: copy r (the
+// partial of band j from rank r) at rows [r * maxband, r * maxband + rows_j)
+// of rank j's slot, pitch w.
+namespace {
+int scatter_geometry(eqc_comm *c, int w, int h, std::vector<int> &row0, int &maxband) {
+  const int n = c->nranks;
+  row0.assign(n + 1, 0);
+  plan_bands(h, n, row0.data());
+  maxband = 0;
+  for (int j = 0; j < n; ++j) maxband = std::max(maxband, row0[j + 1] - row0[j]);
+  return (int64_t)n * maxband * w <= c->p2p.slot_px ? EQC_OK : EQC_E_INVALID;
+}
+}  // namespace
+
+extern "C" int compositor_depth_rle_scatter(eqc_comm *comm, int n_local, const uint8_t *const *color_rle,
+                                            const uint8_t *const *depth_rle, const int64_t *color_bytes,
+                                            const int64_t *depth_bytes, int w, int h, int slot, int32_t *d_status,
+                                            void *stream) {
+  if (!comm || n_local < 1 || n_local > EQC_MAX_SOURCES || !color_rle || !depth_rle || !color_bytes ||
+      !depth_bytes || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || !d_status)
+    return EQC_E_INVALID;
+  if (comm->nranks < 2) return EQC_E_UNSUPPORTED;
+  P2PState &P = comm->p2p;
+  if (P.capable != 1 || P.peer_slot_c[slot].size() != (size_t)comm->nranks) return EQC_E_UNSUPPORTED;
+  std::vector<int> row0;
+  int maxband = 0;
+  EQC_TRY(scatter_geometry(comm, w, h, row0, maxband));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = comm->nranks, me = comm->rank;
+  // the peers' bands first (their stores cross NVLink while the own band is decoded)
+  for (int k = 1; k <= n; ++k) {
+    const int j = (me + k) % n;
+    if (row0[j + 1] <= row0[j]) continue;
+    const size_t off = (size_t)me * maxband * w;
+    EQC_TRY(eqc_depth_rle_band(n_local, color_rle, depth_rle, color_bytes, depth_bytes, w, h, row0[j], row0[j + 1],
+                               P.peer_slot_c[slot][j] + off, P.peer_slot_d[slot][j] + off, w, d_status, s));
+  }
+  return EQC_OK;
+}
+
+extern "C" int compose_direct_send_scattered(eqc_comm *comm, int w, int h, int slot, int dest_rank,
+                                             uint32_t *out_color, int64_t out_pitch, int flags, void *stream) {
+  if (!comm || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || dest_rank < 0 ||
+      dest_rank >= comm->nranks)
+    return EQC_E_INVALID;
+  const int n = comm->nranks, me = comm->rank;
+  if (me == dest_rank && (!out_color || out_pitch < w)) return EQC_E_INVALID;
+  if (n < 2) return EQC_E_UNSUPPORTED;
+  P2PState &P = comm->p2p;
+  if (P.capable != 1 || P.peer_slot_c[slot].size() != (size_t)n) return EQC_E_UNSUPPORTED;
+  std::vector<int> row0;
+  int maxband = 0;
+  EQC_TRY(scatter_geometry(comm, w, h, row0, maxband));
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *stats = comm->st.stats;
+  for (int i = 0; i < 4; ++i) stats[i] = 0;
+  // every rank's scattered bands are in place (and every rank passed this slot)
+  EQC_TRY(p2p_barrier(comm, s, 1, slot));
+  const int y0 = row0[me], rows = row0[me + 1] - row0[me];
+  if (rows > 0) {
+    // band composite of the n copies in my slot (local reads), output pushed
+    // into the destination's frame; global source order rank-major (R-C5)
+    std::vector<const uint32_t *> cs(n), ds(n);
+    for (int q = 0; q < n; ++q) {
+      cs[q] = P.slot_c[slot].as<uint32_t>() + (size_t)q * maxband * w;
+      ds[q] = P.slot_d[slot].as<uint32_t>() + (size_t)q * maxband * w;
+    }
+    uint32_t *out = me == dest_rank ? out_color + (size_t)y0 * out_pitch : P.peer_fin_c[dest_rank] + (size_t)y0 * w;
+    const int64_t opitch = me == dest_rank ? out_pitch : w;
+    eqc_grid_cap = (flags & EQC_FLAG_OVERLAP) ? eqc_num_sms() : 0;
+    const int rc = compositor_depth(n, cs.data(), ds.data(), w, rows, w, out, nullptr, opitch, s);
+    eqc_grid_cap = 0;
+    EQC_TRY(rc);
+    stats[0] = n - 1;
+    stats[3] = (int64_t)(n - 1) * rows * w * 8;  // received (written by the peers' decodes)
+    if (me != dest_rank) {
+      stats[1] = 1;
+      stats[2] = (int64_t)rows * w * 4;
+    }
+  }
+  // every band is on the destination; nobody reads the slot any more
+  EQC_TRY(p2p_barrier(comm, s));
+  if (me == dest_rank && !(out_color == P.fin_c.as<uint32_t>() && out_pitch == w)) {
+    for (int q = 0; q < n; ++q) {
+      const int qy0 = row0[q], qrows = row0[q + 1] - row0[q];
+      if (q == me || qrows == 0) continue;
+      EQC_CUDA_TRY(cudaMemcpy2DAsync(out_color + (size_t)qy0 * out_pitch, out_pitch * 4,
+                                     P.fin_c.as<uint32_t>() + (size_t)qy0 * w, (size_t)w * 4, (size_t)w * 4, qrows,
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return EQC_OK;
 }
 
 extern "C" int eqc_comm_check(eqc_comm *comm, void *stream) {

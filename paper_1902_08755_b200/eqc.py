@@ -71,6 +71,8 @@ def _load():
         "eqc_comm_frame_buffers": ([P, i32, i32, i32, P, P, P, P], i32),
         "eqc_comm_stream_buffers": ([P, i32, i64, i32, P, P], i32),
         "compose_direct_send_rle_pull": ([P, i32, i32, i32, i32, i32, P, i64, P, P], i32),
+        "compositor_depth_rle_scatter": ([P, i32, P, P, P, P, i32, i32, i32, P, P], i32),
+        "compose_direct_send_scattered": ([P, i32, i32, i32, i32, P, i64, i32, P], i32),
         "compose_direct_send_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, i32, P, i64, P, P], i32),
         "compose_direct_send_rle_pull_local": ([i32, i32, P, i64, i32, i32, i32, P, i64, P, P, P], i32),
         "compose_binary_swap_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
@@ -397,6 +399,27 @@ def compose_direct_send_rle_pull(comm, n_local: int, w: int, h: int, slot: int, 
     return _check(_lib.compose_direct_send_rle_pull(comm.handle, n_local, w, h, slot, dest_rank, _addr(out_color),
                                                     opitch, _addr(status), _stream(stream)),
                   "compose_direct_send_rle_pull")
+
+
+def compositor_depth_rle_scatter(comm, color_streams, depth_streams, w: int, h: int, slot: int, d_status,
+                                 color_bytes=None, depth_bytes=None, stream=None):
+    """compositor_depth_rle_scatter: fused decode + depth composite of this
+    rank's sources, band j stored into rank j's frame slot `slot`."""
+    n = len(color_streams)
+    cb = [s.numel() for s in color_streams] if color_bytes is None else color_bytes
+    db = [s.numel() for s in depth_streams] if depth_bytes is None else depth_bytes
+    return _check(_lib.compositor_depth_rle_scatter(comm.handle, n, _ptrs(color_streams), _ptrs(depth_streams),
+                                                    _i64s(cb), _i64s(db), w, h, slot, _addr(d_status),
+                                                    _stream(stream)), "compositor_depth_rle_scatter")
+
+
+def compose_direct_send_scattered(comm, w: int, h: int, slot: int, out_color=None, dest_rank: int = 0,
+                                  flags: int = 0, stream=None):
+    """compose_direct_send_scattered: band composite of the copies the peers
+    scattered into frame slot `slot`; colour to dest_rank's out_color."""
+    opitch = _frame_geom(out_color)[2] if out_color is not None else w
+    return _check(_lib.compose_direct_send_scattered(comm.handle, w, h, slot, dest_rank, _addr(out_color), opitch,
+                                                     flags, _stream(stream)), "compose_direct_send_scattered")
 
 
 def compose_direct_send(comm, colors, depths, out_color=None, dest_rank: int = 0, flags: int = 0,

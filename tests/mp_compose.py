@@ -191,6 +191,36 @@ def main():
         if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.depth_composite(c, d)[0]).all():
             failures.append(f"rle-pull {w}x{h} nl={nl} out={'gather' if k == 3 else 'user'}: mismatch")
         dist.barrier()
+    # the exchange riding the decoder: each rank's fused decode stores band j
+    # of its sources into rank j's frame slot (compositor_depth_rle_scatter),
+    # then every rank composites the copies of its band from its own slot
+    # (compose_direct_send_scattered); unequal bands (h % n != 0) included
+    for k, (nl, w, h, dest) in enumerate([(2, 640, 361, 0), (3, 1920, 1080, world - 1), (1, 300, 41, 1 % world),
+                                          (2, 640, 361, 0)]):
+        N = world * nl
+        c, d = synth.depth_sources(synth.SEED_BASE + 900 + N + w + k, N, w, h)
+        mine = range(rank * nl, (rank + 1) * nl)
+        imgs = [torch.from_numpy(c[i].view(np.int32)).to(dev) for i in mine] + \
+               [torch.from_numpy(d[i].view(np.int32)).to(dev) for i in mine]
+        cap = eqc.image_rle_max_size(w, h)
+        streams = [torch.zeros(cap, dtype=torch.uint8, device=dev) for _ in imgs]
+        sizes = torch.zeros(2 * nl, dtype=torch.int64, device=dev)
+        ws = torch.zeros(eqc.image_rle_workspace_size_batch(2 * nl, w, h), dtype=torch.uint8, device=dev)
+        eqc.image_compress_rle_batch(imgs, [0] * nl + [1] * nl, [1] * nl + [0] * nl, streams, sizes, ws)
+        fb = comm.frame_buffers(w, h, k % 2)
+        out = fb[2] if k == 3 else torch.zeros((h, w), dtype=torch.int32, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        eqc.compositor_depth_rle_scatter(comm, streams[:nl], streams[nl:], w, h, k % 2, status)
+        eqc.compose_direct_send_scattered(comm, w, h, k % 2, out if rank == dest else None, dest_rank=dest,
+                                          flags=eqc.FLAG_OVERLAP if k % 2 else 0)
+        torch.cuda.synchronize()
+        if int(status.item()) != 0:
+            failures.append(f"scatter {w}x{h} nl={nl}: status {int(status.item())}")
+        if rank == dest and not (out.cpu().numpy().view(np.uint32) == oracle.depth_composite(c, d)[0]).all():
+            failures.append(f"scatter {w}x{h} nl={nl} out={'gather' if k == 3 else 'user'}: mismatch")
+        if comm.stats()[0] != world - 1:
+            failures.append(f"scatter: rank {rank} received {comm.stats()[0]} bands, want {world - 1}")
+        dist.barrier()
     comm.destroy()
     t = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(t)
