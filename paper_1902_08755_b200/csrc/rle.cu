@@ -43,12 +43,16 @@ using namespace eqc_rle;
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
-constexpr int kSTChunksPerWarp = 16; // encoder: consecutive chunks per warp run (small: balances uneven chunks)
+#ifndef EQC_RUN_CHUNKS
+#define EQC_RUN_CHUNKS 16
+#endif
+constexpr int kSTChunksPerWarp = EQC_RUN_CHUNKS;  // encoder: consecutive chunks per warp run (small: balances uneven chunks)
 static_assert(kSTChunksPerWarp <= 64, "two table-entry registers per lane");
 constexpr int kEncWarps = EQC_ENC_WARPS;  // coder warps per CTA (encoder); warps are independent
 constexpr int kCompactWarps = 8;          // runs per CTA of the compaction kernel
 constexpr int kRecMax = 4 * (kC + 2);                  // worst-case chunk record bytes (520)
-constexpr int kScratchPerWarp = kSTChunksPerWarp * kRecMax;  // 8320 = 65 x 128 B
+// a run's scratch slot: whole 128-byte lines (the compaction discards them)
+constexpr int kScratchPerWarp = (kSTChunksPerWarp * kRecMax + 127) / 128 * 128;  // 16 chunks: 8320 = 65 x 128 B
 constexpr int kMaxBatch = 64;
 
 // workspace layout: run_size[count * runs_per_image] int32 (the coded bytes
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(kCompactWarps * 32) rle_compact_kernel(const _
 constexpr int kRun3 = kSTChunksPerWarp;  // chunks per encode item (same scratch layout as the RLE-64 path)
 constexpr int kE3Warps = EQC_E3_WARPS;
 
-struct E3Warp {
+struct __align__(16) E3Warp {  // (16-aligned: warps' spans are read as uint4)
   uint8_t span[kRun3 * kRecMax + 16];    // the run's records (+ garbage slack)
   uint8_t tp[(eqc_enc::kTpBytes + 4 + 15) & ~15];  // start list + trash bytes
   uint32_t cps[kRun3];
