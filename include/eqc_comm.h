@@ -422,6 +422,21 @@ EQC_API int compose_direct_send_rle_pull_local(int nranks, int n_local, const ui
                                                int64_t *out_stats, void *stream);
 
 /*
+ * compositor_depth_rle_scatter + compose_direct_send_scattered on ONE GPU
+ * (virtual ranks as above, each with its own frame slot): rank q's n_local
+ * colour / depth streams are color_rle / depth_rle[q * n_local + i] (bytes in
+ * color_bytes / depth_bytes).  Every rank decodes its bands into the ranks'
+ * slots, then composites the copies of its own band; colour lands in
+ * out_color on dest_rank.  d_status as compositor_depth_rle.  Synchronises
+ * `stream`.
+ */
+EQC_API int compose_direct_send_scatter_local(int nranks, int n_local, const uint8_t *const *color_rle,
+                                              const uint8_t *const *depth_rle, const int64_t *color_bytes,
+                                              const int64_t *depth_bytes, int w, int h, int dest_rank,
+                                              uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
+                                              int64_t *out_stats, void *stream);
+
+/*
  * eqc_comm_check -- synchronise `stream`, then report the comm's health:
  * EQC_E_NCCL if NCCL reports an asynchronous error (ncclCommGetAsyncError)
  * or a peer-memory flag wait gave up (a dead or stalled peer: every wait

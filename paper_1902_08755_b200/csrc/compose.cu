@@ -2201,20 +2201,14 @@ int scatter_geometry(eqc_comm *c, int w, int h, std::vector<int> &row0, int &max
 }
 }  // namespace
 
-extern "C" int compositor_depth_rle_scatter(eqc_comm *comm, int n_local, const uint8_t *const *color_rle,
-                                            const uint8_t *const *depth_rle, const int64_t *color_bytes,
-                                            const int64_t *depth_bytes, int w, int h, int slot, int32_t *d_status,
-                                            void *stream) {
-  if (!comm || n_local < 1 || n_local > EQC_MAX_SOURCES || !color_rle || !depth_rle || !color_bytes ||
-      !depth_bytes || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || !d_status)
-    return EQC_E_INVALID;
-  if (comm->nranks < 2) return EQC_E_UNSUPPORTED;
+namespace {
+int scatter_body(eqc_comm *comm, int n_local, const uint8_t *const *color_rle, const uint8_t *const *depth_rle,
+                 const int64_t *color_bytes, const int64_t *depth_bytes, int w, int h, int slot, int32_t *d_status,
+                 cudaStream_t s) {
   P2PState &P = comm->p2p;
-  if (P.capable != 1 || P.peer_slot_c[slot].size() != (size_t)comm->nranks) return EQC_E_UNSUPPORTED;
   std::vector<int> row0;
   int maxband = 0;
   EQC_TRY(scatter_geometry(comm, w, h, row0, maxband));
-  cudaStream_t s = (cudaStream_t)stream;
   const int n = comm->nranks, me = comm->rank;
   // the peers' bands first (their stores cross NVLink while the own band is decoded)
   for (int k = 1; k <= n; ++k) {
@@ -2226,21 +2220,30 @@ extern "C" int compositor_depth_rle_scatter(eqc_comm *comm, int n_local, const u
   }
   return EQC_OK;
 }
+}  // namespace
 
-extern "C" int compose_direct_send_scattered(eqc_comm *comm, int w, int h, int slot, int dest_rank,
-                                             uint32_t *out_color, int64_t out_pitch, int flags, void *stream) {
-  if (!comm || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || dest_rank < 0 ||
-      dest_rank >= comm->nranks)
+extern "C" int compositor_depth_rle_scatter(eqc_comm *comm, int n_local, const uint8_t *const *color_rle,
+                                            const uint8_t *const *depth_rle, const int64_t *color_bytes,
+                                            const int64_t *depth_bytes, int w, int h, int slot, int32_t *d_status,
+                                            void *stream) {
+  if (!comm || n_local < 1 || n_local > EQC_MAX_SOURCES || !color_rle || !depth_rle || !color_bytes ||
+      !depth_bytes || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || !d_status)
     return EQC_E_INVALID;
-  const int n = comm->nranks, me = comm->rank;
-  if (me == dest_rank && (!out_color || out_pitch < w)) return EQC_E_INVALID;
-  if (n < 2) return EQC_E_UNSUPPORTED;
+  if (comm->nranks < 2) return EQC_E_UNSUPPORTED;
   P2PState &P = comm->p2p;
-  if (P.capable != 1 || P.peer_slot_c[slot].size() != (size_t)n) return EQC_E_UNSUPPORTED;
+  if (P.capable != 1 || P.peer_slot_c[slot].size() != (size_t)comm->nranks) return EQC_E_UNSUPPORTED;
+  return scatter_body(comm, n_local, color_rle, depth_rle, color_bytes, depth_bytes, w, h, slot, d_status,
+                      (cudaStream_t)stream);
+}
+
+namespace {
+int scattered_body(eqc_comm *comm, int w, int h, int slot, int dest_rank, uint32_t *out_color, int64_t out_pitch,
+                   int flags, cudaStream_t s) {
+  const int n = comm->nranks, me = comm->rank;
+  P2PState &P = comm->p2p;
   std::vector<int> row0;
   int maxband = 0;
   EQC_TRY(scatter_geometry(comm, w, h, row0, maxband));
-  cudaStream_t s = (cudaStream_t)stream;
   int64_t *stats = comm->st.stats;
   for (int i = 0; i < 4; ++i) stats[i] = 0;
   // every rank's scattered bands are in place (and every rank passed this slot)
@@ -2279,6 +2282,21 @@ extern "C" int compose_direct_send_scattered(eqc_comm *comm, int w, int h, int s
     }
   }
   return EQC_OK;
+}
+
+}  // namespace
+
+extern "C" int compose_direct_send_scattered(eqc_comm *comm, int w, int h, int slot, int dest_rank,
+                                             uint32_t *out_color, int64_t out_pitch, int flags, void *stream) {
+  if (!comm || w <= 0 || h <= 0 || slot < 0 || slot >= P2PState::kSlots || dest_rank < 0 ||
+      dest_rank >= comm->nranks)
+    return EQC_E_INVALID;
+  const int n = comm->nranks, me = comm->rank;
+  if (me == dest_rank && (!out_color || out_pitch < w)) return EQC_E_INVALID;
+  if (n < 2) return EQC_E_UNSUPPORTED;
+  P2PState &P = comm->p2p;
+  if (P.capable != 1 || P.peer_slot_c[slot].size() != (size_t)n) return EQC_E_UNSUPPORTED;
+  return scattered_body(comm, w, h, slot, dest_rank, out_color, out_pitch, flags, (cudaStream_t)stream);
 }
 
 extern "C" int eqc_comm_check(eqc_comm *comm, void *stream) {
@@ -2591,6 +2609,47 @@ extern "C" int compose_direct_send_rle_pull_local(int nranks, int n_local, const
   for (int q = 0; q < nranks; ++q)
     EQC_TRY(rle_pull_body(&V.c[q], n_local, w, h, 0, dest_rank, q == dest_rank ? out_color : nullptr,
                           q == dest_rank ? out_pitch : w, d_status, V.st[q]));
+  return V.join(s, out_stats);
+}
+
+// Virtual ranks on one GPU (test executor): rank q's n_local colour / depth
+// streams are color_rle[q * n_local + i] / depth_rle[q * n_local + i]; every
+// rank gets its own frame slot (plain device memory as "peer" memory).
+extern "C" int compose_direct_send_scatter_local(int nranks, int n_local, const uint8_t *const *color_rle,
+                                                 const uint8_t *const *depth_rle, const int64_t *color_bytes,
+                                                 const int64_t *depth_bytes, int w, int h, int dest_rank,
+                                                 uint32_t *out_color, int64_t out_pitch, int32_t *d_status,
+                                                 int64_t *out_stats, void *stream) {
+  if (nranks < 2 || nranks > EQC_MAX_SOURCES || n_local < 1 || n_local > EQC_MAX_SOURCES || !color_rle ||
+      !depth_rle || !color_bytes || !depth_bytes || w <= 0 || h <= 0 || dest_rank < 0 || dest_rank >= nranks ||
+      !out_color || out_pitch < w || !d_status)
+    return EQC_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  VirtualP2P V;
+  EQC_TRY(V.init(nranks, (int64_t)w * h, s));
+  const int64_t spx = (int64_t)w * h + (int64_t)w * nranks;  // the scattered layout (as eqc_comm_frame_buffers)
+  for (int q = 0; q < nranks; ++q) {  // every allocation before any launch (see VirtualP2P::init)
+    P2PState &P = V.c[q].p2p;
+    EQC_TRY(P.slot_c[0].ensure((size_t)spx * 4));
+    EQC_TRY(P.slot_d[0].ensure((size_t)spx * 4));
+    P.slot_px = spx;
+  }
+  for (int q = 0; q < nranks; ++q) {
+    P2PState &P = V.c[q].p2p;
+    P.peer_slot_c[0].assign(nranks, nullptr);
+    P.peer_slot_d[0].assign(nranks, nullptr);
+    for (int r = 0; r < nranks; ++r) {
+      P.peer_slot_c[0][r] = V.c[r].p2p.slot_c[0].as<uint32_t>();
+      P.peer_slot_d[0][r] = V.c[r].p2p.slot_d[0].as<uint32_t>();
+    }
+  }
+  for (int q = 0; q < nranks; ++q) {
+    const size_t o = (size_t)q * n_local;
+    EQC_TRY(scatter_body(&V.c[q], n_local, color_rle + o, depth_rle + o, color_bytes + o, depth_bytes + o, w, h, 0,
+                         d_status, V.st[q]));
+    EQC_TRY(scattered_body(&V.c[q], w, h, 0, dest_rank, q == dest_rank ? out_color : nullptr,
+                           q == dest_rank ? out_pitch : w, 0, V.st[q]));
+  }
   return V.join(s, out_stats);
 }
 

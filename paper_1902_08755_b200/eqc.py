@@ -73,6 +73,7 @@ def _load():
         "compose_direct_send_rle_pull": ([P, i32, i32, i32, i32, i32, P, i64, P, P], i32),
         "compositor_depth_rle_scatter": ([P, i32, P, P, P, P, i32, i32, i32, P, P], i32),
         "compose_direct_send_scattered": ([P, i32, i32, i32, i32, P, i64, i32, P], i32),
+        "compose_direct_send_scatter_local": ([i32, i32, P, P, P, P, i32, i32, i32, P, i64, P, P, P], i32),
         "compose_direct_send_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, i32, P, i64, P, P], i32),
         "compose_direct_send_rle_pull_local": ([i32, i32, P, i64, i32, i32, i32, P, i64, P, P, P], i32),
         "compose_binary_swap_p2p_local": ([i32, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P, P], i32),
@@ -523,6 +524,24 @@ def compose_direct_send_rle_pull_local(nranks, n_local, rank_streams, cap_bytes,
     rc = _lib.compose_direct_send_rle_pull_local(nranks, n_local, _ptrs(rank_streams), cap_bytes, w, h, dest_rank,
                                                  _addr(out_color), opitch, _addr(status), stats, _stream(stream))
     _check(rc, "compose_direct_send_rle_pull_local")
+    return list(stats)
+
+
+def compose_direct_send_scatter_local(nranks, color_streams, depth_streams, w, h, out_color, status,
+                                      dest_rank: int = 0, color_bytes=None, depth_bytes=None, stream=None):
+    """compositor_depth_rle_scatter + compose_direct_send_scattered for
+    virtual ranks on one GPU: rank q's streams are
+    color_streams[q * n_local : (q + 1) * n_local] (and depth)."""
+    total = len(color_streams)
+    assert total % nranks == 0 and len(depth_streams) == total
+    cb = [x.numel() for x in color_streams] if color_bytes is None else color_bytes
+    db = [x.numel() for x in depth_streams] if depth_bytes is None else depth_bytes
+    opitch = _frame_geom(out_color)[2]
+    stats = (ctypes.c_int64 * 4)()
+    rc = _lib.compose_direct_send_scatter_local(nranks, total // nranks, _ptrs(color_streams), _ptrs(depth_streams),
+                                                _i64s(cb), _i64s(db), w, h, dest_rank, _addr(out_color), opitch,
+                                                _addr(status), stats, _stream(stream))
+    _check(rc, "compose_direct_send_scatter_local")
     return list(stats)
 
 

@@ -144,6 +144,41 @@ def test_rle_pull_virtual_ranks_equal_oracle(eqc, case):
     assert stats[1] == nr - 1
 
 
+SCATTER_CASES = [
+    # (nranks, n_local, w, h, dest): uneven bands (h % n != 0), ragged chunks (w % 128 != 0)
+    (2, 2, 300, 41, 0),
+    (3, 1, 333, 20, 2),
+    (4, 2, 640, 130, 1),
+    (2, 4, 1920, 1080, 1),
+]
+
+
+@pytest.mark.parametrize("case", SCATTER_CASES, ids=[f"n{c[0]}x{c[1]}_{c[2]}x{c[3]}_d{c[4]}" for c in SCATTER_CASES])
+def test_scatter_virtual_ranks_equal_oracle(eqc, case):
+    """compositor_depth_rle_scatter (each rank's fused decode stores band j
+    into rank j's frame slot) + compose_direct_send_scattered (band composite
+    of the copies, colour to the destination) on virtual ranks: bit-exact
+    against O1 over all ranks' sources in rank-major order."""
+    nr, nl, w, h, dest = case
+    N = nr * nl
+    c, d = synth.depth_sources(synth.SEED_BASE + 97 + N, N, w, h)
+    want, _ = oracle.depth_composite(c, d)
+    dc = [to_dev(x) for x in c]
+    dd = [to_dev(x) for x in d]
+    cs, ds = [], []
+    for q in range(nr):
+        b, cap = _encode_rank_streams(eqc, dc[q * nl:(q + 1) * nl], dd[q * nl:(q + 1) * nl], w, h)
+        cs += [b[i * cap:(i + 1) * cap] for i in range(nl)]
+        ds += [b[(nl + i) * cap:(nl + i + 1) * cap] for i in range(nl)]
+    out = out_frame(h, w)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    stats = eqc.compose_direct_send_scatter_local(nr, cs, ds, w, h, out, status, dest_rank=dest)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    np.testing.assert_array_equal(to_host(out), want)
+    assert stats[0] == nr * (nr - 1)  # every rank received a band copy from every peer
+
+
 def test_p2p_flag_wait_timeout_reports_nccl_error():
     # a virtual rank that never arrives (EQC_P2P_DROP_RANK): every other
     # rank's flag wait must give up after EQC_P2P_TIMEOUT_MS (no GPU hang)
