@@ -375,7 +375,8 @@ __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, i
     const bool rep = (c & 0x80) != 0;
     ok = ok && (c & 0x7F) + 1 == L && size == (rep ? 3 : 2 + L);
     if (rep) return (uint32_t)r[2] * 0x01010101u;
-    return ld_window(r, 2 + min(i0, L), 0x3210u);  // (lanes past L: inside the slack)
+    // (lanes past L, and a malformed size: reads stay within r[0, size + 8))
+    return ld_window(r, min(2 + min(i0, L), size), 0x3210u);
   }
   if (ntok <= 4) {
     // token boundaries computed by every lane (uniform); the lane's nibble and
@@ -403,7 +404,7 @@ __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, i
     if (ntok <= 32) {
       // lane t holds token t: starts and payload sums by one packed warp
       // scan, then the mask words by OR-reductions of the token ranges
-      const bool act = lane < ntok;
+      const bool act = lane < ntok && 1 + lane < size;  // (the second test only for a malformed record)
       const int c = act ? r[1 + lane] : 0;
       const int len = act ? (c & 0x7F) + 1 : 0;
       const bool lit = !(c & 0x80);
@@ -423,7 +424,7 @@ __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, i
     } else {
       // lane l holds tokens 4l .. 4l+3 (of at most 128: ntok <= L); S and E
       // as byte markers in the scratch, gathered into words by shuffles
-      const int nt = min(ntok, L);
+      const int nt = min(min(ntok, L), size - 1);  // (reads stay inside a malformed record)
       int sl = 0, sp = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {

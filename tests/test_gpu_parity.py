@@ -6,6 +6,8 @@ Shapes span several 128-pixel chunks / 4-pixel vectors and ragged tails,
 odd widths, pitch > width, misaligned pointers (scalar path), N in
 {1, 2, 3, 8, 16, 64}, all-background, heavy depth ties and uniform noise.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -439,6 +441,48 @@ def test_fused_decode_corruption(eqc):
     t = bytearray(ds); t[pay0 + 1] = 0x80 | 3; cases.append(("depth token lengths", bytes(cs), bytes(t)))
     for name, a, b in cases:
         assert _fused_status(eqc, [a], [b], w, h) == eqc.E_CORRUPT, name
+
+
+def test_decoders_survive_random_corruption(eqc):
+    """Random byte corruption of the payload (ntok bytes, ctrl bytes, values)
+    and of plane sizes in the table: the fused decode and the plain decoder
+    must never fault (their reads stay inside the staged records + slack) and
+    must report EQC_E_CORRUPT whenever the output could be wrong; a stream
+    they accept decodes exactly like the oracle's decoder of the same bytes
+    when that one accepts it too."""
+    rng = np.random.default_rng(SEED + 79)
+    w, h, n = 333, 6, 3
+    c, d = synth.depth_sources(SEED + 79, n, w, h)
+    cs = [bytearray(oracle.rle_encode(x, kind=0, flags=1)) for x in c]
+    ds = [bytearray(oracle.rle_encode(x, kind=1, flags=0)) for x in d]
+    S = (w + 127) // 128
+    pay0 = 32 + 8 * S * h
+    for trial in range(int(os.environ.get("EQC_FUZZ_TRIALS", "60"))):
+        tc = [bytearray(x) for x in cs]
+        td = [bytearray(x) for x in ds]
+        for _ in range(1 + trial % 4):
+            tgt = (tc if rng.integers(2) else td)[int(rng.integers(n))]
+            if rng.integers(5) == 0:  # a plane size of a table entry
+                k = 32 + 8 * int(rng.integers(S * h)) + 4 + int(rng.integers(4))
+            else:  # any payload byte
+                k = pay0 + int(rng.integers(len(tgt) - pay0))
+            tgt[k] = int(rng.integers(256))
+        st = _fused_status(eqc, [bytes(x) for x in tc], [bytes(x) for x in td], w, h)
+        assert st in (0, eqc.E_CORRUPT), (trial, st)
+        for x in tc + td:
+            out = out_frame(h, w)
+            status = torch.zeros(1, dtype=torch.int32, device="cuda")
+            eqc.image_decompress_rle(stream_dev(bytes(x)), out, status)
+            torch.cuda.synchronize()
+            st = int(status.item())
+            assert st in (0, eqc.E_CORRUPT), trial
+            rc, want = oracle.rle_decode(bytes(x), w, h)
+            # the plain decoder decodes every record: it accepts exactly the
+            # streams the oracle accepts, and then decodes them identically
+            assert (st == 0) == (rc == 0), (trial, st, rc)
+            if st == 0:
+                np.testing.assert_array_equal(to_host(out), want)
+    torch.cuda.synchronize()  # no sticky CUDA error
 
 
 def test_encoder_workspace_any_8_byte_alignment(eqc):
