@@ -1282,9 +1282,10 @@ constexpr int kPreWords = 1024; // per-warp record prefetch buffer (4 KB)
 constexpr int kFPos = EQC_FPOS;  // chunk positions per CTA (claimed by its warps from a shared counter)
 
 // One chunk position (128 pixels of one row) of the fused decode, by one warp.
-//  Phase A (lane i takes source i; sources 32.. in a second pass unless ONE):
-//   the depth and colour table entries of every stream are validated and
-//   probed for constant chunks; if every chunk of the position is constant
+//  Phase A (n <= 16: lane q takes stream q; else lane i takes source i's two
+//   streams, sources 32.. in a second pass unless ONE): the depth and colour
+//   table entries of every stream are validated and probed for constant
+//   chunks; if every chunk of the position is constant
 //   the depth composite is evaluated on the scalar values (minimum depth, ties
 //   to the lowest index) and written with one 128-bit store per lane.
 //  Phase B: every non-constant record of the position is prefetched into the
@@ -1313,7 +1314,7 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
   const int L = min(kC, p.w - k * kC);
   constexpr int NP = ONE ? 1 : 2;
   const int npass = ONE ? 1 : (n + 31) >> 5;
-  uint4 ed[NP], ec[NP];  // {offset, plane sizes, value, constant} per pass
+  uint4 ed[NP], ec[NP];  // {offset, plane sizes, value (as coded), constant} per pass
   bool ok = true;
   bool allc = true;
   if (ONE && n <= 16) {
@@ -1337,23 +1338,23 @@ __device__ __forceinline__ bool fused_position(const FusedParams &p, int c, int 
     if (lane >= n) ed[0] = ec[0] = make_uint4(0, 0, 0, 1);
   } else {
 #pragma unroll
-  for (int ps = 0; ps < NP; ++ps) {
-    ed[ps] = ec[ps] = make_uint4(0, 0, 0, 1);
-    if (ps >= npass) continue;
-    const int i = ps * 32 + lane;
-    if (i < n) {
-      int64_t od, oc;
-      uint32_t pd, pc;
-      ok = entry_local(p.src[n + i], s_pb[n + i], nch, c, L, od, pd) && ok;
-      ok = entry_local(p.src[i], s_pb[i], nch, c, L, oc, pc) && ok;
-      uint32_t dv = 0, cv = 0;
-      const bool dc = ok && probe_const(p.src[n + i] + payload0 + od, pd, L, dv);
-      const bool cc = ok && probe_const(p.src[i] + payload0 + oc, pc, L, cv);
-      ed[ps] = make_uint4((uint32_t)od, pd, dv, dc ? 1u : 0u);
-      ec[ps] = make_uint4((uint32_t)oc, pc, cv, cc ? 1u : 0u);
-      allc = allc && dc && cc;
+    for (int ps = 0; ps < NP; ++ps) {
+      ed[ps] = ec[ps] = make_uint4(0, 0, 0, 1);
+      if (ps >= npass) continue;
+      const int i = ps * 32 + lane;
+      if (i < n) {
+        int64_t od, oc;
+        uint32_t pd, pc;
+        ok = entry_local(p.src[n + i], s_pb[n + i], nch, c, L, od, pd) && ok;
+        ok = entry_local(p.src[i], s_pb[i], nch, c, L, oc, pc) && ok;
+        uint32_t dv = 0, cv = 0;
+        const bool dc = ok && probe_const(p.src[n + i] + payload0 + od, pd, L, dv);
+        const bool cc = ok && probe_const(p.src[i] + payload0 + oc, pc, L, cv);
+        ed[ps] = make_uint4((uint32_t)od, pd, dv, dc ? 1u : 0u);
+        ec[ps] = make_uint4((uint32_t)oc, pc, cv, cc ? 1u : 0u);
+        allc = allc && dc && cc;
+      }
     }
-  }
   }
   if (!__all_sync(EQC_FULL, ok)) {
     if (lane == 0) set_corrupt(p.status);
