@@ -168,12 +168,18 @@ EQC_API int compose_direct_send_scattered(eqc_comm *comm, int w, int h, int slot
  * by the tests).
  * eqc_plan_bands: row0[j] = floor(j*h/n), j = 0..n (band j = rows
  *   [row0[j], row0[j+1]), R-C13).
+ * eqc_plan_bands_gather: the bands of the peer-memory direct send with a
+ *   colour gather to `dest` (R-C13, n >= 3): the destination gets
+ *   round(h/(2n-1)) rows, the other ranks equal shares of the rest (so every
+ *   rank's NVLink inbound is about 8(n-1)/(2n-1) bytes per frame pixel);
+ *   n <= 2 (or EQC_P2P_EQUAL_BANDS=1): eqc_plan_bands.
  * eqc_plan_binary_swap: for rank `rank` of n = 2^k ranks, fills k rounds of
  *   6 ints {partner, low (1 if rank's bit r is 0), keep_y0, keep_y1, send_y0,
  *   send_y1} (rows) and returns k; the region after the last round is the
  *   rank's final band.  EQC_E_UNSUPPORTED if n is not a power of two.
  */
 EQC_API int eqc_plan_bands(int h, int n, int *row0);
+EQC_API int eqc_plan_bands_gather(int h, int n, int dest, int *row0);
 EQC_API int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_rounds);
 
 /*

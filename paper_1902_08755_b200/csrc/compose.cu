@@ -2695,6 +2695,12 @@ extern "C" int eqc_plan_bands(int h, int n, int *row0) {
   return EQC_OK;
 }
 
+extern "C" int eqc_plan_bands_gather(int h, int n, int dest, int *row0) {
+  if (h <= 0 || n < 1 || dest < 0 || dest >= n || !row0) return EQC_E_INVALID;
+  plan_bands_gather(h, n, dest, row0);
+  return EQC_OK;
+}
+
 extern "C" int eqc_plan_binary_swap(int h, int n, int rank, int *rounds, int max_rounds) {
   if (h <= 0 || n < 1 || rank < 0 || rank >= n) return EQC_E_INVALID;
   std::vector<BsRound> rr;

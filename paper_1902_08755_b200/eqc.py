@@ -84,6 +84,7 @@ def _load():
         "eqc_comm_check": ([P, P], i32),
         "eqc_comm_abort": ([P], i32),
         "eqc_plan_bands": ([i32, i32, P], i32),
+        "eqc_plan_bands_gather": ([i32, i32, i32, P], i32),
         "eqc_plan_binary_swap": ([i32, i32, i32, P, i32], i32),
         "compose_direct_send": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
         "compose_binary_swap": ([P, i32, P, P, i32, i32, i64, i32, i32, i32, P, i64, P], i32),
@@ -285,6 +286,13 @@ def eqc_plan_bands(h: int, n: int):
     """Row boundaries of the n direct-send bands (R-C13): [row0[0] .. row0[n]]."""
     row0 = (ctypes.c_int * (n + 1))()
     _check(_lib.eqc_plan_bands(h, n, row0), "eqc_plan_bands")
+    return list(row0)
+
+
+def eqc_plan_bands_gather(h: int, n: int, dest: int):
+    """Row boundaries of the peer-memory direct send's gather-aware bands."""
+    row0 = (ctypes.c_int * (n + 1))()
+    _check(_lib.eqc_plan_bands_gather(h, n, dest, row0), "eqc_plan_bands_gather")
     return list(row0)
 
 

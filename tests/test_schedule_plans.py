@@ -23,6 +23,34 @@ def test_bands_partition_and_balance(h, n):
     assert row0 == [j * h // n for j in range(n + 1)]
 
 
+@pytest.mark.parametrize("h,n,dest", [(2160, 3, 0), (2160, 4, 0), (4320, 4, 3), (1081, 5, 2), (2160, 8, 0),
+                                        (7, 8, 7), (1080, 2, 0), (1080, 1, 0)])
+def test_gather_bands_balance_the_links(h, n, dest):
+    """Gather-aware bands (R-C13 refinement, >= 3 ranks): a partition of the
+    rows in rank order; the destination's band is round(h / (2n - 1)); the
+    others differ by at most one row; every rank's NVLink inbound -- band
+    pulls of 8 B/px from each peer plus, at the destination, the other bands'
+    colour (4 B/px) -- is within one row's worth of the others'."""
+    row0 = eqc.eqc_plan_bands_gather(h, n, dest)
+    assert row0[0] == 0 and row0[-1] == h and len(row0) == n + 1
+    sizes = [row0[j + 1] - row0[j] for j in range(n)]
+    assert all(s >= 0 for s in sizes)
+    if n <= 2:
+        assert row0 == eqc.eqc_plan_bands(h, n)
+        return
+    assert sizes[dest] == (h + (2 * n - 1) // 2) // (2 * n - 1)
+    others = [s for j, s in enumerate(sizes) if j != dest]
+    assert max(others) - min(others) <= 1
+    inbound = [8 * (n - 1) * s + (4 * (h - s) if j == dest else 0) for j, s in enumerate(sizes)]
+    # unequal bands trade one rank's excess against the others: at most a
+    # few rows' worth of imbalance remains from the rounding
+    assert max(inbound) - min(inbound) <= 8 * (n - 1) * 2 + 4 * 2
+    # and the destination receives less than with equal bands
+    eq = eqc.eqc_plan_bands(h, n)
+    eq_dest = eq[dest + 1] - eq[dest]
+    assert inbound[dest] < 8 * (n - 1) * eq_dest + 4 * (h - eq_dest)
+
+
 def bitrev(x, k):
     return int(format(x, f"0{k}b")[::-1], 2) if k else 0
 
