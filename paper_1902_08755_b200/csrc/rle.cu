@@ -855,6 +855,11 @@ __device__ __forceinline__ bool probe_const(const uint8_t *rec, uint32_t ps, int
   return ok;
 }
 
+#ifndef EQC_PLANE_UNROLL
+#define EQC_PLANE_UNROLL 1
+#endif
+constexpr int kPlaneUnroll = EQC_PLANE_UNROLL;  // (1: one decode_plane_w call site per pass)
+
 // Decode a staged record into px[0..3], planes in the order 3, 0, 1, 2 (the
 // most significant byte first).  With `check`, when that byte alone makes the
 // source deeper than the current best at every pixel of the chunk (bm: byte j
@@ -872,7 +877,7 @@ __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int
   uint32_t X0 = 0, X1 = 0, X2 = 0, X3 = 0;  // shift register of plane words
   bool ok = true;
   skip = false;
-#pragma unroll 1
+#pragma unroll kPlaneUnroll
   for (int t = 0; t < 4; ++t) {
     const int size = (int)(sz & 0xFFu);
     const uint32_t w = decode_plane_w(r + off, size, L, lane, ok, info);
