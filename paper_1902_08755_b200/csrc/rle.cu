@@ -463,6 +463,7 @@ struct Enc3Params {
   uint32_t *blk;       // [count][NB] block totals (sum of the sizes of 64 consecutive runs)
   int64_t pitch, nchunks;
   int count, w, h, S, R, NB;  // NB = blocks of 64 runs per image
+  float invS, invR;           // 1 / S, 1 / R
   int total_enc;
   int vec;             // 128-bit loads allowed
 };
@@ -495,6 +496,16 @@ __device__ __forceinline__ uint4 ld_stream_u4_if_hint(const void *p, bool pred, 
   return r;
 }
 
+// q = a / b for 0 <= a < 2^22 by a float reciprocal (inv = 1/b), corrected
+// by one; larger a: the integer division.
+__device__ __forceinline__ int div_small(int a, int b, float inv) {
+  if (a >= (1 << 22)) return a / b;
+  int q = (int)((float)a * inv);
+  const int r = a - q * b;
+  q += r < 0 ? -1 : (r >= b ? 1 : 0);
+  return q;
+}
+
 // CONTIG: pitch == w, w % 128 == 0, 16-byte aligned: a run is one contiguous
 // span of full chunks (straight-line loads with immediate offsets).
 // FULL: w % 128 == 0 (every chunk has 128 pixels).
@@ -507,7 +518,7 @@ __device__ void e3_encode_run(const Enc3Params &p, int m, int r, int lane, E3War
   const int c0 = r * kRun3;
   const int cnt = min(kRun3, nch - c0);
   const int Llast = p.w - (p.S - 1) * kC;
-  const int y0 = c0 / p.S, k0 = c0 - y0 * p.S;
+  const int y0 = div_small(c0, p.S, p.invS), k0 = c0 - y0 * p.S;
   const uint32_t *row0 = im.src + (int64_t)y0 * p.pitch;
   auto chunk_ptr = [&](int j, int &L) -> const uint32_t * {
     if (CONTIG) {
@@ -786,7 +797,7 @@ __global__ void __launch_bounds__(kE3Warps * 32, EQC_E3_MINB) rle_encode3_kernel
   while (e < p.total_enc) {
     int en = 0;
     if (lane == 0) en = (int)atomicAdd(ectr, 1u);  // the next ticket, in flight meanwhile
-    const int m = e / p.R;
+    const int m = div_small(e, p.R, p.invR);
     e3_encode_run<FULL, CONTIG>(p, m, e - m * p.R, lane, W, K, s_lut, s_lut + 16);
     e = __shfl_sync(EQC_FULL, en, 0);
   }
@@ -1748,6 +1759,8 @@ extern "C" int image_compress_rle_batch(int count, const uint32_t *const *src, i
       e.S = p.S;
       e.R = R;
       e.NB = NB;
+      e.invS = 1.0f / (float)p.S;
+      e.invR = 1.0f / (float)R;
       e.total_enc = gc * R;
       e.vec = vec ? 1 : 0;
       const int64_t item_ctas = ((int64_t)e.total_enc + kE3Warps - 1) / kE3Warps;
