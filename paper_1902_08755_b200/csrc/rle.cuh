@@ -365,15 +365,18 @@ __device__ __forceinline__ uint32_t ld_window(const uint8_t *r, int pi, uint32_t
 // 32 tokens).
 __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, int L, int lane, bool &ok,
                                                    uint16_t *info) {
-  const int ntok = r[0];  // (size 0: a byte of the next plane or the slack)
-  ok = ok && size >= 2 && ntok >= 1 && 1 + ntok <= size && ntok <= L;
+  // (size 0: ntok is a byte of the next plane or the slack.)  The checks of
+  // each path below imply size >= 2, 1 <= ntok, 1 + ntok <= size, ntok <= L:
+  // a path that sums all ntok lengths to L and their payload bytes to
+  // size - 1 - ntok cannot accept a record that breaks one of them.
+  const int ntok = r[0];
   const int i0 = 4 * lane;
   uint32_t nib;  // advancing positions among 4*lane .. 4*lane+3
   int cntb;      // advancing positions before 4*lane
   if (ntok <= 1) {  // single-token fast paths
     const int c = r[1];
     const bool rep = (c & 0x80) != 0;
-    ok = ok && (c & 0x7F) + 1 == L && size == (rep ? 3 : 2 + L);
+    ok = ok && ntok == 1 && (c & 0x7F) + 1 == L && size == (rep ? 3 : 2 + L);
     if (rep) return (uint32_t)r[2] * 0x01010101u;
     // (lanes past L, and a malformed size: reads stay within r[0, size + 8))
     return ld_window(r, min(2 + min(i0, L), size), 0x3210u);
@@ -425,6 +428,7 @@ __device__ __forceinline__ uint32_t decode_plane_w(const uint8_t *r, int size, i
       // lane l holds tokens 4l .. 4l+3 (of at most 128: ntok <= L); S and E
       // as byte markers in the scratch, gathered into words by shuffles
       const int nt = min(min(ntok, L), size - 1);  // (reads stay inside a malformed record)
+      ok = ok && ntok <= L;                        // (tokens past L are not summed)
       int sl = 0, sp = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
