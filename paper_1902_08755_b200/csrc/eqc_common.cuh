@@ -105,11 +105,15 @@ __device__ __forceinline__ uint32_t bytes_popc_nibble(uint32_t x) {
 // ---- warp scans -----------------------------------------------------------
 // Inclusive prefix sum over lanes (plain integer add; packed byte/halfword
 // lanes are fine as long as no lane's field overflows).
+// (The shuffle's in-range predicate guards the add: two instructions a step.)
 __device__ __forceinline__ uint32_t warp_incl_scan_add(uint32_t v, int lane) {
+  (void)lane;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    uint32_t o = __shfl_up_sync(EQC_FULL, v, d);
-    if (lane >= d) v += o;
-  }
+  for (int d = 1; d < 32; d <<= 1)
+    asm("{\n\t.reg .b32 o;\n\t.reg .pred q;\n\t"
+        "shfl.sync.up.b32 o|q, %0, %1, 0, -1;\n\t"
+        "@q add.u32 %0, %0, o;\n\t}"
+        : "+r"(v)
+        : "r"(d));
   return v;
 }
