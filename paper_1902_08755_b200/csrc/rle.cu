@@ -884,7 +884,7 @@ __device__ __forceinline__ bool decode_staged(const uint8_t *r, uint32_t ps, int
                                               bool &skip, bool swz = false) {
   // plane sizes and record offsets in decode order: rotate plane 3 first
   uint32_t sz = __funnelshift_l(ps, ps, 8);  // bytes: s3, s0, s1, s2
-  int off = (int)(ps & 0xFFu) + (int)((ps >> 8) & 0xFFu) + (int)((ps >> 16) & 0xFFu);
+  int off = (int)__dp4a(ps, 0x00010101u, 0u);  // s0 + s1 + s2
   uint32_t X0 = 0, X1 = 0, X2 = 0, X3 = 0;  // shift register of plane words
   bool ok = true;
   skip = false;
@@ -944,7 +944,7 @@ __device__ __noinline__ const uint8_t *stage_record(const uint8_t *src, int64_t 
 
 // 16-byte units of the aligned window covering a record.
 __device__ __forceinline__ int record_quads(const uint8_t *rec, uint32_t ps) {
-  const int total = (int)(ps & 0xFF) + (int)((ps >> 8) & 0xFF) + (int)((ps >> 16) & 0xFF) + (int)(ps >> 24);
+  const int total = (int)__dp4a(ps, 0x01010101u, 0u);  // the four plane sizes
   return ((int)((uintptr_t)rec & 15) + total + 15) >> 4;
 }
 
