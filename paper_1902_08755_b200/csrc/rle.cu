@@ -1027,8 +1027,8 @@ __device__ __forceinline__ bool entry_lane(const uint8_t *src, int64_t payload_b
 }
 
 // Lane-local variant: loads chunk c-1's entry itself (no warp collective).
-__device__ __forceinline__ bool entry_local(const uint8_t *src, int64_t payload_bytes, int64_t nchunks, int64_t c,
-                                            int L, int64_t &off, uint32_t &ps) {
+__device__ __forceinline__ bool entry_local(const uint8_t *src, int64_t payload_bytes, int nchunks, int c, int L,
+                                            int64_t &off, uint32_t &ps) {
   const uint2 te = __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * c));
   const uint2 tp = c > 0 ? __ldg(reinterpret_cast<const uint2 *>(src + 32 + 8 * (c - 1))) : make_uint2(0u, 0u);
   off = te.x;
