@@ -443,15 +443,16 @@ def test_fused_decode_corruption(eqc):
         assert _fused_status(eqc, [a], [b], w, h) == eqc.E_CORRUPT, name
 
 
-def test_decoders_survive_random_corruption(eqc):
+@pytest.mark.parametrize("n", [3, 20])  # phase A lane per stream (n <= 16) / lane per source
+def test_decoders_survive_random_corruption(eqc, n):
     """Random byte corruption of the payload (ntok bytes, ctrl bytes, values)
     and of plane sizes in the table: the fused decode and the plain decoder
     must never fault (their reads stay inside the staged records + slack) and
     must report EQC_E_CORRUPT whenever the output could be wrong; a stream
     they accept decodes exactly like the oracle's decoder of the same bytes
     when that one accepts it too."""
-    rng = np.random.default_rng(SEED + 79)
-    w, h, n = 333, 6, 3
+    rng = np.random.default_rng(SEED + 79 + n)
+    w, h = 333, 6
     c, d = synth.depth_sources(SEED + 79, n, w, h)
     cs = [bytearray(oracle.rle_encode(x, kind=0, flags=1)) for x in c]
     ds = [bytearray(oracle.rle_encode(x, kind=1, flags=0)) for x in d]
